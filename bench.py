@@ -1,0 +1,340 @@
+#!/usr/bin/env python3
+"""bench.py — DeepEP-style MoE dispatch+combine over the B200 GIN path.
+
+Workload (BASELINE.json configs[3]): high-throughput dispatch/combine with
+4096 tokens per rank, hidden 7168, top-8 of 256 experts, bf16 payloads, one
+rank per GPU (N = --gpus; at N=1 every expert is local and the path is
+HBM-bound; at N>1 the remote share crosses NVLink 5 peer mappings).
+A step = one dispatch (route + NVLink puts + per-expert releases) and one
+combine (expert transform fused into the return puts + flag wait + top-k
+weighted reduce) over one batch of synthetic tokens already in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+For N>1 the driver launches it under torch.distributed.run (one rank per GPU).
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE dispatch+combine µs & GB/s/GPU at 8×B200; put+signal latency vs msg size"
+N_TOK, HIDDEN, TOPK, EXPERTS = 4096, 7168, 8, 256
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--tokens", type=int, default=N_TOK)
+    p.add_argument("--mode", type=int, default=1, help="0 = u16 exact, 1 = bf16")
+    p.add_argument("--layout", type=int, default=1, help="0 = reference layout, 1 = compact")
+    p.add_argument("--ctas", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk.get("hbm_gbs", 6650.0), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# --------------------------------------------------------------------- reference arm
+def ref_sample_bytes(n, T, K=TOPK, H=HIDDEN):
+    return n * T * K * ((2 * H + 16) + 2 * H)
+
+
+def run_reference(args, steps, warmup):
+    """The reference's own CPU implementation (oracle/_ref = ginsim compiled from
+    /root/reference) on a bounded sample of the workload: run_moe_ll with 8
+    in-process ranks (2 host threads each), T=128 tokens/rank, hidden 7168,
+    top-8 of 256.  Metric: dispatch+combine bytes moved per second."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    n_ref, t_ref = 8, 128
+    times = []
+    for i in range(warmup + steps):
+        j = O.ref_run("moe-ll", "--ranks", n_ref, "--experts", EXPERTS, "--topk", TOPK, "--tokens", t_ref,
+                      "--hidden", HIDDEN, "--seed", 1, "--backend", "direct")
+        if i >= warmup:
+            times.append(j["best_s"])
+    t = statistics.median(times)
+    gbs = ref_sample_bytes(n_ref, t_ref) / t / 1e9
+    return {"value": gbs, "s_per_sample": t, "cores": 2 * n_ref,
+            "sample": f"reference run_moe_ll (harness_moe.cpp:252), 8 in-process ranks x 2 threads, T=128/rank, "
+                      f"hidden 7168, top-8 of 256, verification included; median of {len(times)}"}
+
+
+def reference_main(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    r = run_reference(args, max(1, min(args.steps, 5)), min(1, args.warmup))
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
+        return
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s (dispatch+combine bytes, all ranks)",
+            "n_gpus": 0, "steps": max(1, min(args.steps, 5)), "warmup": min(1, args.warmup),
+            "ms_per_step": r["s_per_sample"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "config": {"workload": "DeepEP dispatch/combine sample: 8 ranks x 128 tokens, hidden 7168, top-8/256",
+                       "requested_gpus": args.gpus},
+            "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["cores"], "kind": "reference",
+                             "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_main(args)
+        return
+    rank, world, local = dist_env()
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_15076_b200 as G
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+        def allgather(blob: bytes):
+            out = [None] * world
+            dist.all_gather_object(out, blob)
+            return out
+        comm = G.Comm.create(rank, world, local, allgather, G.Config())
+    else:
+        comm = G.Comm.create_all([local], G.Config())[0]
+
+    T, H, K, E = args.tokens, HIDDEN, TOPK, EXPERTS
+    cfg = G.MoeConfig(E, K, T, H, args.mode, args.layout, args.ctas)
+    moe = G.Moe(comm, cfg)
+    dev = torch.device("cuda", local)
+    x = torch.empty(T * H, dtype=torch.int16, device=dev)
+    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
+    w = torch.empty(T * K, dtype=torch.float32 if args.mode == 1 else torch.int16, device=dev)
+    out = torch.empty(T * H, dtype=torch.int16, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    moe.generate(1, rank, x, idx, w, stream=stream)
+    torch.cuda.synchronize()
+
+    def step():
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+
+    # algorithmic bytes (per rank): dispatch messages + combine messages
+    from numpy import array  # noqa: F401  (torch-only path below)
+    idx_host = idx.cpu().numpy().reshape(T, K)
+    e_local = E // world
+    remote_msgs = int(((idx_host // e_local) != rank).sum())
+    dmsg, cmsg = 2 * H + 16, 2 * H
+    disp_bytes = T * K * dmsg
+    comb_bytes = T * K * cmsg
+    step_bytes_rank = disp_bytes + comb_bytes
+    remote_bytes_rank = remote_msgs * (dmsg + cmsg)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    comm.check_device()
+
+    # --- device-timed region: K steps, events around each kernel ---------------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        ev[i][1].record(stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+        ev[i][2].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    comm.check_device()
+    total_ms = start.elapsed_time(end)
+    d_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    c_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    t = torch.tensor([total_ms, statistics.mean(d_ms), statistics.mean(c_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, d_mean, c_mean = t.tolist()
+    ms_per_step = total_ms / args.steps
+    agg_bytes = step_bytes_rank * world
+    value = agg_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # --- e2e: host buffers through the public API, copies inside the region ---
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        ih = idx.cpu().pin_memory()
+        wh = w.cpu().pin_memory()
+        oh = torch.empty_like(out, device="cpu").pin_memory()
+        e_steps = max(3, args.steps // 2)
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                x.copy_(xh, non_blocking=True)
+                idx.copy_(ih, non_blocking=True)
+                w.copy_(wh, non_blocking=True)
+            step()
+            with torch.cuda.stream(stream):
+                oh.copy_(out, non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        e2.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([s2.elapsed_time(e2)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = te.item() / e_steps
+        e2e = {"value": agg_bytes / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(xh.numel() * 2 + ih.numel() * 4 + wh.numel() * wh.element_size()),
+               "d2h_bytes_per_step": int(oh.numel() * 2)}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = load_peaks()
+    # dominant kernel and its algorithmic HBM bytes per launch
+    disp_hbm = T * H * 2 + T * K * 4 + T * K * dmsg             # read rows + idx, write messages (local HBM side)
+    comb_hbm = 2 * T * K * dmsg + T * K * cmsg + T * H * 2      # read msgs, write/read combine rows, write out
+    if world > 1:
+        # remote writes land in the peers' HBM; the local HBM sees this rank's
+        # reads plus the messages peers write into it (symmetric on average)
+        pass
+    dom = "dispatch" if d_mean >= c_mean else "combine"
+    dom_ms = max(d_mean, c_mean)
+    dom_bytes = disp_hbm if dom == "dispatch" else comb_hbm
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:  # noqa: BLE001
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s (dispatch+combine bytes, all GPUs)",
+        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if args.mode == 1 else "u16", "data": "synthetic",
+        "config": {"workload": f"DeepEP HT dispatch+combine, {T} tokens/rank, hidden {H}, top-{K} of {E} experts, "
+                               f"{world} rank(s) x 1 GPU", "tokens_per_rank": T, "hidden": H, "top_k": K,
+                   "experts": E, "layout": "compact" if args.layout == 1 else "reference",
+                   "parallelism": f"ep{world}", "l2": "inputs larger than L2 (470 MB of messages per phase per rank)"},
+        "us_per_step": ms_per_step * 1e3, "dispatch_us": d_mean * 1e3, "combine_us": c_mean * 1e3,
+        "per_gpu_GBps": value / world,
+        "roofline": {"bound": "hbm", "kernel": f"moe_{dom}_kernel", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": dom_bytes},
+        "clocks": clk, "gpu_launches": 2 * args.steps,
+        "e2e": e2e,
+    }
+    if world > 1:
+        rem_disp = remote_msgs * dmsg
+        line["nvlink"] = {"remote_bytes_per_rank_dispatch": rem_disp,
+                          "dispatch_remote_GBps_per_gpu": rem_disp / (d_mean * 1e-3) / 1e9,
+                          "combine_remote_GBps_per_gpu": remote_msgs * cmsg / (c_mean * 1e-3) / 1e9,
+                          "frac_of_900": rem_disp / (d_mean * 1e-3) / 1e9 / 900.0,
+                          "frac_of_measured_770": rem_disp / (d_mean * 1e-3) / 1e9 / 770.0}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_reference(args, 3, 0)
+        except Exception as e:  # noqa: BLE001
+            r = None
+            line["cpu_baseline_error"] = str(e)[:200]
+        if r:
+            line["cpu_baseline"] = {"value": r["value"], "unit": "GB/s", "cores": r["cores"], "kind": "reference",
+                                    "sample": r["sample"]}
+    print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

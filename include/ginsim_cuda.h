@@ -1,0 +1,300 @@
+/*
+ * ginsim_cuda.h — the C-ABI drop-in boundary of the B200-native GIN hot path.
+ *
+ * Plain C: integer status codes, plain pointers and sizes, no C++ or torch
+ * types.  Every entry point names the reference interface it replaces
+ * (/root/reference-relative file:line).  The reference is C++; a maintainer
+ * binds this header from ginsim's own classes as INTEGRATION.md shows (the
+ * C++ host layer in include/ginsim/*.hpp is exactly that binding).
+ *
+ * Error convention: every function returns a ginsim_status; on failure the
+ * thread-local ginsim_cuda_last_error() holds the message.  The codes mirror
+ * the reference's typed exceptions (proj/core/include/ginsim/errors.hpp:24-52)
+ * one to one so the C++ layer can rethrow the same type.
+ *
+ * Threading: a comm may be used from any host thread (runtime.hpp:128-134);
+ * collective calls (comm_create, window_register) must be entered by every
+ * rank of the comm, in the same order (runtime.cpp:128-175).
+ */
+#ifndef GINSIM_CUDA_H
+#define GINSIM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GINSIM_CUDA_ABI_VERSION 1
+
+typedef enum ginsim_status {
+  GINSIM_OK = 0,
+  GINSIM_E_INVALID_DESCRIPTOR = 1,   /* errors.hpp:25 InvalidDescriptor */
+  GINSIM_E_MALFORMED_DESCRIPTOR = 2, /* errors.hpp:26 */
+  GINSIM_E_OUT_OF_BOUNDS = 3,        /* errors.hpp:27 */
+  GINSIM_E_UNKNOWN_WINDOW = 4,       /* errors.hpp:28 */
+  GINSIM_E_RANK_OUT_OF_RANGE = 5,    /* errors.hpp:29 */
+  GINSIM_E_DUPLICATE_ENDPOINT = 6,   /* errors.hpp:32 */
+  GINSIM_E_UNKNOWN_CHANNEL = 7,      /* errors.hpp:33 */
+  GINSIM_E_MALFORMED_FRAME = 8,      /* errors.hpp:34 */
+  GINSIM_E_UNKNOWN_HANDLE = 9,       /* errors.hpp:37 */
+  GINSIM_E_BACKEND_MISMATCH = 10,    /* errors.hpp:38 */
+  GINSIM_E_INVALID_CONTEXT = 11,     /* errors.hpp:39 */
+  GINSIM_E_CONFIG_MISMATCH = 12,     /* errors.hpp:42 */
+  GINSIM_E_BOOTSTRAP_TIMEOUT = 13,   /* errors.hpp:43 */
+  GINSIM_E_REGISTRATION_MISMATCH = 14, /* errors.hpp:44 */
+  GINSIM_E_INVALID_PEER = 15,        /* errors.hpp:45 */
+  GINSIM_E_INVALID_SIGNAL = 16,      /* errors.hpp:46 */
+  GINSIM_E_INVALID_COUNTER = 17,     /* errors.hpp:47 */
+  GINSIM_E_RESET_WHILE_OUTSTANDING = 18, /* errors.hpp:48 */
+  GINSIM_E_TIMEOUT = 19,             /* errors.hpp:49 */
+  GINSIM_E_VERIFICATION_FAILURE = 20, /* errors.hpp:52 */
+  GINSIM_E_FLOW_CONTROL_VIOLATION = 21, /* errors.hpp:53 */
+  GINSIM_E_CHILD_FAILURE = 22,       /* errors.hpp:54 */
+  GINSIM_E_USAGE = 23,               /* errors.hpp:55 UsageError */
+  GINSIM_E_CUDA = 24,                /* a CUDA runtime/driver call failed */
+  GINSIM_E_GENERIC = 25              /* plain ginsim::Error */
+} ginsim_status;
+
+/* Thread-local message of the last failure on this thread (never NULL). */
+const char* ginsim_cuda_last_error(void);
+int ginsim_cuda_abi_version(void);
+
+/* ---------------------------------------------------------------- config
+ * proj/core/include/ginsim/runtime.hpp:29-44 (Config).  Latency-model fields
+ * of the simulator have no meaning on hardware and are absent. */
+typedef struct ginsim_cuda_config {
+  uint32_t n_contexts;    /* default 4 */
+  uint32_t backend;       /* 0 = direct (NVLink stores), 1 = proxy (GPU->CPU ring) */
+  uint32_t signal_cells;  /* default 256; top 64 reserved for barriers */
+  uint32_t counter_cells; /* default 256 */
+  uint32_t queue_depth;   /* proxy ring capacity per context, power of two; default 1024 */
+  uint32_t reserved;
+  uint64_t timeout_ms;    /* default 30000 */
+} ginsim_cuda_config;
+
+/* Config{} defaults (runtime.hpp:29-44). */
+void ginsim_cuda_config_default(ginsim_cuda_config* cfg);
+/* config_from_env (runtime.cpp:42-60): GINSIM_BACKEND / GINSIM_QUEUE_DEPTH /
+ * GINSIM_TIMEOUT_MS.  USAGE on an unparsable value. */
+int ginsim_cuda_config_from_env(ginsim_cuda_config* cfg);
+
+/* ---------------------------------------------------------------- bootstrap
+ * Out-of-band exchange used only during comm/window setup (NCCL or an
+ * in-process group; never on the data path).  allgather: every rank passes
+ * `bytes` bytes; recv receives world*bytes, rank-major.  Returns 0 on success. */
+typedef struct ginsim_cuda_bootstrap {
+  void* ctx;
+  int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes);
+} ginsim_cuda_bootstrap;
+
+typedef struct ginsim_cuda_group_s* ginsim_cuda_group_t;
+typedef struct ginsim_cuda_comm_s* ginsim_cuda_comm_t;
+
+/* InProcGroup::create (runtime.hpp:73).  Ranks are host threads of this
+ * process (one per GPU, or several emulated ranks sharing one GPU). */
+int ginsim_cuda_inproc_group_create(uint32_t world_size, ginsim_cuda_group_t* out);
+int ginsim_cuda_inproc_group_destroy(ginsim_cuda_group_t group);
+/* A bootstrap vtable for `rank` of an in-process group. */
+int ginsim_cuda_inproc_bootstrap(ginsim_cuda_group_t group, uint32_t rank, ginsim_cuda_bootstrap* out);
+
+/* comm_init (runtime.hpp:251-252, runtime.cpp:582-599).  Collective.
+ * Allocates this rank's signal/counter tables on `device`, exchanges and maps
+ * every peer's signal table, starts the proxy agent when backend == proxy.
+ * CONFIG_MISMATCH when ranks disagree on cfg (runtime.cpp:86-105). */
+int ginsim_cuda_comm_create(uint32_t rank, uint32_t world_size, int device,
+                            const ginsim_cuda_config* cfg, const ginsim_cuda_bootstrap* boot,
+                            ginsim_cuda_comm_t* out);
+/* Convenience for tests and single-process launchers (harness_launch.cpp:16-63):
+ * creates all `world_size` comms of a fresh in-process group, one host thread
+ * per rank.  devices[r] may repeat (emulated ranks on one GPU). */
+int ginsim_cuda_comm_create_all(uint32_t world_size, const int* devices,
+                                const ginsim_cuda_config* cfg, ginsim_cuda_comm_t* out);
+int ginsim_cuda_comm_destroy(ginsim_cuda_comm_t comm);
+int ginsim_cuda_comm_info(ginsim_cuda_comm_t comm, uint32_t* rank, uint32_t* world, int* device,
+                          uint32_t* backend);
+/* Device pointer to the GinDevCommView kernels take (the ncclDevComm analogue). */
+int ginsim_cuda_devcomm_view(ginsim_cuda_comm_t comm, const void** device_view);
+
+/* ---------------------------------------------------------------- memory
+ * gin_mem_alloc: cuMemCreate + cuMemMap on the comm's device
+ * with a POSIX-FD shareable handle so peers can map it.  Zero-filled. */
+int ginsim_cuda_mem_alloc(ginsim_cuda_comm_t comm, uint64_t bytes, void** ptr);
+int ginsim_cuda_mem_free(ginsim_cuda_comm_t comm, void* ptr);
+
+/* DevComm::window_register (runtime.hpp:141, runtime.cpp:347-371).  Collective:
+ * every rank contributes `bytes` at `local` (from ginsim_cuda_mem_alloc; or
+ * any device pointer when every rank lives in this process); sizes may
+ * differ, 0 is allowed.  Dense ids in call order on every rank;
+ * REGISTRATION_MISMATCH when ranks disagree on the id. */
+int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t bytes, uint32_t* window_id);
+/* Collective registration for every rank of an in-process group from one
+ * caller thread (one helper thread per rank, like the reference's launcher,
+ * harness_launch.cpp:16-63).  ptrs[r]/bytes[r] as for window_register. */
+int ginsim_cuda_window_register_all(const ginsim_cuda_comm_t* comms, uint32_t n, void* const* ptrs,
+                                    const uint64_t* bytes, uint32_t* window_id);
+/* Window::size_of (types.hpp:105) and the peer mapping of rank's region. */
+int ginsim_cuda_window_size(ginsim_cuda_comm_t comm, uint32_t window_id, uint32_t rank, uint64_t* bytes);
+int ginsim_cuda_window_ptr(ginsim_cuda_comm_t comm, uint32_t window_id, uint32_t rank, void** ptr);
+
+/* ---------------------------------------------------------------- host ops
+ * Host-issued one-sided ops (Gin, runtime.hpp:260-306), executed on the GPU
+ * in stream order: the direct backend runs them as a one-warp device op, the
+ * proxy backend hands them to the host agent.  `stream` is a cudaStream_t of
+ * the comm's device (NULL = legacy default stream). */
+typedef struct ginsim_cuda_action {
+  int32_t signal_id;   /* -1 none */
+  uint32_t signal_add; /* 0 = SignalInc, 1 = SignalAdd(operand) */
+  uint64_t operand;
+  int32_t counter_id;  /* -1 none */
+  uint32_t reserved;
+} ginsim_cuda_action;
+
+int ginsim_cuda_put(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32_t dst_window,
+                    uint64_t dst_offset, uint32_t src_window, uint64_t src_offset, uint64_t bytes,
+                    const ginsim_cuda_action* action, void* stream);
+int ginsim_cuda_put_value(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32_t dst_window,
+                          uint64_t dst_offset, uint64_t le_value, uint32_t width,
+                          const ginsim_cuda_action* action, void* stream);
+int ginsim_cuda_signal(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32_t signal_id,
+                       uint32_t signal_add, uint64_t operand, const ginsim_cuda_action* extra,
+                       void* stream);
+/* DevComm::flush (runtime.cpp:460-470): local completion of ctx's ops. */
+int ginsim_cuda_flush(ginsim_cuda_comm_t comm, uint32_t ctx, void* stream);
+/* Cells (runtime.cpp:404-443).  read/snapshot synchronise the device. */
+int ginsim_cuda_read_signal(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* value);
+int ginsim_cuda_wait_signal(ginsim_cuda_comm_t comm, uint32_t id, uint64_t expected);
+int ginsim_cuda_reset_signal(ginsim_cuda_comm_t comm, uint32_t id);
+int ginsim_cuda_read_counter(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* value);
+int ginsim_cuda_wait_counter(ginsim_cuda_comm_t comm, uint32_t id, uint64_t expected);
+int ginsim_cuda_reset_counter(ginsim_cuda_comm_t comm, uint32_t id);
+/* DevComm::snapshot_cells (runtime.hpp:178): signal_cells + counter_cells u64. */
+int ginsim_cuda_snapshot_cells(ginsim_cuda_comm_t comm, uint64_t* signals, uint64_t* counters);
+/* Device error word (device-side Timeout / OutOfBounds ...), 0 if clean;
+ * clear != 0 resets it. */
+int ginsim_cuda_device_error(ginsim_cuda_comm_t comm, uint32_t* code, int clear);
+/* Proxy agent statistics: descriptors consumed, memcpy calls issued. */
+int ginsim_cuda_proxy_stats(ginsim_cuda_comm_t comm, uint64_t* descriptors, uint64_t* copies,
+                            uint64_t* busy_ns, uint64_t* wall_ns);
+
+/* ---------------------------------------------------------------- descriptor codec
+ * proj/core/src/descriptor.cpp:148-199 (encode_descriptor / decode_descriptor),
+ * 64-byte little-endian layout of descriptor.hpp:13-27. */
+typedef struct ginsim_cuda_descriptor {
+  uint8_t opcode;   /* 1 PUT, 2 PUT_INLINE, 3 SIGNAL_ONLY */
+  uint8_t flags;    /* bit0 HAS_SIGNAL, bit1 SIGNAL_IS_ADD, bit2 HAS_COUNTER */
+  uint16_t team;
+  uint32_t peer;
+  uint32_t dst_window;
+  uint32_t src_window; /* 0xFFFFFFFF = inline */
+  uint64_t dst_offset;
+  uint64_t src_offset_or_value;
+  uint64_t bytes;
+  uint32_t signal_id;
+  uint32_t counter_id;
+  uint64_t signal_operand;
+} ginsim_cuda_descriptor;
+/* INVALID_DESCRIPTOR when d violates an invariant (descriptor.cpp:32-60). */
+int ginsim_cuda_descriptor_encode(const ginsim_cuda_descriptor* d, uint8_t out[64]);
+/* MALFORMED_DESCRIPTOR on unknown opcode / nonzero reserved / bad fields. */
+int ginsim_cuda_descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* d);
+
+/* ---------------------------------------------------------------- kernels
+ * All launchers take an array of `n` comms driven by this process: n == 1
+ * for one rank per process; n > 1 requires every comm on one device and runs
+ * them as emulated ranks in ONE cooperative launch (blocks of different
+ * ranks wait on one another, so they must be co-resident).  Streams are per
+ * call (one per comm device). */
+
+/* put+signal ping-pong (harness_bench.cpp:47-90, K14): rank 0 of the pair
+ * puts `bytes` with SignalInc to rank 1 and waits for the echo, `iters`
+ * timed iterations after `warmup`; a single persistent CTA per rank times
+ * every round trip with %globaltimer into rtt_ns_out (device, iters u64,
+ * written by rank 0).  window `send_win` / `recv_win` of >= bytes. */
+int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1,
+                         uint32_t send_win, uint32_t recv_win, uint64_t bytes, uint32_t iters,
+                         uint32_t warmup, uint32_t signal_id, uint32_t threads, uint64_t* rtt_ns_out,
+                         void* stream);
+
+/* One-sided all-to-all via put+signal: every rank puts
+ * `bytes_per_peer` from send_win[dst*M] to dst's recv_win[src*M] and signals
+ * `signal_id` on dst; then waits until the cell >= expected. */
+int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_win,
+                         uint32_t recv_win, uint64_t bytes_per_peer, uint32_t signal_id,
+                         uint64_t expected, uint32_t ctas, void* stream);
+
+/* Ring exchange (harness_ring.cpp:18-57) on the device: `rounds` rounds of
+ * put+SignalInc to (r+1)%n, wait, verify the (rank, round) pattern, reset,
+ * flush, barrier.  VERIFICATION_FAILURE through the device error word. */
+int ginsim_cuda_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_win,
+                     uint32_t recv_win, uint64_t bytes, uint32_t rounds, void* stream);
+
+/* moe-ht circular-buffer flow control (harness_moe.cpp:283-382) on the
+ * device: `channels` channels, `slots`-deep rings of 256-byte stamped slots,
+ * `messages` per channel; head/tail signals and stage counters exactly as the
+ * reference maps them through pool_select (runtime.hpp:51-58).  Each rank's
+ * pool of comms is comms_pool[r*n_pool .. +n_pool) with windows recv/stage
+ * registered in order (2 per comm).  One CTA per channel. */
+int ginsim_cuda_moe_ht_ring(const ginsim_cuda_comm_t* comms_pool, uint32_t n, uint32_t n_pool,
+                            uint32_t channels, uint32_t slots, uint32_t messages, uint64_t seed,
+                            void* stream);
+
+/* ---- DeepEP-style MoE dispatch / combine (harness_moe.cpp:105-250) ---- */
+typedef struct ginsim_cuda_moe_config {
+  uint32_t experts;  /* E, divisible by world */
+  uint32_t top_k;    /* K */
+  uint32_t tokens;   /* T per rank */
+  uint32_t hidden;   /* elements per token (2-byte elements) */
+  uint32_t mode;     /* 0 = u16 exact (reference arithmetic), 1 = bf16 */
+  uint32_t layout;   /* 0 = reference layout ((e_loc*n+src)*T+slot)*dmsg,
+                        1 = compact per-source layout (src*T*K + prefix + slot)*dmsg */
+  uint32_t ctas;     /* CTAs per rank (0 = as many as fit) */
+  uint32_t reserved;
+} ginsim_cuda_moe_config;
+
+typedef struct ginsim_cuda_moe_s* ginsim_cuda_moe_t;
+
+/* Registers (collectively) the dispatch-receive, count and combine-receive
+ * windows of the config on `comm` (moe_ll_rank_program's window set,
+ * harness_moe.cpp:122-130, minus the CPU staging windows the device path
+ * does not need).  Window ids are returned for inspection. */
+int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config* cfg, ginsim_cuda_moe_t* out);
+/* moe_create for every rank of an in-process group from one caller thread. */
+int ginsim_cuda_moe_create_all(const ginsim_cuda_comm_t* comms, uint32_t n, const ginsim_cuda_moe_config* cfg,
+                               ginsim_cuda_moe_t* out);
+int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe);
+int ginsim_cuda_moe_windows(ginsim_cuda_moe_t moe, uint32_t* dispatch_win, uint32_t* count_win,
+                            uint32_t* combine_win);
+
+/* Synthetic workload of the reference (harness_moe.cpp:25-42), generated on
+ * the device for rank `src`: x [T][hidden] (token_element in mode 0, the bf16
+ * generator in mode 1), topk_idx [T][K] int32 (route_token, bit-exact), and
+ * weights [T][K] (combine_weight: u16 in mode 0, float w/8 in mode 1). */
+int ginsim_cuda_moe_generate(ginsim_cuda_moe_t moe, uint64_t seed, uint32_t src, void* x,
+                             int32_t* topk_idx, void* weights, void* stream);
+
+/* Dispatch: route every (t,k) row of x to its expert's owner with NVLink
+ * puts into the owner's dispatch window at the reference slot order
+ * (slot = per-expert count in (t,k) order, harness_moe.cpp:143-150), write
+ * per-(expert,source) counts, release each expert with
+ * SignalAdd((1<<32)+count) (:163-167), and return once every local expert
+ * has been released by every source. */
+int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* x,
+                             const int32_t* const* topk_idx, void* stream);
+
+/* Combine: expert transform (u16: 3x+17e+1; bf16: x*s_e+c_e) fused with the
+ * put back to the source's combine window at (token*K+k)*cmsg, per-(src,ctx)
+ * SignalAdd(count) on the combine flag (:169-223), then the weighted top-k
+ * reduction out[t] = sum_k w_k*y_k (u16 wraparound, or fp32 accumulate ->
+ * bf16) once the flag reaches T*K (:227-242). */
+int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* weights,
+                            void* const* out, void* stream);
+
+/* Per-launch kernel count of the last dispatch/combine (for bench evidence). */
+int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t* threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GINSIM_CUDA_H */

@@ -1,0 +1,775 @@
+// kernels_moe.cu — DeepEP-style MoE dispatch / combine over the GIN device API.
+//
+// Reference program: proj/core/src/harness_moe.cpp:105-250 (moe_ll_rank_program)
+// and its data functions :17-98.  What is preserved bit-exactly:
+//   * slot order: slot = sent_to_expert[e]++ in (t ascending, k ascending)
+//     order (:143-150);
+//   * dispatch message = hidden u16 payload + 16-byte LE meta {src, token, k,
+//     tag = k+1} (:82-98), placed at ((e_loc*n+src)*T+slot)*dmsg in the
+//     owner's dispatch window (:135-137) [layout 0], or at the compact
+//     per-source position (src*T*K + prefix(e_loc) + slot)*dmsg [layout 1];
+//   * per-expert release SignalAdd((1<<32)+count) on cell e_loc (:163-167);
+//   * expert transform y = u16(3x+17e+1) (:36-38) fused into the combine put
+//     to the source at (token*K+k)*cmsg (:203-205);
+//   * per-(src, ctx) SignalAdd(count) on the combine flag e_local (:217-223);
+//   * weighted reduction out = sum_k u16(w_k*y_k) in u16 wraparound (:227-242).
+// bf16 mode (not in the reference) moves the same bytes and computes the
+// transform/reduction in fp32 with single rounding per op.
+//
+// Data path (B200): one warp owns a (token, part) work item: it streams the
+// part of the token row from HBM once with 128-bit non-allocating loads and
+// issues K 128-bit stores per vector, straight into the K destination
+// windows (local HBM or a peer's HBM over NVLink 5).  Per-expert slot numbers
+// come from a per-CTA histogram prefix (no atomics on the data path), the
+// release is issued by the last CTA to finish (device-scope arrival counter,
+// fence.acq_rel.sys on both sides), so one red.release.sys per expert covers
+// every warp's stores.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "gin_device.cuh"
+#include "runtime_internal.h"
+
+namespace ginsim_b200 {
+
+constexpr int kMoeThreads = 512;
+constexpr int kMoeWarps = kMoeThreads / 32;
+constexpr uint32_t kMaxExperts = 1024;
+
+struct MoeRankArgs {
+  const GinDevCommView* view;
+  unsigned int* ws;           // per-moe arrival counters [0] dispatch [1] combine
+  const uint16_t* x;          // [T][H]
+  const int32_t* idx;         // [T][K]
+  const void* weights;        // [T][K] u16 (mode 0) / f32 (mode 1)
+  uint16_t* out;              // [T][H]
+  uint64_t iteration;         // 1-based
+};
+
+struct MoeLaunch {
+  MoeRankArgs r[GIN_MAX_RANKS];
+  uint32_t E, K, T, H, mode, layout, e_local, parts;
+  uint32_t win_dispatch, win_counts, win_combine, pad;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t u16x2_transform(uint32_t two, uint32_t add) {
+  // two u16 lanes: y = 3x + (17e+1), each lane mod 2^16
+  const uint32_t lo = ((two & 0xFFFFu) * 3u + add) & 0xFFFFu;
+  const uint32_t hi = ((two >> 16) * 3u + add) & 0xFFFFu;
+  return lo | (hi << 16);
+}
+
+__device__ __forceinline__ uint32_t bf16x2_transform(uint32_t two, float s, float c) {
+  const float a = __uint_as_float(two << 16), b = __uint_as_float(two & 0xFFFF0000u);
+  const __nv_bfloat16 ya = __float2bfloat16_rn(__fadd_rn(__fmul_rn(a, s), c));
+  const __nv_bfloat16 yb = __float2bfloat16_rn(__fadd_rn(__fmul_rn(b, s), c));
+  return (uint32_t)__bfloat16_as_ushort(ya) | ((uint32_t)__bfloat16_as_ushort(yb) << 16);
+}
+
+__device__ __forceinline__ uint4 transform_vec(uint4 v, uint32_t mode, uint32_t e) {
+  if (mode == 0) {
+    const uint32_t add = (e * 17u + 1u) & 0xFFFFu;
+    v.x = u16x2_transform(v.x, add);
+    v.y = u16x2_transform(v.y, add);
+    v.z = u16x2_transform(v.z, add);
+    v.w = u16x2_transform(v.w, add);
+  } else {
+    const float s = 1.0f + (float)(e % 7u) / 8.0f;
+    const float c = ((float)(e % 9u) - 4.0f) / 16.0f;
+    v.x = bf16x2_transform(v.x, s, c);
+    v.y = bf16x2_transform(v.y, s, c);
+    v.z = bf16x2_transform(v.z, s, c);
+    v.w = bf16x2_transform(v.w, s, c);
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of n <= 4*kMoeThreads u32 values in smem.
+__device__ void block_exclusive_scan(uint32_t* data, uint32_t n, uint32_t* warp_tot, uint32_t* total_out) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (n + kMoeThreads - 1) / kMoeThreads;
+  const uint32_t lo = tid * per, hi = min(lo + per, n);
+  uint32_t local = 0;
+  for (uint32_t i = lo; i < hi; ++i) local += data[i];
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kMoeWarps ? warp_tot[lane] : 0;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= (uint32_t)o) wi += y;
+    }
+    if (lane < kMoeWarps) warp_tot[lane] = wi - w;
+    if (lane == kMoeWarps - 1 && total_out) *total_out = wi;
+  }
+  __syncthreads();
+  uint32_t run = warp_tot[warp] + incl - local;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const uint32_t d = data[i];
+    data[i] = run;
+    run += d;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ dispatch
+template <int KMAX>
+__global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_kernel(MoeLaunch L) {
+  const MoeRankArgs& R = L.r[blockIdx.y];
+  const GinDevCommView* v = R.view;
+  gin::Gin gin(v, 0);
+  const uint32_t n = v->world, rank = v->rank;
+  const uint32_t E = L.E, K = L.K, T = L.T, H = L.H, e_local = L.e_local;
+  const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t dmsg = 2ull * H + 16;
+  const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
+
+  __shared__ uint32_t hist_all[kMaxExperts], run[kMaxExperts], prefix_e[kMaxExperts];
+  __shared__ uint32_t warp_tot[kMoeWarps];
+  __shared__ int is_last;
+  extern __shared__ uint32_t slots[];  // [(t1-t0)*K]
+
+  for (uint32_t e = tid; e < E; e += kMoeThreads) {
+    hist_all[e] = 0;
+    run[e] = 0;
+  }
+  __syncthreads();
+  // Phase A: per-expert totals and the prefix of tokens before this CTA.
+  const uint32_t TK = T * K, pre_end = t0 * K;
+  for (uint32_t j = tid; j < TK; j += kMoeThreads) {
+    const uint32_t e = (uint32_t)R.idx[j];
+    atomicAdd(&hist_all[e], 1u);
+    if (j < pre_end) atomicAdd(&run[e], 1u);
+  }
+  __syncthreads();
+  // Destination base offsets for the compact layout: exclusive prefix of this
+  // source's counts within each destination's expert group.
+  if (L.layout == 1) {
+    for (uint32_t d = tid; d < n; d += kMoeThreads) {
+      uint32_t acc = 0;
+      for (uint32_t e = d * e_local; e < (d + 1) * e_local; ++e) {
+        prefix_e[e] = acc;
+        acc += hist_all[e];
+      }
+    }
+  }
+  // Slots of this CTA's tokens, in (t, k) order (harness_moe.cpp:143-150).
+  if (warp == 0) {
+    for (uint32_t t = t0; t < t1; ++t) {
+      if (lane < K) {
+        const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
+        const uint32_t s = run[e];
+        run[e] = s + 1;  // experts of one token are distinct
+        slots[(t - t0) * K + lane] = s;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  // Phase B: (token, part) work items, one warp each.
+  const uint32_t parts = L.parts;
+  const uint32_t payload = 2u * H;
+  const bool vec_ok = (payload % 16u) == 0;
+  const uint32_t nvec = payload / 16u;
+  const uint32_t vec_per_part = (nvec + parts - 1) / parts;
+  char* const* bases = v->win[L.win_dispatch].base;
+  const uint32_t items = (t1 - t0) * parts;
+  for (uint32_t it = warp; it < items; it += kMoeWarps) {
+    const uint32_t t = t0 + it / parts, p = it % parts;
+    // lane k < K: destination of message (t, k)
+    char* my_dst = nullptr;
+    if (lane < K) {
+      const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
+      const uint32_t dst = e / e_local, e_loc = e % e_local;
+      const uint32_t slot = slots[(t - t0) * K + lane];
+      const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
+                                         : ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
+      my_dst = bases[dst] + off;
+    }
+    char* dptr[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) dptr[k] = (char*)__shfl_sync(0xffffffffu, (uintptr_t)my_dst, k < 32 ? k : 0);
+    const char* src = reinterpret_cast<const char*>(R.x) + (uint64_t)t * payload;
+    if (vec_ok) {
+      const uint32_t vlo = p * vec_per_part, vhi = min(vlo + vec_per_part, nvec);
+      uint32_t i = vlo + lane;
+      for (; i + 96 < vhi; i += 128) {
+        const uint4 a = gin::ld_nc_v4(src + 16ull * i), bb = gin::ld_nc_v4(src + 16ull * (i + 32));
+        const uint4 c = gin::ld_nc_v4(src + 16ull * (i + 64)), d = gin::ld_nc_v4(src + 16ull * (i + 96));
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+          if (k < (int)K) {
+            gin::st_v4(dptr[k] + 16ull * i, a);
+            gin::st_v4(dptr[k] + 16ull * (i + 32), bb);
+            gin::st_v4(dptr[k] + 16ull * (i + 64), c);
+            gin::st_v4(dptr[k] + 16ull * (i + 96), d);
+          }
+        }
+      }
+      for (; i < vhi; i += 32) {
+        const uint4 a = gin::ld_nc_v4(src + 16ull * i);
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < (int)K) gin::st_v4(dptr[k] + 16ull * i, a);
+      }
+    } else if (p == 0) {
+      for (uint32_t j = lane; j < payload; j += 32) {
+        const char byte = src[j];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < (int)K) dptr[k][j] = byte;
+      }
+    }
+    if (p == 0 && lane < K) {  // meta {src, token, k, tag = k+1}
+      char* m = my_dst + payload;
+      if ((((uintptr_t)m) & 15) == 0) {
+        gin::st_v4(m, make_uint4(rank, t, lane, lane + 1));
+      } else {
+        const uint32_t w[4] = {rank, t, lane, lane + 1};
+        for (int q = 0; q < 16; ++q) m[q] = (char)(w[q >> 2] >> (8 * (q & 3)));
+      }
+    }
+  }
+
+  // Phase C: the last CTA to finish releases every expert.
+  __syncthreads();
+  if (tid == 0) {
+    gin::fence_acq_rel_sys();
+    const unsigned prev = atomicAdd(R.ws + 0, 1u);
+    is_last = (prev + 1 == (unsigned)(R.iteration * G));
+    if (is_last) gin::fence_acq_rel_sys();
+  }
+  __syncthreads();
+  if (is_last) {
+    uint32_t* const* cbase = reinterpret_cast<uint32_t* const*>(v->win[L.win_counts].base);
+    for (uint32_t e = tid; e < E; e += kMoeThreads) {
+      const uint32_t dst = e / e_local, e_loc = e % e_local;
+      gin::st_relaxed_sys32(cbase[dst] + (uint64_t)e_loc * n + rank, hist_all[e]);
+      gin.release_signal_raw(dst, e_loc, (1ull << 32) + hist_all[e]);
+    }
+  }
+  // Phase D: return once every local expert has been released by every source.
+  if (tid == 0) {
+    const uint64_t want = R.iteration * ((uint64_t)n << 32);
+    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) {
+      const uint64_t t_start = gin::globaltimer();
+      uint32_t spins = 0;
+      while (gin.read_signal(e_loc) < want) {
+        if (++spins > 32) __nanosleep(64);
+        if ((spins & 1023) == 0 && gin::globaltimer() - t_start > v->timeout_ns) {
+          gin::raise_error(v, GIN_DEVERR_TIMEOUT);
+          break;
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ combine
+__global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L) {
+  const MoeRankArgs& R = L.r[blockIdx.y];
+  const GinDevCommView* v = R.view;
+  gin::Gin gin(v, 0);
+  const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
+  const uint32_t E = L.E, K = L.K, T = L.T, H = L.H, e_local = L.e_local;
+  const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t dmsg = 2ull * H + 16, cmsg = 2ull * H;
+  const uint32_t payload = 2u * H;
+
+  __shared__ uint32_t cnt[kMaxExperts], pair_start[kMaxExperts + 1], src_prefix[kMaxExperts];
+  __shared__ uint32_t warp_tot[kMoeWarps];
+  __shared__ uint32_t total_msgs;
+  __shared__ int is_last;
+
+  // Received counts: pair (e_loc, src) in e_loc-major order (reference scan
+  // order, harness_moe.cpp:174-179).
+  const uint32_t P = e_local * n;
+  const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
+  for (uint32_t i = tid; i < P; i += kMoeThreads) {
+    const uint32_t c = gin::ld_acquire_sys32(counts + i);
+    cnt[i] = c;
+    pair_start[i] = c;
+  }
+  __syncthreads();
+  if (L.layout == 1) {
+    for (uint32_t s = tid; s < n; s += kMoeThreads) {
+      uint32_t acc = 0;
+      for (uint32_t e = 0; e < e_local; ++e) {
+        src_prefix[e * n + s] = acc;
+        acc += cnt[e * n + s];
+      }
+    }
+  }
+  block_exclusive_scan(pair_start, P, warp_tot, &total_msgs);
+  if (tid == 0) pair_start[P] = total_msgs;
+  __syncthreads();
+
+  // Expert side: (message, part) items over every warp of this rank.
+  const uint32_t parts = L.parts;
+  const bool vec_ok = (payload % 16u) == 0;
+  const uint32_t nvec = payload / 16u;
+  const uint32_t vec_per_part = (nvec + parts - 1) / parts;
+  const uint64_t items = (uint64_t)total_msgs * parts;
+  const char* recv = v->win[L.win_dispatch].base[rank];
+  char* const* cbases = v->win[L.win_combine].base;
+  for (uint64_t it = (uint64_t)b * kMoeWarps + warp; it < items; it += (uint64_t)G * kMoeWarps) {
+    const uint32_t m = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
+    // pair containing m: last i with pair_start[i] <= m
+    uint32_t lo = 0, hi = P;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (pair_start[mid] <= m) lo = mid; else hi = mid;
+    }
+    const uint32_t e_loc = lo / n, src = lo % n, slot = m - pair_start[lo];
+    const uint64_t moff = L.layout == 0 ? (((uint64_t)e_loc * n + src) * T + slot) * dmsg
+                                        : ((uint64_t)src * T * K + src_prefix[lo] + slot) * dmsg;
+    const char* msg = recv + moff;
+    const unsigned char* meta = reinterpret_cast<const unsigned char*>(msg + payload);
+    uint32_t token, k;
+    if ((((uintptr_t)meta) & 3) == 0) {
+      token = reinterpret_cast<const uint32_t*>(meta)[1];
+      k = reinterpret_cast<const uint32_t*>(meta)[2];
+    } else {
+      token = meta[4] | (meta[5] << 8) | (meta[6] << 16) | ((uint32_t)meta[7] << 24);
+      k = meta[8] | (meta[9] << 8) | (meta[10] << 16) | ((uint32_t)meta[11] << 24);
+    }
+    const uint32_t e = rank * e_local + e_loc;
+    char* dst = cbases[src] + ((uint64_t)token * K + k) * cmsg;
+    if (vec_ok) {
+      const uint32_t vlo = p * vec_per_part, vhi = min(vlo + vec_per_part, nvec);
+      uint32_t i = vlo + lane;
+      for (; i + 96 < vhi; i += 128) {
+        uint4 a = gin::ld_nc_v4(msg + 16ull * i), bb = gin::ld_nc_v4(msg + 16ull * (i + 32));
+        uint4 c = gin::ld_nc_v4(msg + 16ull * (i + 64)), d = gin::ld_nc_v4(msg + 16ull * (i + 96));
+        gin::st_v4(dst + 16ull * i, transform_vec(a, L.mode, e));
+        gin::st_v4(dst + 16ull * (i + 32), transform_vec(bb, L.mode, e));
+        gin::st_v4(dst + 16ull * (i + 64), transform_vec(c, L.mode, e));
+        gin::st_v4(dst + 16ull * (i + 96), transform_vec(d, L.mode, e));
+      }
+      for (; i < vhi; i += 32) gin::st_v4(dst + 16ull * i, transform_vec(gin::ld_nc_v4(msg + 16ull * i), L.mode, e));
+    } else if (p == 0) {
+      const uint16_t* s16 = reinterpret_cast<const uint16_t*>(msg);
+      uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+      for (uint32_t j = lane; j < H; j += 32) {
+        const uint32_t two = transform_vec(make_uint4(s16[j], 0, 0, 0), L.mode, e).x;
+        d16[j] = (uint16_t)(two & 0xFFFFu);
+      }
+    }
+  }
+
+  // Release: the last CTA signals each (source, context) with its count.
+  __syncthreads();
+  if (tid == 0) {
+    gin::fence_acq_rel_sys();
+    const unsigned prev = atomicAdd(R.ws + 1, 1u);
+    is_last = (prev + 1 == (unsigned)(R.iteration * G));
+    if (is_last) gin::fence_acq_rel_sys();
+  }
+  __syncthreads();
+  if (is_last) {
+    for (uint32_t sc = tid; sc < n * n_ctx; sc += kMoeThreads) {
+      const uint32_t src = sc / n_ctx, ctx = sc % n_ctx;
+      uint32_t c = 0;
+      for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
+        if ((rank * e_local + e_loc) % n_ctx == ctx) c += cnt[e_loc * n + src];
+      if (c) gin.release_signal_raw(src, e_local, c);
+    }
+  }
+
+  // Source side: acquire all T*K outputs, then reduce with the top-k weights.
+  if (tid == 0) {
+    const uint64_t want = R.iteration * (uint64_t)T * K;
+    const uint64_t t_start = gin::globaltimer();
+    uint32_t spins = 0;
+    while (gin.read_signal(e_local) < want) {
+      if (++spins > 32) __nanosleep(64);
+      if ((spins & 1023) == 0 && gin::globaltimer() - t_start > v->timeout_ns) {
+        gin::raise_error(v, GIN_DEVERR_TIMEOUT);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const char* crecv = v->win[L.win_combine].base[rank];
+  const uint64_t ritems = (uint64_t)T * parts;
+  for (uint64_t it = (uint64_t)b * kMoeWarps + warp; it < ritems; it += (uint64_t)G * kMoeWarps) {
+    const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
+    char* o = reinterpret_cast<char*>(R.out) + (uint64_t)t * payload;
+    if (vec_ok) {
+      const uint32_t vlo = p * vec_per_part, vhi = min(vlo + vec_per_part, nvec);
+      for (uint32_t i = vlo + lane; i < vhi; i += 32) {
+        if (L.mode == 0) {
+          uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          const uint16_t* w = reinterpret_cast<const uint16_t*>(R.weights) + (uint64_t)t * K;
+          for (uint32_t k = 0; k < K; ++k) {
+            const uint32_t wk = w[k];
+            const uint4 y = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+            const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc[2 * q] += wk * (ys[q] & 0xFFFFu);
+              acc[2 * q + 1] += wk * (ys[q] >> 16);
+            }
+          }
+          uint4 r;
+          r.x = (acc[0] & 0xFFFFu) | (acc[1] << 16);
+          r.y = (acc[2] & 0xFFFFu) | (acc[3] << 16);
+          r.z = (acc[4] & 0xFFFFu) | (acc[5] << 16);
+          r.w = (acc[6] & 0xFFFFu) | (acc[7] << 16);
+          gin::st_v4(o + 16ull * i, r);
+        } else {
+          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          const float* w = reinterpret_cast<const float*>(R.weights) + (uint64_t)t * K;
+          for (uint32_t k = 0; k < K; ++k) {
+            const float wk = w[k];
+            const uint4 y = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+            const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc[2 * q] = __fadd_rn(acc[2 * q], __fmul_rn(wk, __uint_as_float(ys[q] << 16)));
+              acc[2 * q + 1] = __fadd_rn(acc[2 * q + 1], __fmul_rn(wk, __uint_as_float(ys[q] & 0xFFFF0000u)));
+            }
+          }
+          uint32_t pk[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            pk[q] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc[2 * q])) |
+                    ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc[2 * q + 1])) << 16);
+          }
+          gin::st_v4(o + 16ull * i, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+        }
+      }
+    } else if (p == 0) {
+      uint16_t* o16 = reinterpret_cast<uint16_t*>(o);
+      for (uint32_t j = lane; j < H; j += 32) {
+        if (L.mode == 0) {
+          uint32_t acc = 0;
+          const uint16_t* w = reinterpret_cast<const uint16_t*>(R.weights) + (uint64_t)t * K;
+          for (uint32_t k = 0; k < K; ++k)
+            acc += (uint32_t)w[k] * reinterpret_cast<const uint16_t*>(crecv + ((uint64_t)t * K + k) * cmsg)[j];
+          o16[j] = (uint16_t)acc;
+        } else {
+          float acc = 0.f;
+          const float* w = reinterpret_cast<const float*>(R.weights) + (uint64_t)t * K;
+          for (uint32_t k = 0; k < K; ++k) {
+            const uint16_t y = reinterpret_cast<const uint16_t*>(crecv + ((uint64_t)t * K + k) * cmsg)[j];
+            acc = __fadd_rn(acc, __fmul_rn(w[k], __uint_as_float((uint32_t)y << 16)));
+          }
+          o16[j] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ synthetic inputs
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// route_token (harness_moe.cpp:25-30): std::mt19937_64 seeded with
+// mix64(seed ^ mix64(src*100003 + token)), draws % E until K distinct, sorted.
+__global__ void moe_route_kernel(int32_t* idx, uint64_t seed, uint32_t src, uint32_t T, uint32_t E, uint32_t K) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  uint64_t mt[312];
+  mt[0] = mix64(seed ^ mix64((uint64_t)src * 100003ull + t));
+  for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+  int pos = 312;
+  int32_t picked[32];
+  uint32_t got = 0;
+  while (got < K) {
+    if (pos >= 312) {
+      for (int i = 0; i < 312; ++i) {
+        const uint64_t y = (mt[i] & 0xFFFFFFFF80000000ull) | (mt[(i + 1) % 312] & 0x7FFFFFFFull);
+        uint64_t nv = mt[(i + 156) % 312] ^ (y >> 1);
+        if (y & 1) nv ^= 0xB5026F5AA96619E9ull;
+        mt[i] = nv;
+      }
+      pos = 0;
+    }
+    uint64_t x = mt[pos++];
+    x ^= (x >> 29) & 0x5555555555555555ull;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+    x ^= (x << 37) & 0xFFF7EEE000000000ull;
+    x ^= x >> 43;
+    const int32_t e = (int32_t)(x % E);
+    uint32_t p = 0;
+    while (p < got && picked[p] < e) ++p;
+    if (p < got && picked[p] == e) continue;
+    for (uint32_t j = got; j > p; --j) picked[j] = picked[j - 1];
+    picked[p] = e;
+    ++got;
+  }
+  for (uint32_t k = 0; k < K; ++k) idx[(uint64_t)t * K + k] = picked[k];
+}
+
+// token_element (harness_moe.cpp:32-34) or the bf16 generator.
+__global__ void moe_tokens_kernel(uint16_t* x, uint64_t seed, uint32_t src, uint32_t T, uint32_t H, uint32_t mode) {
+  const uint64_t total = (uint64_t)T * H;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < total; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(j / H), i = (uint32_t)(j % H);
+    if (mode == 0) {
+      x[j] = (uint16_t)(seed + src * 7919u + t * 131u + i * 13u);
+    } else {
+      const uint64_t h = mix64(seed ^ mix64(((uint64_t)src << 40) ^ ((uint64_t)t << 20) ^ i));
+      const uint16_t sign = (uint16_t)((h >> 63) << 15);
+      const uint16_t expo = (uint16_t)(120u + (uint32_t)((h >> 8) % 12u));
+      x[j] = (uint16_t)(sign | (expo << 7) | (uint16_t)(h & 0x7Fu));
+    }
+  }
+}
+
+// combine_weight (harness_moe.cpp:40-42); bf16 mode uses w/8 as fp32.
+__global__ void moe_weights_kernel(void* w, uint32_t src, uint32_t T, uint32_t K, uint32_t mode) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= T * K) return;
+  const uint32_t t = j / K, k = j % K;
+  const uint16_t cw = (uint16_t)(1u + (src + 3u * t + 5u * k) % 7u);
+  if (mode == 0) reinterpret_cast<uint16_t*>(w)[j] = cw;
+  else reinterpret_cast<float*>(w)[j] = (float)cw / 8.0f;
+}
+
+}  // namespace ginsim_b200
+
+// ------------------------------------------------------------------ C ABI
+using namespace ginsim_b200;
+
+struct ginsim_cuda_moe_s {
+  Comm* comm = nullptr;
+  ginsim_cuda_moe_config cfg{};
+  uint32_t e_local = 0, parts = 4, G = 0;
+  uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0;
+  void* buf_dispatch = nullptr;
+  void* buf_counts = nullptr;
+  void* buf_combine = nullptr;
+  unsigned int* ws = nullptr;
+  uint64_t iteration_dispatch = 0, iteration_combine = 0;
+  uint32_t last_ctas = 0;
+};
+
+extern "C" {
+
+int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config* cfg, ginsim_cuda_moe_t* out) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  if (cfg->experts == 0 || cfg->experts % c->world) fail(GINSIM_E_USAGE, "experts must be divisible by ranks");
+  if (cfg->experts > kMaxExperts) fail(GINSIM_E_USAGE, "at most 1024 experts");
+  if (cfg->tokens == 0 || cfg->top_k == 0 || cfg->top_k > cfg->experts || cfg->top_k > 32)
+    fail(GINSIM_E_USAGE, "need 1..min(experts,32) routed experts per token and at least one token");
+  if (cfg->hidden == 0) fail(GINSIM_E_USAGE, "hidden must be positive");
+  if (cfg->mode > 1 || cfg->layout > 1) fail(GINSIM_E_USAGE, "mode/layout must be 0 or 1");
+  const uint32_t e_local = cfg->experts / c->world;
+  if (e_local + 1 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
+    fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag exceed the signal table");
+  auto m = std::make_unique<ginsim_cuda_moe_s>();
+  m->comm = c;
+  m->cfg = *cfg;
+  m->e_local = e_local;
+  m->parts = cfg->hidden >= 1024 ? 4 : 1;
+  const uint64_t dmsg = 2ull * cfg->hidden + 16, cmsg = 2ull * cfg->hidden;
+  const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
+  const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
+  const uint64_t nbytes = (uint64_t)e_local * n * 4;
+  const uint64_t cbytes = T * K * cmsg;
+  if (ginsim_cuda_mem_alloc(comm, dbytes, &m->buf_dispatch)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+  if (ginsim_cuda_mem_alloc(comm, nbytes, &m->buf_counts)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+  if (ginsim_cuda_mem_alloc(comm, cbytes, &m->buf_combine)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+  int rc;
+  if ((rc = ginsim_cuda_window_register(comm, m->buf_dispatch, dbytes, &m->win_dispatch))) fail(rc, ginsim_cuda_last_error());
+  if ((rc = ginsim_cuda_window_register(comm, m->buf_counts, nbytes, &m->win_counts))) fail(rc, ginsim_cuda_last_error());
+  if ((rc = ginsim_cuda_window_register(comm, m->buf_combine, cbytes, &m->win_combine))) fail(rc, ginsim_cuda_last_error());
+  DeviceGuard g(c->device);
+  GIN_CUDA(cudaMalloc(&m->ws, 256));
+  GIN_CUDA(cudaMemset(m->ws, 0, 256));
+  *out = m.release();
+  GIN_API_END
+}
+
+int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
+  GIN_API_BEGIN
+  if (!moe) return GINSIM_OK;
+  {
+    DeviceGuard g(moe->comm->device);
+    cudaDeviceSynchronize();
+    if (moe->ws) cudaFree(moe->ws);
+  }
+  // window memory stays mapped until the comm is destroyed (windows are
+  // never deregistered in the reference either).
+  delete moe;
+  GIN_API_END
+}
+
+int ginsim_cuda_moe_windows(ginsim_cuda_moe_t moe, uint32_t* d, uint32_t* c, uint32_t* cb) {
+  if (d) *d = moe->win_dispatch;
+  if (c) *c = moe->win_counts;
+  if (cb) *cb = moe->win_combine;
+  return GINSIM_OK;
+}
+
+int ginsim_cuda_moe_generate(ginsim_cuda_moe_t moe, uint64_t seed, uint32_t src, void* x, int32_t* idx, void* w,
+                             void* stream) {
+  GIN_API_BEGIN
+  const auto& cfg = moe->cfg;
+  DeviceGuard g(moe->comm->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (idx) {
+    moe_route_kernel<<<(cfg.tokens + 63) / 64, 64, 0, s>>>(idx, seed, src, cfg.tokens, cfg.experts, cfg.top_k);
+    GIN_CUDA(cudaGetLastError());
+  }
+  if (x) {
+    moe_tokens_kernel<<<1184, 256, 0, s>>>(static_cast<uint16_t*>(x), seed, src, cfg.tokens, cfg.hidden, cfg.mode);
+    GIN_CUDA(cudaGetLastError());
+  }
+  if (w) {
+    moe_weights_kernel<<<(cfg.tokens * cfg.top_k + 255) / 256, 256, 0, s>>>(w, src, cfg.tokens, cfg.top_k, cfg.mode);
+    GIN_CUDA(cudaGetLastError());
+  }
+  GIN_API_END
+}
+
+static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
+  MoeLaunch L{};
+  const auto& cfg = moes[0]->cfg;
+  L.E = cfg.experts;
+  L.K = cfg.top_k;
+  L.T = cfg.tokens;
+  L.H = cfg.hidden;
+  L.mode = cfg.mode;
+  L.layout = cfg.layout;
+  L.e_local = moes[0]->e_local;
+  L.parts = moes[0]->parts;
+  L.win_dispatch = moes[0]->win_dispatch;
+  L.win_counts = moes[0]->win_counts;
+  L.win_combine = moes[0]->win_combine;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
+      fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
+    L.r[i].view = moes[i]->comm->dev_view;
+    L.r[i].ws = moes[i]->ws;
+  }
+  return L;
+}
+
+// Grid and work split, fixed at the first launch of a handle (the arrival
+// counters count CTAs per iteration, so G never changes afterwards).  Every
+// CTA must be co-resident: CTAs spin on signals other CTAs release.
+static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
+  ginsim_cuda_moe_t m = moes[0];
+  if (m->G) return;
+  const void* kd = m->cfg.top_k <= 8 ? (const void*)moe_dispatch_kernel<8> : (const void*)moe_dispatch_kernel<32>;
+  GIN_CUDA(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  const size_t guess = (size_t)((m->cfg.tokens + 147) / 148 + 1) * m->cfg.top_k * 4;
+  const int cap_d = max_coresident_ctas(kd, kMoeThreads, guess, m->comm->device);
+  const int cap_c = max_coresident_ctas((const void*)moe_combine_kernel, kMoeThreads, 0, m->comm->device);
+  int cap = std::min(cap_d, cap_c) / (int)n;
+  uint32_t G = m->cfg.ctas ? std::min<uint32_t>(m->cfg.ctas, (uint32_t)cap) : (uint32_t)cap;
+  if (G > m->cfg.tokens) G = m->cfg.tokens;
+  if (G < 1) fail(GINSIM_E_USAGE, "kernel does not fit on the device");
+  const uint32_t nvec = (2u * m->cfg.hidden) % 16u == 0 ? 2u * m->cfg.hidden / 16u : 0u;
+  uint32_t parts = 1;
+  if (nvec >= 32) {
+    const uint32_t want = (2u * G * kMoeWarps + m->cfg.tokens - 1) / m->cfg.tokens;
+    parts = std::max(1u, std::min(want, nvec / 32u));
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    moes[i]->G = G;
+    moes[i]->parts = parts;
+  }
+}
+
+static void launch_coop(const void* kernel, uint32_t G, uint32_t n, size_t smem, MoeLaunch& L, cudaStream_t s) {
+  void* args[] = {&L};
+  GIN_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(G, n), dim3(kMoeThreads), args, smem, s));
+}
+
+int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* x,
+                             const int32_t* const* idx, void* stream) {
+  GIN_API_BEGIN
+  if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "launch needs 1..8 ranks");
+  for (uint32_t i = 1; i < n; ++i)
+    if (moes[i]->comm->device != moes[0]->comm->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
+  MoeLaunch L = make_launch(moes, n);
+  DeviceGuard g(moes[0]->comm->device);
+  const void* kernel = L.K <= 8 ? (const void*)moe_dispatch_kernel<8> : (const void*)moe_dispatch_kernel<32>;
+  plan(moes, n);
+  L.parts = moes[0]->parts;
+  const uint32_t G = moes[0]->G;
+  const size_t smem = (size_t)((L.T + G - 1) / G + 1) * L.K * 4;
+  if (smem > 160 * 1024) fail(GINSIM_E_USAGE, "too many tokens per CTA for the slot table");
+  for (uint32_t i = 0; i < n; ++i) {
+    moes[i]->iteration_dispatch += 1;
+    L.r[i].x = static_cast<const uint16_t*>(x[i]);
+    L.r[i].idx = idx[i];
+    L.r[i].iteration = moes[i]->iteration_dispatch;
+  }
+  launch_coop(kernel, G, n, smem, L, (cudaStream_t)stream);
+  moes[0]->last_ctas = G * n;
+  GIN_API_END
+}
+
+int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* weights, void* const* out,
+                            void* stream) {
+  GIN_API_BEGIN
+  if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "launch needs 1..8 ranks");
+  for (uint32_t i = 1; i < n; ++i)
+    if (moes[i]->comm->device != moes[0]->comm->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
+  MoeLaunch L = make_launch(moes, n);
+  DeviceGuard g(moes[0]->comm->device);
+  const void* kernel = (const void*)moe_combine_kernel;
+  plan(moes, n);
+  L.parts = moes[0]->parts;
+  const uint32_t G = moes[0]->G;
+  for (uint32_t i = 0; i < n; ++i) {
+    moes[i]->iteration_combine += 1;
+    if (moes[i]->iteration_combine != moes[i]->iteration_dispatch)
+      fail(GINSIM_E_USAGE, "combine must follow exactly one dispatch");
+    L.r[i].weights = weights[i];
+    L.r[i].out = static_cast<uint16_t*>(out[i]);
+    L.r[i].iteration = moes[i]->iteration_combine;
+  }
+  launch_coop(kernel, G, n, 0, L, (cudaStream_t)stream);
+  moes[0]->last_ctas = G * n;
+  GIN_API_END
+}
+
+int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t* threads) {
+  if (ctas) *ctas = moe->last_ctas;
+  if (threads) *threads = kMoeThreads;
+  return GINSIM_OK;
+}
+
+}  // extern "C"
+
+extern "C" int ginsim_cuda_moe_create_all(const ginsim_cuda_comm_t* comms, uint32_t n,
+                                          const ginsim_cuda_moe_config* cfg, ginsim_cuda_moe_t* out) {
+  GIN_API_BEGIN
+  std::vector<int> rcs(n, 0);
+  std::vector<std::string> msgs(n);
+  std::vector<std::thread> ts;
+  for (uint32_t r = 0; r < n; ++r) {
+    ts.emplace_back([&, r] {
+      rcs[r] = ginsim_cuda_moe_create(comms[r], cfg, &out[r]);
+      if (rcs[r]) msgs[r] = ginsim_cuda_last_error();
+    });
+  }
+  for (auto& t : ts) t.join();
+  for (uint32_t r = 0; r < n; ++r)
+    if (rcs[r]) fail(rcs[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+  GIN_API_END
+}

@@ -1,0 +1,412 @@
+// kernels_p2p.cu — point-to-point workloads of the reference harness, run as
+// device programs over the GIN device API:
+//   ping-pong   proj/core/src/harness_bench.cpp:47-90  (K14)
+//   all-to-all  SURVEY.md §8(d)-2 (one-sided put+signal on windows, K15)
+//   ring        proj/core/src/harness_ring.cpp:18-57   (Listing 2 of the paper)
+//   moe-ht      proj/core/src/harness_moe.cpp:283-382  (circular-buffer flow control, K13)
+// Every launcher takes the comms this process drives; several comms on one
+// device are emulated ranks in ONE cooperative launch (blockIdx.y = rank lane).
+#include <algorithm>
+#include <map>
+#include <cstring>
+#include <vector>
+
+#include "gin_device.cuh"
+#include "runtime_internal.h"
+
+namespace ginsim_b200 {
+
+struct LaneViews {
+  const GinDevCommView* v[GIN_MAX_RANKS];
+  unsigned int* ws[GIN_MAX_RANKS];
+  uint64_t base[GIN_MAX_RANKS];   // per-lane signal baseline / iteration
+};
+
+// ------------------------------------------------------------------ ping-pong
+struct PingArgs {
+  LaneViews lv;
+  uint32_t peer0, peer1, send_win, recv_win, sig, iters, warmup, ctas;
+  uint64_t bytes;
+  uint64_t* rtt;  // device, iters entries (written by peer0's lane)
+};
+
+// One put+SignalInc per direction per iteration.  With ctas > 1 the payload
+// is split across CTAs and the last CTA of each round issues the release
+// (arrival counter), so the signal still covers every CTA's stores.
+__global__ void pingpong_kernel(PingArgs A) {
+  const GinDevCommView* v = A.lv.v[blockIdx.y];
+  unsigned int* ws = A.lv.ws[blockIdx.y];
+  const uint64_t base = A.lv.base[blockIdx.y];
+  gin::Gin gin(v, 0);
+  gin::CoopCta cta;
+  const uint32_t me = v->rank;
+  if (me != A.peer0 && me != A.peer1) return;
+  const bool initiator = me == A.peer0;
+  const uint32_t other = initiator ? A.peer1 : A.peer0;
+  const uint32_t total = A.warmup + A.iters;
+  const uint64_t chunk = ((A.bytes + A.ctas - 1) / A.ctas + 15) & ~15ull;
+  const uint64_t lo = std::min<uint64_t>(A.bytes, chunk * blockIdx.x);
+  const uint64_t hi = std::min<uint64_t>(A.bytes, lo + chunk);
+  __shared__ int last;
+  auto send = [&](uint32_t round) {
+    if (hi > lo) {
+      gin::coop_copy(cta, gin.window_ptr(A.recv_win, other, lo), gin.window_ptr(A.send_win, me, lo), hi - lo);
+    }
+    if (A.ctas == 1) {
+      cta.sync();
+      if (threadIdx.x == 0) gin.release_signal_raw(other, A.sig, 1);
+      return;
+    }
+    cta.sync();
+    if (threadIdx.x == 0) {
+      gin::fence_acq_rel_sys();
+      const unsigned prev = atomicAdd(ws, 1u);
+      last = prev + 1 == round * A.ctas;
+      if (last) {
+        gin::fence_acq_rel_sys();
+        gin.release_signal_raw(other, A.sig, 1);
+      }
+    }
+  };
+  auto wait = [&](uint64_t want) {
+    if (threadIdx.x == 0) gin.wait_ge_signal(A.sig, want);
+    cta.sync();
+  };
+  // ws counts rounds across calls: continue from the host-provided offset.
+  const uint32_t round0 = (uint32_t)(base >> 32);
+  const uint64_t sig0 = base & 0xFFFFFFFFull;
+  for (uint32_t i = 1; i <= total; ++i) {
+    if (initiator) {
+      const uint64_t t0 = gin::globaltimer();
+      send(round0 + i);
+      wait(sig0 + i);
+      const uint64_t t1 = gin::globaltimer();
+      if (blockIdx.x == 0 && threadIdx.x == 0 && i > A.warmup) A.rtt[i - 1 - A.warmup] = t1 - t0;
+    } else {
+      wait(sig0 + i);
+      send(round0 + i);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ all-to-all
+struct A2aArgs {
+  LaneViews lv;
+  uint32_t send_win, recv_win, sig, ctas_per_peer;
+  uint64_t bytes;     // per peer
+  uint64_t expected;  // wait target for the local cell
+};
+
+// CTA b serves peer index b / ctas_per_peer (skipping self) and slice
+// b % ctas_per_peer of its M bytes; the last CTA of each peer releases it.
+__global__ void alltoall_kernel(A2aArgs A) {
+  const GinDevCommView* v = A.lv.v[blockIdx.y];
+  unsigned int* ws = A.lv.ws[blockIdx.y];
+  const uint64_t iter = A.lv.base[blockIdx.y];
+  gin::Gin gin(v, 0);
+  gin::CoopCta cta;
+  const uint32_t n = v->world, me = v->rank;
+  const uint32_t pi = blockIdx.x / A.ctas_per_peer, slice = blockIdx.x % A.ctas_per_peer;
+  const uint32_t peer = (me + 1 + pi) % n;  // stagger so every link is busy from the start
+  const uint64_t chunk = ((A.bytes + A.ctas_per_peer - 1) / A.ctas_per_peer + 15) & ~15ull;
+  const uint64_t lo = std::min<uint64_t>(A.bytes, chunk * slice), hi = std::min<uint64_t>(A.bytes, lo + chunk);
+  __shared__ int last;
+  if (hi > lo) {
+    gin::coop_copy(cta, gin.window_ptr(A.recv_win, peer, (uint64_t)me * A.bytes + lo),
+                   gin.window_ptr(A.send_win, me, (uint64_t)peer * A.bytes + lo), hi - lo);
+  }
+  cta.sync();
+  if (threadIdx.x == 0) {
+    gin::fence_acq_rel_sys();
+    const unsigned prev = atomicAdd(ws + 16 + peer, 1u);
+    last = prev + 1 == (unsigned)(iter * A.ctas_per_peer);
+    if (last) {
+      gin::fence_acq_rel_sys();
+      gin.release_signal_raw(peer, A.sig, 1);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) gin.wait_ge_signal(A.sig, A.expected);
+}
+
+// ------------------------------------------------------------------ ring
+struct RingArgs {
+  LaneViews lv;
+  uint32_t send_win, recv_win, rounds;
+  uint64_t bytes;
+};
+
+__device__ __forceinline__ uint8_t ring_byte(uint32_t sender, uint32_t round, uint64_t i) {
+  return (uint8_t)(sender * 131u + round * 31u + i * 7u + 1u);
+}
+
+__global__ void ring_kernel(RingArgs A) {
+  const GinDevCommView* v = A.lv.v[blockIdx.y];
+  gin::Gin gin(v, 0);
+  gin::CoopCta cta;
+  const gin::Team world = gin::WorldTeam(v->world);
+  const uint32_t n = v->world, r = v->rank, peer = (r + 1) % n, pred = (r + n - 1) % n;
+  const uint64_t S = A.bytes;
+  gin::BarrierSession barrier(gin, world, 0, A.lv.base[blockIdx.y]);
+  __shared__ int bad;
+  for (uint32_t round = 0; round < A.rounds; ++round) {
+    char* send = gin.window_ptr(A.send_win, r, (uint64_t)peer * S);
+    for (uint64_t i = threadIdx.x; i < S; i += blockDim.x) send[i] = (char)ring_byte(r, round, i);
+    cta.sync();
+    gin.put(cta, world, peer, A.recv_win, (uint64_t)r * S, A.send_win, (uint64_t)peer * S, S,
+            gin::SignalAction(0, gin::SignalInc()));
+    gin.wait_signal(cta, 0, 1);
+    if (threadIdx.x == 0) bad = 0;
+    cta.sync();
+    const char* recv = gin.window_ptr(A.recv_win, r, (uint64_t)pred * S);
+    for (uint64_t i = threadIdx.x; i < S; i += blockDim.x)
+      if ((uint8_t)recv[i] != ring_byte(pred, round, i)) bad = 1;
+    cta.sync();
+    if (bad) {
+      if (threadIdx.x == 0) gin::raise_error(v, GIN_DEVERR_VERIFY);
+      return;
+    }
+    if (threadIdx.x == 0) gin.reset_signal(0);
+    gin.flush(cta);     // sources reusable before the next round overwrites them
+    barrier.sync(cta);  // no peer may signal round+1 before everyone reset
+  }
+}
+
+// ------------------------------------------------------------------ moe-ht flow control
+struct HtArgs {
+  const GinDevCommView* pool[GIN_MAX_RANKS][8];  // [rank lane][comm index]
+  uint32_t channels, slots, messages, n_pool;
+  uint64_t seed;
+};
+
+__device__ __forceinline__ uint8_t ht_byte(uint32_t channel, uint32_t msg, uint64_t i, uint64_t seed) {
+  return (uint8_t)(seed + channel * 37u + msg * 11u + i);
+}
+
+// One CTA per (rank lane, channel).  Producer step then consumer step per
+// message, exactly as moe_ht_rank_program; windows 0 = recv, 1 = stage.
+__global__ void moe_ht_kernel(HtArgs A) {
+  const uint32_t channel = blockIdx.x;
+  const uint32_t comm_idx = channel / 4;  // pool_select with n_ctx from the view
+  const GinDevCommView* v0 = A.pool[blockIdx.y][0];
+  const uint32_t n_ctx = v0->n_ctx;
+  const uint32_t ci = channel / n_ctx, ctx = channel % n_ctx;
+  (void)comm_idx;
+  const GinDevCommView* v = A.pool[blockIdx.y][ci];
+  gin::Gin gin(v, ctx);
+  gin::CoopCta cta;
+  const gin::Team world = gin::WorldTeam(v->world);
+  const uint32_t n = v->world, r = v->rank, succ = (r + 1) % n, pred = (r + n - 1) % n;
+  const uint32_t B = A.slots, M = A.messages;
+  const uint32_t tail_sig = 2 * ctx, head_sig = 2 * ctx + 1, stage_ctr = ctx;
+  const uint64_t lane = (uint64_t)ctx * B * 256;
+  __shared__ int bad;
+  for (uint32_t m = 0; m < M; ++m) {
+    // -- producer step
+    if (m >= B) {
+      gin.wait_signal(cta, head_sig, m + 1 - B);   // remote slot consumed
+      gin.wait_counter(cta, stage_ctr, m + 1 - B); // stage slot locally complete
+    }
+    if (threadIdx.x == 0 && gin.read_signal(head_sig) > m) gin::raise_error(v, GIN_DEVERR_FLOW_CONTROL);
+    char* slot = gin.window_ptr(1, r, lane + (uint64_t)(m % B) * 256);
+    const uint64_t generation = (uint64_t)m + 1;
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
+      slot[i] = i < 8 ? (char)(generation >> (8 * i)) : (char)ht_byte(channel, m, i - 8, A.seed);
+    cta.sync();
+    gin.put(cta, world, succ, 0, lane + (uint64_t)(m % B) * 256, 1, lane + (uint64_t)(m % B) * 256, 256,
+            gin::CounterAction(stage_ctr));
+    gin.signal(cta, world, succ, tail_sig, gin::SignalAdd(1));
+    // -- consumer step
+    gin.wait_signal(cta, tail_sig, m + 1);
+    if (threadIdx.x == 0) bad = 0;
+    cta.sync();
+    const char* got = gin.window_ptr(0, r, lane + (uint64_t)(m % B) * 256);
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+      const uint8_t want = i < 8 ? (uint8_t)(generation >> (8 * i)) : ht_byte(channel, m, i - 8, A.seed);
+      if ((uint8_t)got[i] != want) bad = i < 8 ? 2 : 1;
+    }
+    cta.sync();
+    if (bad) {
+      if (threadIdx.x == 0) gin::raise_error(v, bad == 2 ? GIN_DEVERR_FLOW_CONTROL : GIN_DEVERR_VERIFY);
+      return;
+    }
+    gin.signal(cta, world, pred, head_sig, gin::SignalAdd(1));
+  }
+  gin.wait_signal(cta, head_sig, M);
+  gin.flush(cta);
+}
+
+// ------------------------------------------------------------------ host helpers
+static LaneViews lanes(const ginsim_cuda_comm_t* comms, uint32_t n) {
+  LaneViews lv{};
+  for (uint32_t i = 0; i < n; ++i) {
+    lv.v[i] = comms[i]->impl.dev_view;
+    lv.ws[i] = comms[i]->impl.host_view.workspace;
+  }
+  return lv;
+}
+
+static void coop_launch(const void* kernel, dim3 grid, dim3 block, void* arg, cudaStream_t s) {
+  void* args[] = {arg};
+  GIN_CUDA(cudaLaunchCooperativeKernel(kernel, grid, block, args, 0, s));
+}
+
+static void sync_and_check(const ginsim_cuda_comm_t* comms, uint32_t n, cudaStream_t s) {
+  GIN_CUDA(cudaStreamSynchronize(s));
+  for (uint32_t i = 0; i < n; ++i) check_device_error(&comms[i]->impl);
+}
+
+// Host-side per-comm launch/round counters: the device arrival counters in
+// the comm workspace are monotone, so each launch passes where they stand.
+static uint64_t bump_host_counter(Comm* c, uint32_t slot, uint64_t by) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->op_counter[slot] += by;
+  return c->op_counter[slot];
+}
+
+}  // namespace ginsim_b200
+
+using namespace ginsim_b200;
+
+extern "C" {
+
+int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1,
+                         uint32_t send_win, uint32_t recv_win, uint64_t bytes, uint32_t iters, uint32_t warmup,
+                         uint32_t signal_id, uint32_t threads, uint64_t* rtt_ns_out, void* stream) {
+  GIN_API_BEGIN
+  check_same_device(comms, n);
+  Comm* c0 = &comms[0]->impl;
+  if (peer0 == peer1 || peer0 >= c0->world || peer1 >= c0->world) fail(GINSIM_E_INVALID_PEER, "ping-pong needs two distinct ranks");
+  if (signal_id >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range");
+  if (iters == 0) fail(GINSIM_E_USAGE, "bench iterations must be positive");
+  DeviceGuard g(c0->device);
+  PingArgs A{};
+  A.lv = lanes(comms, n);
+  A.peer0 = peer0;
+  A.peer1 = peer1;
+  A.send_win = send_win;
+  A.recv_win = recv_win;
+  A.sig = signal_id;
+  A.iters = iters;
+  A.warmup = warmup;
+  A.bytes = bytes;
+  A.rtt = rtt_ns_out;
+  A.ctas = bytes >= (1u << 20) ? 16 : (bytes >= (256u << 10) ? 4 : 1);
+  for (uint32_t i = 0; i < n; ++i) {
+    Comm* c = &comms[i]->impl;
+    if (c->rank != peer0 && c->rank != peer1) continue;
+    for (uint32_t w : {send_win, recv_win}) {
+      if (w >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "ping-pong window not registered");
+    }
+    if (c->windows[send_win].sizes[c->rank] < bytes) fail(GINSIM_E_OUT_OF_BOUNDS, "send window smaller than message");
+    const uint32_t other = c->rank == peer0 ? peer1 : peer0;
+    if (c->windows[recv_win].sizes[other] < bytes) fail(GINSIM_E_OUT_OF_BOUNDS, "peer recv window smaller than message");
+    uint64_t cur = 0;
+    if (int rc = ginsim_cuda_read_signal(comms[i], signal_id, &cur)) fail(rc, ginsim_cuda_last_error());
+    const uint64_t rounds_before = bump_host_counter(c, 0, (uint64_t)(warmup + iters)) - (warmup + iters);
+    A.lv.base[i] = (rounds_before << 32) | (cur & 0xFFFFFFFFull);
+  }
+  const uint32_t thr = threads ? threads : 512;
+  coop_launch((const void*)pingpong_kernel, dim3(A.ctas, n), dim3(thr), &A, (cudaStream_t)stream);
+  sync_and_check(comms, n, (cudaStream_t)stream);
+  GIN_API_END
+}
+
+int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_win, uint32_t recv_win,
+                         uint64_t bytes_per_peer, uint32_t signal_id, uint64_t expected, uint32_t ctas,
+                         void* stream) {
+  GIN_API_BEGIN
+  check_same_device(comms, n);
+  Comm* c0 = &comms[0]->impl;
+  const uint32_t world = c0->world;
+  if (world < 2) fail(GINSIM_E_USAGE, "all-to-all needs at least 2 ranks");
+  if (signal_id >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range");
+  for (uint32_t i = 0; i < n; ++i) {
+    Comm* c = &comms[i]->impl;
+    if (send_win >= c->windows.size() || recv_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+    for (uint32_t r = 0; r < world; ++r) {
+      if (c->windows[recv_win].sizes[r] < (uint64_t)world * bytes_per_peer ||
+          c->windows[send_win].sizes[r] < (uint64_t)world * bytes_per_peer)
+        fail(GINSIM_E_OUT_OF_BOUNDS, "windows must hold world * bytes_per_peer");
+    }
+  }
+  DeviceGuard g(c0->device);
+  A2aArgs A{};
+  A.lv = lanes(comms, n);
+  A.send_win = send_win;
+  A.recv_win = recv_win;
+  A.sig = signal_id;
+  A.bytes = bytes_per_peer;
+  A.expected = expected;
+  int sms = 0;
+  GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device));
+  const uint32_t want = ctas ? ctas : (uint32_t)sms;
+  uint32_t per_peer = std::max<uint32_t>(1, want / (world - 1));
+  const uint64_t max_useful = std::max<uint64_t>(1, bytes_per_peer / (16u << 10));
+  per_peer = (uint32_t)std::min<uint64_t>(per_peer, max_useful);
+  // cooperative capacity
+  const int cap = max_coresident_ctas((const void*)alltoall_kernel, 512, 0, c0->device) / (int)n;
+  while (per_peer > 1 && (int)(per_peer * (world - 1)) > cap) --per_peer;
+  A.ctas_per_peer = per_peer;
+  for (uint32_t i = 0; i < n; ++i) A.lv.base[i] = bump_host_counter(&comms[i]->impl, 1, 1);
+  coop_launch((const void*)alltoall_kernel, dim3(per_peer * (world - 1), n), dim3(512), &A, (cudaStream_t)stream);
+  GIN_API_END
+}
+
+int ginsim_cuda_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_win, uint32_t recv_win, uint64_t bytes,
+                     uint32_t rounds, void* stream) {
+  GIN_API_BEGIN
+  check_same_device(comms, n);
+  Comm* c0 = &comms[0]->impl;
+  if (c0->world < 2) fail(GINSIM_E_USAGE, "ring exchange needs at least 2 ranks");
+  for (uint32_t i = 0; i < n; ++i) {
+    Comm* c = &comms[i]->impl;
+    if (send_win >= c->windows.size() || recv_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+    for (uint32_t r = 0; r < c->world; ++r)
+      if (c->windows[send_win].sizes[r] < c->world * bytes || c->windows[recv_win].sizes[r] < c->world * bytes)
+        fail(GINSIM_E_OUT_OF_BOUNDS, "ring windows must hold world * bytes");
+  }
+  DeviceGuard g(c0->device);
+  RingArgs A{};
+  A.lv = lanes(comms, n);
+  A.send_win = send_win;
+  A.recv_win = recv_win;
+  A.rounds = rounds;
+  A.bytes = bytes;
+  for (uint32_t i = 0; i < n; ++i) A.lv.base[i] = bump_host_counter(&comms[i]->impl, 2, rounds) - rounds;
+  coop_launch((const void*)ring_kernel, dim3(1, n), dim3(512), &A, (cudaStream_t)stream);
+  sync_and_check(comms, n, (cudaStream_t)stream);
+  GIN_API_END
+}
+
+int ginsim_cuda_moe_ht_ring(const ginsim_cuda_comm_t* pool, uint32_t n, uint32_t n_pool, uint32_t channels,
+                            uint32_t slots, uint32_t messages, uint64_t seed, void* stream) {
+  GIN_API_BEGIN
+  if (n == 0 || n > GIN_MAX_RANKS || n_pool == 0 || n_pool > 8) fail(GINSIM_E_USAGE, "bad pool shape");
+  if (slots == 0 || channels == 0 || messages == 0) fail(GINSIM_E_USAGE, "moe-ht needs slots, channels, and messages");
+  Comm* c0 = &pool[0]->impl;
+  if (c0->world < 2) fail(GINSIM_E_USAGE, "moe-ht needs at least 2 ranks");
+  const uint32_t n_ctx = c0->cfg.n_contexts;
+  if ((channels + n_ctx - 1) / n_ctx > n_pool) fail(GINSIM_E_USAGE, "comm pool too small for the channel count");
+  HtArgs A{};
+  for (uint32_t r = 0; r < n; ++r) {
+    for (uint32_t p = 0; p < n_pool; ++p) {
+      Comm* c = &pool[r * n_pool + p]->impl;
+      if (c->device != c0->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
+      if (c->windows.size() < 2) fail(GINSIM_E_UNKNOWN_WINDOW, "each pool comm needs recv and stage windows");
+      if (c->windows[0].sizes[c->rank] < (uint64_t)n_ctx * slots * 256) fail(GINSIM_E_OUT_OF_BOUNDS, "recv window too small");
+      A.pool[r][p] = c->dev_view;
+    }
+  }
+  A.channels = channels;
+  A.slots = slots;
+  A.messages = messages;
+  A.n_pool = n_pool;
+  A.seed = seed;
+  DeviceGuard g(c0->device);
+  coop_launch((const void*)moe_ht_kernel, dim3(channels, n), dim3(256), &A, (cudaStream_t)stream);
+  std::vector<ginsim_cuda_comm_t> all(pool, pool + n * n_pool);
+  sync_and_check(all.data(), n * n_pool, (cudaStream_t)stream);
+  GIN_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+// proxy.cu — the Proxy backend's host agent (the paper's CPU proxy thread,
+// PAPER.md:651-669; reference ProxyBackend, proj/core/src/proxy_backend.cpp).
+//
+//   GPU producer (gin_device.cuh, Gin::submit): ticket from a device counter,
+//     wait slot.seq == ticket, write the 64-byte descriptor into pinned host
+//     memory, publish slot.seq = ticket + 1 (proxy_backend.cpp:19-29).
+//   Host consumer (this file): drain <= 64 descriptors per ring per pass
+//     (proxy_backend.hpp:67-68, cpp:64-113), decode (descriptor.cpp), and post
+//     through the plugin's iput / iput_signal analogue: cudaMemcpyAsync for
+//     the payload (peer VMM mapping, copy engine) followed, in stream order,
+//     by cuStreamWriteValue64 stores for the signal and counter cells.
+//
+// Signals without SM atomics: rank d's cell id is the sum over sources s of a
+// sub-cell [s][id] that only s writes (gin_types.h).  The agent is the single
+// writer of its rank's sub-cells in proxy mode, so it keeps the running value
+// on the host and writes it with a stream memop after the put's copy -- the
+// signal is ordered after every earlier put of the channel (fabric.cpp:63-79)
+// and no kernel is launched, so a persistent user kernel that occupies every
+// SM can never starve the agent.  Counters (local completion,
+// proxy_backend.cpp:95-110) are written the same way after the copy.
+#include <sched.h>
+#include <time.h>
+
+#include <chrono>
+#include <cstring>
+
+#include "runtime_internal.h"
+
+namespace ginsim_b200 {
+
+static uint64_t now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
+}
+
+struct ProxyAgent {
+  Comm* c = nullptr;
+  uint32_t n_ctx = 0, cap = 0;
+  std::vector<GinRingSlot*> slots;       // pinned host, device-mapped
+  std::vector<uint64_t> tail;            // next ticket to consume per ctx
+  cudaStream_t stream = nullptr;
+  std::thread th;
+  std::atomic<bool> stop{false};
+
+  // running cell values this agent owns
+  std::vector<uint64_t> sig_value;       // [peer][cell] sub-cell (peer, my rank)
+  std::vector<uint64_t> ctr_value;       // [cell]
+
+  // inline payload staging (pinned), recycled by pass
+  static constexpr uint32_t kStage = 8192;
+  uint64_t* stage = nullptr;
+  uint32_t stage_next = 0;
+
+  // completion tracking: one event per pass with work
+  struct Pass {
+    cudaEvent_t ev;
+    std::vector<uint64_t> host_done;     // per ctx host tickets complete after this pass
+    std::vector<uint32_t> counters;      // counter ids completed by this pass
+    uint32_t stage_end;
+  };
+  std::deque<Pass> inflight;
+  std::vector<cudaEvent_t> free_events;
+
+  // host-submitted ops
+  std::mutex hq_mu;
+  std::deque<std::pair<uint32_t, std::array<uint8_t, 64>>> host_queue;
+  std::vector<uint64_t> host_submitted;            // per ctx (under hq_mu)
+  std::vector<std::atomic<uint64_t>> host_completed;
+  std::vector<uint64_t> host_taken;                // per ctx, agent thread only
+  std::vector<std::atomic<uint32_t>> counter_pending;
+
+  std::atomic<uint64_t> n_desc{0}, n_copies{0}, busy_ns{0};
+  uint64_t t_start = 0;
+  std::string failure;
+  std::atomic<bool> failed{false};
+
+  ProxyAgent(Comm* comm)
+      : c(comm),
+        host_completed(comm->cfg.n_contexts),
+        counter_pending(comm->cfg.counter_cells) {}
+
+  cudaEvent_t get_event() {
+    if (!free_events.empty()) {
+      cudaEvent_t e = free_events.back();
+      free_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    GIN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }
+
+  void write64(uint64_t* dev_addr, uint64_t v) {
+    GIN_CU(cuapi().cuStreamWriteValue64((CUstream)stream, (CUdeviceptr)dev_addr, v, CU_STREAM_WRITE_VALUE_DEFAULT));
+  }
+
+  // iput / iput_signal (plugin.hpp:86-90) for one decoded descriptor.
+  void post(uint32_t ctx, const ginsim_cuda_descriptor& d, Pass& pass) {
+    const GinDevCommView& v = c->host_view;
+    const uint32_t peer = d.peer;  // team 0 = world: team-relative == world rank
+    if (peer >= v.world) fail(GINSIM_E_INVALID_PEER, "proxy: descriptor peer out of range");
+    if (d.opcode != GIN_OP_SIGNAL_ONLY && d.bytes > 0) {
+      if (d.dst_window >= v.n_windows) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown destination window");
+      const GinWindowView& dw = v.win[d.dst_window];
+      if (d.dst_offset > dw.size[peer] || d.bytes > dw.size[peer] - d.dst_offset)
+        fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: destination range exceeds capacity");
+      char* dst = dw.base[peer] + d.dst_offset;
+      if (d.opcode == GIN_OP_PUT) {
+        if (d.src_window >= v.n_windows) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown source window");
+        const GinWindowView& sw = v.win[d.src_window];
+        if (d.src_offset_or_value > sw.size[v.rank] || d.bytes > sw.size[v.rank] - d.src_offset_or_value)
+          fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: source range exceeds capacity");
+        GIN_CUDA(cudaMemcpyAsync(dst, sw.base[v.rank] + d.src_offset_or_value, d.bytes, cudaMemcpyDefault, stream));
+      } else {
+        uint64_t* s = stage + (stage_next++ % kStage);
+        *s = d.src_offset_or_value;
+        GIN_CUDA(cudaMemcpyAsync(dst, s, d.bytes, cudaMemcpyHostToDevice, stream));
+      }
+      n_copies.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (d.flags & GIN_FLAG_HAS_SIGNAL) {
+      if (d.signal_id >= v.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "proxy: signal out of range");
+      uint64_t& val = sig_value[(size_t)peer * v.signal_cells + d.signal_id];
+      val += (d.flags & GIN_FLAG_SIGNAL_IS_ADD) ? d.signal_operand : 1ull;
+      write64(v.signals[peer] + (uint64_t)v.rank * v.signal_cells + d.signal_id, val);
+    }
+    if (d.flags & GIN_FLAG_HAS_COUNTER) {
+      if (d.counter_id >= v.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "proxy: counter out of range");
+      ctr_value[d.counter_id] += 1;
+      write64(v.counters + d.counter_id, ctr_value[d.counter_id]);
+      pass.counters.push_back(d.counter_id);
+    }
+    (void)ctx;
+  }
+
+  void retire_completed(bool block) {
+    while (!inflight.empty()) {
+      Pass& p = inflight.front();
+      cudaError_t q = block ? cudaEventSynchronize(p.ev) : cudaEventQuery(p.ev);
+      if (q == cudaErrorNotReady) return;
+      GIN_CUDA(q);
+      for (uint32_t i = 0; i < n_ctx; ++i) {
+        if (p.host_done[i] > host_completed[i].load(std::memory_order_relaxed))
+          host_completed[i].store(p.host_done[i], std::memory_order_release);
+      }
+      for (uint32_t id : p.counters) counter_pending[id].fetch_sub(1, std::memory_order_acq_rel);
+      free_events.push_back(p.ev);
+      inflight.pop_front();
+    }
+  }
+
+  size_t progress_once() {
+    size_t work = 0;
+    Pass pass;
+    pass.host_done.assign(n_ctx, 0);
+    std::vector<uint64_t> consumed(n_ctx, 0);
+    bool any_dev = false;
+    for (uint32_t ctx = 0; ctx < n_ctx; ++ctx) {
+      for (uint32_t i = 0; i < 64; ++i) {
+        const uint64_t t = tail[ctx];
+        GinRingSlot* slot = slots[ctx] + (t & (cap - 1));
+        if (__atomic_load_n(&slot->seq, __ATOMIC_ACQUIRE) != t + 1) break;
+        uint8_t raw[64];
+        std::memcpy(raw, slot->bytes, 64);
+        __atomic_store_n(&slot->seq, t + cap, __ATOMIC_RELEASE);
+        tail[ctx] = t + 1;
+        ginsim_cuda_descriptor d;
+        descriptor_decode(raw, &d);  // a malformed descriptor is a protocol bug: fail the run
+        if (d.flags & GIN_FLAG_HAS_COUNTER) counter_pending[d.counter_id].fetch_add(1, std::memory_order_acq_rel);
+        post(ctx, d, pass);
+        ++work;
+        any_dev = true;
+        consumed[ctx] = t + 1;
+      }
+    }
+    {
+      std::unique_lock<std::mutex> lk(hq_mu);
+      for (uint32_t i = 0; i < 256 && !host_queue.empty(); ++i) {
+        auto item = host_queue.front();
+        host_queue.pop_front();
+        lk.unlock();
+        ginsim_cuda_descriptor d;
+        descriptor_decode(item.second.data(), &d);
+        post(item.first, d, pass);
+        host_taken[item.first] += 1;
+        pass.host_done[item.first] = host_taken[item.first];
+        ++work;
+        lk.lock();
+      }
+    }
+    if (work) {
+      for (uint32_t ctx = 0; ctx < n_ctx; ++ctx) {
+        if (!pass.host_done[ctx]) pass.host_done[ctx] = host_taken[ctx];
+        // device-visible flush word: every ticket consumed so far is complete
+        // once the copies above have completed (stream order).
+        if (any_dev && consumed[ctx]) write64(c->host_view.proxy.completed + ctx, consumed[ctx]);
+      }
+      pass.ev = get_event();
+      GIN_CUDA(cudaEventRecord(pass.ev, stream));
+      pass.stage_end = stage_next;
+      inflight.push_back(std::move(pass));
+      n_desc.fetch_add(work, std::memory_order_relaxed);
+    }
+    // never let the inline staging ring lap an unfinished copy
+    while (!inflight.empty() && stage_next - inflight.front().stage_end + 512 > kStage) retire_completed(true);
+    retire_completed(false);
+    return work;
+  }
+
+  void main() {
+    DeviceGuard g(c->device);
+    t_start = now_ns();
+    uint32_t idle = 0;
+    while (!stop.load(std::memory_order_acquire)) {
+      const uint64_t t0 = now_ns();
+      size_t w = 0;
+      try {
+        w = progress_once();
+      } catch (const std::exception& e) {
+        failure = e.what();
+        failed.store(true);
+        uint32_t code = GIN_DEVERR_VERIFY;
+        cudaMemcpy(c->host_view.error, &code, 4, cudaMemcpyHostToDevice);
+        return;
+      }
+      if (w || !inflight.empty()) {
+        busy_ns.fetch_add(now_ns() - t0, std::memory_order_relaxed);
+        idle = 0;
+        continue;
+      }
+      if (++idle < 20000) {
+        busy_ns.fetch_add(now_ns() - t0, std::memory_order_relaxed);
+        __builtin_ia32_pause();
+      } else if (idle < 40000) {
+        sched_yield();
+      } else {
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+    }
+    retire_completed(true);
+  }
+};
+
+ProxyPtr proxy_start(Comm* c) {
+  ProxyPtr p(new ProxyAgent(c));
+  p->n_ctx = c->cfg.n_contexts;
+  p->cap = c->cfg.queue_depth;
+  DeviceGuard g(c->device);
+  GIN_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  p->slots.resize(p->n_ctx);
+  p->tail.assign(p->n_ctx, 0);
+  p->host_submitted.assign(p->n_ctx, 0);
+  p->host_taken.assign(p->n_ctx, 0);
+  for (uint32_t i = 0; i < p->n_ctx; ++i) {
+    void* mem = nullptr;
+    GIN_CUDA(cudaHostAlloc(&mem, sizeof(GinRingSlot) * p->cap, cudaHostAllocMapped | cudaHostAllocPortable));
+    auto* s = static_cast<GinRingSlot*>(mem);
+    for (uint32_t k = 0; k < p->cap; ++k) {
+      s[k].seq = k;
+      std::memset(s[k].bytes, 0, 64);
+    }
+    p->slots[i] = s;
+    void* dptr = nullptr;
+    GIN_CUDA(cudaHostGetDevicePointer(&dptr, mem, 0));
+    c->host_view.proxy.slots[i] = static_cast<GinRingSlot*>(dptr);
+  }
+  void* st = nullptr;
+  GIN_CUDA(cudaHostAlloc(&st, sizeof(uint64_t) * ProxyAgent::kStage, cudaHostAllocPortable));
+  p->stage = static_cast<uint64_t*>(st);
+  p->sig_value.assign((size_t)c->world * c->cfg.signal_cells, 0);
+  p->ctr_value.assign(c->cfg.counter_cells, 0);
+  ProxyAgent* raw = p.get();
+  p->th = std::thread([raw] { raw->main(); });
+  return p;
+}
+
+void ProxyDeleter::operator()(ProxyAgent* p) const { delete p; }
+
+void proxy_stop(ProxyPtr& p) {
+  if (!p) return;
+  p->stop.store(true, std::memory_order_release);
+  if (p->th.joinable()) p->th.join();
+  DeviceGuard g(p->c->device);
+  cudaStreamSynchronize(p->stream);
+  for (auto& f : p->inflight) cudaEventDestroy(f.ev);
+  for (auto e : p->free_events) cudaEventDestroy(e);
+  for (auto s : p->slots) cudaFreeHost(s);
+  if (p->stage) cudaFreeHost(p->stage);
+  cudaStreamDestroy(p->stream);
+  p.reset();
+}
+
+void proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]) {
+  ProxyAgent* p = c->proxy.get();
+  if (p->failed.load()) fail(GINSIM_E_GENERIC, "proxy agent failed: " + p->failure);
+  std::array<uint8_t, 64> d;
+  std::memcpy(d.data(), desc, 64);
+  ginsim_cuda_descriptor dd;
+  descriptor_decode(desc, &dd);
+  if (dd.flags & GIN_FLAG_HAS_COUNTER) p->counter_pending[dd.counter_id].fetch_add(1, std::memory_order_acq_rel);
+  std::lock_guard<std::mutex> lk(p->hq_mu);
+  p->host_queue.emplace_back(ctx, d);
+  p->host_submitted[ctx] += 1;
+}
+
+void proxy_host_flush(Comm* c, uint32_t ctx) {
+  ProxyAgent* p = c->proxy.get();
+  uint64_t snap;
+  {
+    std::lock_guard<std::mutex> lk(p->hq_mu);
+    snap = p->host_submitted[ctx];
+  }
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(c->cfg.timeout_ms);
+  while (p->host_completed[ctx].load(std::memory_order_acquire) < snap) {
+    if (p->failed.load()) fail(GINSIM_E_GENERIC, "proxy agent failed: " + p->failure);
+    if (std::chrono::steady_clock::now() > deadline) fail(GINSIM_E_TIMEOUT, "flush: exceeded timeout");
+    std::this_thread::yield();
+  }
+}
+
+bool proxy_counter_pending(Comm* c, uint32_t id) {
+  return c->proxy && c->proxy->counter_pending[id].load(std::memory_order_acquire) != 0;
+}
+
+void proxy_stats(Comm* c, uint64_t* descs, uint64_t* copies, uint64_t* busy, uint64_t* wall) {
+  ProxyAgent* p = c->proxy.get();
+  if (descs) *descs = p->n_desc.load();
+  if (copies) *copies = p->n_copies.load();
+  if (busy) *busy = p->busy_ns.load();
+  if (wall) *wall = now_ns() - p->t_start;
+}
+
+}  // namespace ginsim_b200

@@ -1,0 +1,165 @@
+// runtime_internal.h — host-side communicator state behind the C ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <array>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/ginsim_cuda.h"
+#include "gin_types.h"
+
+namespace ginsim_b200 {
+
+// Internal exception carrying a C-ABI status; the C layer converts it.
+struct GinError : std::runtime_error {
+  int code;
+  GinError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void set_last_error(const char* msg);
+#define GIN_API_BEGIN try {
+#define GIN_API_END                                      \
+  return GINSIM_OK;                                      \
+  }                                                      \
+  catch (const ::ginsim_b200::GinError& e) {             \
+    ::ginsim_b200::set_last_error(e.what());             \
+    return e.code;                                       \
+  }                                                      \
+  catch (const std::exception& e) {                      \
+    ::ginsim_b200::set_last_error(e.what());             \
+    return GINSIM_E_GENERIC;                             \
+  }
+void cuda_check(cudaError_t e, const char* what);
+void cu_check(CUresult r, const char* what);
+#define GIN_CUDA(x) ::ginsim_b200::cuda_check((x), #x)
+#define GIN_CU(x) ::ginsim_b200::cu_check((x), #x)
+
+
+// Driver API through cudaGetDriverEntryPoint: the library never links
+// libcuda, so it loads (and its host-only codec runs) on a machine without a
+// GPU driver; the first driver call resolves the table or fails loudly.
+struct CuApi {
+  decltype(&::cuStreamWriteValue64) cuStreamWriteValue64 = nullptr;
+  decltype(&::cuGetErrorString) cuGetErrorString = nullptr;
+  decltype(&::cuMemAddressFree) cuMemAddressFree = nullptr;
+  decltype(&::cuMemAddressReserve) cuMemAddressReserve = nullptr;
+  decltype(&::cuMemCreate) cuMemCreate = nullptr;
+  decltype(&::cuMemExportToShareableHandle) cuMemExportToShareableHandle = nullptr;
+  decltype(&::cuMemGetAllocationGranularity) cuMemGetAllocationGranularity = nullptr;
+  decltype(&::cuMemImportFromShareableHandle) cuMemImportFromShareableHandle = nullptr;
+  decltype(&::cuMemMap) cuMemMap = nullptr;
+  decltype(&::cuMemRelease) cuMemRelease = nullptr;
+  decltype(&::cuMemSetAccess) cuMemSetAccess = nullptr;
+  decltype(&::cuMemUnmap) cuMemUnmap = nullptr;
+};
+const CuApi& cuapi();
+
+// Scoped current-device switch.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+// One exportable VMM allocation (cuMemCreate + cuMemMap) owned by this process.
+struct VmmAlloc {
+  CUmemGenericAllocationHandle handle = 0;
+  CUdeviceptr ptr = 0;
+  uint64_t size = 0;  // granularity-rounded
+  int device = 0;
+  int fd = -1;        // exported POSIX FD, kept open while the allocation lives
+};
+
+// Blob exchanged through the bootstrap for every window / signal table.
+struct ExportBlob {
+  int32_t pid;
+  int32_t fd;
+  int32_t device;
+  int32_t is_vmm;
+  uint64_t alloc_size;
+  uint64_t offset;      // of the region inside the allocation
+  uint64_t bytes;       // region size (window capacity)
+  uint64_t ptr;         // owner's VA of the region (valid in the owner process)
+  uint32_t window_id;
+  uint32_t pad;
+};
+
+struct Mapping {  // an imported peer allocation
+  CUmemGenericAllocationHandle handle = 0;
+  CUdeviceptr ptr = 0;
+  uint64_t size = 0;
+};
+
+struct ProxyAgent;  // proxy.cu
+struct ProxyDeleter {
+  void operator()(ProxyAgent* p) const;
+};
+using ProxyPtr = std::unique_ptr<ProxyAgent, ProxyDeleter>;
+
+struct Comm {
+  uint32_t rank = 0, world = 1;
+  int device = 0;
+  ginsim_cuda_config cfg{};
+  ginsim_cuda_bootstrap boot{};
+
+  VmmAlloc signal_alloc;                      // [world][signal_cells] u64, exported
+  void* local_block = nullptr;                // cudaMalloc: bases, counters, error, workspace
+  std::vector<Mapping> imported;              // peer mappings owned by this comm
+  std::vector<std::pair<uint64_t, uint64_t>> window_sizes_dummy;
+
+  struct Window {
+    std::vector<uint64_t> sizes;
+    std::vector<char*> bases;
+  };
+  std::vector<Window> windows;
+
+  GinDevCommView host_view{};
+  GinDevCommView* dev_view = nullptr;         // device copy
+
+  std::map<CUdeviceptr, VmmAlloc> allocs;     // ginsim_cuda_mem_alloc'd regions
+  std::mutex mu;
+
+  cudaStream_t op_stream = nullptr;           // host-issued ops / cell reads
+  uint64_t op_counter[8] = {};                // per-workload launch/round counters (host side)
+  ProxyPtr proxy;
+
+  void allgather(const void* send, void* recv, size_t bytes);
+  void barrier();
+  void sync_view();                           // push host_view to dev_view
+  char* map_blob(const ExportBlob& b);        // import a peer region into this process
+};
+
+// Launch helpers shared by the kernel translation units.
+void check_same_device(const ginsim_cuda_comm_t* comms, uint32_t n);
+int max_coresident_ctas(const void* kernel, int threads, size_t smem, int device);
+void check_device_error(Comm* c);
+
+// Proxy agent lifecycle (proxy.cu).
+ProxyPtr proxy_start(Comm* c);
+void proxy_stop(ProxyPtr& p);
+void proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]);
+void proxy_host_flush(Comm* c, uint32_t ctx);
+bool proxy_counter_pending(Comm* c, uint32_t id);
+void proxy_stats(Comm* c, uint64_t* descs, uint64_t* copies, uint64_t* busy_ns, uint64_t* wall_ns);
+
+// Descriptor codec (descriptor.cpp).
+int descriptor_check(const ginsim_cuda_descriptor* d);
+void descriptor_encode(const ginsim_cuda_descriptor* d, uint8_t out[64]);  // throws InvalidDescriptor
+void descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* d);   // throws MalformedDescriptor
+
+}  // namespace ginsim_b200
+
+struct ginsim_cuda_comm_s {
+  ginsim_b200::Comm impl;
+};
