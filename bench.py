@@ -167,9 +167,9 @@ def main():
             out = [None] * world
             dist.all_gather_object(out, blob)
             return out
-        comm = G.Comm.create(rank, world, local, allgather, G.Config())
+        comm = G.Comm.create(rank, world, local, allgather, G.Config(signal_cells=512))
     else:
-        comm = G.Comm.create_all([local], G.Config())[0]
+        comm = G.Comm.create_all([local], G.Config(signal_cells=512))[0]
 
     T, H, K, E = args.tokens, HIDDEN, TOPK, EXPERTS
     cfg = G.MoeConfig(E, K, T, H, args.mode, args.layout, args.ctas)

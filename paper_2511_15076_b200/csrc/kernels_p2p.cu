@@ -302,7 +302,9 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
     if (c->windows[recv_win].sizes[other] < bytes) fail(GINSIM_E_OUT_OF_BOUNDS, "peer recv window smaller than message");
     uint64_t cur = 0;
     if (int rc = ginsim_cuda_read_signal(comms[i], signal_id, &cur)) fail(rc, ginsim_cuda_last_error());
-    const uint64_t rounds_before = bump_host_counter(c, 0, (uint64_t)(warmup + iters)) - (warmup + iters);
+    // the arrival counter only advances on multi-CTA launches
+    const uint64_t adv = A.ctas > 1 ? (uint64_t)(warmup + iters) : 0;
+    const uint64_t rounds_before = bump_host_counter(c, 0, adv) - adv;
     A.lv.base[i] = (rounds_before << 32) | (cur & 0xFFFFFFFFull);
   }
   const uint32_t thr = threads ? threads : 512;

@@ -1,0 +1,95 @@
+"""One rank of a multi-process (torchrun) parity run: real GPUs, one process
+per GPU, NVLink peer mappings imported through POSIX-FD handles.
+Launched by tests/test_gpu_multi.py; prints one JSON line per rank."""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_15076_b200 as G
+    from oracle import oracle as O
+
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+
+    def allgather(blob):
+        out = [None] * world
+        dist.all_gather_object(out, blob)
+        return out
+
+    T = int(os.environ.get("MP_TOKENS", "256"))
+    mode = int(os.environ.get("MP_MODE", "0"))
+    layout = int(os.environ.get("MP_LAYOUT", "1"))
+    E, K, H, seed = 256, 8, 7168, 1
+    comm = G.Comm.create(rank, world, local, allgather, G.Config(signal_cells=512, timeout_ms=20000))
+    cfg = G.MoeConfig(E, K, T, H, mode, layout, 0)
+    moe = G.Moe(comm, cfg)
+    dev = torch.device("cuda", local)
+    x = torch.empty(T * H, dtype=torch.int16, device=dev)
+    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
+    w = torch.empty(T * K, dtype=torch.float32 if mode else torch.int16, device=dev)
+    out = torch.empty(T * H, dtype=torch.int16, device=dev)
+    moe.generate(seed, rank, x, idx, w)
+    torch.cuda.synchronize()
+    res = {"rank": rank, "ok": True}
+    for it in range(3):
+        G.Moe.dispatch([moe], [x], [idx])
+        G.Moe.combine([moe], [w], [out])
+        torch.cuda.synchronize()
+        comm.check_device()
+    got = out.cpu().numpy().view(np.uint16).reshape(T, H)
+    exp, _ = O.combine(seed, E, K, H, rank, T, mode=mode)
+    res["combine_exact"] = bool((got == exp).all())
+    cnt = O.counts(seed, world, E, K, T)
+    sig, _ = comm.snapshot_cells(512, 256)
+    e_local = E // world
+    res["cells_exact"] = all(sig[e] == 3 * ((world << 32) + int(cnt[rank * e_local + e].sum())) for e in range(e_local)) \
+        and sig[e_local] == 3 * T * K
+    if layout == 0 and T <= 256:
+        from tests import gpu_util as U
+        d, comb, _ = O.moe_rank_state(seed, world, E, K, T, H, rank, mode=mode)
+        win = U.d2h(comm.window_ptr(moe.win_dispatch, rank), len(d))
+        res["dispatch_window_exact"] = bool((win == d).all())
+        cwin = U.d2h(comm.window_ptr(moe.win_combine, rank), len(comb))
+        res["combine_window_exact"] = bool((cwin == comb).all())
+    # put+signal ping-pong over NVLink between ranks 0 and 1 (K14)
+    if world >= 2 and os.environ.get("MP_PINGPONG", "1") == "1":
+        size = 1 << 22
+        sbuf = comm.mem_alloc(size)
+        rbuf = comm.mem_alloc(size)
+        ws = comm.window_register(sbuf, size)
+        wr = comm.window_register(rbuf, size)
+        rows = []
+        rtt = torch.zeros(1000, dtype=torch.int64, device=dev)
+        for sz in [8, 64, 512, 4096, 32768, 262144, 1 << 20, 1 << 22]:
+            iters = 1000 if sz <= 65536 else 200
+            if rank in (0, 1):
+                G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, iters, 100, 0, 512,
+                                                     rtt.data_ptr(), None))
+            dist.barrier()
+            if rank == 0:
+                t = np.sort(rtt[:iters].cpu().numpy())
+                rows.append({"size": sz, "iters": iters, "p50_ns": int(t[iters // 2]),
+                             "p99_ns": int(t[min(iters - 1, iters * 99 // 100)]), "mean_ns": float(t.mean())})
+        res["pingpong"] = rows
+    dist.barrier()
+    out_dir = os.environ.get("MP_OUT")
+    if out_dir:
+        with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+            json.dump(res, f)
+    print("MPRESULT " + json.dumps(res), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,54 @@
+"""Real multi-GPU runs (one process per GPU over torchrun, NVLink peer
+mappings).  Skipped when fewer than 2 GPUs are visible; run with
+`gpurun --gpus 2|4 -- python -m pytest tests/test_gpu_multi.py -m gpu`."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from tests.conftest import gpu_count
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _torchrun(n, env):
+    import tempfile
+    out = tempfile.mkdtemp(prefix="mp")
+    e = dict(os.environ, MP_OUT=out, **{k: str(v) for k, v in env.items()})
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + (os.getpid() % 1000)),
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    r = subprocess.run(cmd, env=e, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    results = []
+    for i in range(n):
+        with open(os.path.join(out, f"rank{i}.json")) as f:
+            results.append(json.load(f))
+    return results
+
+
+@pytest.mark.parametrize("layout,tokens,mode", [(0, 128, 0), (1, 256, 0), (1, 4096, 1)])
+def test_multiprocess_moe_parity(layout, tokens, mode):
+    n = gpu_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = 4 if n >= 4 else 2
+    res = _torchrun(n, {"MP_TOKENS": tokens, "MP_LAYOUT": layout, "MP_MODE": mode, "MP_PINGPONG": 0})
+    for r in res:
+        assert r["combine_exact"] and r["cells_exact"], r
+        if "dispatch_window_exact" in r:
+            assert r["dispatch_window_exact"] and r["combine_window_exact"], r
+
+
+def test_multiprocess_pingpong_nvlink():
+    n = gpu_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    res = _torchrun(2, {"MP_TOKENS": 128, "MP_PINGPONG": 1})
+    rows = res[0]["pingpong"]
+    assert len(rows) == 8
+    print(json.dumps(rows))
+    assert rows[0]["p50_ns"] > 0

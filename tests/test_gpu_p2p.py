@@ -216,8 +216,8 @@ def test_pingpong_payload_and_counts():
     cs = world(2)
     try:
         size = 4096
-        ws, sp = register(cs, size)
-        wr, rp = register(cs, size)
+        ws, sp = register(cs, 1 << 20)
+        wr, rp = register(cs, 1 << 20)
         for r in range(2):
             U.h2d(sp[r], O.pingpong_payload(r, size))
         rtt = U.malloc(8 * 50)
