@@ -41,6 +41,7 @@ def parse():
     p.add_argument("--mode", type=int, default=1, help="0 = u16 exact, 1 = bf16")
     p.add_argument("--layout", type=int, default=1, help="0 = reference layout, 1 = compact")
     p.add_argument("--ctas", type=int, default=0)
+    p.add_argument("--engine", type=int, default=0, help="0 = auto (TMA), 1 = LSU stores, 2 = TMA")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -172,7 +173,7 @@ def main():
         comm = G.Comm.create_all([local], G.Config(signal_cells=512))[0]
 
     T, H, K, E = args.tokens, HIDDEN, TOPK, EXPERTS
-    cfg = G.MoeConfig(E, K, T, H, args.mode, args.layout, args.ctas)
+    cfg = G.MoeConfig(E, K, T, H, args.mode, args.layout, args.ctas, args.engine)
     moe = G.Moe(comm, cfg)
     dev = torch.device("cuda", local)
     x = torch.empty(T * H, dtype=torch.int16, device=dev)

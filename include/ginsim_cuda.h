@@ -114,6 +114,8 @@ int ginsim_cuda_comm_create_all(uint32_t world_size, const int* devices,
 int ginsim_cuda_comm_destroy(ginsim_cuda_comm_t comm);
 int ginsim_cuda_comm_info(ginsim_cuda_comm_t comm, uint32_t* rank, uint32_t* world, int* device,
                           uint32_t* backend);
+/* DevComm::config (runtime.hpp:131): the config the comm was created with. */
+int ginsim_cuda_comm_config(ginsim_cuda_comm_t comm, ginsim_cuda_config* out);
 /* Device pointer to the GinDevCommView kernels take (the ncclDevComm analogue). */
 int ginsim_cuda_devcomm_view(ginsim_cuda_comm_t comm, const void** device_view);
 
@@ -217,6 +219,14 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
                          uint32_t warmup, uint32_t signal_id, uint32_t threads, uint64_t* rtt_ns_out,
                          void* stream);
 
+/* Roofline probe: copy `bytes` from this rank's src window into `peer`'s dst
+ * window (peer == own rank: local HBM copy) `iters` times with the put path's
+ * engines (0 = 128-bit LSU stores, 1 = TMA bulk copies through shared
+ * memory); *ms_out = mean milliseconds per copy.  No signals. */
+int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t dst_win, uint32_t peer,
+                           uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t iters, float* ms_out,
+                           void* stream);
+
 /* One-sided all-to-all via put+signal: every rank puts
  * `bytes_per_peer` from send_win[dst*M] to dst's recv_win[src*M] and signals
  * `signal_id` on dst; then waits until the cell >= expected. */
@@ -250,7 +260,8 @@ typedef struct ginsim_cuda_moe_config {
   uint32_t layout;   /* 0 = reference layout ((e_loc*n+src)*T+slot)*dmsg,
                         1 = compact per-source layout (src*T*K + prefix + slot)*dmsg */
   uint32_t ctas;     /* CTAs per rank (0 = as many as fit) */
-  uint32_t reserved;
+  uint32_t engine;   /* data mover: 0 = auto (TMA bulk copies when messages are
+                        16-byte aligned), 1 = 128-bit LSU stores, 2 = TMA */
 } ginsim_cuda_moe_config;
 
 typedef struct ginsim_cuda_moe_s* ginsim_cuda_moe_t;

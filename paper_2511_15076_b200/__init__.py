@@ -119,10 +119,10 @@ class Descriptor(ctypes.Structure):
 
 class MoeConfig(ctypes.Structure):
     _fields_ = [("experts", c_uint32), ("top_k", c_uint32), ("tokens", c_uint32), ("hidden", c_uint32),
-                ("mode", c_uint32), ("layout", c_uint32), ("ctas", c_uint32), ("reserved", c_uint32)]
+                ("mode", c_uint32), ("layout", c_uint32), ("ctas", c_uint32), ("engine", c_uint32)]
 
-    def __init__(self, experts=256, top_k=8, tokens=128, hidden=7168, mode=0, layout=0, ctas=0):
-        super().__init__(experts, top_k, tokens, hidden, mode, layout, ctas, 0)
+    def __init__(self, experts=256, top_k=8, tokens=128, hidden=7168, mode=0, layout=0, ctas=0, engine=0):
+        super().__init__(experts, top_k, tokens, hidden, mode, layout, ctas, engine)
 
     @property
     def dispatch_message_bytes(self):  # harness.hpp:112
@@ -172,6 +172,7 @@ def _declare(L):
         "ginsim_cuda_comm_destroy": ([P], c_int),
         "ginsim_cuda_comm_info": ([P, POINTER(c_uint32), POINTER(c_uint32), POINTER(c_int), POINTER(c_uint32)], c_int),
         "ginsim_cuda_devcomm_view": ([P, POINTER(P)], c_int),
+        "ginsim_cuda_comm_config": ([P, POINTER(Config)], c_int),
         "ginsim_cuda_mem_alloc": ([P, c_uint64, POINTER(P)], c_int),
         "ginsim_cuda_mem_free": ([P, P], c_int),
         "ginsim_cuda_window_register": ([P, P, c_uint64, POINTER(c_uint32)], c_int),
@@ -197,7 +198,9 @@ def _declare(L):
         "ginsim_cuda_pingpong": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32,
                                   c_uint32, c_uint32, c_uint32, P, P], c_int),
         "ginsim_cuda_alltoall": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint64, c_uint32, P], c_int),
-        "ginsim_cuda_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, P], c_int),
+        "ginsim_cuda_copy_bench": ([P, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, c_uint32,
+                                    POINTER(ctypes.c_float), P], c_int),
+        "ginsim_cuda_ring":([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, P], c_int),
         "ginsim_cuda_moe_ht_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, P], c_int),
         "ginsim_cuda_moe_create": ([P, POINTER(MoeConfig), POINTER(P)], c_int),
         "ginsim_cuda_moe_destroy": ([P], c_int),
@@ -255,6 +258,8 @@ class Comm:
         r, w, d, b = c_uint32(), c_uint32(), c_int(), c_uint32()
         check(lib().ginsim_cuda_comm_info(self.h, byref(r), byref(w), byref(d), byref(b)))
         self.rank, self.world_size, self.device, self.backend = r.value, w.value, d.value, b.value
+        self.config = Config()
+        check(lib().ginsim_cuda_comm_config(self.h, byref(self.config)))
         self.n_windows = 0
 
     # -- construction
@@ -362,9 +367,10 @@ class Comm:
     def reset_counter(self, cid):
         check(lib().ginsim_cuda_reset_counter(self.h, cid))
 
-    def snapshot_cells(self, signal_cells=256, counter_cells=256):
-        s = (c_uint64 * signal_cells)()
-        c = (c_uint64 * counter_cells)()
+    def snapshot_cells(self, signal_cells=None, counter_cells=None):
+        """DevComm::snapshot_cells (runtime.hpp:178): every signal and counter cell."""
+        s = (c_uint64 * self.config.signal_cells)()
+        c = (c_uint64 * self.config.counter_cells)()
         check(lib().ginsim_cuda_snapshot_cells(self.h, s, c))
         return list(s), list(c)
 

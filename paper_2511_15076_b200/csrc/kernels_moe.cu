@@ -31,6 +31,7 @@
 
 #include "gin_device.cuh"
 #include "runtime_internal.h"
+#include "tma.cuh"
 
 namespace ginsim_b200 {
 
@@ -125,7 +126,7 @@ __device__ void block_exclusive_scan(uint32_t* data, uint32_t n, uint32_t* warp_
 
 // ------------------------------------------------------------------ dispatch
 template <int KMAX>
-__global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_kernel(MoeLaunch L) {
+__global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
 }
 
 // ------------------------------------------------------------------ combine
-__global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L) {
+__global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
@@ -474,6 +475,393 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
   }
 }
 
+// ------------------------------------------------------------------ TMA engine
+// Same protocol as the LSU kernels above, with the data path moved onto the
+// TMA engine: each warp runs its own kTmaStages-deep pipeline in which lane 0
+// bulk-loads a message chunk (<= 8 KiB) from HBM into shared memory on an
+// mbarrier and bulk-stores it to the K destinations (local HBM or NVLink
+// peer mappings).  No registers or scoreboard slots are held by in-flight
+// data, so one CTA of 8 warps per SM keeps ~170 KiB of loads and K times
+// that of stores in flight.  Used whenever messages are 16-byte aligned.
+constexpr int kTmaThreads = 256;
+constexpr int kTmaWarps = kTmaThreads / 32;
+constexpr int kTmaStages = 3;
+
+struct TmaSmem {  // per-warp control block, followed by the staging buffers
+  uint64_t bar[kTmaStages];
+  char* dptr[32];
+};
+
+__device__ __forceinline__ uint32_t tma_chunk_len(uint32_t payload, uint32_t chunk, uint32_t p) {
+  return min(chunk, payload - p * chunk);
+}
+
+// out = sum_k w_k * y_k for one 16-byte vector (8 elements) of token t:
+// u16 wraparound (harness_moe.cpp:227-242) or fp32 accumulate in k order
+// with single rounding per op, rounded once to bf16.
+template <int KMAX>
+__device__ __forceinline__ uint4 reduce_vec(const uint4* y, uint32_t K, uint32_t mode, const void* weights, uint32_t t) {
+  if (mode == 0) {
+    const uint16_t* w = reinterpret_cast<const uint16_t*>(weights) + (uint64_t)t * K;
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k < (int)K) {
+        const uint32_t wk = w[k];
+        const uint32_t ys[4] = {y[k].x, y[k].y, y[k].z, y[k].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[2 * c] += wk * (ys[c] & 0xFFFFu);
+          acc[2 * c + 1] += wk * (ys[c] >> 16);
+        }
+      }
+    }
+    return make_uint4((acc[0] & 0xFFFFu) | (acc[1] << 16), (acc[2] & 0xFFFFu) | (acc[3] << 16),
+                      (acc[4] & 0xFFFFu) | (acc[5] << 16), (acc[6] & 0xFFFFu) | (acc[7] << 16));
+  }
+  const float* w = reinterpret_cast<const float*>(weights) + (uint64_t)t * K;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < (int)K) {
+      const float wk = w[k];
+      const uint32_t ys[4] = {y[k].x, y[k].y, y[k].z, y[k].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[2 * c] = __fadd_rn(acc[2 * c], __fmul_rn(wk, __uint_as_float(ys[c] << 16)));
+        acc[2 * c + 1] = __fadd_rn(acc[2 * c + 1], __fmul_rn(wk, __uint_as_float(ys[c] & 0xFFFF0000u)));
+      }
+    }
+  }
+  uint32_t pk[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    pk[c] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc[2 * c])) |
+            ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(acc[2 * c + 1])) << 16);
+  return make_uint4(pk[0], pk[1], pk[2], pk[3]);
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLaunch L, uint32_t chunk) {
+  const MoeRankArgs& R = L.r[blockIdx.y];
+  const GinDevCommView* v = R.view;
+  gin::Gin gin(v, 0);
+  const uint32_t n = v->world, rank = v->rank;
+  const uint32_t E = L.E, K = L.K, T = L.T, H = L.H, e_local = L.e_local;
+  const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t dmsg = 2ull * H + 16;
+  const uint32_t payload = 2u * H, parts = L.parts;
+  const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
+
+  __shared__ uint32_t hist_all[kMaxExperts], run[kMaxExperts], prefix_e[kMaxExperts];
+  __shared__ int is_last;
+  extern __shared__ __align__(128) char dsm[];
+  TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
+  char* stage = dsm + sizeof(TmaSmem) * kTmaWarps + (size_t)warp * kTmaStages * chunk;
+  uint32_t* slots = reinterpret_cast<uint32_t*>(dsm + sizeof(TmaSmem) * kTmaWarps + (size_t)kTmaWarps * kTmaStages * chunk);
+
+  for (uint32_t e = tid; e < E; e += kTmaThreads) {
+    hist_all[e] = 0;
+    run[e] = 0;
+  }
+  if (lane == 0) {
+    for (int s = 0; s < kTmaStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
+    gin::tma::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t TK = T * K, pre_end = t0 * K;
+  for (uint32_t j = tid; j < TK; j += kTmaThreads) {
+    const uint32_t e = (uint32_t)R.idx[j];
+    atomicAdd(&hist_all[e], 1u);
+    if (j < pre_end) atomicAdd(&run[e], 1u);
+  }
+  __syncthreads();
+  if (L.layout == 1) {
+    for (uint32_t d = tid; d < n; d += kTmaThreads) {
+      uint32_t acc = 0;
+      for (uint32_t e = d * e_local; e < (d + 1) * e_local; ++e) {
+        prefix_e[e] = acc;
+        acc += hist_all[e];
+      }
+    }
+  }
+  if (warp == 0) {
+    for (uint32_t t = t0; t < t1; ++t) {
+      if (lane < K) {
+        const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
+        const uint32_t s = run[e];
+        run[e] = s + 1;
+        slots[(t - t0) * K + lane] = s;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  // Phase B: per-warp TMA pipeline over (token, chunk) items of this CTA.
+  char* const* bases = v->win[L.win_dispatch].base;
+  const uint32_t items = (t1 - t0) * parts;
+  const char* x = reinterpret_cast<const char*>(R.x);
+  auto issue_load = [&](int s, uint32_t item) {
+    const uint32_t t = t0 + item / parts, p = item % parts;
+    const uint32_t len = tma_chunk_len(payload, chunk, p);
+    gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len);
+    gin::tma::load(stage + (size_t)s * chunk, x + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      const uint32_t item = warp + s * kTmaWarps;
+      if (item < items) issue_load(s, item);
+    }
+  }
+  for (uint32_t j = 0;; ++j) {
+    const uint32_t item = warp + j * kTmaWarps;
+    if (item >= items) break;
+    const uint32_t t = t0 + item / parts, p = item % parts;
+    const int s = (int)(j % kTmaStages);
+    if (lane < K) {
+      const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
+      const uint32_t dst = e / e_local, e_loc = e % e_local;
+      const uint32_t slot = slots[(t - t0) * K + lane];
+      const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
+                                         : ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
+      char* d = bases[dst] + off;
+      ctl->dptr[lane] = d;
+      if (p == 0) gin::st_v4(d + payload, make_uint4(rank, t, lane, lane + 1));  // meta
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t len = tma_chunk_len(payload, chunk, p);
+      gin::tma::mbar_wait(&ctl->bar[s], (j / kTmaStages) & 1);
+      for (uint32_t k = 0; k < K; ++k) gin::tma::store(ctl->dptr[k] + (uint64_t)p * chunk, stage + (size_t)s * chunk, len);
+      gin::tma::commit();
+      // Refill the stage of the PREVIOUS item: its stores were committed one
+      // iteration ago, so their shared-memory reads overlapped this wait.
+      if (j >= 1) {
+        gin::tma::wait_read<1>();
+        const uint32_t nxt = item - kTmaWarps + kTmaStages * kTmaWarps;
+        if (nxt < items) issue_load((int)((j - 1) % kTmaStages), nxt);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    gin::tma::wait_all();
+    gin::tma::fence_proxy_async_global();
+  }
+
+  // Phase C/D exactly as the LSU kernel.
+  __syncthreads();
+  if (tid == 0) {
+    gin::fence_acq_rel_sys();
+    const unsigned prev = atomicAdd(R.ws + 0, 1u);
+    is_last = (prev + 1 == (unsigned)(R.iteration * G));
+    if (is_last) gin::fence_acq_rel_sys();
+  }
+  __syncthreads();
+  if (is_last) {
+    uint32_t* const* cbase = reinterpret_cast<uint32_t* const*>(v->win[L.win_counts].base);
+    for (uint32_t e = tid; e < E; e += kTmaThreads) {
+      const uint32_t dst = e / e_local, e_loc = e % e_local;
+      gin::st_relaxed_sys32(cbase[dst] + (uint64_t)e_loc * n + rank, hist_all[e]);
+      gin.release_signal_raw(dst, e_loc, (1ull << 32) + hist_all[e]);
+    }
+  }
+  if (tid == 0) {
+    const uint64_t want = R.iteration * ((uint64_t)n << 32);
+    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(e_loc, want);
+  }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kTmaThreads, 1) moe_combine_tma_kernel(MoeLaunch L, uint32_t chunk) {
+  const MoeRankArgs& R = L.r[blockIdx.y];
+  const GinDevCommView* v = R.view;
+  gin::Gin gin(v, 0);
+  const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
+  const uint32_t K = L.K, T = L.T, H = L.H, e_local = L.e_local;
+  const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t dmsg = 2ull * H + 16, cmsg = 2ull * H;
+  const uint32_t payload = 2u * H, parts = L.parts;
+
+  __shared__ uint32_t cnt[kMaxExperts], pair_start[kMaxExperts + 1], src_prefix[kMaxExperts];
+  __shared__ uint32_t warp_tot[kMoeWarps];
+  __shared__ uint32_t total_msgs;
+  __shared__ int is_last;
+  extern __shared__ __align__(128) char dsm[];
+  TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
+  char* stage = dsm + sizeof(TmaSmem) * kTmaWarps + (size_t)warp * kTmaStages * chunk;
+
+  const uint32_t P = e_local * n;
+  const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
+  for (uint32_t i = tid; i < P; i += kTmaThreads) {
+    const uint32_t c = gin::ld_acquire_sys32(counts + i);
+    cnt[i] = c;
+    pair_start[i] = c;
+  }
+  if (tid < kMoeWarps) warp_tot[tid] = 0;
+  if (lane == 0) {
+    for (int s = 0; s < kTmaStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
+    gin::tma::fence_mbar_init();
+  }
+  __syncthreads();
+  if (L.layout == 1) {
+    for (uint32_t s = tid; s < n; s += kTmaThreads) {
+      uint32_t acc = 0;
+      for (uint32_t e = 0; e < e_local; ++e) {
+        src_prefix[e * n + s] = acc;
+        acc += cnt[e * n + s];
+      }
+    }
+  }
+  // exclusive scan of P <= 1024 entries with 256 threads (4 per thread)
+  {
+    const uint32_t per = (P + kTmaThreads - 1) / kTmaThreads;
+    const uint32_t lo = tid * per, hi = min(lo + per, P);
+    uint32_t local = 0;
+    for (uint32_t i = lo; i < hi; ++i) local += pair_start[i];
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc = 0;
+      for (int w = 0; w < kTmaWarps; ++w) {
+        const uint32_t x = warp_tot[w];
+        warp_tot[w] = acc;
+        acc += x;
+      }
+      total_msgs = acc;
+    }
+    __syncthreads();
+    uint32_t r = warp_tot[warp] + incl - local;
+    for (uint32_t i = lo; i < hi; ++i) {
+      const uint32_t d = pair_start[i];
+      pair_start[i] = r;
+      r += d;
+    }
+    __syncthreads();
+    if (tid == 0) pair_start[P] = total_msgs;
+    __syncthreads();
+  }
+
+  const char* recv = v->win[L.win_dispatch].base[rank];
+  char* const* cbases = v->win[L.win_combine].base;
+  const uint64_t items = (uint64_t)total_msgs * parts;
+  const uint64_t gw = (uint64_t)b * kTmaWarps + warp, stride = (uint64_t)G * kTmaWarps;
+  auto locate = [&](uint32_t m, uint32_t& lo_pair) -> const char* {
+    uint32_t lo = 0, hi = P;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (pair_start[mid] <= m) lo = mid; else hi = mid;
+    }
+    lo_pair = lo;
+    const uint32_t e_loc = lo / n, src = lo % n, slot = m - pair_start[lo];
+    const uint64_t moff = L.layout == 0 ? (((uint64_t)e_loc * n + src) * T + slot) * dmsg
+                                        : ((uint64_t)src * T * K + src_prefix[lo] + slot) * dmsg;
+    return recv + moff;
+  };
+  auto issue_load = [&](int s, uint64_t it) {
+    uint32_t pr;
+    const char* msg = locate((uint32_t)(it / parts), pr);
+    const uint32_t p = (uint32_t)(it % parts);
+    const uint32_t len = tma_chunk_len(payload, chunk, p);
+    gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len);
+    gin::tma::load(stage + (size_t)s * chunk, msg + (uint64_t)p * chunk, len, &ctl->bar[s]);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      const uint64_t it = gw + s * stride;
+      if (it < items) issue_load(s, it);
+    }
+  }
+  for (uint64_t j = 0;; ++j) {
+    const uint64_t it = gw + j * stride;
+    if (it >= items) break;
+    const int s = (int)(j % kTmaStages);
+    const uint32_t m = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
+    uint32_t pr;
+    const char* msg = locate(m, pr);
+    const uint32_t e = rank * e_local + pr / n, src = pr % n;
+    const uint4 meta = *reinterpret_cast<const uint4*>(msg + payload);
+    const uint32_t token = meta.y, k = meta.z;
+    const uint32_t len = tma_chunk_len(payload, chunk, p);
+    gin::tma::mbar_wait(&ctl->bar[s], (uint32_t)((j / kTmaStages) & 1));
+    uint4* buf = reinterpret_cast<uint4*>(stage + (size_t)s * chunk);
+    for (uint32_t i = lane; i < len / 16; i += 32) buf[i] = transform_vec(buf[i], L.mode, e);
+    gin::tma::fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) {
+      gin::tma::store(cbases[src] + ((uint64_t)token * K + k) * cmsg + (uint64_t)p * chunk, buf, len);
+      gin::tma::commit();
+      if (j >= 1) {  // refill the previous item's stage (its store has been reading meanwhile)
+        gin::tma::wait_read<1>();
+        const uint64_t nxt = it - stride + kTmaStages * stride;
+        if (nxt < items) issue_load((int)((j - 1) % kTmaStages), nxt);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    gin::tma::wait_all();
+    gin::tma::fence_proxy_async_global();
+  }
+
+  __syncthreads();
+  if (tid == 0) {
+    gin::fence_acq_rel_sys();
+    const unsigned prev = atomicAdd(R.ws + 1, 1u);
+    is_last = (prev + 1 == (unsigned)(R.iteration * G));
+    if (is_last) gin::fence_acq_rel_sys();
+  }
+  __syncthreads();
+  if (is_last) {
+    for (uint32_t sc = tid; sc < n * n_ctx; sc += kTmaThreads) {
+      const uint32_t src = sc / n_ctx, ctx = sc % n_ctx;
+      uint32_t c = 0;
+      for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
+        if ((rank * e_local + e_loc) % n_ctx == ctx) c += cnt[e_loc * n + src];
+      if (c) gin.release_signal_raw(src, e_local, c);
+    }
+  }
+}
+
+// Source side of the combine, split off the TMA send kernel so it runs at
+// full occupancy (32 warps/SM; the TMA kernel holds 1 CTA/SM for its staging
+// buffers): acquire the combine flag (>= T*K per iteration, harness_moe.cpp:
+// 227) then the top-k weighted reduction, two 16-byte vectors per thread with
+// all 2K loads in flight before any use.  No CTA waits on another CTA of
+// this launch, so it needs no co-residency.
+template <int KMAX>
+__global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeLaunch L, uint32_t /*chunk*/) {
+  const MoeRankArgs& R = L.r[blockIdx.y];
+  const GinDevCommView* v = R.view;
+  gin::Gin gin(v, 0);
+  const uint32_t rank = v->rank;
+  const uint32_t K = L.K, T = L.T, H = L.H, e_local = L.e_local;
+  const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const uint64_t cmsg = 2ull * H;
+  const uint32_t payload = 2u * H;
+  if (tid == 0) gin.wait_ge_signal(e_local, R.iteration * (uint64_t)T * K);
+  __syncthreads();
+  const char* crecv = v->win[L.win_combine].base[rank];
+  const uint32_t nvec = payload / 16;
+  const uint64_t ritems = (uint64_t)T * nvec, rstride = (uint64_t)G * kMoeThreads;
+  for (uint64_t q = (uint64_t)b * kMoeThreads + tid; q < ritems; q += rstride) {
+    const uint32_t t = (uint32_t)(q / nvec), i = (uint32_t)(q % nvec);
+    uint4 y[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < (int)K) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+    gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
+               reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
+  }
+}
+
 // ------------------------------------------------------------------ synthetic inputs
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -553,7 +941,7 @@ using namespace ginsim_b200;
 struct ginsim_cuda_moe_s {
   Comm* comm = nullptr;
   ginsim_cuda_moe_config cfg{};
-  uint32_t e_local = 0, parts = 4, G = 0;
+  uint32_t e_local = 0, parts = 4, G = 0, Gc = 0, Gr = 0, chunk = 0;
   uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0;
   void* buf_dispatch = nullptr;
   void* buf_counts = nullptr;
@@ -669,56 +1057,134 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
 // Grid and work split, fixed at the first launch of a handle (the arrival
 // counters count CTAs per iteration, so G never changes afterwards).  Every
 // CTA must be co-resident: CTAs spin on signals other CTAs release.
+// Engines: 1 = LSU everywhere; 2 = TMA dispatch + TMA combine-send + reduce
+// kernel; 3 = TMA dispatch + LSU combine; 0 = auto (2 when aligned).
+struct MoeKernels {
+  const void* dispatch;
+  const void* combine;   // cooperative: expert side (+ fused reduce when reduce == nullptr)
+  const void* reduce;    // optional separate source-side reduction
+  int threads;           // of dispatch / combine
+  bool tma_dispatch, tma_combine;
+};
+
+static uint32_t engine_of(const ginsim_cuda_moe_t m) {
+  const bool aligned = (2u * m->cfg.hidden) % 16u == 0;
+  if (!aligned) return 1;
+  return m->cfg.engine == 0 ? 2 : m->cfg.engine;
+}
+static bool use_tma(const ginsim_cuda_moe_t m) { return engine_of(m) != 1; }
+
+static MoeKernels kernels_of(const ginsim_cuda_moe_t m) {
+  const bool k8 = m->cfg.top_k <= 8;
+  const uint32_t e = engine_of(m);
+  MoeKernels k{};
+  if (e == 1) {
+    k.dispatch = k8 ? (const void*)moe_dispatch_kernel<8> : (const void*)moe_dispatch_kernel<32>;
+    k.combine = (const void*)moe_combine_kernel;
+    k.threads = kMoeThreads;
+    return k;
+  }
+  k.dispatch = k8 ? (const void*)moe_dispatch_tma_kernel<8> : (const void*)moe_dispatch_tma_kernel<32>;
+  k.threads = kTmaThreads;
+  k.tma_dispatch = true;
+  if (e == 3) {
+    k.combine = (const void*)moe_combine_kernel;
+  } else {
+    k.combine = k8 ? (const void*)moe_combine_tma_kernel<8> : (const void*)moe_combine_tma_kernel<32>;
+    k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8> : (const void*)moe_combine_reduce_kernel<32>;
+    k.tma_combine = true;
+  }
+  return k;
+}
+
+static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
+  const size_t slots = (size_t)((m->cfg.tokens + G - 1) / G + 1) * m->cfg.top_k * 4;
+  if (!kernels_of(m).tma_dispatch) return slots;
+  return sizeof(TmaSmem) * kTmaWarps + (size_t)kTmaWarps * kTmaStages * m->chunk + slots;
+}
+static size_t combine_smem(const ginsim_cuda_moe_t m) {
+  if (!kernels_of(m).tma_combine) return 0;
+  return sizeof(TmaSmem) * kTmaWarps + (size_t)kTmaWarps * kTmaStages * m->chunk;
+}
+static int combine_threads(const MoeKernels& k) { return k.tma_combine ? kTmaThreads : kMoeThreads; }
+
 static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   ginsim_cuda_moe_t m = moes[0];
   if (m->G) return;
-  const void* kd = m->cfg.top_k <= 8 ? (const void*)moe_dispatch_kernel<8> : (const void*)moe_dispatch_kernel<32>;
-  GIN_CUDA(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  const size_t guess = (size_t)((m->cfg.tokens + 147) / 148 + 1) * m->cfg.top_k * 4;
-  const int cap_d = max_coresident_ctas(kd, kMoeThreads, guess, m->comm->device);
-  const int cap_c = max_coresident_ctas((const void*)moe_combine_kernel, kMoeThreads, 0, m->comm->device);
-  int cap = std::min(cap_d, cap_c) / (int)n;
-  uint32_t G = m->cfg.ctas ? std::min<uint32_t>(m->cfg.ctas, (uint32_t)cap) : (uint32_t)cap;
-  if (G > m->cfg.tokens) G = m->cfg.tokens;
-  if (G < 1) fail(GINSIM_E_USAGE, "kernel does not fit on the device");
-  const uint32_t nvec = (2u * m->cfg.hidden) % 16u == 0 ? 2u * m->cfg.hidden / 16u : 0u;
-  uint32_t parts = 1;
-  if (nvec >= 32) {
-    const uint32_t want = (2u * G * kMoeWarps + m->cfg.tokens - 1) / m->cfg.tokens;
-    parts = std::max(1u, std::min(want, nvec / 32u));
+  const MoeKernels k = kernels_of(m);
+  const uint32_t payload = 2u * m->cfg.hidden;
+  uint32_t parts = 1, chunk = 0;
+  if (use_tma(m)) {
+    parts = (payload + 8191) / 8192;
+    chunk = ((payload + parts - 1) / parts + 15) / 16 * 16;
+    m->chunk = chunk;
+  }
+  int sms = 0;
+  GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->comm->device));
+  const uint32_t G0 = std::max<uint32_t>(1, (uint32_t)sms / n);
+  const size_t ds = dispatch_smem(m, G0), cs = combine_smem(m);
+  GIN_CUDA(cudaFuncSetAttribute(k.dispatch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(ds, 1)));
+  GIN_CUDA(cudaFuncSetAttribute(k.combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(cs, 1)));
+  const int cap_d = max_coresident_ctas(k.dispatch, k.threads, ds, m->comm->device) / (int)n;
+  const int cap_c = max_coresident_ctas(k.combine, combine_threads(k), cs, m->comm->device) / (int)n;
+  auto pick = [&](int cap) {
+    uint32_t G = m->cfg.ctas ? std::min<uint32_t>(m->cfg.ctas, (uint32_t)cap) : (uint32_t)cap;
+    if (G > m->cfg.tokens) G = m->cfg.tokens;
+    if (G < 1) fail(GINSIM_E_USAGE, "kernel does not fit on the device");
+    return G;
+  };
+  const uint32_t Gd = pick(cap_d), Gc = pick(cap_c);
+  uint32_t Gr = 0;
+  if (k.reduce) Gr = std::max<uint32_t>(1, (uint32_t)max_coresident_ctas(k.reduce, kMoeThreads, 0, m->comm->device) / n);
+  if (!use_tma(m) || !k.tma_combine) {
+    // LSU combine: (message, part) work items sized to the warp count
+    const uint32_t nvec = payload % 16u == 0 ? payload / 16u : 0u;
+    if (nvec >= 32 && !k.tma_dispatch) {
+      const uint32_t want = (2u * Gd * kMoeWarps + m->cfg.tokens - 1) / m->cfg.tokens;
+      parts = std::max(1u, std::min(want, nvec / 32u));
+    }
   }
   for (uint32_t i = 0; i < n; ++i) {
-    moes[i]->G = G;
+    moes[i]->G = Gd;
+    moes[i]->Gc = Gc;
+    moes[i]->Gr = Gr;
     moes[i]->parts = parts;
+    moes[i]->chunk = chunk;
   }
 }
 
-static void launch_coop(const void* kernel, uint32_t G, uint32_t n, size_t smem, MoeLaunch& L, cudaStream_t s) {
-  void* args[] = {&L};
-  GIN_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(G, n), dim3(kMoeThreads), args, smem, s));
+static void launch_coop(const void* kernel, uint32_t G, uint32_t n, int threads, size_t smem, void** args,
+                        cudaStream_t s) {
+  GIN_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(G, n), dim3(threads), args, smem, s));
+}
+
+static void check_launch_set(const ginsim_cuda_moe_t* moes, uint32_t n) {
+  if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "launch needs 1..8 ranks");
+  for (uint32_t i = 1; i < n; ++i)
+    if (moes[i]->comm->device != moes[0]->comm->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
 }
 
 int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* x,
                              const int32_t* const* idx, void* stream) {
   GIN_API_BEGIN
-  if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "launch needs 1..8 ranks");
-  for (uint32_t i = 1; i < n; ++i)
-    if (moes[i]->comm->device != moes[0]->comm->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
+  check_launch_set(moes, n);
   MoeLaunch L = make_launch(moes, n);
   DeviceGuard g(moes[0]->comm->device);
-  const void* kernel = L.K <= 8 ? (const void*)moe_dispatch_kernel<8> : (const void*)moe_dispatch_kernel<32>;
   plan(moes, n);
+  const MoeKernels k = kernels_of(moes[0]);
   L.parts = moes[0]->parts;
   const uint32_t G = moes[0]->G;
-  const size_t smem = (size_t)((L.T + G - 1) / G + 1) * L.K * 4;
-  if (smem > 160 * 1024) fail(GINSIM_E_USAGE, "too many tokens per CTA for the slot table");
+  uint32_t chunk = moes[0]->chunk;
+  const size_t smem = dispatch_smem(moes[0], G);
+  if (smem > 227 * 1024) fail(GINSIM_E_USAGE, "too many tokens per CTA for the slot table");
   for (uint32_t i = 0; i < n; ++i) {
     moes[i]->iteration_dispatch += 1;
     L.r[i].x = static_cast<const uint16_t*>(x[i]);
     L.r[i].idx = idx[i];
     L.r[i].iteration = moes[i]->iteration_dispatch;
   }
-  launch_coop(kernel, G, n, smem, L, (cudaStream_t)stream);
+  void* args[] = {&L, &chunk};
+  launch_coop(k.dispatch, G, n, k.threads, smem, args, (cudaStream_t)stream);
   moes[0]->last_ctas = G * n;
   GIN_API_END
 }
@@ -726,15 +1192,13 @@ int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const vo
 int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* weights, void* const* out,
                             void* stream) {
   GIN_API_BEGIN
-  if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "launch needs 1..8 ranks");
-  for (uint32_t i = 1; i < n; ++i)
-    if (moes[i]->comm->device != moes[0]->comm->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
+  check_launch_set(moes, n);
   MoeLaunch L = make_launch(moes, n);
   DeviceGuard g(moes[0]->comm->device);
-  const void* kernel = (const void*)moe_combine_kernel;
   plan(moes, n);
+  const MoeKernels k = kernels_of(moes[0]);
   L.parts = moes[0]->parts;
-  const uint32_t G = moes[0]->G;
+  uint32_t chunk = moes[0]->chunk;
   for (uint32_t i = 0; i < n; ++i) {
     moes[i]->iteration_combine += 1;
     if (moes[i]->iteration_combine != moes[i]->iteration_dispatch)
@@ -743,14 +1207,19 @@ int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const voi
     L.r[i].out = static_cast<uint16_t*>(out[i]);
     L.r[i].iteration = moes[i]->iteration_combine;
   }
-  launch_coop(kernel, G, n, 0, L, (cudaStream_t)stream);
-  moes[0]->last_ctas = G * n;
+  void* args[] = {&L, &chunk};
+  const uint32_t Gc = moes[0]->Gc;
+  launch_coop(k.combine, Gc, n, combine_threads(k), combine_smem(moes[0]), args, (cudaStream_t)stream);
+  if (k.reduce) {
+    GIN_CUDA(cudaLaunchKernel(k.reduce, dim3(moes[0]->Gr, n), dim3(kMoeThreads), args, 0, (cudaStream_t)stream));
+  }
+  moes[0]->last_ctas = Gc * n;
   GIN_API_END
 }
 
 int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t* threads) {
   if (ctas) *ctas = moe->last_ctas;
-  if (threads) *threads = kMoeThreads;
+  if (threads) *threads = (uint32_t)kernels_of(moe).threads;
   return GINSIM_OK;
 }
 

@@ -591,6 +591,11 @@ int ginsim_cuda_comm_info(ginsim_cuda_comm_t comm, uint32_t* rank, uint32_t* wor
   GIN_API_END
 }
 
+int ginsim_cuda_comm_config(ginsim_cuda_comm_t comm, ginsim_cuda_config* out) {
+  *out = comm->impl.cfg;
+  return GINSIM_OK;
+}
+
 int ginsim_cuda_devcomm_view(ginsim_cuda_comm_t comm, const void** view) {
   *view = comm->impl.dev_view;
   return GINSIM_OK;
