@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--engine", type=int, default=0, help="0 = auto (TMA), 1 = LSU stores, 2 = TMA")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip the LL and ping-pong sub-measurements")
     return p.parse_args()
 
 
@@ -148,6 +149,74 @@ def reference_main(args):
     print(json.dumps(line))
 
 
+# --------------------------------------------------------------------- secondary configs
+def measure_ll(G, comm, rank, world, dist, torch, dev, stream, steps=50):
+    """BASELINE configs[2]: LL dispatch/combine, 128 tokens/rank, hidden 7168,
+    top-8 of 256, bf16 — per-phase device time (max over ranks), µs."""
+    T, H, K, E = 128, HIDDEN, TOPK, EXPERTS
+    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 1, 0, 0, 0))
+    x = torch.empty(T * H, dtype=torch.int16, device=dev)
+    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
+    w = torch.empty(T * K, dtype=torch.float32, device=dev)
+    out = torch.empty(T * H, dtype=torch.int16, device=dev)
+    moe.generate(1, rank, x, idx, w, stream=stream)
+    for _ in range(5):
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for i in range(steps):
+        ev[i][0].record(stream)
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        ev[i][1].record(stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    comm.check_device()
+    d = sorted(e[0].elapsed_time(e[1]) for e in ev)
+    c = sorted(e[1].elapsed_time(e[2]) for e in ev)
+    t = torch.tensor([d[len(d) // 2], c[len(c) // 2]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dmsg, cmsg = 2 * H + 16, 2 * H
+    disp_us, comb_us = t[0].item() * 1e3, t[1].item() * 1e3
+    return {"workload": f"DeepEP LL dispatch/combine, {T} tokens/rank, hidden {H}, top-{K} of {E}, bf16, {world} GPU(s)",
+            "dispatch_us_p50": disp_us, "combine_us_p50": comb_us,
+            "dispatch_GBps_per_gpu": T * K * dmsg / (disp_us * 1e-6) / 1e9,
+            "combine_GBps_per_gpu": T * K * cmsg / (comb_us * 1e-6) / 1e9,
+            "paper_h100_reference_us": {"dispatch": 40.62, "combine": 69.0}}
+
+
+def measure_pingpong(G, comm, rank, world, dist, torch, dev):
+    """BASELINE configs[0] on hardware: put+SignalInc ping-pong between ranks 0
+    and 1 over NVLink (harness_bench.cpp:47-90), 8 B .. 4 MiB, %globaltimer
+    inside one persistent kernel; zero-byte put+signal = the raw release/
+    acquire round-trip floor."""
+    import ctypes  # noqa: F401
+    import numpy as np
+    size_max = 4 << 20
+    sb, rb = comm.mem_alloc(size_max), comm.mem_alloc(size_max)
+    ws, wr = comm.window_register(sb, size_max), comm.window_register(rb, size_max)
+    rtt = torch.zeros(1000, dtype=torch.int64, device=dev)
+    rows = []
+    for sz in [0, 8, 64, 512, 4096, 32768, 262144, 1 << 20, 4 << 20]:
+        iters = 1000 if sz <= 65536 else 200
+        if rank in (0, 1):
+            G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, iters, 100, 0, 512,
+                                                 rtt.data_ptr(), None))
+        dist.barrier()
+        if rank == 0:
+            t = np.sort(rtt[:iters].cpu().numpy())
+            p50 = int(t[iters // 2])
+            rows.append({"size_bytes": sz, "iters": iters, "p50_ns": p50, "p99_ns": int(t[min(iters - 1, iters * 99 // 100)]),
+                         "mean_ns": float(t.mean()), "one_way_ns": p50 / 2,
+                         "GBps_per_direction": (2 * sz / (p50 * 1e-9) / 1e9) if sz else None})
+    return {"rows": rows, "target_us": 5.0, "floor_ns": rows[0]["p50_ns"] if rows else None,
+            "csv_schema": "size_bytes,iters,p50_ns,p99_ns,mean_ns,backend=direct,transport=nvlink"}
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -238,6 +307,10 @@ def main():
     agg_bytes = step_bytes_rank * world
     value = agg_bytes / (ms_per_step * 1e-3) / 1e9
 
+    # --- secondary configs on the same ranks: LL latency and put+signal RTT ---
+    ll = None if args.no_extras else measure_ll(G, comm, rank, world, dist, torch, dev, stream)
+    pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm, rank, world, dist, torch, dev)
+
     # --- e2e: host buffers through the public API, copies inside the region ---
     e2e = None
     if not args.no_e2e:
@@ -312,8 +385,12 @@ def main():
         "roofline": {"bound": "hbm", "kernel": f"moe_{dom}_kernel", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": dom_bytes},
-        "clocks": clk, "gpu_launches": 2 * args.steps,
+        "clocks": clk,
+        # dispatch + combine-send + reduce kernels per step (2 with the LSU engines)
+        "gpu_launches": (3 if args.engine in (0, 2) else 2) * args.steps,
         "e2e": e2e,
+        "ll": ll,
+        "pingpong": pp,
     }
     if world > 1:
         rem_disp = remote_msgs * dmsg

@@ -51,7 +51,7 @@ struct MoeRankArgs {
 
 struct MoeLaunch {
   MoeRankArgs r[GIN_MAX_RANKS];
-  uint32_t E, K, T, H, mode, layout, e_local, parts;
+  uint32_t E, K, T, H, mode, layout, e_local, parts, cparts;
   uint32_t win_dispatch, win_counts, win_combine, pad;
 };
 
@@ -485,6 +485,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
 // that of stores in flight.  Used whenever messages are 16-byte aligned.
 constexpr int kTmaThreads = 256;
 constexpr int kTmaWarps = kTmaThreads / 32;
+constexpr int kCmbThreads = 512;
+constexpr int kCmbWarps = kCmbThreads / 32;
 constexpr int kTmaStages = 3;
 
 struct TmaSmem {  // per-warp control block, followed by the staging buffers
@@ -674,7 +676,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
 }
 
 template <int KMAX>
-__global__ void __launch_bounds__(kTmaThreads, 1) moe_combine_tma_kernel(MoeLaunch L, uint32_t chunk) {
+__global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaunch L, uint32_t chunk) {
+  // The transform pass keeps the SM busy between TMA waits, so this kernel
+  // runs 16 warps with smaller (<= 4 KiB) chunks instead of the dispatch's 8.
+  constexpr int kTmaThreads = kCmbThreads;
+  constexpr int kTmaWarps = kCmbThreads / 32;
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
@@ -682,7 +688,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_combine_tma_kernel(MoeLaun
   const uint32_t K = L.K, T = L.T, H = L.H, e_local = L.e_local;
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t dmsg = 2ull * H + 16, cmsg = 2ull * H;
-  const uint32_t payload = 2u * H, parts = L.parts;
+  const uint32_t payload = 2u * H, parts = L.cparts;
 
   __shared__ uint32_t cnt[kMaxExperts], pair_start[kMaxExperts + 1], src_prefix[kMaxExperts];
   __shared__ uint32_t warp_tot[kMoeWarps];
@@ -792,7 +798,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_combine_tma_kernel(MoeLaun
     const uint32_t len = tma_chunk_len(payload, chunk, p);
     gin::tma::mbar_wait(&ctl->bar[s], (uint32_t)((j / kTmaStages) & 1));
     uint4* buf = reinterpret_cast<uint4*>(stage + (size_t)s * chunk);
-    for (uint32_t i = lane; i < len / 16; i += 32) buf[i] = transform_vec(buf[i], L.mode, e);
+    {
+      const uint32_t nv = len / 16;
+      uint32_t i = lane;
+      for (; i + 96 < nv; i += 128) {  // 4 independent vectors per lane in flight
+        const uint4 a = buf[i], c = buf[i + 32], d = buf[i + 64], f = buf[i + 96];
+        buf[i] = transform_vec(a, L.mode, e);
+        buf[i + 32] = transform_vec(c, L.mode, e);
+        buf[i + 64] = transform_vec(d, L.mode, e);
+        buf[i + 96] = transform_vec(f, L.mode, e);
+      }
+      for (; i < nv; i += 32) buf[i] = transform_vec(buf[i], L.mode, e);
+    }
     gin::tma::fence_proxy_async_shared();
     __syncwarp();
     if (lane == 0) {
@@ -941,7 +958,7 @@ using namespace ginsim_b200;
 struct ginsim_cuda_moe_s {
   Comm* comm = nullptr;
   ginsim_cuda_moe_config cfg{};
-  uint32_t e_local = 0, parts = 4, G = 0, Gc = 0, Gr = 0, chunk = 0;
+  uint32_t e_local = 0, parts = 4, G = 0, Gc = 0, Gr = 0, chunk = 0, cparts = 1, cchunk = 0;
   uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0;
   void* buf_dispatch = nullptr;
   void* buf_counts = nullptr;
@@ -1104,27 +1121,37 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
 }
 static size_t combine_smem(const ginsim_cuda_moe_t m) {
   if (!kernels_of(m).tma_combine) return 0;
-  return sizeof(TmaSmem) * kTmaWarps + (size_t)kTmaWarps * kTmaStages * m->chunk;
+  return sizeof(TmaSmem) * kCmbWarps + (size_t)kCmbWarps * kTmaStages * m->cchunk;
 }
-static int combine_threads(const MoeKernels& k) { return k.tma_combine ? kTmaThreads : kMoeThreads; }
+static int combine_threads(const MoeKernels& k) { return k.tma_combine ? kCmbThreads : kMoeThreads; }
 
 static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   ginsim_cuda_moe_t m = moes[0];
   if (m->G) return;
   const MoeKernels k = kernels_of(m);
   const uint32_t payload = 2u * m->cfg.hidden;
-  uint32_t parts = 1, chunk = 0;
+  uint32_t parts = 1, chunk = 0, cparts = 1, cchunk = 0;
   if (use_tma(m)) {
     parts = (payload + 8191) / 8192;
     chunk = ((payload + parts - 1) / parts + 15) / 16 * 16;
     m->chunk = chunk;
+    cparts = (payload + 4095) / 4096;
+    cchunk = ((payload + cparts - 1) / cparts + 15) / 16 * 16;
+    m->cchunk = cchunk;
   }
   int sms = 0;
   GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->comm->device));
   const uint32_t G0 = std::max<uint32_t>(1, (uint32_t)sms / n);
   const size_t ds = dispatch_smem(m, G0), cs = combine_smem(m);
-  GIN_CUDA(cudaFuncSetAttribute(k.dispatch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(ds, 1)));
-  GIN_CUDA(cudaFuncSetAttribute(k.combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(cs, 1)));
+  // Opt every kernel into the full shared-memory budget once; the per-launch
+  // dynamic size (which differs between handles) stays below it.
+  for (const void* f : {k.dispatch, k.combine}) {
+    cudaFuncAttributes fa{};
+    GIN_CUDA(cudaFuncGetAttributes(&fa, f));
+    int optin = 0;
+    GIN_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->comm->device));
+    GIN_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+  }
   const int cap_d = max_coresident_ctas(k.dispatch, k.threads, ds, m->comm->device) / (int)n;
   const int cap_c = max_coresident_ctas(k.combine, combine_threads(k), cs, m->comm->device) / (int)n;
   auto pick = [&](int cap) {
@@ -1150,6 +1177,8 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
     moes[i]->Gr = Gr;
     moes[i]->parts = parts;
     moes[i]->chunk = chunk;
+    moes[i]->cparts = cparts;
+    moes[i]->cchunk = cchunk;
   }
 }
 
@@ -1198,7 +1227,8 @@ int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const voi
   plan(moes, n);
   const MoeKernels k = kernels_of(moes[0]);
   L.parts = moes[0]->parts;
-  uint32_t chunk = moes[0]->chunk;
+  L.cparts = k.tma_combine ? moes[0]->cparts : moes[0]->parts;
+  uint32_t chunk = k.tma_combine ? moes[0]->cchunk : moes[0]->chunk;
   for (uint32_t i = 0; i < n; ++i) {
     moes[i]->iteration_combine += 1;
     if (moes[i]->iteration_combine != moes[i]->iteration_dispatch)

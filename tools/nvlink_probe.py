@@ -32,6 +32,21 @@ def main():
                 out["rows"].append({"engine": ["lsu", "tma"][engine], "ctas": ctas or 148,
                                     "target": "local" if peer == 0 else "peer", "ms": ms.value,
                                     "GBps": size / (ms.value * 1e-3) / 1e9})
+    # HBM direction probes: write-only (fill) and read-only (sum) streams, 4 GiB
+    buf = torch.empty(1 << 31, dtype=torch.int16, device="cuda:0")
+    for name, fn, nbytes in [("write_only_fill", lambda: buf.fill_(3), buf.numel() * 2),
+                             ("read_only_sum", lambda: buf.sum(dtype=torch.int32), buf.numel() * 2),
+                             ("copy_rw", lambda: buf[: buf.numel() // 2].copy_(buf[buf.numel() // 2:]), buf.numel() * 2)]:
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(10):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / 10
+        out["rows"].append({"engine": "torch", "target": name, "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9})
     print(json.dumps(out))
 
 
