@@ -355,12 +355,13 @@ def main():
 
     peak, peak_kind = load_peaks()
     # dominant kernel and its algorithmic HBM bytes per launch
-    disp_hbm = T * H * 2 + T * K * 4 + T * K * dmsg             # read rows + idx, write messages (local HBM side)
-    comb_hbm = 2 * T * K * dmsg + T * K * cmsg + T * H * 2      # read msgs, write/read combine rows, write out
-    if world > 1:
-        # remote writes land in the peers' HBM; the local HBM sees this rank's
-        # reads plus the messages peers write into it (symmetric on average)
-        pass
+    # Per-launch algorithmic HBM bytes.  Symmetric traffic: every message this
+    # rank writes lands in some rank's HBM and, on average, as many land here.
+    #   dispatch: read T rows (2H) + idx, write T*K messages (dmsg)
+    #   combine (send + reduce kernels): read T*K messages, write T*K combine
+    #   rows (cmsg), read them back, write T output rows (+ weights)
+    disp_hbm = T * H * 2 + T * K * 4 + T * K * dmsg
+    comb_hbm = T * K * dmsg + 2 * T * K * cmsg + T * H * 2 + T * K * 4
     dom = "dispatch" if d_mean >= c_mean else "combine"
     dom_ms = max(d_mean, c_mean)
     dom_bytes = disp_hbm if dom == "dispatch" else comb_hbm
@@ -368,7 +369,8 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+            tr = json.load(f)
+        traffic = tr.get("dispatch") if dom == "dispatch" else tr.get("combine", 0) + tr.get("reduce", 0)
     except Exception:  # noqa: BLE001
         pass
     line = {

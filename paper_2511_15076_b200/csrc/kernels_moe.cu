@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "gin_device.cuh"
@@ -41,7 +42,8 @@ constexpr uint32_t kMaxExperts = 1024;
 
 struct MoeRankArgs {
   const GinDevCommView* view;
-  unsigned int* ws;           // per-moe arrival counters [0] dispatch [1] combine
+  unsigned int* ws;           // per-moe arrival counters [0] dispatch [1] combine [2] slot barrier
+  uint32_t* slot_g;           // [T][K] slot table published for interleaved dispatch (or null)
   const uint16_t* x;          // [T][H]
   const int32_t* idx;         // [T][K]
   const void* weights;        // [T][K] u16 (mode 0) / f32 (mode 1)
@@ -52,7 +54,7 @@ struct MoeRankArgs {
 struct MoeLaunch {
   MoeRankArgs r[GIN_MAX_RANKS];
   uint32_t E, K, T, H, mode, layout, e_local, parts, cparts;
-  uint32_t win_dispatch, win_counts, win_combine, pad;
+  uint32_t win_dispatch, win_counts, win_combine, interleave;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -600,31 +602,55 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   }
   __syncthreads();
 
-  // Phase B: per-warp TMA pipeline over (token, chunk) items of this CTA.
+  // Phase B: per-warp TMA pipeline over (token, chunk) items.  With more
+  // tokens than CTAs the slot numbers are published to a global table and,
+  // after a grid barrier, items are interleaved over EVERY warp of the rank
+  // (item = warp_id + j * total_warps): each warp gets a random mix of local
+  // and remote destinations, so no CTA is left holding a remote-heavy tail.
   char* const* bases = v->win[L.win_dispatch].base;
-  const uint32_t items = (t1 - t0) * parts;
+  const bool global = L.interleave && R.slot_g != nullptr && T > G;
+  if (global) {
+    for (uint32_t q = tid; q < (t1 - t0) * K; q += kTmaThreads) R.slot_g[(uint64_t)t0 * K + q] = slots[q];
+    __syncthreads();
+    if (tid == 0) {
+      gin::fence_acq_rel_gpu();
+      atomicAdd(R.ws + 2, 1u);
+      const unsigned want = (unsigned)(R.iteration * G);
+      while (true) {
+        unsigned cur;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(R.ws + 2) : "memory");
+        if (cur >= want) break;
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+  }
+  const uint32_t items = global ? T * parts : (t1 - t0) * parts;
+  const uint32_t wid = global ? b * kTmaWarps + warp : warp;
+  const uint32_t wstride = global ? G * kTmaWarps : kTmaWarps;
+  const uint32_t tbase = global ? 0 : t0;
   const char* x = reinterpret_cast<const char*>(R.x);
   auto issue_load = [&](int s, uint32_t item) {
-    const uint32_t t = t0 + item / parts, p = item % parts;
+    const uint32_t t = tbase + item / parts, p = item % parts;
     const uint32_t len = tma_chunk_len(payload, chunk, p);
     gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len);
     gin::tma::load(stage + (size_t)s * chunk, x + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
   };
   if (lane == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
-      const uint32_t item = warp + s * kTmaWarps;
+      const uint32_t item = wid + s * wstride;
       if (item < items) issue_load(s, item);
     }
   }
   for (uint32_t j = 0;; ++j) {
-    const uint32_t item = warp + j * kTmaWarps;
+    const uint32_t item = wid + j * wstride;
     if (item >= items) break;
-    const uint32_t t = t0 + item / parts, p = item % parts;
+    const uint32_t t = tbase + item / parts, p = item % parts;
     const int s = (int)(j % kTmaStages);
     if (lane < K) {
       const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
       const uint32_t dst = e / e_local, e_loc = e % e_local;
-      const uint32_t slot = slots[(t - t0) * K + lane];
+      const uint32_t slot = global ? R.slot_g[(uint64_t)t * K + lane] : slots[(t - t0) * K + lane];
       const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
                                          : ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
       char* d = bases[dst] + off;
@@ -641,7 +667,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
       // iteration ago, so their shared-memory reads overlapped this wait.
       if (j >= 1) {
         gin::tma::wait_read<1>();
-        const uint32_t nxt = item - kTmaWarps + kTmaStages * kTmaWarps;
+        const uint32_t nxt = item - wstride + kTmaStages * wstride;
         if (nxt < items) issue_load((int)((j - 1) % kTmaStages), nxt);
       }
     }
@@ -964,6 +990,7 @@ struct ginsim_cuda_moe_s {
   void* buf_counts = nullptr;
   void* buf_combine = nullptr;
   unsigned int* ws = nullptr;
+  uint32_t* slot_g = nullptr;
   uint64_t iteration_dispatch = 0, iteration_combine = 0;
   uint32_t last_ctas = 0;
 };
@@ -1001,6 +1028,7 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   if ((rc = ginsim_cuda_window_register(comm, m->buf_combine, cbytes, &m->win_combine))) fail(rc, ginsim_cuda_last_error());
   DeviceGuard g(c->device);
   GIN_CUDA(cudaMalloc(&m->ws, 256));
+  GIN_CUDA(cudaMalloc(&m->slot_g, (size_t)cfg->tokens * cfg->top_k * 4));
   GIN_CUDA(cudaMemset(m->ws, 0, 256));
   *out = m.release();
   GIN_API_END
@@ -1013,6 +1041,7 @@ int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
     DeviceGuard g(moe->comm->device);
     cudaDeviceSynchronize();
     if (moe->ws) cudaFree(moe->ws);
+    if (moe->slot_g) cudaFree(moe->slot_g);
   }
   // window memory stays mapped until the comm is destroyed (windows are
   // never deregistered in the reference either).
@@ -1062,11 +1091,19 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.win_dispatch = moes[0]->win_dispatch;
   L.win_counts = moes[0]->win_counts;
   L.win_combine = moes[0]->win_combine;
+  // Interleaved dispatch (global slot table + grid barrier) measured slightly
+  // slower at 2 GPUs; opt in with GINSIM_DISPATCH_INTERLEAVE=1.
+  static const bool interleave = [] {
+    const char* v = std::getenv("GINSIM_DISPATCH_INTERLEAVE");
+    return v && v[0] == '1';
+  }();
+  L.interleave = interleave ? 1u : 0u;
   for (uint32_t i = 0; i < n; ++i) {
     if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
     L.r[i].view = moes[i]->comm->dev_view;
     L.r[i].ws = moes[i]->ws;
+    L.r[i].slot_g = moes[i]->slot_g;
   }
   return L;
 }

@@ -160,7 +160,8 @@ def test_zero_size_windows_and_config_mismatch():
 
 
 @pytest.mark.parametrize("n,S,rounds,backend", [(2, 256, 3, "direct"), (4, 512, 25, "direct"),
-                                                 (8, 4096, 10, "direct")])
+                                                 (8, 4096, 10, "direct"), (2, 256, 3, "proxy"),
+                                                 (4, 512, 25, "proxy")])
 def test_ring_matches_reference_final_state(n, S, rounds, backend):
     """Device ring program (harness_ring.cpp:18-57 on the GPU) ends in the same
     windows and cells as the reference's run_ring (tests/golden/ring.json)."""
@@ -180,13 +181,17 @@ def test_ring_matches_reference_final_state(n, S, rounds, backend):
         close(cs)
 
 
-@pytest.mark.parametrize("channels,slots,messages", [(24, 4, 64), (6, 4, 16), (2, 1, 8)])
-def test_moe_ht_flow_control(channels, slots, messages):
+@pytest.mark.parametrize("channels,slots,messages,backend", [(24, 4, 64, "direct"), (6, 4, 16, "direct"),
+                                                             (2, 1, 8, "direct"), (6, 4, 16, "proxy"),
+                                                             (2, 1, 8, "proxy")])
+def test_moe_ht_flow_control(channels, slots, messages, backend):
     """moe-ht circular buffers (harness_moe.cpp:283-382): every message delivered
-    in order with correct stamps, final receive planes equal the oracle."""
+    in order with correct stamps, final receive planes equal the oracle.  The
+    proxy variant drives every put/signal through the GPU-producer descriptor
+    ring and the host agent."""
     n, n_ctx, seed = 2, 4, 9
     n_pool = (channels + n_ctx - 1) // n_ctx
-    pools = [world(n) for _ in range(n_pool)]  # pool p: comms of every rank
+    pools = [world(n, backend) for _ in range(n_pool)]  # pool p: comms of every rank
     try:
         recv_ptrs = []
         for p in range(n_pool):
