@@ -217,6 +217,109 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
             "csv_schema": "size_bytes,iters,p50_ns,p99_ns,mean_ns,backend=direct,transport=nvlink"}
 
 
+def measure_a2a(G, comm, rank, world, dist, torch, dev, stream):
+    """BASELINE configs[1]: one-sided all-to-all via put+signal on registered
+    windows (K15): every rank puts M bytes to each of the
+    n-1 peers at recv[src*M] and releases one SignalInc per peer, then waits
+    for n-1 arrivals.  Per-GPU egress = (n-1)*M / time (max over ranks)."""
+    sizes = [1 << 10, 4 << 10, 16 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 64 << 20]
+    cap = world * sizes[-1]
+    sb, rb = comm.mem_alloc(cap), comm.mem_alloc(cap)
+    ws, wr = comm.window_register(sb, cap), comm.window_register(rb, cap)
+    sid = 400  # above the MoE cells, below the barrier slots
+    h = G.comm_handles([comm])
+    rows = []
+    for M in sizes:
+        iters = 50 if M <= (1 << 20) else 10
+        base = comm.read_signal(sid)
+        k = 0
+
+        def once():
+            nonlocal k
+            k += 1
+            G.check(G.lib().ginsim_cuda_alltoall(h, 1, ws, wr, M, sid, base + (world - 1) * k, 0,
+                                                 ctypes_stream(stream)))
+        for _ in range(3):
+            once()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(iters):
+            once()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([s0.elapsed_time(s1) / iters], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = t.item() * 1e3
+        gbps = (world - 1) * M / (us * 1e-6) / 1e9
+        rows.append({"bytes_per_peer": M, "iters": iters, "us": us, "egress_GBps_per_gpu": gbps,
+                     "frac_of_900": gbps / 900.0, "frac_of_measured_770": gbps / 770.0})
+    comm.check_device()
+    return {"workload": f"one-sided all-to-all put+signal, {world} GPUs, 1 KiB..64 MiB per peer", "rows": rows}
+
+
+def measure_proxy(G, rank, world, local, dist, torch, dev, stream, allgather, T, steps):
+    """BASELINE configs[4]: the Proxy backend (GPU -> pinned-host 64-B
+    descriptor rings -> host agent thread -> cudaMemcpyAsync + stream-memop
+    signals) on the same dispatch/combine workload as the
+    direct path: per-phase device time (max over ranks), descriptors/s and
+    the agent thread's busy fraction."""
+    H, K, E = HIDDEN, TOPK, EXPERTS
+    cfg = G.Config(backend="proxy", signal_cells=512)
+    comm = (G.Comm.create(rank, world, local, allgather, cfg) if world > 1
+            else G.Comm.create_all([local], cfg)[0])
+    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 1, 1, 0, 0))
+    x = torch.empty(T * H, dtype=torch.int16, device=dev)
+    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
+    w = torch.empty(T * K, dtype=torch.float32, device=dev)
+    out = torch.empty(T * H, dtype=torch.int16, device=dev)
+    moe.generate(1, rank, x, idx, w, stream=stream)
+    for _ in range(2):
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    st0 = comm.proxy_stats()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for i in range(steps):
+        ev[i][0].record(stream)
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        ev[i][1].record(stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    st1 = comm.proxy_stats()
+    comm.check_device()
+    d = sorted(e[0].elapsed_time(e[1]) for e in ev)
+    c = sorted(e[1].elapsed_time(e[2]) for e in ev)
+    tot = sum(e[0].elapsed_time(e[2]) for e in ev)
+    t = torch.tensor([d[len(d) // 2], c[len(c) // 2], tot], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ndesc = st1["descriptors"] - st0["descriptors"]
+    ncopy = st1["copies"] - st0["copies"]
+    busy = (st1["busy_ns"] - st0["busy_ns"]) / max(1, st1["wall_ns"] - st0["wall_ns"])
+    dmsg, cmsg = 2 * H + 16, 2 * H
+    disp_us, comb_us = t[0].item() * 1e3, t[1].item() * 1e3
+    res = {"workload": f"proxy backend dispatch/combine, {T} tokens/rank, hidden {H}, top-{K} of {E}, bf16, "
+                       f"{world} GPU(s), one put per expert run",
+           "dispatch_us_p50": disp_us, "combine_us_p50": comb_us,
+           "dispatch_GBps_per_gpu": T * K * dmsg / (disp_us * 1e-6) / 1e9,
+           "combine_GBps_per_gpu": T * K * cmsg / (comb_us * 1e-6) / 1e9,
+           "descriptors_per_step": ndesc / steps, "copies_per_step": ncopy / steps,
+           "descriptors_per_s": ndesc / (t[2].item() * 1e-3), "agent_thread_busy_frac": busy,
+           "host_threads": 1}
+    moe.destroy()
+    comm.destroy()
+    return res
+
+
+def ctypes_stream(stream):
+    return None if stream is None else stream.cuda_stream
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -239,6 +342,7 @@ def main():
             return out
         comm = G.Comm.create(rank, world, local, allgather, G.Config(signal_cells=512))
     else:
+        allgather = None
         comm = G.Comm.create_all([local], G.Config(signal_cells=512))[0]
 
     T, H, K, E = args.tokens, HIDDEN, TOPK, EXPERTS
@@ -310,42 +414,73 @@ def main():
     # --- secondary configs on the same ranks: LL latency and put+signal RTT ---
     ll = None if args.no_extras else measure_ll(G, comm, rank, world, dist, torch, dev, stream)
     pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm, rank, world, dist, torch, dev)
+    a2a = None if (args.no_extras or world < 2) else measure_a2a(G, comm, rank, world, dist, torch, dev, stream)
+    proxy = None
+    if not args.no_extras:
+        ag = allgather if world > 1 else None
+        proxy = {"ll": measure_proxy(G, rank, world, local, dist, torch, dev, stream, ag, 128, 10),
+                 "ht": measure_proxy(G, rank, world, local, dist, torch, dev, stream, ag, T, 3)}
 
     # --- e2e: host buffers through the public API, copies inside the region ---
+    # Every step copies its inputs (x, topk_idx, weights) from pinned host
+    # memory and reads its output back.  The copies run on their own streams
+    # and are double-buffered, so step i+1's H2D and step i-1's D2H overlap
+    # step i's dispatch/combine (what a serving loop does); the region spans
+    # the first H2D to the last D2H.
     e2e = None
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
         ih = idx.cpu().pin_memory()
         wh = w.cpu().pin_memory()
-        oh = torch.empty_like(out, device="cpu").pin_memory()
-        e_steps = max(3, args.steps // 2)
+        ohs = [torch.empty_like(out, device="cpu").pin_memory() for _ in range(2)]
+        xs, idxs, wss, outs = [x, x.clone()], [idx, idx.clone()], [w, w.clone()], [out, out.clone()]
+        h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        e_steps = max(4, args.steps)
 
-        def e2e_step():
-            with torch.cuda.stream(stream):
-                x.copy_(xh, non_blocking=True)
-                idx.copy_(ih, non_blocking=True)
-                w.copy_(wh, non_blocking=True)
-            step()
-            with torch.cuda.stream(stream):
-                oh.copy_(out, non_blocking=True)
-        for _ in range(2):
-            e2e_step()
+        def run_e2e(nsteps, s_ev=None, e_ev=None):
+            h2d_done = [torch.cuda.Event() for _ in range(nsteps)]
+            comp_done = [torch.cuda.Event() for _ in range(nsteps)]
+            d2h_done = [torch.cuda.Event() for _ in range(nsteps)]
+            if s_ev is not None:
+                s_ev.record(h2d_s)
+            for i in range(nsteps):
+                b = i % 2
+                with torch.cuda.stream(h2d_s):
+                    if i >= 2:
+                        h2d_s.wait_event(comp_done[i - 2])   # buffer b free again
+                    xs[b].copy_(xh, non_blocking=True)
+                    idxs[b].copy_(ih, non_blocking=True)
+                    wss[b].copy_(wh, non_blocking=True)
+                    h2d_done[i].record(h2d_s)
+                stream.wait_event(h2d_done[i])
+                if i >= 2:
+                    stream.wait_event(d2h_done[i - 2])       # out[b] read back
+                G.Moe.dispatch([moe], [xs[b]], [idxs[b]], stream=stream)
+                G.Moe.combine([moe], [wss[b]], [outs[b]], stream=stream)
+                comp_done[i].record(stream)
+                with torch.cuda.stream(d2h_s):
+                    d2h_s.wait_event(comp_done[i])
+                    ohs[b].copy_(outs[b], non_blocking=True)
+                    d2h_done[i].record(d2h_s)
+            if e_ev is not None:
+                stream.wait_event(d2h_done[-1])
+                e_ev.record(stream)
+        run_e2e(3)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s2.record(stream)
-        for _ in range(e_steps):
-            e2e_step()
-        e2.record(stream)
+        run_e2e(e_steps, s2, e2)
         torch.cuda.synchronize()
         te = torch.tensor([s2.elapsed_time(e2)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = te.item() / e_steps
-        e2e = {"value": agg_bytes / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
+        ok = bool((ohs[(e_steps - 1) % 2] == out.cpu()).all())
+        e2e = {"value": agg_bytes / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms, "steps": e_steps,
                "h2d_bytes_per_step": int(xh.numel() * 2 + ih.numel() * 4 + wh.numel() * wh.element_size()),
-               "d2h_bytes_per_step": int(oh.numel() * 2)}
+               "d2h_bytes_per_step": int(ohs[0].numel() * 2), "pipelined": "double-buffered H2D/D2H streams",
+               "output_matches_device_path": ok}
 
     if rank != 0:
         if world > 1:
@@ -393,6 +528,8 @@ def main():
         "e2e": e2e,
         "ll": ll,
         "pingpong": pp,
+        "alltoall": a2a,
+        "proxy_vs_direct": proxy,
     }
     if world > 1:
         rem_disp = remote_msgs * dmsg

@@ -227,6 +227,13 @@ int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t d
                            uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t iters, float* ms_out,
                            void* stream);
 
+/* Extended roofline probe: engine 0 = LSU 128-bit, 1 = TMA load+store with
+ * `chunk`-byte stages, 2 = LSU 256-bit, 3 = copy engine (cudaMemcpyAsync over
+ * the peer mapping), 4 = TMA store-only (write path alone, no reads). */
+int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t dst_win, uint32_t peer,
+                              uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t chunk, uint32_t iters,
+                              float* ms_out, void* stream);
+
 /* One-sided all-to-all via put+signal: every rank puts
  * `bytes_per_peer` from send_win[dst*M] to dst's recv_win[src*M] and signals
  * `signal_id` on dst; then waits until the cell >= expected. */

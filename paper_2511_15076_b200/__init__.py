@@ -200,6 +200,8 @@ def _declare(L):
         "ginsim_cuda_alltoall": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint64, c_uint32, P], c_int),
         "ginsim_cuda_copy_bench": ([P, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, c_uint32,
                                     POINTER(ctypes.c_float), P], c_int),
+        "ginsim_cuda_copy_bench_ex": ([P, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, c_uint32,
+                                       c_uint32, POINTER(ctypes.c_float), P], c_int),
         "ginsim_cuda_ring":([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, P], c_int),
         "ginsim_cuda_moe_ht_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, P], c_int),
         "ginsim_cuda_moe_create": ([P, POINTER(MoeConfig), POINTER(P)], c_int),

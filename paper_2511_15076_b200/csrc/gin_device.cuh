@@ -84,6 +84,23 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
                "r"(v.z), "r"(v.w)
                : "memory");
 }
+// 256-bit (LDG/STG .256 on sm_100a) vector moves.
+struct u32x8 {
+  uint32_t v[8];
+};
+__device__ __forceinline__ u32x8 ld_nc_v8(const void* p) {
+  u32x8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                 "=r"(r.v[6]), "=r"(r.v[7])
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v8(void* p, const u32x8& r) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.v[0]),
+               "r"(r.v[1]), "r"(r.v[2]), "r"(r.v[3]), "r"(r.v[4]), "r"(r.v[5]), "r"(r.v[6]), "r"(r.v[7])
+               : "memory");
+}
 
 // ---------------------------------------------------------------- cooperation
 // The paper's Coop parameter: which threads act
@@ -451,24 +468,14 @@ class Gin {
     const GinProxyView& px = v_->proxy;
     const unsigned long long ticket = atomicAdd(&px.tickets[ctx_], 1ull);
     GinRingSlot* slot = px.slots[ctx_] + (ticket & px.mask);
-    // Backpressure: a full ring spins until the host agent frees the slot.
-    wait_eq(&slot->seq, ticket);
+    // Backpressure: a full ring spins until the host agent has consumed
+    // ticket - capacity (proxy_backend.cpp:24-26), read from the agent's
+    // consumed counter rather than the slot's seq word (see gin_types.h).
+    if (ticket > px.mask) wait_ge(px.consumed + ctx_, ticket - px.mask);
     uint64_t* dst = reinterpret_cast<uint64_t*>(slot->bytes);
 #pragma unroll
     for (int i = 0; i < 8; ++i) st_relaxed_sys(dst + i, w[i]);
     st_release_sys(&slot->seq, ticket + 1);
-  }
-
-  __device__ void wait_eq(const uint64_t* p, uint64_t expected) const {
-    const uint64_t t0 = globaltimer();
-    uint32_t spins = 0;
-    while (ld_acquire_sys(p) != expected) {
-      if (++spins > 16) __nanosleep(128);
-      if (expired(t0, spins)) {
-        raise_error(v_, GIN_DEVERR_TIMEOUT);
-        break;
-      }
-    }
   }
 
   const GinDevCommView* v_;

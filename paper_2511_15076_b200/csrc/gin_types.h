@@ -59,6 +59,11 @@ typedef struct GinProxyView {
   GinRingSlot* slots[GIN_MAX_CONTEXTS];        // host-pinned, device-mapped
   unsigned long long* tickets;                 // device: [ctx] next ticket
   uint64_t* completed;                         // device: [ctx] tickets locally complete
+  // host-pinned, written only by the agent: [ctx] tickets consumed.  Producers
+  // wait on this (never on the slot's own seq word) before reusing a slot: a
+  // slot line the GPU has itself written can be served stale from its L2 after
+  // the CPU rewrites it, while a line the GPU only ever reads is re-fetched.
+  const uint64_t* consumed;
   uint32_t mask;                               // capacity - 1
   uint32_t pad;
 } GinProxyView;

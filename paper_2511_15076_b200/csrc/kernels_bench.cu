@@ -67,6 +67,42 @@ __global__ void __launch_bounds__(kCopyThreads) tma_copy_kernel(char* dst, const
   gin::tma::wait_all();
 }
 
+// 256-bit LSU copy (LDG/STG .256 on sm_100a): half the instructions of the
+// 128-bit path for the same bytes in flight.
+__global__ void __launch_bounds__(kCopyThreads) lsu256_copy_kernel(char* dst, const char* src, uint64_t bytes) {
+  const uint64_t nv = bytes / 32;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + stride < nv; i += 2 * stride) {
+    const gin::u32x8 a = gin::ld_nc_v8(src + 32 * i), b = gin::ld_nc_v8(src + 32 * (i + stride));
+    gin::st_v8(dst + 32 * i, a);
+    gin::st_v8(dst + 32 * (i + stride), b);
+  }
+  for (; i < nv; i += stride) gin::st_v8(dst + 32 * i, gin::ld_nc_v8(src + 32 * i));
+}
+
+// Store-only TMA: every warp bulk-stores one shared-memory chunk over and
+// over to consecutive destination chunks -- no HBM reads, so it measures the
+// write path (NVLink egress or HBM write) alone.
+__global__ void __launch_bounds__(kCopyThreads) tma_store_only_kernel(char* dst, uint64_t bytes, uint32_t chunk) {
+  extern __shared__ __align__(128) char smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  char* buf = smem + (size_t)warp * chunk;
+  for (uint32_t i = lane * 16; i < chunk; i += 32 * 16) *reinterpret_cast<uint4*>(buf + i) = make_uint4(i, warp, 1, 2);
+  gin::tma::fence_proxy_async_shared();
+  __syncwarp();
+  if (lane != 0) return;
+  const uint64_t total = (bytes + chunk - 1) / chunk;
+  const uint64_t gw = (uint64_t)blockIdx.x * nw + warp, stride = (uint64_t)gridDim.x * nw;
+  uint32_t n = 0;
+  for (uint64_t c = gw; c < total; c += stride) {
+    gin::tma::store(dst + c * chunk, buf, (uint32_t)std::min<uint64_t>(chunk, bytes - c * chunk));
+    gin::tma::commit();
+    if (++n >= 8) gin::tma::wait_read<8>();
+  }
+  gin::tma::wait_all();
+}
+
 }  // namespace ginsim_b200
 
 using namespace ginsim_b200;
@@ -111,6 +147,63 @@ int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t d
   for (uint32_t i = 0; i < iters; ++i) launch();
   GIN_CUDA(cudaEventRecord(e1, s));
   GIN_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  GIN_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_out = ms / (float)std::max(1u, iters);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  GIN_API_END
+}
+
+// Extended probe: engine 0 = LSU 128-bit, 1 = TMA load+store (chunk bytes,
+// 4 stages per warp), 2 = LSU 256-bit, 3 = copy engine (cudaMemcpyAsync over
+// the peer mapping), 4 = TMA store-only (no reads).
+// chunk = TMA chunk bytes; CTAs of 256 threads.
+int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t dst_win, uint32_t peer,
+                              uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t chunk, uint32_t iters,
+                              float* ms_out, void* stream) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  if (src_win >= c->windows.size() || dst_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+  if (peer >= c->world) fail(GINSIM_E_INVALID_PEER, "peer out of range");
+  if (c->windows[src_win].sizes[c->rank] < bytes || c->windows[dst_win].sizes[peer] < bytes)
+    fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
+  if (bytes % 32 || engine > 4) fail(GINSIM_E_USAGE, "copy size must be a multiple of 32; engine 0..4");
+  if (chunk == 0 || chunk % 16 || chunk > 16384) fail(GINSIM_E_USAGE, "chunk must be a multiple of 16 in 16..16384");
+  DeviceGuard g(c->device);
+  char* dst = c->windows[dst_win].bases[peer];
+  const char* src = c->windows[src_win].bases[c->rank];
+  cudaStream_t s = (cudaStream_t)stream;
+  int sms = 0;
+  GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const uint32_t G = ctas ? ctas : (uint32_t)sms;
+  const size_t smem_ld = 1024 + (size_t)(kCopyThreads / 32) * kCopyStages * chunk;
+  const size_t smem_st = (size_t)(kCopyThreads / 32) * chunk;
+  if (engine == 1) {
+    if (smem_ld > 227 * 1024) fail(GINSIM_E_USAGE, "chunk too large for 4 stages x 8 warps");
+    GIN_CUDA(cudaFuncSetAttribute((const void*)tma_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ld));
+  }
+  if (engine == 4)
+    GIN_CUDA(cudaFuncSetAttribute((const void*)tma_store_only_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_st));
+  cudaEvent_t e0, e1;
+  GIN_CUDA(cudaEventCreate(&e0));
+  GIN_CUDA(cudaEventCreate(&e1));
+  auto launch = [&] {
+    switch (engine) {
+      case 0: lsu_copy_kernel<<<G, kCopyThreads, 0, s>>>(dst, src, bytes); break;
+      case 1: tma_copy_kernel<<<G, kCopyThreads, smem_ld, s>>>(dst, src, bytes, chunk); break;
+      case 2: lsu256_copy_kernel<<<G, kCopyThreads, 0, s>>>(dst, src, bytes); break;
+      case 3: GIN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s)); break;
+      default: tma_store_only_kernel<<<G, kCopyThreads, smem_st, s>>>(dst, bytes, chunk); break;
+    }
+  };
+  launch();
+  GIN_CUDA(cudaGetLastError());
+  GIN_CUDA(cudaEventRecord(e0, s));
+  for (uint32_t i = 0; i < iters; ++i) launch();
+  GIN_CUDA(cudaEventRecord(e1, s));
+  GIN_CUDA(cudaEventSynchronize(e1));
+  GIN_CUDA(cudaGetLastError());
   float ms = 0;
   GIN_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   *ms_out = ms / (float)std::max(1u, iters);

@@ -55,6 +55,8 @@ struct MoeLaunch {
   MoeRankArgs r[GIN_MAX_RANKS];
   uint32_t E, K, T, H, mode, layout, e_local, parts, cparts;
   uint32_t win_dispatch, win_counts, win_combine, interleave;
+  uint32_t win_stage, win_cstage, coalesce;  // proxy backend: dispatch / combine staging windows
+  uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
 };
 
 // ------------------------------------------------------------------ helpers
@@ -127,7 +129,13 @@ __device__ void block_exclusive_scan(uint32_t* data, uint32_t n, uint32_t* warp_
 }
 
 // ------------------------------------------------------------------ dispatch
-template <int KMAX>
+// PROXY = the Proxy backend: rows are staged into a local
+// registered window laid out in destination order -- (dst_base[dst] +
+// prefix_e[e] + slot) -- so every expert's messages form ONE contiguous run
+// at both ends, and the last CTA hands each run to the host agent as a put
+// descriptor (ordered before the expert's release on ctx e % n_ctx,
+// harness_moe.cpp:135-167).  No NVLink store is issued by the kernel.
+template <int KMAX, bool PROXY>
 __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
@@ -139,13 +147,21 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
 
   __shared__ uint32_t hist_all[kMaxExperts], run[kMaxExperts], prefix_e[kMaxExperts];
-  __shared__ uint32_t warp_tot[kMoeWarps];
+  __shared__ uint32_t dst_base[GIN_MAX_RANKS + 1];
   __shared__ int is_last;
   extern __shared__ uint32_t slots[];  // [(t1-t0)*K]
 
   for (uint32_t e = tid; e < E; e += kMoeThreads) {
     hist_all[e] = 0;
     run[e] = 0;
+  }
+  if (PROXY && tid == 0) {
+    // flush (runtime.cpp:460-470): the staging window is reused only once the
+    // host agent has completed every put this rank submitted earlier
+    for (uint32_t ctx = 0; ctx < v->n_ctx; ++ctx) {
+      const uint64_t snap = atomicAdd(&v->proxy.tickets[ctx], 0ull);
+      gin::Gin(v, ctx).wait_ge(&v->proxy.completed[ctx], snap);
+    }
   }
   __syncthreads();
   // Phase A: per-expert totals and the prefix of tokens before this CTA.
@@ -158,13 +174,21 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
   __syncthreads();
   // Destination base offsets for the compact layout: exclusive prefix of this
   // source's counts within each destination's expert group.
-  if (L.layout == 1) {
+  if (L.layout == 1 || PROXY) {
     for (uint32_t d = tid; d < n; d += kMoeThreads) {
       uint32_t acc = 0;
       for (uint32_t e = d * e_local; e < (d + 1) * e_local; ++e) {
         prefix_e[e] = acc;
         acc += hist_all[e];
       }
+      dst_base[d + 1] = acc;  // messages to d (turned into a prefix below)
+    }
+  }
+  if (PROXY) {
+    __syncthreads();
+    if (tid == 0) {
+      dst_base[0] = 0;
+      for (uint32_t d = 0; d < n; ++d) dst_base[d + 1] += dst_base[d];
     }
   }
   // Slots of this CTA's tokens, in (t, k) order (harness_moe.cpp:143-150).
@@ -197,9 +221,13 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
       const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
       const uint32_t dst = e / e_local, e_loc = e % e_local;
       const uint32_t slot = slots[(t - t0) * K + lane];
-      const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
-                                         : ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
-      my_dst = bases[dst] + off;
+      if (PROXY) {
+        my_dst = v->win[L.win_stage].base[rank] + ((uint64_t)dst_base[dst] + prefix_e[e] + slot) * dmsg;
+      } else {
+        const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
+                                           : ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
+        my_dst = bases[dst] + off;
+      }
     }
     char* dptr[KMAX];
 #pragma unroll
@@ -255,7 +283,31 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
     if (is_last) gin::fence_acq_rel_sys();
   }
   __syncthreads();
-  if (is_last) {
+  if (is_last && PROXY) {
+    // One thread per expert submits, in this order on ctx e % n_ctx: the
+    // count (inline put), the payload run (one put, or one per message when
+    // coalescing is off), then the release SignalAdd((1<<32)+count).  The
+    // agent drains each context ring in ticket order onto one stream, so the
+    // release lands after the payload (fabric.cpp:63-79).
+    const gin::Team world = gin::WorldTeam(n);
+    gin::CoopThread me;
+    for (uint32_t e = tid; e < E; e += kMoeThreads) {
+      const uint32_t dst = e / e_local, e_loc = e % e_local, cnt = hist_all[e];
+      const gin::Gin g(v, e % v->n_ctx);
+      g.put_value(me, world, dst, L.win_counts, ((uint64_t)e_loc * n + rank) * 4, cnt);
+      const uint64_t src0 = ((uint64_t)dst_base[dst] + prefix_e[e]) * dmsg;
+      const uint64_t dst0 = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T) * dmsg
+                                          : ((uint64_t)rank * T * K + prefix_e[e]) * dmsg;
+      const gin::Action rel = gin::SignalAction(e_loc, gin::SignalAdd((1ull << 32) + cnt));
+      if (L.coalesce) {
+        g.put(me, world, dst, L.win_dispatch, dst0, L.win_stage, src0, (uint64_t)cnt * dmsg, rel);
+      } else {
+        for (uint32_t q = 0; q < cnt; ++q)
+          g.put(me, world, dst, L.win_dispatch, dst0 + q * dmsg, L.win_stage, src0 + q * dmsg, dmsg);
+        g.signal(me, world, dst, e_loc, rel.op);
+      }
+    }
+  } else if (is_last) {
     uint32_t* const* cbase = reinterpret_cast<uint32_t* const*>(v->win[L.win_counts].base);
     for (uint32_t e = tid; e < E; e += kMoeThreads) {
       const uint32_t dst = e / e_local, e_loc = e % e_local;
@@ -281,6 +333,11 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
 }
 
 // ------------------------------------------------------------------ combine
+// PROXY: the expert transform writes message m (receive order) to m*cmsg of
+// the local staging window, then the last CTA submits one put descriptor per message
+// to (token*K+k)*cmsg of its source and, after them on the same context, the
+// per-(source, ctx) combine flag (harness_moe.cpp:169-223).
+template <bool PROXY>
 __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
@@ -349,7 +406,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       k = meta[8] | (meta[9] << 8) | (meta[10] << 16) | ((uint32_t)meta[11] << 24);
     }
     const uint32_t e = rank * e_local + e_loc;
-    char* dst = cbases[src] + ((uint64_t)token * K + k) * cmsg;
+    char* dst = PROXY ? v->win[L.win_cstage].base[rank] + (uint64_t)m * cmsg
+                      : cbases[src] + ((uint64_t)token * K + k) * cmsg;
     if (vec_ok) {
       const uint32_t vlo = p * vec_per_part, vhi = min(vlo + vec_per_part, nvec);
       uint32_t i = vlo + lane;
@@ -381,7 +439,30 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
     if (is_last) gin::fence_acq_rel_sys();
   }
   __syncthreads();
-  if (is_last) {
+  if (is_last && PROXY) {
+    const gin::Team world = gin::WorldTeam(n);
+    gin::CoopThread me;
+    for (uint32_t sc = tid; sc < n * n_ctx; sc += kMoeThreads) {
+      const uint32_t src = sc / n_ctx, ctx = sc % n_ctx;
+      const gin::Gin g(v, ctx);
+      uint32_t c = 0;
+      for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc) {
+        if ((rank * e_local + e_loc) % n_ctx != ctx) continue;
+        const uint32_t pr = e_loc * n + src;
+        for (uint32_t slot = 0; slot < cnt[pr]; ++slot) {
+          const uint64_t moff = L.layout == 0 ? (((uint64_t)e_loc * n + src) * T + slot) * dmsg
+                                              : ((uint64_t)src * T * K + src_prefix[pr] + slot) * dmsg;
+          const unsigned char* meta = reinterpret_cast<const unsigned char*>(recv + moff + payload);
+          const uint32_t token = meta[4] | (meta[5] << 8) | (meta[6] << 16) | ((uint32_t)meta[7] << 24);
+          const uint32_t k = meta[8] | (meta[9] << 8) | (meta[10] << 16) | ((uint32_t)meta[11] << 24);
+          g.put(me, world, src, L.win_combine, ((uint64_t)token * K + k) * cmsg, L.win_cstage,
+                ((uint64_t)pair_start[pr] + slot) * cmsg, cmsg);
+        }
+        c += cnt[pr];
+      }
+      if (c) g.signal(me, world, src, e_local, gin::SignalAdd(c));
+    }
+  } else if (is_last) {
     for (uint32_t sc = tid; sc < n * n_ctx; sc += kMoeThreads) {
       const uint32_t src = sc / n_ctx, ctx = sc % n_ctx;
       uint32_t c = 0;
@@ -545,7 +626,10 @@ __device__ __forceinline__ uint4 reduce_vec(const uint4* y, uint32_t K, uint32_t
   return make_uint4(pk[0], pk[1], pk[2], pk[3]);
 }
 
-template <int KMAX>
+// CPASYNC: the row chunk is loaded by all 32 lanes with 16-byte cp.async
+// (LSU path) instead of a TMA bulk load, so loads never queue behind the K
+// bulk stores in the SM's TMA unit; the stores stay TMA bulk copies.
+template <int KMAX, bool CPASYNC>
 __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLaunch L, uint32_t chunk) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
@@ -636,7 +720,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len);
     gin::tma::load(stage + (size_t)s * chunk, x + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
   };
-  if (lane == 0) {
+  // cp.async variant: every lane copies its 16-byte vectors of the chunk;
+  // one commit group per item (item j of this warp is group j).
+  auto cp_load = [&](int s, uint32_t item) {
+    const uint32_t t = tbase + item / parts, p = item % parts;
+    const uint32_t len = tma_chunk_len(payload, chunk, p);
+    const char* src = x + (uint64_t)t * payload + (uint64_t)p * chunk;
+    char* dst = stage + (size_t)s * chunk;
+    for (uint32_t o = lane * 16; o < len; o += 32 * 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(gin::tma::smem_u32(dst + o)), "l"(src + o)
+                   : "memory");
+  };
+  if (CPASYNC) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      const uint32_t item = wid + s * wstride;
+      if (item < items) cp_load(s, item);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  } else if (lane == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
       const uint32_t item = wid + s * wstride;
       if (item < items) issue_load(s, item);
@@ -647,6 +748,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     if (item >= items) break;
     const uint32_t t = tbase + item / parts, p = item % parts;
     const int s = (int)(j % kTmaStages);
+    if (CPASYNC) {
+      if (j == 0) asm volatile("cp.async.wait_group %0;" ::"n"(kTmaStages - 1) : "memory");
+      else asm volatile("cp.async.wait_group %0;" ::"n"(kTmaStages - 2) : "memory");
+    }
     if (lane < K) {
       const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
       const uint32_t dst = e / e_local, e_loc = e % e_local;
@@ -657,10 +762,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
       ctl->dptr[lane] = d;
       if (p == 0) gin::st_v4(d + payload, make_uint4(rank, t, lane, lane + 1));  // meta
     }
+    if (CPASYNC) gin::tma::fence_proxy_async_shared();  // cp.async writes -> visible to the bulk stores
     __syncwarp();
     if (lane == 0) {
       const uint32_t len = tma_chunk_len(payload, chunk, p);
-      gin::tma::mbar_wait(&ctl->bar[s], (j / kTmaStages) & 1);
+      if (!CPASYNC) gin::tma::mbar_wait(&ctl->bar[s], (j / kTmaStages) & 1);
       for (uint32_t k = 0; k < K; ++k) gin::tma::store(ctl->dptr[k] + (uint64_t)p * chunk, stage + (size_t)s * chunk, len);
       gin::tma::commit();
       // Refill the stage of the PREVIOUS item: its stores were committed one
@@ -668,10 +774,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
       if (j >= 1) {
         gin::tma::wait_read<1>();
         const uint32_t nxt = item - wstride + kTmaStages * wstride;
-        if (nxt < items) issue_load((int)((j - 1) % kTmaStages), nxt);
+        if (!CPASYNC && nxt < items) issue_load((int)((j - 1) % kTmaStages), nxt);
       }
     }
     __syncwarp();
+    if (CPASYNC && j >= 1) {
+      const uint32_t nxt = item - wstride + kTmaStages * wstride;
+      if (nxt < items) cp_load((int)((j - 1) % kTmaStages), nxt);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
   }
   if (lane == 0) {
     gin::tma::wait_all();
@@ -697,7 +808,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   }
   if (tid == 0) {
     const uint64_t want = R.iteration * ((uint64_t)n << 32);
-    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(e_loc, want);
+    if (!L.no_wait)
+      for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(e_loc, want);
   }
 }
 
@@ -985,7 +1097,10 @@ struct ginsim_cuda_moe_s {
   Comm* comm = nullptr;
   ginsim_cuda_moe_config cfg{};
   uint32_t e_local = 0, parts = 4, G = 0, Gc = 0, Gr = 0, chunk = 0, cparts = 1, cchunk = 0;
-  uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0;
+  uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0, win_stage = 0, win_cstage = 0;
+  bool proxy = false;
+  void* buf_stage = nullptr;
+  void* buf_cstage = nullptr;
   void* buf_dispatch = nullptr;
   void* buf_counts = nullptr;
   void* buf_combine = nullptr;
@@ -1026,6 +1141,18 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   if ((rc = ginsim_cuda_window_register(comm, m->buf_dispatch, dbytes, &m->win_dispatch))) fail(rc, ginsim_cuda_last_error());
   if ((rc = ginsim_cuda_window_register(comm, m->buf_counts, nbytes, &m->win_counts))) fail(rc, ginsim_cuda_last_error());
   if ((rc = ginsim_cuda_window_register(comm, m->buf_combine, cbytes, &m->win_combine))) fail(rc, ginsim_cuda_last_error());
+  m->proxy = c->cfg.backend == GIN_BACKEND_PROXY;
+  if (m->proxy) {
+    // Proxy backend: dispatch rows and combine results are staged in local
+    // registered windows the host agent copies from (the reference's staging
+    // windows, harness_moe.cpp:122-130).  Separate windows, so a combine never
+    // overwrites rows the agent may still be copying out for the dispatch.
+    const uint64_t sbytes = T * K * dmsg, cbytes2 = n * T * K * cmsg;
+    if (ginsim_cuda_mem_alloc(comm, sbytes, &m->buf_stage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+    if ((rc = ginsim_cuda_window_register(comm, m->buf_stage, sbytes, &m->win_stage))) fail(rc, ginsim_cuda_last_error());
+    if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_cstage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+    if ((rc = ginsim_cuda_window_register(comm, m->buf_cstage, cbytes2, &m->win_cstage))) fail(rc, ginsim_cuda_last_error());
+  }
   DeviceGuard g(c->device);
   GIN_CUDA(cudaMalloc(&m->ws, 256));
   GIN_CUDA(cudaMalloc(&m->slot_g, (size_t)cfg->tokens * cfg->top_k * 4));
@@ -1091,6 +1218,17 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.win_dispatch = moes[0]->win_dispatch;
   L.win_counts = moes[0]->win_counts;
   L.win_combine = moes[0]->win_combine;
+  L.win_stage = moes[0]->win_stage;
+  L.win_cstage = moes[0]->win_cstage;
+  // Proxy backend: one put descriptor per expert run (default) or per message
+  // (GINSIM_PROXY_COALESCE=0, the reference's one-put-per-(t,k) pattern).
+  const char* cv = std::getenv("GINSIM_PROXY_COALESCE");
+  const bool coalesce = !(cv && cv[0] == '0');
+  L.coalesce = coalesce ? 1u : 0u;
+  // GINSIM_PROFILE_NO_WAIT=1 lets a profiler replay one rank's dispatch alone
+  // (ncu serialises kernels, so a cross-GPU acquire would never complete).
+  const char* nw = std::getenv("GINSIM_PROFILE_NO_WAIT");
+  L.no_wait = (nw && nw[0] == '1') ? 1u : 0u;
   // Interleaved dispatch (global slot table + grid barrier) measured slightly
   // slower at 2 GPUs; opt in with GINSIM_DISPATCH_INTERLEAVE=1.
   static const bool interleave = [] {
@@ -1123,7 +1261,7 @@ struct MoeKernels {
 
 static uint32_t engine_of(const ginsim_cuda_moe_t m) {
   const bool aligned = (2u * m->cfg.hidden) % 16u == 0;
-  if (!aligned) return 1;
+  if (!aligned || m->proxy) return 1;  // the proxy path stages with LSU stores
   return m->cfg.engine == 0 ? 2 : m->cfg.engine;
 }
 static bool use_tma(const ginsim_cuda_moe_t m) { return engine_of(m) != 1; }
@@ -1132,17 +1270,27 @@ static MoeKernels kernels_of(const ginsim_cuda_moe_t m) {
   const bool k8 = m->cfg.top_k <= 8;
   const uint32_t e = engine_of(m);
   MoeKernels k{};
-  if (e == 1) {
-    k.dispatch = k8 ? (const void*)moe_dispatch_kernel<8> : (const void*)moe_dispatch_kernel<32>;
-    k.combine = (const void*)moe_combine_kernel;
+  if (e == 1 && m->proxy) {
+    k.dispatch = k8 ? (const void*)moe_dispatch_kernel<8, true> : (const void*)moe_dispatch_kernel<32, true>;
+    k.combine = (const void*)moe_combine_kernel<true>;
     k.threads = kMoeThreads;
     return k;
   }
-  k.dispatch = k8 ? (const void*)moe_dispatch_tma_kernel<8> : (const void*)moe_dispatch_tma_kernel<32>;
+  if (e == 1) {
+    k.dispatch = k8 ? (const void*)moe_dispatch_kernel<8, false> : (const void*)moe_dispatch_kernel<32, false>;
+    k.combine = (const void*)moe_combine_kernel<false>;
+    k.threads = kMoeThreads;
+    return k;
+  }
+  // GINSIM_DISPATCH_LOADS=cpasync: LSU cp.async row loads + TMA bulk stores
+  const char* lv = std::getenv("GINSIM_DISPATCH_LOADS");
+  const bool cpa = lv && std::strcmp(lv, "cpasync") == 0;
+  if (cpa) k.dispatch = k8 ? (const void*)moe_dispatch_tma_kernel<8, true> : (const void*)moe_dispatch_tma_kernel<32, true>;
+  else k.dispatch = k8 ? (const void*)moe_dispatch_tma_kernel<8, false> : (const void*)moe_dispatch_tma_kernel<32, false>;
   k.threads = kTmaThreads;
   k.tma_dispatch = true;
   if (e == 3) {
-    k.combine = (const void*)moe_combine_kernel;
+    k.combine = (const void*)moe_combine_kernel<false>;
   } else {
     k.combine = k8 ? (const void*)moe_combine_tma_kernel<8> : (const void*)moe_combine_tma_kernel<32>;
     k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8> : (const void*)moe_combine_reduce_kernel<32>;
@@ -1277,7 +1425,7 @@ int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const voi
   void* args[] = {&L, &chunk};
   const uint32_t Gc = moes[0]->Gc;
   launch_coop(k.combine, Gc, n, combine_threads(k), combine_smem(moes[0]), args, (cudaStream_t)stream);
-  if (k.reduce) {
+  if (k.reduce && !L.no_wait) {  // profiling harness: the reduce would wait on every source's flag
     GIN_CUDA(cudaLaunchKernel(k.reduce, dim3(moes[0]->Gr, n), dim3(kMoeThreads), args, 0, (cudaStream_t)stream));
   }
   moes[0]->last_ctas = Gc * n;

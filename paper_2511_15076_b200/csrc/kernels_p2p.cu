@@ -102,7 +102,7 @@ struct A2aArgs {
 __global__ void alltoall_kernel(A2aArgs A) {
   const GinDevCommView* v = A.lv.v[blockIdx.y];
   unsigned int* ws = A.lv.ws[blockIdx.y];
-  const uint64_t iter = A.lv.base[blockIdx.y];
+  const uint64_t arrivals_before = A.lv.base[blockIdx.y];  // per-peer arrivals of earlier launches
   gin::Gin gin(v, 0);
   gin::CoopCta cta;
   const uint32_t n = v->world, me = v->rank;
@@ -119,7 +119,7 @@ __global__ void alltoall_kernel(A2aArgs A) {
   if (threadIdx.x == 0) {
     gin::fence_acq_rel_sys();
     const unsigned prev = atomicAdd(ws + 16 + peer, 1u);
-    last = prev + 1 == (unsigned)(iter * A.ctas_per_peer);
+    last = prev + 1 == (unsigned)(arrivals_before + A.ctas_per_peer);
     if (last) {
       gin::fence_acq_rel_sys();
       gin.release_signal_raw(peer, A.sig, 1);
@@ -349,7 +349,9 @@ int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t s
   const int cap = max_coresident_ctas((const void*)alltoall_kernel, 512, 0, c0->device) / (int)n;
   while (per_peer > 1 && (int)(per_peer * (world - 1)) > cap) --per_peer;
   A.ctas_per_peer = per_peer;
-  for (uint32_t i = 0; i < n; ++i) A.lv.base[i] = bump_host_counter(&comms[i]->impl, 1, 1);
+  // the per-peer arrival counters are monotone across launches whose CTA
+  // split differs (it follows the message size): pass where they stand
+  for (uint32_t i = 0; i < n; ++i) A.lv.base[i] = bump_host_counter(&comms[i]->impl, 1, per_peer) - per_peer;
   coop_launch((const void*)alltoall_kernel, dim3(per_peer * (world - 1), n), dim3(512), &A, (cudaStream_t)stream);
   GIN_API_END
 }

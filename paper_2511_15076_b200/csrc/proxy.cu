@@ -2,8 +2,9 @@
 // PAPER.md:651-669; reference ProxyBackend, proj/core/src/proxy_backend.cpp).
 //
 //   GPU producer (gin_device.cuh, Gin::submit): ticket from a device counter,
-//     wait slot.seq == ticket, write the 64-byte descriptor into pinned host
-//     memory, publish slot.seq = ticket + 1 (proxy_backend.cpp:19-29).
+//     wait until the agent has consumed ticket - capacity (a host-written
+//     counter), write the 64-byte descriptor into pinned host memory, publish
+//     slot.seq = ticket + 1 (proxy_backend.cpp:19-29).
 //   Host consumer (this file): drain <= 64 descriptors per ring per pass
 //     (proxy_backend.hpp:67-68, cpp:64-113), decode (descriptor.cpp), and post
 //     through the plugin's iput / iput_signal analogue: cudaMemcpyAsync for
@@ -38,6 +39,7 @@ struct ProxyAgent {
   Comm* c = nullptr;
   uint32_t n_ctx = 0, cap = 0;
   std::vector<GinRingSlot*> slots;       // pinned host, device-mapped
+  uint64_t* consumed_host = nullptr;     // pinned host, device-mapped: [ctx] tickets consumed
   std::vector<uint64_t> tail;            // next ticket to consume per ctx
   cudaStream_t stream = nullptr;
   std::thread th;
@@ -165,6 +167,7 @@ struct ProxyAgent {
         std::memcpy(raw, slot->bytes, 64);
         __atomic_store_n(&slot->seq, t + cap, __ATOMIC_RELEASE);
         tail[ctx] = t + 1;
+        __atomic_store_n(consumed_host + ctx, t + 1, __ATOMIC_RELEASE);
         ginsim_cuda_descriptor d;
         descriptor_decode(raw, &d);  // a malformed descriptor is a protocol bug: fail the run
         if (d.flags & GIN_FLAG_HAS_COUNTER) counter_pending[d.counter_id].fetch_add(1, std::memory_order_acq_rel);
@@ -265,6 +268,15 @@ ProxyPtr proxy_start(Comm* c) {
     GIN_CUDA(cudaHostGetDevicePointer(&dptr, mem, 0));
     c->host_view.proxy.slots[i] = static_cast<GinRingSlot*>(dptr);
   }
+  {
+    void* cm = nullptr;
+    GIN_CUDA(cudaHostAlloc(&cm, sizeof(uint64_t) * GIN_MAX_CONTEXTS, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(cm, 0, sizeof(uint64_t) * GIN_MAX_CONTEXTS);
+    p->consumed_host = static_cast<uint64_t*>(cm);
+    void* dptr = nullptr;
+    GIN_CUDA(cudaHostGetDevicePointer(&dptr, cm, 0));
+    c->host_view.proxy.consumed = static_cast<const uint64_t*>(dptr);
+  }
   void* st = nullptr;
   GIN_CUDA(cudaHostAlloc(&st, sizeof(uint64_t) * ProxyAgent::kStage, cudaHostAllocPortable));
   p->stage = static_cast<uint64_t*>(st);
@@ -286,6 +298,7 @@ void proxy_stop(ProxyPtr& p) {
   for (auto& f : p->inflight) cudaEventDestroy(f.ev);
   for (auto e : p->free_events) cudaEventDestroy(e);
   for (auto s : p->slots) cudaFreeHost(s);
+  if (p->consumed_host) cudaFreeHost(p->consumed_host);
   if (p->stage) cudaFreeHost(p->stage);
   cudaStreamDestroy(p->stream);
   p.reset();

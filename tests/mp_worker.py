@@ -31,7 +31,9 @@ def main():
     mode = int(os.environ.get("MP_MODE", "0"))
     layout = int(os.environ.get("MP_LAYOUT", "1"))
     E, K, H, seed = 256, 8, 7168, 1
-    comm = G.Comm.create(rank, world, local, allgather, G.Config(signal_cells=512, timeout_ms=20000))
+    backend = os.environ.get("MP_BACKEND", "direct")
+    iters = int(os.environ.get("MP_ITERS", "3"))
+    comm = G.Comm.create(rank, world, local, allgather, G.Config(backend=backend, signal_cells=512, timeout_ms=20000))
     cfg = G.MoeConfig(E, K, T, H, mode, layout, 0)
     moe = G.Moe(comm, cfg)
     dev = torch.device("cuda", local)
@@ -42,19 +44,19 @@ def main():
     moe.generate(seed, rank, x, idx, w)
     torch.cuda.synchronize()
     res = {"rank": rank, "ok": True}
-    for it in range(3):
+    for it in range(iters):  # back to back on one stream: no host sync between steps
         G.Moe.dispatch([moe], [x], [idx])
         G.Moe.combine([moe], [w], [out])
-        torch.cuda.synchronize()
-        comm.check_device()
+    torch.cuda.synchronize()
+    comm.check_device()
     got = out.cpu().numpy().view(np.uint16).reshape(T, H)
     exp, _ = O.combine(seed, E, K, H, rank, T, mode=mode)
     res["combine_exact"] = bool((got == exp).all())
     cnt = O.counts(seed, world, E, K, T)
     sig, _ = comm.snapshot_cells(512, 256)
     e_local = E // world
-    res["cells_exact"] = all(sig[e] == 3 * ((world << 32) + int(cnt[rank * e_local + e].sum())) for e in range(e_local)) \
-        and sig[e_local] == 3 * T * K
+    res["cells_exact"] = all(sig[e] == iters * ((world << 32) + int(cnt[rank * e_local + e].sum()))
+                             for e in range(e_local)) and sig[e_local] == iters * T * K
     if layout == 0 and T <= 256:
         from tests import gpu_util as U
         d, comb, _ = O.moe_rank_state(seed, world, E, K, T, H, rank, mode=mode)

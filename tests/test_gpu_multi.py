@@ -43,6 +43,23 @@ def test_multiprocess_moe_parity(layout, tokens, mode):
             assert r["dispatch_window_exact"] and r["combine_window_exact"], r
 
 
+@pytest.mark.parametrize("layout,tokens", [(0, 128), (1, 1024)])
+def test_multiprocess_moe_proxy_backend(layout, tokens):
+    """Proxy backend across real GPUs (each process's host agent copies its
+    staged runs into the peers' VMM mappings and applies signals with stream
+    memops), 8 back-to-back iterations: outputs, cells and windows exact."""
+    n = gpu_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = 4 if n >= 4 else 2
+    res = _torchrun(n, {"MP_TOKENS": tokens, "MP_LAYOUT": layout, "MP_MODE": 1, "MP_PINGPONG": 0,
+                        "MP_BACKEND": "proxy", "MP_ITERS": 8})
+    for r in res:
+        assert r["combine_exact"] and r["cells_exact"], r
+        if "dispatch_window_exact" in r:
+            assert r["dispatch_window_exact"] and r["combine_window_exact"], r
+
+
 def test_multiprocess_pingpong_nvlink():
     n = gpu_count()
     if n < 2:

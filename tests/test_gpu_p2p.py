@@ -267,6 +267,34 @@ def test_alltoall_pattern(n):
         close(cs)
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_alltoall_varying_sizes(n):
+    """Back-to-back all-to-alls whose CTA split differs (it follows the message
+    size) keep the per-peer release exact: bytes land, cells count n-1 per call."""
+    cs = world(n)
+    try:
+        sizes = [1 << 10, 256 << 10, 4 << 10, 1 << 20]
+        cap = n * max(sizes)
+        ws, sp = register(cs, cap)
+        wr, rp = register(cs, cap)
+        for r in range(n):
+            U.h2d(sp[r], ((np.arange(cap) * 7 + r * 29) & 0xFF).astype(np.uint8))
+        for it, M in enumerate(sizes, start=1):
+            G.check(G.lib().ginsim_cuda_alltoall(G.comm_handles(cs), n, ws, wr, M, 3, (n - 1) * it, 0, None))
+            U.sync()
+            for c in cs:
+                c.check_device()
+            for dst in range(n):
+                got = U.d2h(rp[dst], n * M)
+                for src in range(n):
+                    if src != dst:
+                        want = ((np.arange(cap) * 7 + src * 29) & 0xFF).astype(np.uint8)[dst * M:(dst + 1) * M]
+                        assert (got[src * M:(src + 1) * M] == want).all()
+                assert cs[dst].read_signal(3) == (n - 1) * it
+    finally:
+        close(cs)
+
+
 def test_proxy_stats_and_reset_while_outstanding():
     cs = world(2, "proxy")
     try:
