@@ -234,6 +234,12 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
                               uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t chunk, uint32_t iters,
                               float* ms_out, void* stream);
 
+/* Launches a kernel that holds every SM (ctas_per_sm x 1024 threads per SM,
+ * 1..2) until *release_word (host-mapped) becomes nonzero or timeout_ms
+ * passes: the proxy agent's copies and memops must progress meanwhile. */
+int ginsim_cuda_occupy(int device, uint32_t ctas_per_sm, const uint32_t* release_word, uint64_t timeout_ms,
+                       void* stream);
+
 /* One-sided all-to-all via put+signal: every rank puts
  * `bytes_per_peer` from send_win[dst*M] to dst's recv_win[src*M] and signals
  * `signal_id` on dst; then waits until the cell >= expected. */
@@ -308,6 +314,13 @@ int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const vo
  * bf16) once the flag reaches T*K (:227-242). */
 int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* weights,
                             void* const* out, void* stream);
+
+/* Phase timeline of the last dispatch (kernel 0), combine send (1) and
+ * combine reduce (2) launches: per CTA, 8 %globaltimer stamps (ns; unused = 0)
+ * into out[1024*8]; *ctas = that kernel's grid.  Needs GINSIM_PROFILE_PHASES=1
+ * when the moe handle was created.  Dispatch stamps: start, route tables done,
+ * puts issued+drained, releases issued, experts acquired. */
+int ginsim_cuda_moe_phase_times(ginsim_cuda_moe_t moe, uint32_t kernel, uint64_t* out, uint32_t* ctas);
 
 /* Per-launch kernel count of the last dispatch/combine (for bench evidence). */
 int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t* threads);

@@ -16,7 +16,7 @@ from ctypes import (POINTER, byref, c_char_p, c_int, c_int32, c_size_t, c_uint8,
                     c_uint64, c_void_p)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libginsim_b200.so")
+LIB_PATH = os.environ.get("GINSIM_LIB") or os.path.join(_HERE, "_lib", "libginsim_b200.so")
 
 # --------------------------------------------------------------------- errors
 # One class per ginsim exception (errors.hpp:24-52), codes as in ginsim_cuda.h.
@@ -202,6 +202,7 @@ def _declare(L):
                                     POINTER(ctypes.c_float), P], c_int),
         "ginsim_cuda_copy_bench_ex": ([P, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, c_uint32,
                                        c_uint32, POINTER(ctypes.c_float), P], c_int),
+        "ginsim_cuda_occupy": ([c_int, c_uint32, P, c_uint64, P], c_int),
         "ginsim_cuda_ring":([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, P], c_int),
         "ginsim_cuda_moe_ht_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, P], c_int),
         "ginsim_cuda_moe_create": ([P, POINTER(MoeConfig), POINTER(P)], c_int),
@@ -210,10 +211,15 @@ def _declare(L):
         "ginsim_cuda_moe_generate": ([P, c_uint64, c_uint32, P, P, P, P], c_int),
         "ginsim_cuda_moe_dispatch": ([POINTER(P), c_uint32, POINTER(P), POINTER(P), P], c_int),
         "ginsim_cuda_moe_combine": ([POINTER(P), c_uint32, POINTER(P), POINTER(P), P], c_int),
+        "ginsim_cuda_moe_phase_times": ([P, c_uint32, POINTER(c_uint64), POINTER(c_uint32)], c_int),
         "ginsim_cuda_moe_last_launch": ([P, POINTER(c_uint32), POINTER(c_uint32)], c_int),
     }
     for name, (args, res) in sigs.items():
-        fn = getattr(L, name)
+        fn = getattr(L, name, None)
+        if fn is None and os.environ.get("GINSIM_LIB"):  # an older build loaded for an A/B comparison
+            continue
+        if fn is None:
+            raise ImportError(f"{LIB_PATH} does not export {name}")
         fn.argtypes = args
         fn.restype = res
 
@@ -500,6 +506,15 @@ class Moe:
         a, b = c_uint32(), c_uint32()
         check(lib().ginsim_cuda_moe_last_launch(self.h, byref(a), byref(b)))
         return a.value, b.value
+
+    def phase_times(self, kernel):
+        """[ctas][8] %globaltimer stamps of the last launch of `kernel` (0 dispatch,
+        1 combine send, 2 reduce); needs GINSIM_PROFILE_PHASES=1 at creation."""
+        import numpy as np
+        buf = (c_uint64 * (1024 * 8))()
+        g = c_uint32()
+        check(lib().ginsim_cuda_moe_phase_times(self.h, kernel, buf, byref(g)))
+        return np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8)[:g.value].copy()
 
     def destroy(self):
         if self.h:

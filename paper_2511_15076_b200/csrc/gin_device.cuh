@@ -216,10 +216,16 @@ class Gin {
     const uint32_t p = team.world_rank(peer);
     if (!check_range(dst_win, p, dst_off, bytes) || !check_range(src_win, v_->rank, src_off, bytes)) return;
     if (v_->backend == GIN_BACKEND_PROXY) {
+      // Loopback (peer == self): a same-device cudaMemcpyAsync runs as a copy
+      // KERNEL, which cannot start while the issuing kernel holds every SM
+      // (tools/copy_engine_probe.py), so the coop moves the bytes itself and
+      // the descriptor carries only the completion action (a zero-byte put).
+      const bool loopback = p == v_->rank;
+      if (loopback && bytes) coop_copy(c, window_ptr(dst_win, p, dst_off), window_ptr(src_win, v_->rank, src_off), bytes);
       c.sync();
       if (c.rank() == 0) {
         uint8_t flags = 0;
-        submit(GIN_OP_PUT, team, peer, dst_win, dst_off, src_win, src_off, bytes, a, flags);
+        submit(GIN_OP_PUT, team, peer, dst_win, dst_off, src_win, src_off, loopback ? 0 : bytes, a, flags);
       }
       c.sync();
       return;

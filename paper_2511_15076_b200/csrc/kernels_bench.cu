@@ -103,6 +103,18 @@ __global__ void __launch_bounds__(kCopyThreads) tma_store_only_kernel(char* dst,
   gin::tma::wait_all();
 }
 
+// Occupies every SM (ctas_per_sm CTAs of 1024 threads each) until the
+// host-mapped release word becomes nonzero: used to check that the proxy
+// agent's copies and stream memops progress while a persistent kernel holds
+// the whole GPU (they must run on the copy engines / front end, not on SMs).
+__global__ void __launch_bounds__(1024) occupy_kernel(const volatile uint32_t* release, uint64_t timeout_ns) {
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = gin::globaltimer();
+    while (*release == 0 && gin::globaltimer() - t0 < timeout_ns) __nanosleep(1000);
+  }
+  __syncthreads();
+}
+
 }  // namespace ginsim_b200
 
 using namespace ginsim_b200;
@@ -209,6 +221,19 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
   *ms_out = ms / (float)std::max(1u, iters);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  GIN_API_END
+}
+
+int ginsim_cuda_occupy(int device, uint32_t ctas_per_sm, const uint32_t* release_word, uint64_t timeout_ms,
+                       void* stream) {
+  GIN_API_BEGIN
+  DeviceGuard g(device);
+  int sms = 0;
+  GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const uint32_t per = std::max(1u, std::min(ctas_per_sm, 2u));
+  occupy_kernel<<<sms * per, 1024, 0, (cudaStream_t)stream>>>(reinterpret_cast<const volatile uint32_t*>(release_word),
+                                                              timeout_ms * 1000000ull);
+  GIN_CUDA(cudaGetLastError());
   GIN_API_END
 }
 

@@ -39,24 +39,36 @@ namespace ginsim_b200 {
 constexpr int kMoeThreads = 512;
 constexpr int kMoeWarps = kMoeThreads / 32;
 constexpr uint32_t kMaxExperts = 1024;
+constexpr uint32_t kMaxGrid = 1024;  // CTAs per rank of one launch
 
 struct MoeRankArgs {
   const GinDevCommView* view;
   unsigned int* ws;           // per-moe arrival counters [0] dispatch [1] combine [2] slot barrier
-  uint32_t* slot_g;           // [T][K] slot table published for interleaved dispatch (or null)
+  uint32_t* route;            // TMA dispatch scratch: hist [kMaxGrid][E], prefix [kMaxGrid][E], totals [E]
+  char** dst_g;               // TMA dispatch: [T][Kp] destination pointer of every (t, k) pair
   const uint16_t* x;          // [T][H]
   const int32_t* idx;         // [T][K]
   const void* weights;        // [T][K] u16 (mode 0) / f32 (mode 1)
   uint16_t* out;              // [T][H]
   uint64_t iteration;         // 1-based
+  uint64_t* prof;             // optional per-CTA %globaltimer stamps [3 kernels][1024 CTAs][8]
 };
+
+// Phase timeline (GINSIM_PROFILE_PHASES=1): thread 0 of each CTA stamps
+// %globaltimer at its phase boundaries; ginsim_cuda_moe_phase_times reads them.
+#define MOE_STAMP(R, kern, slot)                                                                  \
+  do {                                                                                            \
+    if ((R).prof && threadIdx.x == 0)                                                             \
+      (R).prof[((uint64_t)(kern) * 1024 + blockIdx.x) * 8 + (slot)] = gin::globaltimer();         \
+  } while (0)
 
 struct MoeLaunch {
   MoeRankArgs r[GIN_MAX_RANKS];
   uint32_t E, K, T, H, mode, layout, e_local, parts, cparts;
-  uint32_t win_dispatch, win_counts, win_combine, interleave;
+  uint32_t win_dispatch, win_counts, win_combine;
   uint32_t win_stage, win_cstage, coalesce;  // proxy backend: dispatch / combine staging windows
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
+  uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -90,6 +102,47 @@ __device__ __forceinline__ uint4 transform_vec(uint4 v, uint32_t mode, uint32_t 
     v.w = bf16x2_transform(v.w, s, c);
   }
   return v;
+}
+
+// Per-source exclusive prefix over the experts of this rank (compact layout):
+// src_prefix[e*n+s] = sum_{e'<e} cnt[e'*n+s]; one warp per source.
+template <int WARPS>
+__device__ __forceinline__ void source_prefix(const uint32_t* cnt, uint32_t* src_prefix, uint32_t n, uint32_t e_local) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t sidx = warp; sidx < n; sidx += WARPS) {
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < e_local; c0 += 32) {
+      const uint32_t e = c0 + lane;
+      const uint32_t xv = e < e_local ? cnt[e * n + sidx] : 0u;
+      uint32_t incl = xv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      if (e < e_local) src_prefix[e * n + sidx] = carry + incl - xv;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+}
+
+// Per-expert release of one dispatch (harness_moe.cpp:163-167) issued by the
+// last CTA: one thread per destination rank writes that rank's counts, fences
+// once, then adds (1<<32)+count to each of its experts' cells with relaxed
+// reductions -- a release pattern (fence.acq_rel.sys then strong writes by the
+// same thread) that costs one .sys fence per destination instead of one
+// MEMBAR.SYS per expert (red.release.sys).
+__device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDevCommView* v, uint32_t win_counts,
+                                                const uint32_t* hist, uint32_t n, uint32_t rank, uint32_t e_local) {
+  const uint32_t d = threadIdx.x;
+  if (d >= n) return;
+  uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[win_counts].base[d]);
+  gin::fence_acq_rel_sys();
+  for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
+    gin::st_relaxed_sys32(cb + (uint64_t)e_loc * n + rank, hist[d * e_local + e_loc]);
+  gin::fence_acq_rel_sys();
+  for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
+    gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_loc), (1ull << 32) + hist[d * e_local + e_loc]);
 }
 
 // Block-wide exclusive scan of n <= 4*kMoeThreads u32 values in smem.
@@ -129,6 +182,42 @@ __device__ void block_exclusive_scan(uint32_t* data, uint32_t n, uint32_t* warp_
 }
 
 // ------------------------------------------------------------------ dispatch
+// Phase A of every dispatch kernel: per-expert totals over the whole route
+// table (hist), the counts of the pairs before this CTA's first token (run)
+// and, optionally, a copy of this CTA's own pairs [pre_end, pre_end+nq).
+// Every CTA reads all T*K indices from L2, so the loads are issued 16 bytes
+// and 8 entries per thread at a time -- a scalar loop with a data-dependent
+// store in its body is not unrolled by the compiler and serialises T*K/threads
+// L2 round trips (~40 us at T=4096, measured).
+template <int THREADS>
+__device__ __forceinline__ void histogram_pass(const int32_t* idx, uint32_t TK, uint32_t pre_end, uint32_t nq,
+                                               uint32_t* hist, uint32_t* run, uint32_t* own) {
+  const uint32_t tid = threadIdx.x;
+  auto take = [&](uint32_t j, uint32_t e) {
+    atomicAdd(&hist[e], 1u);
+    if (j < pre_end) atomicAdd(&run[e], 1u);
+    else if (own && j - pre_end < nq) own[j - pre_end] = e;
+  };
+  uint32_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(idx) & 15) == 0) {
+    const int4* v = reinterpret_cast<const int4*>(idx);
+    const uint32_t n4 = TK / 4;
+    uint32_t q = tid;
+    for (; q + THREADS < n4; q += 2 * THREADS) {
+      const int4 a = __ldg(v + q), b = __ldg(v + q + THREADS);
+      take(4 * q, a.x), take(4 * q + 1, a.y), take(4 * q + 2, a.z), take(4 * q + 3, a.w);
+      const uint32_t jb = 4 * (q + THREADS);
+      take(jb, b.x), take(jb + 1, b.y), take(jb + 2, b.z), take(jb + 3, b.w);
+    }
+    for (; q < n4; q += THREADS) {
+      const int4 a = __ldg(v + q);
+      take(4 * q, a.x), take(4 * q + 1, a.y), take(4 * q + 2, a.z), take(4 * q + 3, a.w);
+    }
+    done = n4 * 4;
+  }
+  for (uint32_t j = done + tid; j < TK; j += THREADS) take(j, (uint32_t)__ldg(idx + j));
+}
+
 // PROXY = the Proxy backend: rows are staged into a local
 // registered window laid out in destination order -- (dst_base[dst] +
 // prefix_e[e] + slot) -- so every expert's messages form ONE contiguous run
@@ -166,11 +255,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
   __syncthreads();
   // Phase A: per-expert totals and the prefix of tokens before this CTA.
   const uint32_t TK = T * K, pre_end = t0 * K;
-  for (uint32_t j = tid; j < TK; j += kMoeThreads) {
-    const uint32_t e = (uint32_t)R.idx[j];
-    atomicAdd(&hist_all[e], 1u);
-    if (j < pre_end) atomicAdd(&run[e], 1u);
-  }
+  histogram_pass<kMoeThreads>(R.idx, TK, pre_end, 0, hist_all, run, nullptr);
   __syncthreads();
   // Destination base offsets for the compact layout: exclusive prefix of this
   // source's counts within each destination's expert group.
@@ -221,7 +306,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
       const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
       const uint32_t dst = e / e_local, e_loc = e % e_local;
       const uint32_t slot = slots[(t - t0) * K + lane];
-      if (PROXY) {
+      if (PROXY && dst != rank) {
         my_dst = v->win[L.win_stage].base[rank] + ((uint64_t)dst_base[dst] + prefix_e[e] + slot) * dmsg;
       } else {
         const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
@@ -299,7 +384,11 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
       const uint64_t dst0 = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T) * dmsg
                                           : ((uint64_t)rank * T * K + prefix_e[e]) * dmsg;
       const gin::Action rel = gin::SignalAction(e_loc, gin::SignalAdd((1ull << 32) + cnt));
-      if (L.coalesce) {
+      if (dst == rank) {
+        // own experts: rows were written in place by the SMs (a same-device
+        // copy by the agent would need SMs this kernel holds); release only
+        g.signal(me, world, dst, e_loc, rel.op);
+      } else if (L.coalesce) {
         g.put(me, world, dst, L.win_dispatch, dst0, L.win_stage, src0, (uint64_t)cnt * dmsg, rel);
       } else {
         for (uint32_t q = 0; q < cnt; ++q)
@@ -308,12 +397,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
       }
     }
   } else if (is_last) {
-    uint32_t* const* cbase = reinterpret_cast<uint32_t* const*>(v->win[L.win_counts].base);
-    for (uint32_t e = tid; e < E; e += kMoeThreads) {
-      const uint32_t dst = e / e_local, e_loc = e % e_local;
-      gin::st_relaxed_sys32(cbase[dst] + (uint64_t)e_loc * n + rank, hist_all[e]);
-      gin.release_signal_raw(dst, e_loc, (1ull << 32) + hist_all[e]);
-    }
+    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local);
   }
   // Phase D: return once every local expert has been released by every source.
   if (tid == 0) {
@@ -363,15 +447,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
     pair_start[i] = c;
   }
   __syncthreads();
-  if (L.layout == 1) {
-    for (uint32_t s = tid; s < n; s += kMoeThreads) {
-      uint32_t acc = 0;
-      for (uint32_t e = 0; e < e_local; ++e) {
-        src_prefix[e * n + s] = acc;
-        acc += cnt[e * n + s];
-      }
-    }
-  }
+  if (L.layout == 1) source_prefix<kMoeWarps>(cnt, src_prefix, n, e_local);
   block_exclusive_scan(pair_start, P, warp_tot, &total_msgs);
   if (tid == 0) pair_start[P] = total_msgs;
   __syncthreads();
@@ -406,8 +482,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       k = meta[8] | (meta[9] << 8) | (meta[10] << 16) | ((uint32_t)meta[11] << 24);
     }
     const uint32_t e = rank * e_local + e_loc;
-    char* dst = PROXY ? v->win[L.win_cstage].base[rank] + (uint64_t)m * cmsg
-                      : cbases[src] + ((uint64_t)token * K + k) * cmsg;
+    char* dst = (PROXY && src != rank) ? v->win[L.win_cstage].base[rank] + (uint64_t)m * cmsg
+                                       : cbases[src] + ((uint64_t)token * K + k) * cmsg;
     if (vec_ok) {
       const uint32_t vlo = p * vec_per_part, vhi = min(vlo + vec_per_part, nvec);
       uint32_t i = vlo + lane;
@@ -449,7 +525,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc) {
         if ((rank * e_local + e_loc) % n_ctx != ctx) continue;
         const uint32_t pr = e_loc * n + src;
-        for (uint32_t slot = 0; slot < cnt[pr]; ++slot) {
+        for (uint32_t slot = 0; src != rank && slot < cnt[pr]; ++slot) {  // own tokens were written in place
           const uint64_t moff = L.layout == 0 ? (((uint64_t)e_loc * n + src) * T + slot) * dmsg
                                               : ((uint64_t)src * T * K + src_prefix[pr] + slot) * dmsg;
           const unsigned char* meta = reinterpret_cast<const unsigned char*>(recv + moff + payload);
@@ -575,7 +651,10 @@ constexpr int kTmaStages = 3;
 struct TmaSmem {  // per-warp control block, followed by the staging buffers
   uint64_t bar[kTmaStages];
   char* dptr[32];
+  uint64_t itm[kTmaStages];  // item held by each stage (~0 = none)
+  uint64_t cur, end;         // item source: static sequence number, or the grabbed batch [cur, end)
 };
+constexpr uint64_t kNoItem = ~0ull;
 
 __device__ __forceinline__ uint32_t tma_chunk_len(uint32_t payload, uint32_t chunk, uint32_t p) {
   return min(chunk, payload - p * chunk);
@@ -626,10 +705,43 @@ __device__ __forceinline__ uint4 reduce_vec(const uint4* y, uint32_t K, uint32_t
   return make_uint4(pk[0], pk[1], pk[2], pk[3]);
 }
 
-// CPASYNC: the row chunk is loaded by all 32 lanes with 16-byte cp.async
-// (LSU path) instead of a TMA bulk load, so loads never queue behind the K
-// bulk stores in the SM's TMA unit; the stores stay TMA bulk copies.
-template <int KMAX, bool CPASYNC>
+// Grid-wide barrier among the G CTAs of one rank's cooperative launch: a
+// monotone arrival counter (target = iteration * G), so it needs no reset.
+__device__ __forceinline__ void rank_grid_barrier(unsigned int* ctr, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gin::fence_acq_rel_gpu();
+    atomicAdd(ctr, 1u);
+    while (true) {
+      unsigned cur;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+      if (cur >= target) break;
+      __nanosleep(20);
+    }
+  }
+  __syncthreads();
+}
+
+// Dispatch over the TMA engine.
+//  Phase A (route tables, cooperative): CTA b histograms only its own token
+//    range into a global row hist[b][E]; after a grid barrier, warp w of CTA
+//    b scans expert e = b + w*G down the G rows (exclusive prefix = the slots
+//    already taken by earlier CTAs, total = the expert's count); after a
+//    second barrier every CTA reads its prefix row and assigns the reference
+//    slot numbers to its own (t, k) pairs in (t, k) order
+//    (harness_moe.cpp:143-150), writing each pair's destination pointer to a
+//    global table dst_g[t][Kp]; a third barrier publishes the table.  Every
+//    CTA touches O(E + own pairs) entries instead of scanning all T*K routes
+//    with shared-memory atomics (which cost ~20 us per launch at T=4096).
+//  Phase B (puts): per-warp 3-stage TMA pipeline over (token, chunk) items;
+//    a stage's mbarrier covers both the row chunk and the token's K
+//    destination pointers (one 64-byte bulk load from dst_g), so no lane ever
+//    waits on a global load; lane 0 bulk-stores the chunk to the K
+//    destinations (local HBM or NVLink peer mappings).  Items come from a
+//    device counter in one-token batches (L.dyn), so warps whose messages go
+//    to slower destinations take fewer tokens and the grid ends together.
+//  Phase C/D: last-CTA release per expert, then acquire of local experts.
+template <int KMAX>
 __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLaunch L, uint32_t chunk) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
@@ -639,157 +751,210 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t dmsg = 2ull * H + 16;
   const uint32_t payload = 2u * H, parts = L.parts;
+  const uint32_t Kp = (K + 1) & ~1u;  // dst_g row stride: 16-byte rows for the bulk load
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
+  const unsigned int bar_target = (unsigned int)(R.iteration * G);
+  MOE_STAMP(R, 0, 0);
 
   __shared__ uint32_t hist_all[kMaxExperts], run[kMaxExperts], prefix_e[kMaxExperts];
+  __shared__ char* sbase[GIN_MAX_RANKS];
   __shared__ int is_last;
   extern __shared__ __align__(128) char dsm[];
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
-  char* stage = dsm + sizeof(TmaSmem) * kTmaWarps + (size_t)warp * kTmaStages * chunk;
-  uint32_t* slots = reinterpret_cast<uint32_t*>(dsm + sizeof(TmaSmem) * kTmaWarps + (size_t)kTmaWarps * kTmaStages * chunk);
+  // per stage: [dst pointers: Kp * 8 bytes, padded to 128][row chunk]
+  const uint32_t dhead = (Kp * 8 + 127) & ~127u;
+  const uint32_t sstride = dhead + chunk;
+  char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kTmaStages * sstride;
+  uint32_t* own = reinterpret_cast<uint32_t*>(dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) +
+                                              (size_t)kTmaWarps * kTmaStages * sstride);  // [(t1-t0)*K]
+  uint32_t* g_hist = R.route;                                  // [G][E]
+  uint32_t* g_pre = R.route + (size_t)kMaxGrid * kMaxExperts;  // [G][E]
+  uint32_t* g_tot = R.route + 2 * (size_t)kMaxGrid * kMaxExperts;  // [E]
+  char** dst_g = R.dst_g;                                      // [T][Kp]
 
-  for (uint32_t e = tid; e < E; e += kTmaThreads) {
-    hist_all[e] = 0;
-    run[e] = 0;
-  }
+  for (uint32_t e = tid; e < E; e += kTmaThreads) hist_all[e] = 0;
   if (lane == 0) {
     for (int s = 0; s < kTmaStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
     gin::tma::fence_mbar_init();
   }
+  if (tid < n) sbase[tid] = v->win[L.win_dispatch].base[tid];
   __syncthreads();
-  const uint32_t TK = T * K, pre_end = t0 * K;
-  for (uint32_t j = tid; j < TK; j += kTmaThreads) {
-    const uint32_t e = (uint32_t)R.idx[j];
+  // Work source for Phase B.
+  const char* x = reinterpret_cast<const char*>(R.x);
+  const uint64_t items = (uint64_t)T * parts;
+  const uint64_t gw = (uint64_t)b * kTmaWarps + warp, wstride = (uint64_t)G * kTmaWarps;
+  unsigned long long* grab_ctr = reinterpret_cast<unsigned long long*>(R.ws + 10);
+  auto next_item = [&]() -> uint64_t {  // lane 0 only
+    uint64_t it;
+    if (L.dyn) {
+      if (ctl->cur >= ctl->end) {  // one token per grab, after the static first round
+        ctl->cur = (uint64_t)kTmaStages * wstride + atomicAdd(grab_ctr, (unsigned long long)parts);
+        ctl->end = ctl->cur + parts;
+      }
+      it = ctl->cur++;
+    } else {
+      it = gw + (ctl->cur++) * wstride;
+    }
+    return it < items ? it : kNoItem;
+  };
+  // A stage's mbarrier expects the row chunk AND the token's destination row;
+  // the row chunk does not depend on routing, so it can be requested first.
+  auto issue_row = [&](int s, uint64_t it) {  // lane 0
+    const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
+    const uint32_t len = tma_chunk_len(payload, chunk, p);
+    char* sb = stage + (size_t)s * sstride;
+    gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len + Kp * 8);
+    gin::tma::load(sb + dhead, x + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
+  };
+  auto issue_dst = [&](int s, uint64_t it) {  // lane 0, once dst_g is published
+    const uint32_t t = (uint32_t)(it / parts);
+    gin::tma::load(stage + (size_t)s * sstride, dst_g + (uint64_t)t * Kp, Kp * 8, &ctl->bar[s]);
+  };
+  if (lane == 0) {
+    // first round static (warp gw: items [gw*S, gw*S+S)), so 1000+ warps do
+    // not all hit the grab counter at once when the kernel starts
+    ctl->cur = L.dyn ? gw * kTmaStages : 0;
+    ctl->end = L.dyn ? gw * kTmaStages + kTmaStages : 0;
+    for (int s = 0; s < kTmaStages; ++s) {
+      const uint64_t it = next_item();
+      ctl->itm[s] = it;
+      if (it != kNoItem) issue_row(s, it);
+    }
+  }
+  // A0: own routes -> smem + own histogram -> global row
+  const uint32_t nq = (t1 - t0) * K;
+  for (uint32_t q = tid; q < nq; q += kTmaThreads) {
+    const uint32_t e = (uint32_t)__ldg(R.idx + (uint64_t)t0 * K + q);
+    own[q] = e;
     atomicAdd(&hist_all[e], 1u);
-    if (j < pre_end) atomicAdd(&run[e], 1u);
   }
   __syncthreads();
-  if (L.layout == 1) {
-    for (uint32_t d = tid; d < n; d += kTmaThreads) {
-      uint32_t acc = 0;
-      for (uint32_t e = d * e_local; e < (d + 1) * e_local; ++e) {
-        prefix_e[e] = acc;
-        acc += hist_all[e];
+  for (uint32_t e = tid; e < E; e += kTmaThreads) g_hist[(size_t)b * E + e] = hist_all[e];
+  MOE_STAMP(R, 0, 1);
+  rank_grid_barrier(R.ws + 3, bar_target);
+  // A1: column scans, one warp per expert e = b + w*G
+  for (uint32_t e = b + warp * G; e < E; e += kTmaWarps * G) {
+    uint32_t carry = 0;
+    auto scan_chunk = [&](uint32_t c0, uint32_t x) {
+      uint32_t incl = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      if (c0 + lane < G) g_pre[(size_t)(c0 + lane) * E + e] = carry + incl - x;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    };
+    uint32_t pre[8];  // the first 256 rows' loads in flight together
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t bb = c * 32 + lane;
+      pre[c] = bb < G ? __ldcg(g_hist + (size_t)bb * E + e) : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if ((uint32_t)c * 32 < G) scan_chunk(c * 32, pre[c]);
+    for (uint32_t c0 = 256; c0 < G; c0 += 32)
+      scan_chunk(c0, c0 + lane < G ? __ldcg(g_hist + (size_t)(c0 + lane) * E + e) : 0u);
+    if (lane == 0) g_tot[e] = carry;
+  }
+  MOE_STAMP(R, 0, 2);
+  rank_grid_barrier(R.ws + 4, bar_target);
+  // A2: this CTA's prefix row and the totals; reference slot numbers
+  for (uint32_t e = tid; e < E; e += kTmaThreads) {
+    run[e] = __ldcg(g_pre + (size_t)b * E + e);
+    hist_all[e] = __ldcg(g_tot + e);
+  }
+  __syncthreads();
+  if (L.layout == 1) {  // per-destination exclusive prefix of the expert totals, one warp per destination
+    for (uint32_t d = warp; d < n; d += kTmaWarps) {
+      uint32_t carry = 0;
+      for (uint32_t c0 = 0; c0 < e_local; c0 += 32) {
+        const uint32_t e = d * e_local + c0 + lane;
+        const uint32_t xv = c0 + lane < e_local ? hist_all[e] : 0u;
+        uint32_t incl = xv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        if (c0 + lane < e_local) prefix_e[e] = carry + incl - xv;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
   }
+  __syncthreads();
   if (warp == 0) {
-    for (uint32_t t = t0; t < t1; ++t) {
-      if (lane < K) {
-        const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
-        const uint32_t s = run[e];
-        run[e] = s + 1;
-        slots[(t - t0) * K + lane] = s;
+    // Reference slot order (t, k ascending): 32 pairs at a time; lanes with the
+    // same expert rank themselves by lane (match_any) and the group's lowest
+    // lane advances the expert's running count.
+    for (uint32_t c0 = 0; c0 < nq; c0 += 32) {
+      const uint32_t q = c0 + lane;
+      const bool valid = q < nq;
+      const uint32_t e = valid ? own[q] : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, e);
+      const uint32_t before = __popc(peers & ((1u << lane) - 1u));
+      const uint32_t base = valid ? run[e] : 0u;
+      __syncwarp();
+      if (valid) {
+        if (before == 0) run[e] = base + __popc(peers);
+        const uint32_t slot = base + before;
+        const uint32_t t = t0 + q / K, k = q % K;
+        const uint32_t dst = e / e_local, e_loc = e % e_local;
+        const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
+                                           : ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
+        dst_g[(uint64_t)t * Kp + k] = sbase[dst] + off;
       }
       __syncwarp();
     }
+    gin::tma::fence_proxy_async_global();  // generic writes of dst_g -> read by other CTAs' bulk loads
   }
-  __syncthreads();
+  MOE_STAMP(R, 0, 3);
+  rank_grid_barrier(R.ws + 5, bar_target);
+  MOE_STAMP(R, 0, 4);
 
-  // Phase B: per-warp TMA pipeline over (token, chunk) items.  With more
-  // tokens than CTAs the slot numbers are published to a global table and,
-  // after a grid barrier, items are interleaved over EVERY warp of the rank
-  // (item = warp_id + j * total_warps): each warp gets a random mix of local
-  // and remote destinations, so no CTA is left holding a remote-heavy tail.
-  char* const* bases = v->win[L.win_dispatch].base;
-  const bool global = L.interleave && R.slot_g != nullptr && T > G;
-  if (global) {
-    for (uint32_t q = tid; q < (t1 - t0) * K; q += kTmaThreads) R.slot_g[(uint64_t)t0 * K + q] = slots[q];
-    __syncthreads();
-    if (tid == 0) {
-      gin::fence_acq_rel_gpu();
-      atomicAdd(R.ws + 2, 1u);
-      const unsigned want = (unsigned)(R.iteration * G);
-      while (true) {
-        unsigned cur;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(R.ws + 2) : "memory");
-        if (cur >= want) break;
-        __nanosleep(32);
-      }
-    }
-    __syncthreads();
+  // Phase B (the first stages' row chunks were requested before Phase A)
+  if (lane == 0) {
+    gin::tma::fence_proxy_async_global();
+    for (int s = 0; s < kTmaStages; ++s)
+      if (ctl->itm[s] != kNoItem) issue_dst(s, ctl->itm[s]);
   }
-  const uint32_t items = global ? T * parts : (t1 - t0) * parts;
-  const uint32_t wid = global ? b * kTmaWarps + warp : warp;
-  const uint32_t wstride = global ? G * kTmaWarps : kTmaWarps;
-  const uint32_t tbase = global ? 0 : t0;
-  const char* x = reinterpret_cast<const char*>(R.x);
-  auto issue_load = [&](int s, uint32_t item) {
-    const uint32_t t = tbase + item / parts, p = item % parts;
-    const uint32_t len = tma_chunk_len(payload, chunk, p);
-    gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len);
-    gin::tma::load(stage + (size_t)s * chunk, x + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
-  };
-  // cp.async variant: every lane copies its 16-byte vectors of the chunk;
-  // one commit group per item (item j of this warp is group j).
-  auto cp_load = [&](int s, uint32_t item) {
-    const uint32_t t = tbase + item / parts, p = item % parts;
-    const uint32_t len = tma_chunk_len(payload, chunk, p);
-    const char* src = x + (uint64_t)t * payload + (uint64_t)p * chunk;
-    char* dst = stage + (size_t)s * chunk;
-    for (uint32_t o = lane * 16; o < len; o += 32 * 16)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(gin::tma::smem_u32(dst + o)), "l"(src + o)
-                   : "memory");
-  };
-  if (CPASYNC) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      const uint32_t item = wid + s * wstride;
-      if (item < items) cp_load(s, item);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-  } else if (lane == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      const uint32_t item = wid + s * wstride;
-      if (item < items) issue_load(s, item);
-    }
-  }
+  __syncwarp();
   for (uint32_t j = 0;; ++j) {
-    const uint32_t item = wid + j * wstride;
-    if (item >= items) break;
-    const uint32_t t = tbase + item / parts, p = item % parts;
     const int s = (int)(j % kTmaStages);
-    if (CPASYNC) {
-      if (j == 0) asm volatile("cp.async.wait_group %0;" ::"n"(kTmaStages - 1) : "memory");
-      else asm volatile("cp.async.wait_group %0;" ::"n"(kTmaStages - 2) : "memory");
-    }
-    if (lane < K) {
-      const uint32_t e = (uint32_t)R.idx[(uint64_t)t * K + lane];
-      const uint32_t dst = e / e_local, e_loc = e % e_local;
-      const uint32_t slot = global ? R.slot_g[(uint64_t)t * K + lane] : slots[(t - t0) * K + lane];
-      const uint64_t off = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T + slot) * dmsg
-                                         : ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
-      char* d = bases[dst] + off;
-      ctl->dptr[lane] = d;
-      if (p == 0) gin::st_v4(d + payload, make_uint4(rank, t, lane, lane + 1));  // meta
-    }
-    if (CPASYNC) gin::tma::fence_proxy_async_shared();  // cp.async writes -> visible to the bulk stores
-    __syncwarp();
+    const uint64_t it = ctl->itm[s];
+    if (it == kNoItem) break;
+    const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
+    char* sb = stage + (size_t)s * sstride;
+    char* const* dp = reinterpret_cast<char* const*>(sb);
+    gin::tma::mbar_wait(&ctl->bar[s], (j / kTmaStages) & 1);
+    if (p == 0 && lane < K) gin::st_v4(dp[lane] + payload, make_uint4(rank, t, lane, lane + 1));  // meta
     if (lane == 0) {
       const uint32_t len = tma_chunk_len(payload, chunk, p);
-      if (!CPASYNC) gin::tma::mbar_wait(&ctl->bar[s], (j / kTmaStages) & 1);
-      for (uint32_t k = 0; k < K; ++k) gin::tma::store(ctl->dptr[k] + (uint64_t)p * chunk, stage + (size_t)s * chunk, len);
+      for (uint32_t k = 0; k < K; ++k) gin::tma::store(dp[k] + (uint64_t)p * chunk, sb + dhead, len);
       gin::tma::commit();
       // Refill the stage of the PREVIOUS item: its stores were committed one
       // iteration ago, so their shared-memory reads overlapped this wait.
       if (j >= 1) {
         gin::tma::wait_read<1>();
-        const uint32_t nxt = item - wstride + kTmaStages * wstride;
-        if (!CPASYNC && nxt < items) issue_load((int)((j - 1) % kTmaStages), nxt);
+        const int ps = (int)((j - 1) % kTmaStages);
+        const uint64_t nxt = next_item();
+        ctl->itm[ps] = nxt;
+        if (nxt != kNoItem) {
+          issue_row(ps, nxt);
+          issue_dst(ps, nxt);
+        }
       }
     }
     __syncwarp();
-    if (CPASYNC && j >= 1) {
-      const uint32_t nxt = item - wstride + kTmaStages * wstride;
-      if (nxt < items) cp_load((int)((j - 1) % kTmaStages), nxt);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
   }
   if (lane == 0) {
     gin::tma::wait_all();
     gin::tma::fence_proxy_async_global();
   }
 
-  // Phase C/D exactly as the LSU kernel.
+  // Phase C/D as the LSU kernel.
+  MOE_STAMP(R, 0, 5);
   __syncthreads();
   if (tid == 0) {
     gin::fence_acq_rel_sys();
@@ -799,18 +964,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   }
   __syncthreads();
   if (is_last) {
-    uint32_t* const* cbase = reinterpret_cast<uint32_t* const*>(v->win[L.win_counts].base);
-    for (uint32_t e = tid; e < E; e += kTmaThreads) {
-      const uint32_t dst = e / e_local, e_loc = e % e_local;
-      gin::st_relaxed_sys32(cbase[dst] + (uint64_t)e_loc * n + rank, hist_all[e]);
-      gin.release_signal_raw(dst, e_loc, (1ull << 32) + hist_all[e]);
-    }
+    if (tid == 0) *grab_ctr = 0;  // every CTA is past Phase B
+    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local);
   }
+  MOE_STAMP(R, 0, 6);
   if (tid == 0) {
     const uint64_t want = R.iteration * ((uint64_t)n << 32);
     if (!L.no_wait)
       for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(e_loc, want);
   }
+  MOE_STAMP(R, 0, 7);
 }
 
 template <int KMAX>
@@ -827,6 +990,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t dmsg = 2ull * H + 16, cmsg = 2ull * H;
   const uint32_t payload = 2u * H, parts = L.cparts;
+  MOE_STAMP(R, 1, 0);
 
   __shared__ uint32_t cnt[kMaxExperts], pair_start[kMaxExperts + 1], src_prefix[kMaxExperts];
   __shared__ uint32_t warp_tot[kMoeWarps];
@@ -849,15 +1013,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     gin::tma::fence_mbar_init();
   }
   __syncthreads();
-  if (L.layout == 1) {
-    for (uint32_t s = tid; s < n; s += kTmaThreads) {
-      uint32_t acc = 0;
-      for (uint32_t e = 0; e < e_local; ++e) {
-        src_prefix[e * n + s] = acc;
-        acc += cnt[e * n + s];
-      }
-    }
-  }
+  if (L.layout == 1) source_prefix<kTmaWarps>(cnt, src_prefix, n, e_local);
   // exclusive scan of P <= 1024 entries with 256 threads (4 per thread)
   {
     const uint32_t per = (P + kTmaThreads - 1) / kTmaThreads;
@@ -893,6 +1049,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     __syncthreads();
   }
 
+  MOE_STAMP(R, 1, 1);
   const char* recv = v->win[L.win_dispatch].base[rank];
   char* const* cbases = v->win[L.win_combine].base;
   const uint64_t items = (uint64_t)total_msgs * parts;
@@ -917,16 +1074,38 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len);
     gin::tma::load(stage + (size_t)s * chunk, msg + (uint64_t)p * chunk, len, &ctl->bar[s]);
   };
+  // Work source.  Static: warp gw takes items gw, gw+stride, ...  Dynamic
+  // (L.dyn): warps grab batches of one message's parts from a device counter,
+  // so CTAs whose messages go to slower (remote) destinations take fewer
+  // and the kernel has no straggler tail; the last CTA resets the counter.
+  unsigned long long* grab_ctr = reinterpret_cast<unsigned long long*>(R.ws + 8);
+  auto next_item = [&]() -> uint64_t {  // lane 0 only
+    uint64_t it;
+    if (L.dyn) {
+      if (ctl->cur >= ctl->end) {  // one message per grab, after the static first round
+        ctl->cur = (uint64_t)kTmaStages * stride + atomicAdd(grab_ctr, (unsigned long long)parts);
+        ctl->end = ctl->cur + parts;
+      }
+      it = ctl->cur++;
+    } else {
+      it = gw + (ctl->cur++) * stride;
+    }
+    return it < items ? it : kNoItem;
+  };
   if (lane == 0) {
+    ctl->cur = L.dyn ? gw * kTmaStages : 0;
+    ctl->end = L.dyn ? gw * kTmaStages + kTmaStages : 0;
     for (int s = 0; s < kTmaStages; ++s) {
-      const uint64_t it = gw + s * stride;
-      if (it < items) issue_load(s, it);
+      const uint64_t it = next_item();
+      ctl->itm[s] = it;
+      if (it != kNoItem) issue_load(s, it);
     }
   }
+  __syncwarp();
   for (uint64_t j = 0;; ++j) {
-    const uint64_t it = gw + j * stride;
-    if (it >= items) break;
     const int s = (int)(j % kTmaStages);
+    const uint64_t it = ctl->itm[s];
+    if (it == kNoItem) break;
     const uint32_t m = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
     uint32_t pr;
     const char* msg = locate(m, pr);
@@ -955,8 +1134,10 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       gin::tma::commit();
       if (j >= 1) {  // refill the previous item's stage (its store has been reading meanwhile)
         gin::tma::wait_read<1>();
-        const uint64_t nxt = it - stride + kTmaStages * stride;
-        if (nxt < items) issue_load((int)((j - 1) % kTmaStages), nxt);
+        const int ps = (int)((j - 1) % kTmaStages);
+        const uint64_t nxt = next_item();
+        ctl->itm[ps] = nxt;
+        if (nxt != kNoItem) issue_load(ps, nxt);
       }
     }
     __syncwarp();
@@ -965,6 +1146,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     gin::tma::wait_all();
     gin::tma::fence_proxy_async_global();
   }
+  MOE_STAMP(R, 1, 2);
 
   __syncthreads();
   if (tid == 0) {
@@ -975,6 +1157,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   }
   __syncthreads();
   if (is_last) {
+    if (tid == 0) *grab_ctr = 0;  // every CTA is past its loop: ready for the next launch
     for (uint32_t sc = tid; sc < n * n_ctx; sc += kTmaThreads) {
       const uint32_t src = sc / n_ctx, ctx = sc % n_ctx;
       uint32_t c = 0;
@@ -983,6 +1166,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       if (c) gin.release_signal_raw(src, e_local, c);
     }
   }
+  MOE_STAMP(R, 1, 3);
 }
 
 // Source side of the combine, split off the TMA send kernel so it runs at
@@ -1001,8 +1185,10 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   const uint64_t cmsg = 2ull * H;
   const uint32_t payload = 2u * H;
+  MOE_STAMP(R, 2, 0);
   if (tid == 0) gin.wait_ge_signal(e_local, R.iteration * (uint64_t)T * K);
   __syncthreads();
+  MOE_STAMP(R, 2, 1);
   const char* crecv = v->win[L.win_combine].base[rank];
   const uint32_t nvec = payload / 16;
   const uint64_t ritems = (uint64_t)T * nvec, rstride = (uint64_t)G * kMoeThreads;
@@ -1015,6 +1201,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
     gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
                reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
   }
+  MOE_STAMP(R, 2, 2);
 }
 
 // ------------------------------------------------------------------ synthetic inputs
@@ -1105,7 +1292,9 @@ struct ginsim_cuda_moe_s {
   void* buf_counts = nullptr;
   void* buf_combine = nullptr;
   unsigned int* ws = nullptr;
-  uint32_t* slot_g = nullptr;
+  uint32_t* route = nullptr;
+  char** dst_g = nullptr;
+  uint64_t* prof = nullptr;  // GINSIM_PROFILE_PHASES=1: [3][1024][8] %globaltimer stamps
   uint64_t iteration_dispatch = 0, iteration_combine = 0;
   uint32_t last_ctas = 0;
 };
@@ -1155,8 +1344,14 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   }
   DeviceGuard g(c->device);
   GIN_CUDA(cudaMalloc(&m->ws, 256));
-  GIN_CUDA(cudaMalloc(&m->slot_g, (size_t)cfg->tokens * cfg->top_k * 4));
+  GIN_CUDA(cudaMalloc(&m->route, (2 * (size_t)kMaxGrid + 1) * kMaxExperts * 4));
+  GIN_CUDA(cudaMalloc(&m->dst_g, (size_t)cfg->tokens * ((cfg->top_k + 1) & ~1u) * sizeof(char*)));
   GIN_CUDA(cudaMemset(m->ws, 0, 256));
+  const char* pp = std::getenv("GINSIM_PROFILE_PHASES");
+  if (pp && pp[0] == '1') {
+    GIN_CUDA(cudaMalloc(&m->prof, 3 * 1024 * 8 * sizeof(uint64_t)));
+    GIN_CUDA(cudaMemset(m->prof, 0, 3 * 1024 * 8 * sizeof(uint64_t)));
+  }
   *out = m.release();
   GIN_API_END
 }
@@ -1168,7 +1363,9 @@ int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
     DeviceGuard g(moe->comm->device);
     cudaDeviceSynchronize();
     if (moe->ws) cudaFree(moe->ws);
-    if (moe->slot_g) cudaFree(moe->slot_g);
+    if (moe->route) cudaFree(moe->route);
+    if (moe->dst_g) cudaFree(moe->dst_g);
+    if (moe->prof) cudaFree(moe->prof);
   }
   // window memory stays mapped until the comm is destroyed (windows are
   // never deregistered in the reference either).
@@ -1229,19 +1426,16 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   // (ncu serialises kernels, so a cross-GPU acquire would never complete).
   const char* nw = std::getenv("GINSIM_PROFILE_NO_WAIT");
   L.no_wait = (nw && nw[0] == '1') ? 1u : 0u;
-  // Interleaved dispatch (global slot table + grid barrier) measured slightly
-  // slower at 2 GPUs; opt in with GINSIM_DISPATCH_INTERLEAVE=1.
-  static const bool interleave = [] {
-    const char* v = std::getenv("GINSIM_DISPATCH_INTERLEAVE");
-    return v && v[0] == '1';
-  }();
-  L.interleave = interleave ? 1u : 0u;
+  const char* dy = std::getenv("GINSIM_MOE_SCHED");
+  L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
   for (uint32_t i = 0; i < n; ++i) {
     if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
     L.r[i].view = moes[i]->comm->dev_view;
     L.r[i].ws = moes[i]->ws;
-    L.r[i].slot_g = moes[i]->slot_g;
+    L.r[i].route = moes[i]->route;
+    L.r[i].dst_g = moes[i]->dst_g;
+    L.r[i].prof = moes[i]->prof;
   }
   return L;
 }
@@ -1282,11 +1476,7 @@ static MoeKernels kernels_of(const ginsim_cuda_moe_t m) {
     k.threads = kMoeThreads;
     return k;
   }
-  // GINSIM_DISPATCH_LOADS=cpasync: LSU cp.async row loads + TMA bulk stores
-  const char* lv = std::getenv("GINSIM_DISPATCH_LOADS");
-  const bool cpa = lv && std::strcmp(lv, "cpasync") == 0;
-  if (cpa) k.dispatch = k8 ? (const void*)moe_dispatch_tma_kernel<8, true> : (const void*)moe_dispatch_tma_kernel<32, true>;
-  else k.dispatch = k8 ? (const void*)moe_dispatch_tma_kernel<8, false> : (const void*)moe_dispatch_tma_kernel<32, false>;
+  k.dispatch = k8 ? (const void*)moe_dispatch_tma_kernel<8> : (const void*)moe_dispatch_tma_kernel<32>;
   k.threads = kTmaThreads;
   k.tma_dispatch = true;
   if (e == 3) {
@@ -1300,9 +1490,13 @@ static MoeKernels kernels_of(const ginsim_cuda_moe_t m) {
 }
 
 static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
-  const size_t slots = (size_t)((m->cfg.tokens + G - 1) / G + 1) * m->cfg.top_k * 4;
-  if (!kernels_of(m).tma_dispatch) return slots;
-  return sizeof(TmaSmem) * kTmaWarps + (size_t)kTmaWarps * kTmaStages * m->chunk + slots;
+  const size_t pairs = (size_t)((m->cfg.tokens + G - 1) / G + 1) * m->cfg.top_k;
+  if (!kernels_of(m).tma_dispatch) return pairs * 4;
+  // control blocks | stages of [destination row (padded to 128 B) | chunk] | own route indices
+  const size_t kp = (m->cfg.top_k + 1) & ~1u;
+  const size_t dhead = (kp * 8 + 127) & ~(size_t)127;
+  return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kTmaStages * (dhead + m->chunk) +
+         pairs * 4;
 }
 static size_t combine_smem(const ginsim_cuda_moe_t m) {
   if (!kernels_of(m).tma_combine) return 0;
@@ -1345,7 +1539,11 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
     if (G < 1) fail(GINSIM_E_USAGE, "kernel does not fit on the device");
     return G;
   };
-  const uint32_t Gd = pick(cap_d), Gc = pick(cap_c);
+  // Proxy backend: leave half the CTA slots free.  When ranks are emulated on
+  // one GPU every agent copy is a same-device copy, which the CUDA runtime
+  // runs as a kernel; it must find room next to the waiting MoE kernel.
+  const int div = m->proxy ? 2 : 1;
+  const uint32_t Gd = pick(std::max(1, cap_d / div)), Gc = pick(std::max(1, cap_c / div));
   uint32_t Gr = 0;
   if (k.reduce) Gr = std::max<uint32_t>(1, (uint32_t)max_coresident_ctas(k.reduce, kMoeThreads, 0, m->comm->device) / n);
   if (!use_tma(m) || !k.tma_combine) {
@@ -1429,6 +1627,17 @@ int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const voi
     GIN_CUDA(cudaLaunchKernel(k.reduce, dim3(moes[0]->Gr, n), dim3(kMoeThreads), args, 0, (cudaStream_t)stream));
   }
   moes[0]->last_ctas = Gc * n;
+  GIN_API_END
+}
+
+int ginsim_cuda_moe_phase_times(ginsim_cuda_moe_t moe, uint32_t kernel, uint64_t* out, uint32_t* ctas) {
+  GIN_API_BEGIN
+  if (!moe->prof) fail(GINSIM_E_USAGE, "phase stamps need GINSIM_PROFILE_PHASES=1 at moe_create");
+  if (kernel > 2) fail(GINSIM_E_USAGE, "kernel: 0 dispatch, 1 combine send, 2 combine reduce");
+  DeviceGuard g(moe->comm->device);
+  GIN_CUDA(cudaDeviceSynchronize());
+  GIN_CUDA(cudaMemcpy(out, moe->prof + (uint64_t)kernel * 1024 * 8, 1024 * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (ctas) *ctas = kernel == 0 ? moe->G : (kernel == 1 ? moe->Gc : moe->Gr);
   GIN_API_END
 }
 

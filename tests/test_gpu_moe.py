@@ -137,17 +137,19 @@ def test_moe_engines_agree(engine, layout, mode):
         run.close()
 
 
+@pytest.mark.parametrize("sched", ["static", "dynamic"])
 @pytest.mark.parametrize("layout,mode", [(0, 0), (1, 1)])
-def test_moe_dispatch_cpasync_loads(layout, mode, monkeypatch):
-    """TMA dispatch with LSU cp.async row loads (GINSIM_DISPATCH_LOADS=cpasync):
-    identical windows, cells and outputs."""
-    monkeypatch.setenv("GINSIM_DISPATCH_LOADS", "cpasync")
+def test_moe_tma_schedules(sched, layout, mode, monkeypatch):
+    """TMA dispatch/combine-send with static work assignment or warps grabbing
+    work from a device counter (GINSIM_MOE_SCHED): identical windows, cells
+    and outputs over repeated steps (the grab counters reset per launch)."""
+    monkeypatch.setenv("GINSIM_MOE_SCHED", sched)
     n, E, K, T, H, seed = 8, 64, 8, 48, 7168, 4
     run = MoeRun(n, E, K, T, H, mode=mode, layout=layout, engine=2)
     try:
         run.generate(seed)
-        run.step()
-        run.step()
+        for _ in range(3):
+            run.step()
         cnt = O.counts(seed, n, E, K, T)
         for r in range(n):
             d, comb, _ = O.moe_rank_state(seed, n, E, K, T, H, r, mode=mode)
@@ -158,6 +160,26 @@ def test_moe_dispatch_cpasync_loads(layout, mode, monkeypatch):
             assert (run.combine_window(r) == comb).all(), r
             exp, _ = O.combine(seed, E, K, H, r, T, mode=mode)
             assert (run.output(r) == exp).all(), r
+    finally:
+        run.close()
+
+
+def test_moe_routing_changes_between_steps():
+    """A new routing every step (different seed per step): the route tables,
+    slot numbers and counts are rebuilt per launch -- every step bit-exact."""
+    n, E, K, T, H = 4, 32, 4, 40, 256
+    run = MoeRun(n, E, K, T, H, layout=1, engine=2)
+    try:
+        for seed in (3, 8, 13):
+            run.generate(seed)
+            run.step()
+            cnt = O.counts(seed, n, E, K, T)
+            for r in range(n):
+                d, comb, _ = O.moe_rank_state(seed, n, E, K, T, H, r)
+                win = O.compact_to_reference(run.dispatch_window(r), cnt, r, n, E // n, T, K, 2 * H + 16)
+                assert (win == d).all(), (seed, r)
+                exp, _ = O.combine(seed, E, K, H, r, T)
+                assert (run.output(r) == exp).all(), (seed, r)
     finally:
         run.close()
 

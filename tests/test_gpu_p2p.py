@@ -12,6 +12,8 @@ import paper_2511_15076_b200 as G
 from oracle import oracle as O
 from tests import gpu_util as U
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 pytestmark = pytest.mark.gpu
 BACKENDS = ["direct", "proxy"]
 
@@ -308,3 +310,21 @@ def test_proxy_stats_and_reset_while_outstanding():
         assert st["descriptors"] >= 200 and st["copies"] >= 200
     finally:
         close(cs)
+
+
+def test_agent_copies_progress_while_every_sm_is_held():
+    """The proxy agent's data movers must not need SMs: with a kernel holding
+    every SM, an H2D inline-put copy (pinned -> VMM window) and a copy into a
+    peer's VMM mapping complete on the copy engines.  (A same-device D2D copy
+    does NOT -- the runtime runs it as a kernel -- which is why loopback puts
+    are moved by the issuing SMs in proxy mode, gin_device.cuh Gin::put.)"""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "copy_engine_probe.py")], capture_output=True,
+                       text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = {x["case"]: x for x in json.loads(r.stdout.strip().splitlines()[-1])["rows"]}
+    assert rows["h2d_pinned_to_vmm_8B"]["completed_while_sms_held"]
+    if "d2d_vmm_to_peer_mapping" in rows:
+        assert rows["d2d_vmm_to_peer_mapping"]["completed_while_sms_held"]
+        assert rows["h2d_pinned_to_peer_mapping_8B"]["completed_while_sms_held"]
