@@ -67,6 +67,7 @@ struct MoeLaunch {
   uint32_t E, K, T, H, mode, layout, e_local, parts, cparts;
   uint32_t win_dispatch, win_counts, win_combine;
   uint32_t win_stage, win_cstage, coalesce;  // proxy backend: dispatch / combine staging windows
+  uint32_t coop;                 // TMA dispatch: cooperative route tables + all-token work (large T*K)
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
 };
@@ -126,23 +127,42 @@ __device__ __forceinline__ void source_prefix(const uint32_t* cnt, uint32_t* src
   }
 }
 
-// Per-expert release of one dispatch (harness_moe.cpp:163-167) issued by the
-// last CTA: one thread per destination rank writes that rank's counts, fences
-// once, then adds (1<<32)+count to each of its experts' cells with relaxed
-// reductions -- a release pattern (fence.acq_rel.sys then strong writes by the
-// same thread) that costs one .sys fence per destination instead of one
-// MEMBAR.SYS per expert (red.release.sys).
+// Grid arrival at the end of a phase: the last CTA of this rank's launch to
+// arrive returns true (in every thread).  CTAs order their own traffic
+// before the arrival at GPU scope (fence.acq_rel.gpu, much cheaper than a
+// .sys fence per CTA); the last CTA then holds, by cumulativity, every CTA's
+// puts, and its .sys release (one fence per releasing warp) publishes them to
+// the peers (the paper's ordering rule, fabric.cpp:63-79).
+__device__ __forceinline__ bool arrive_last(unsigned int* ctr, unsigned int target, int* flag_smem) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gin::fence_acq_rel_gpu();
+    const unsigned prev = atomicAdd(ctr, 1u);
+    const bool last = prev + 1 == target;
+    if (last) gin::fence_acq_rel_gpu();
+    *flag_smem = last ? 1 : 0;
+  }
+  __syncthreads();
+  return *flag_smem != 0;
+}
+
+// Per-expert release of one dispatch (harness_moe.cpp:163-167) by the last
+// CTA: warp d takes destination rank d; each lane fences once (one MEMBAR per
+// warp instruction), writes its experts' counts, fences again and adds
+// (1<<32)+count to their cells with relaxed reductions -- a release pattern
+// per lane, two .sys fences per destination instead of one per expert.
 __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDevCommView* v, uint32_t win_counts,
                                                 const uint32_t* hist, uint32_t n, uint32_t rank, uint32_t e_local) {
-  const uint32_t d = threadIdx.x;
-  if (d >= n) return;
-  uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[win_counts].base[d]);
-  gin::fence_acq_rel_sys();
-  for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
-    gin::st_relaxed_sys32(cb + (uint64_t)e_loc * n + rank, hist[d * e_local + e_loc]);
-  gin::fence_acq_rel_sys();
-  for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
-    gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_loc), (1ull << 32) + hist[d * e_local + e_loc]);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (uint32_t d = warp; d < n; d += nw) {
+    uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[win_counts].base[d]);
+    gin::fence_acq_rel_sys();
+    for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
+      gin::st_relaxed_sys32(cb + (uint64_t)e_loc * n + rank, hist[d * e_local + e_loc]);
+    gin::fence_acq_rel_sys();
+    for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
+      gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_loc), (1ull << 32) + hist[d * e_local + e_loc]);
+  }
 }
 
 // Block-wide exclusive scan of n <= 4*kMoeThreads u32 values in smem.
@@ -360,14 +380,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
   }
 
   // Phase C: the last CTA to finish releases every expert.
-  __syncthreads();
-  if (tid == 0) {
-    gin::fence_acq_rel_sys();
-    const unsigned prev = atomicAdd(R.ws + 0, 1u);
-    is_last = (prev + 1 == (unsigned)(R.iteration * G));
-    if (is_last) gin::fence_acq_rel_sys();
-  }
-  __syncthreads();
+  arrive_last(R.ws + 0, (unsigned)(R.iteration * G), &is_last);
   if (is_last && PROXY) {
     // One thread per expert submits, in this order on ctx e % n_ctx: the
     // count (inline put), the payload run (one put, or one per message when
@@ -507,14 +520,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
   }
 
   // Release: the last CTA signals each (source, context) with its count.
-  __syncthreads();
-  if (tid == 0) {
-    gin::fence_acq_rel_sys();
-    const unsigned prev = atomicAdd(R.ws + 1, 1u);
-    is_last = (prev + 1 == (unsigned)(R.iteration * G));
-    if (is_last) gin::fence_acq_rel_sys();
-  }
-  __syncthreads();
+  arrive_last(R.ws + 1, (unsigned)(R.iteration * G), &is_last);
   if (is_last && PROXY) {
     const gin::Team world = gin::WorldTeam(n);
     gin::CoopThread me;
@@ -652,7 +658,8 @@ struct TmaSmem {  // per-warp control block, followed by the staging buffers
   uint64_t bar[kTmaStages];
   char* dptr[32];
   uint64_t itm[kTmaStages];  // item held by each stage (~0 = none)
-  uint64_t cur, end;         // item source: static sequence number, or the grabbed batch [cur, end)
+  uint64_t cur;              // static sequence number (first round / static schedule)
+  uint64_t itc, end;         // dynamic schedule: the grabbed batch [itc, end)
 };
 constexpr uint64_t kNoItem = ~0ull;
 
@@ -754,6 +761,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   const uint32_t Kp = (K + 1) & ~1u;  // dst_g row stride: 16-byte rows for the bulk load
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
   const unsigned int bar_target = (unsigned int)(R.iteration * G);
+  // coop: route tables built cooperatively + work over all tokens (large T*K);
+  // local: every CTA histograms the whole (small) route table and moves only
+  // its own tokens -- no grid barrier on the latency-bound LL path
+  const bool coop = L.coop != 0;
   MOE_STAMP(R, 0, 0);
 
   __shared__ uint32_t hist_all[kMaxExperts], run[kMaxExperts], prefix_e[kMaxExperts];
@@ -772,7 +783,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   uint32_t* g_tot = R.route + 2 * (size_t)kMaxGrid * kMaxExperts;  // [E]
   char** dst_g = R.dst_g;                                      // [T][Kp]
 
-  for (uint32_t e = tid; e < E; e += kTmaThreads) hist_all[e] = 0;
+  for (uint32_t e = tid; e < E; e += kTmaThreads) {
+    hist_all[e] = 0;
+    run[e] = 0;
+  }
   if (lane == 0) {
     for (int s = 0; s < kTmaStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
     gin::tma::fence_mbar_init();
@@ -781,17 +795,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   __syncthreads();
   // Work source for Phase B.
   const char* x = reinterpret_cast<const char*>(R.x);
-  const uint64_t items = (uint64_t)T * parts;
+  const uint64_t items = coop ? (uint64_t)T * parts : (uint64_t)t1 * parts;
   const uint64_t gw = (uint64_t)b * kTmaWarps + warp, wstride = (uint64_t)G * kTmaWarps;
+  const uint64_t lbase = (uint64_t)t0 * parts + warp;  // local mode: warp takes lbase + j*kTmaWarps
   unsigned long long* grab_ctr = reinterpret_cast<unsigned long long*>(R.ws + 10);
   auto next_item = [&]() -> uint64_t {  // lane 0 only
     uint64_t it;
-    if (L.dyn) {
-      if (ctl->cur >= ctl->end) {  // one token per grab, after the static first round
-        ctl->cur = (uint64_t)kTmaStages * wstride + atomicAdd(grab_ctr, (unsigned long long)parts);
-        ctl->end = ctl->cur + parts;
+    if (!coop) {
+      it = lbase + (ctl->cur++) * kTmaWarps;
+    } else if (L.dyn && ctl->cur >= kTmaStages) {
+      // after a static, interleaved first round (items gw + s*wstride, so
+      // 1000+ warps do not all hit the counter at once and a small launch
+      // still spreads over every CTA): one token per grab
+      if (ctl->end == 0 || ctl->itc >= ctl->end) {
+        ctl->itc = (uint64_t)kTmaStages * wstride + atomicAdd(grab_ctr, (unsigned long long)parts);
+        ctl->end = ctl->itc + parts;
       }
-      it = ctl->cur++;
+      it = ctl->itc++;
     } else {
       it = gw + (ctl->cur++) * wstride;
     }
@@ -813,16 +833,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   if (lane == 0) {
     // first round static (warp gw: items [gw*S, gw*S+S)), so 1000+ warps do
     // not all hit the grab counter at once when the kernel starts
-    ctl->cur = L.dyn ? gw * kTmaStages : 0;
-    ctl->end = L.dyn ? gw * kTmaStages + kTmaStages : 0;
+    ctl->cur = 0;
+    ctl->end = 0;
     for (int s = 0; s < kTmaStages; ++s) {
       const uint64_t it = next_item();
       ctl->itm[s] = it;
       if (it != kNoItem) issue_row(s, it);
     }
   }
-  // A0: own routes -> smem + own histogram -> global row
   const uint32_t nq = (t1 - t0) * K;
+  if (!coop) {
+    // local: the whole route table is small; totals, this CTA's prefix and
+    // its own pairs in one vectorised pass (no grid barrier)
+    histogram_pass<kTmaThreads>(R.idx, T * K, t0 * K, nq, hist_all, run, own);
+    __syncthreads();
+  } else {
+  // A0: own routes -> smem + own histogram -> global row
   for (uint32_t q = tid; q < nq; q += kTmaThreads) {
     const uint32_t e = (uint32_t)__ldg(R.idx + (uint64_t)t0 * K + q);
     own[q] = e;
@@ -866,6 +892,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     hist_all[e] = __ldcg(g_tot + e);
   }
   __syncthreads();
+  }  // coop
   if (L.layout == 1) {  // per-destination exclusive prefix of the expert totals, one warp per destination
     for (uint32_t d = warp; d < n; d += kTmaWarps) {
       uint32_t carry = 0;
@@ -910,7 +937,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     gin::tma::fence_proxy_async_global();  // generic writes of dst_g -> read by other CTAs' bulk loads
   }
   MOE_STAMP(R, 0, 3);
-  rank_grid_barrier(R.ws + 5, bar_target);
+  if (coop) rank_grid_barrier(R.ws + 5, bar_target);
+  else __syncthreads();  // this CTA's own dst rows, read back by its own bulk loads
   MOE_STAMP(R, 0, 4);
 
   // Phase B (the first stages' row chunks were requested before Phase A)
@@ -955,14 +983,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
 
   // Phase C/D as the LSU kernel.
   MOE_STAMP(R, 0, 5);
-  __syncthreads();
-  if (tid == 0) {
-    gin::fence_acq_rel_sys();
-    const unsigned prev = atomicAdd(R.ws + 0, 1u);
-    is_last = (prev + 1 == (unsigned)(R.iteration * G));
-    if (is_last) gin::fence_acq_rel_sys();
-  }
-  __syncthreads();
+  arrive_last(R.ws + 0, (unsigned)(R.iteration * G), &is_last);
   if (is_last) {
     if (tid == 0) *grab_ctr = 0;  // every CTA is past Phase B
     release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local);
@@ -1081,20 +1102,20 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   unsigned long long* grab_ctr = reinterpret_cast<unsigned long long*>(R.ws + 8);
   auto next_item = [&]() -> uint64_t {  // lane 0 only
     uint64_t it;
-    if (L.dyn) {
-      if (ctl->cur >= ctl->end) {  // one message per grab, after the static first round
-        ctl->cur = (uint64_t)kTmaStages * stride + atomicAdd(grab_ctr, (unsigned long long)parts);
-        ctl->end = ctl->cur + parts;
+    if (L.dyn && ctl->cur >= kTmaStages) {  // one message per grab after the interleaved first round
+      if (ctl->end == 0 || ctl->itc >= ctl->end) {
+        ctl->itc = (uint64_t)kTmaStages * stride + atomicAdd(grab_ctr, (unsigned long long)parts);
+        ctl->end = ctl->itc + parts;
       }
-      it = ctl->cur++;
+      it = ctl->itc++;
     } else {
       it = gw + (ctl->cur++) * stride;
     }
     return it < items ? it : kNoItem;
   };
   if (lane == 0) {
-    ctl->cur = L.dyn ? gw * kTmaStages : 0;
-    ctl->end = L.dyn ? gw * kTmaStages + kTmaStages : 0;
+    ctl->cur = 0;
+    ctl->end = 0;
     for (int s = 0; s < kTmaStages; ++s) {
       const uint64_t it = next_item();
       ctl->itm[s] = it;
@@ -1148,14 +1169,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   }
   MOE_STAMP(R, 1, 2);
 
-  __syncthreads();
-  if (tid == 0) {
-    gin::fence_acq_rel_sys();
-    const unsigned prev = atomicAdd(R.ws + 1, 1u);
-    is_last = (prev + 1 == (unsigned)(R.iteration * G));
-    if (is_last) gin::fence_acq_rel_sys();
-  }
-  __syncthreads();
+  arrive_last(R.ws + 1, (unsigned)(R.iteration * G), &is_last);
   if (is_last) {
     if (tid == 0) *grab_ctr = 0;  // every CTA is past its loop: ready for the next launch
     for (uint32_t sc = tid; sc < n * n_ctx; sc += kTmaThreads) {
@@ -1294,6 +1308,7 @@ struct ginsim_cuda_moe_s {
   unsigned int* ws = nullptr;
   uint32_t* route = nullptr;
   char** dst_g = nullptr;
+  bool coop = false;  // TMA dispatch route-table mode, fixed per handle (grid-barrier counters)
   uint64_t* prof = nullptr;  // GINSIM_PROFILE_PHASES=1: [3][1024][8] %globaltimer stamps
   uint64_t iteration_dispatch = 0, iteration_combine = 0;
   uint32_t last_ctas = 0;
@@ -1347,6 +1362,11 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   GIN_CUDA(cudaMalloc(&m->route, (2 * (size_t)kMaxGrid + 1) * kMaxExperts * 4));
   GIN_CUDA(cudaMalloc(&m->dst_g, (size_t)cfg->tokens * ((cfg->top_k + 1) & ~1u) * sizeof(char*)));
   GIN_CUDA(cudaMemset(m->ws, 0, 256));
+  // Cooperative route tables from this many (token, k) pairs per rank on
+  // (GINSIM_DISPATCH_COOP_MIN_PAIRS; the LL shape, 1024 pairs, stays local).
+  const char* cm = std::getenv("GINSIM_DISPATCH_COOP_MIN_PAIRS");
+  const uint64_t coop_min = cm ? std::strtoull(cm, nullptr, 10) : 8192ull;
+  m->coop = (uint64_t)cfg->tokens * cfg->top_k >= coop_min;
   const char* pp = std::getenv("GINSIM_PROFILE_PHASES");
   if (pp && pp[0] == '1') {
     GIN_CUDA(cudaMalloc(&m->prof, 3 * 1024 * 8 * sizeof(uint64_t)));
@@ -1428,6 +1448,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.no_wait = (nw && nw[0] == '1') ? 1u : 0u;
   const char* dy = std::getenv("GINSIM_MOE_SCHED");
   L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
+  L.coop = moes[0]->coop ? 1u : 0u;
   for (uint32_t i = 0; i < n; ++i) {
     if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");

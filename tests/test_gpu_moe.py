@@ -137,13 +137,16 @@ def test_moe_engines_agree(engine, layout, mode):
         run.close()
 
 
+@pytest.mark.parametrize("route", ["coop", "local"])
 @pytest.mark.parametrize("sched", ["static", "dynamic"])
 @pytest.mark.parametrize("layout,mode", [(0, 0), (1, 1)])
-def test_moe_tma_schedules(sched, layout, mode, monkeypatch):
-    """TMA dispatch/combine-send with static work assignment or warps grabbing
+def test_moe_tma_schedules(route, sched, layout, mode, monkeypatch):
+    """TMA dispatch with cooperative route tables (3 grid barriers, all-token
+    work) or per-CTA local tables, static work assignment or warps grabbing
     work from a device counter (GINSIM_MOE_SCHED): identical windows, cells
-    and outputs over repeated steps (the grab counters reset per launch)."""
+    and outputs over repeated steps (grab counters and barriers are reused)."""
     monkeypatch.setenv("GINSIM_MOE_SCHED", sched)
+    monkeypatch.setenv("GINSIM_DISPATCH_COOP_MIN_PAIRS", "1" if route == "coop" else "100000000")
     n, E, K, T, H, seed = 8, 64, 8, 48, 7168, 4
     run = MoeRun(n, E, K, T, H, mode=mode, layout=layout, engine=2)
     try:
