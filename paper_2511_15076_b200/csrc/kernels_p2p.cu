@@ -13,6 +13,7 @@
 
 #include "gin_device.cuh"
 #include "runtime_internal.h"
+#include "tma.cuh"
 
 namespace ginsim_b200 {
 
@@ -97,33 +98,73 @@ struct A2aArgs {
   uint64_t expected;  // wait target for the local cell
 };
 
-// CTA b serves peer index b / ctas_per_peer (skipping self) and slice
-// b % ctas_per_peer of its M bytes; the last CTA of each peer releases it.
-__global__ void alltoall_kernel(A2aArgs A) {
+constexpr int kA2aThreads = 256;
+constexpr int kA2aWarps = kA2aThreads / 32;
+constexpr int kA2aStages = 4;
+constexpr uint32_t kA2aChunk = 4096;
+
+// CTA b serves peer index b / ctas_per_peer (staggered: peer = me+1+pi, so
+// every link is busy from the start) and slice b % ctas_per_peer of its M
+// bytes.  Each warp streams its 4 KiB chunks of the slice through a
+// 4-stage TMA pipeline (bulk load from the local send window into shared
+// memory, bulk store into the peer's recv window over NVLink).  The last CTA
+// of each peer releases it with one red.release.sys (SignalInc).
+__global__ void __launch_bounds__(kA2aThreads) alltoall_kernel(A2aArgs A) {
+  extern __shared__ __align__(128) char smem[];
   const GinDevCommView* v = A.lv.v[blockIdx.y];
   unsigned int* ws = A.lv.ws[blockIdx.y];
   const uint64_t arrivals_before = A.lv.base[blockIdx.y];  // per-peer arrivals of earlier launches
   gin::Gin gin(v, 0);
-  gin::CoopCta cta;
   const uint32_t n = v->world, me = v->rank;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t pi = blockIdx.x / A.ctas_per_peer, slice = blockIdx.x % A.ctas_per_peer;
-  const uint32_t peer = (me + 1 + pi) % n;  // stagger so every link is busy from the start
-  const uint64_t chunk = ((A.bytes + A.ctas_per_peer - 1) / A.ctas_per_peer + 15) & ~15ull;
-  const uint64_t lo = std::min<uint64_t>(A.bytes, chunk * slice), hi = std::min<uint64_t>(A.bytes, lo + chunk);
+  const uint32_t peer = (me + 1 + pi) % n;
+  const uint64_t per = ((A.bytes + A.ctas_per_peer - 1) / A.ctas_per_peer + 15) & ~15ull;
+  const uint64_t lo = std::min<uint64_t>(A.bytes, per * slice), hi = std::min<uint64_t>(A.bytes, lo + per);
   __shared__ int last;
-  if (hi > lo) {
-    gin::coop_copy(cta, gin.window_ptr(A.recv_win, peer, (uint64_t)me * A.bytes + lo),
-                   gin.window_ptr(A.send_win, me, (uint64_t)peer * A.bytes + lo), hi - lo);
+  const char* src = gin.window_ptr(A.send_win, me, (uint64_t)peer * A.bytes);
+  char* dst = gin.window_ptr(A.recv_win, peer, (uint64_t)me * A.bytes);
+  if ((((uintptr_t)src | (uintptr_t)dst | A.bytes) & 15) == 0) {
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * kA2aStages;
+    char* buf = smem + 1024 + (size_t)warp * kA2aStages * kA2aChunk;
+    const uint64_t nch = (hi - lo + kA2aChunk - 1) / kA2aChunk;
+    if (lane == 0) {
+      for (int s = 0; s < kA2aStages; ++s) gin::tma::mbar_init(bars + s, 1);
+      gin::tma::fence_mbar_init();
+      auto len = [&](uint64_t c) { return (uint32_t)std::min<uint64_t>(kA2aChunk, hi - lo - c * kA2aChunk); };
+      for (int s = 0; s < kA2aStages; ++s) {
+        const uint64_t c = warp + (uint64_t)s * kA2aWarps;
+        if (c < nch) {
+          gin::tma::mbar_arrive_expect_tx(bars + s, len(c));
+          gin::tma::load(buf + (size_t)s * kA2aChunk, src + lo + c * kA2aChunk, len(c), bars + s);
+        }
+      }
+      for (uint64_t i = 0;; ++i) {
+        const uint64_t c = warp + i * kA2aWarps;
+        if (c >= nch) break;
+        const int s = (int)(i % kA2aStages);
+        gin::tma::mbar_wait(bars + s, (uint32_t)((i / kA2aStages) & 1));
+        gin::tma::store(dst + lo + c * kA2aChunk, buf + (size_t)s * kA2aChunk, len(c));
+        gin::tma::commit();
+        gin::tma::wait_read<0>();
+        const uint64_t cn = c + (uint64_t)kA2aStages * kA2aWarps;
+        if (cn < nch) {
+          gin::tma::mbar_arrive_expect_tx(bars + s, len(cn));
+          gin::tma::load(buf + (size_t)s * kA2aChunk, src + lo + cn * kA2aChunk, len(cn), bars + s);
+        }
+      }
+      gin::tma::wait_all();
+      gin::tma::fence_proxy_async_global();
+    }
+  } else if (hi > lo) {
+    gin::coop_copy(gin::CoopCta{}, dst + lo, src + lo, hi - lo);
   }
-  cta.sync();
+  __syncthreads();
   if (threadIdx.x == 0) {
-    gin::fence_acq_rel_sys();
+    gin::fence_acq_rel_gpu();
     const unsigned prev = atomicAdd(ws + 16 + peer, 1u);
     last = prev + 1 == (unsigned)(arrivals_before + A.ctas_per_peer);
-    if (last) {
-      gin::fence_acq_rel_sys();
-      gin.release_signal_raw(peer, A.sig, 1);
-    }
+    if (last) gin.release_signal_raw(peer, A.sig, 1);  // red.release.sys: cumulative over the peer's CTAs
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) gin.wait_ge_signal(A.sig, A.expected);
 }
@@ -339,20 +380,35 @@ int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t s
   A.sig = signal_id;
   A.bytes = bytes_per_peer;
   A.expected = expected;
-  int sms = 0;
-  GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device));
+  // occupancy is queried once per device (it is a driver round trip)
+  static int sms_of[64] = {0}, cap_of[64] = {0};
+  const size_t smem = 1024 + (size_t)kA2aWarps * kA2aStages * kA2aChunk;
+  const int dv = c0->device & 63;
+  if (!sms_of[dv]) {
+    GIN_CUDA(cudaFuncSetAttribute((const void*)alltoall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GIN_CUDA(cudaDeviceGetAttribute(&sms_of[dv], cudaDevAttrMultiProcessorCount, c0->device));
+    cap_of[dv] = max_coresident_ctas((const void*)alltoall_kernel, kA2aThreads, smem, c0->device);
+  }
+  const int sms = sms_of[dv], cap_per_dev = cap_of[dv];
   const uint32_t want = ctas ? ctas : (uint32_t)sms;
   uint32_t per_peer = std::max<uint32_t>(1, want / (world - 1));
   const uint64_t max_useful = std::max<uint64_t>(1, bytes_per_peer / (16u << 10));
   per_peer = (uint32_t)std::min<uint64_t>(per_peer, max_useful);
-  // cooperative capacity
-  const int cap = max_coresident_ctas((const void*)alltoall_kernel, 512, 0, c0->device) / (int)n;
+  const int cap = cap_per_dev / (int)n;  // emulated ranks share one device's co-residency
   while (per_peer > 1 && (int)(per_peer * (world - 1)) > cap) --per_peer;
   A.ctas_per_peer = per_peer;
   // the per-peer arrival counters are monotone across launches whose CTA
   // split differs (it follows the message size): pass where they stand
   for (uint32_t i = 0; i < n; ++i) A.lv.base[i] = bump_host_counter(&comms[i]->impl, 1, per_peer) - per_peer;
-  coop_launch((const void*)alltoall_kernel, dim3(per_peer * (world - 1), n), dim3(512), &A, (cudaStream_t)stream);
+  const dim3 grid(per_peer * (world - 1), n);
+  if (n == 1) {  // one rank per process: CTAs never wait on one another
+    alltoall_kernel<<<grid, kA2aThreads, smem, (cudaStream_t)stream>>>(A);
+    GIN_CUDA(cudaGetLastError());
+  } else {
+    void* args[] = {&A};
+    GIN_CUDA(cudaLaunchCooperativeKernel((const void*)alltoall_kernel, grid, dim3(kA2aThreads), args, smem,
+                                         (cudaStream_t)stream));
+  }
   GIN_API_END
 }
 

@@ -13,7 +13,7 @@ COLS = [("gpu__time_duration.sum", "duration"), ("nvltx__bytes.sum", "tx"), ("nv
         ("nvltx__bytes_data_protocol.sum", "tx_proto"), ("nvlrx__bytes.sum", "rx"),
         ("nvlrx__bytes_data_user.sum", "rx_user"), ("dram__bytes_read.sum", "dram_rd"),
         ("dram__bytes_write.sum", "dram_wr")]
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3,
          "second": 1}
 
 
