@@ -87,6 +87,19 @@ __device__ __forceinline__ uint32_t bf16x2_transform(uint32_t two, float s, floa
   return (uint32_t)__bfloat16_as_ushort(ya) | ((uint32_t)__bfloat16_as_ushort(yb) << 16);
 }
 
+// 8 bf16 lanes: y = bf16(fp32(x)*s + c), single-rounded mul and add, packed
+// back two at a time (cvt.rn.bf16x2.f32) -- same rounding as bf16x2_transform.
+__device__ __forceinline__ uint32_t bf16x2_pack_transform(uint32_t two, float s, float c) {
+  const float a = __fadd_rn(__fmul_rn(__uint_as_float(two << 16), s), c);
+  const float b = __fadd_rn(__fmul_rn(__uint_as_float(two & 0xFFFF0000u), s), c);
+  const __nv_bfloat162 r = __floats2bfloat162_rn(a, b);  // .x = a (low half), .y = b
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+__device__ __forceinline__ uint4 bf16x8_transform(uint4 v, float s, float c) {
+  return make_uint4(bf16x2_pack_transform(v.x, s, c), bf16x2_pack_transform(v.y, s, c),
+                    bf16x2_pack_transform(v.z, s, c), bf16x2_pack_transform(v.w, s, c));
+}
+
 __device__ __forceinline__ uint4 transform_vec(uint4 v, uint32_t mode, uint32_t e) {
   if (mode == 0) {
     const uint32_t add = (e * 17u + 1u) & 0xFFFFu;
@@ -147,19 +160,21 @@ __device__ __forceinline__ bool arrive_last(unsigned int* ctr, unsigned int targ
 }
 
 // Per-expert release of one dispatch (harness_moe.cpp:163-167) by the last
-// CTA: warp d takes destination rank d; each lane fences once (one MEMBAR per
-// warp instruction), writes its experts' counts, fences again and adds
-// (1<<32)+count to their cells with relaxed reductions -- a release pattern
-// per lane, two .sys fences per destination instead of one per expert.
+// CTA: warp d takes destination rank d; each lane writes its experts' counts,
+// fences (one MEMBAR per warp instruction) and adds (1<<32)+count to their
+// cells with relaxed reductions -- a release pattern per lane, one .sys fence
+// per destination instead of one per expert.
 __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDevCommView* v, uint32_t win_counts,
                                                 const uint32_t* hist, uint32_t n, uint32_t rank, uint32_t e_local) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (uint32_t d = warp; d < n; d += nw) {
     uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[win_counts].base[d]);
-    gin::fence_acq_rel_sys();
+    // the counts need no ordering against the puts, only before the cells:
+    // one fence between them releases both the puts (by cumulativity) and
+    // the counts; for own experts the acquirer is on this GPU (GPU scope)
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::st_relaxed_sys32(cb + (uint64_t)e_loc * n + rank, hist[d * e_local + e_loc]);
-    gin::fence_acq_rel_sys();
+    if (d == rank) gin::fence_acq_rel_gpu(); else gin::fence_acq_rel_sys();
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_loc), (1ull << 32) + hist[d * e_local + e_loc]);
   }
@@ -1019,7 +1034,9 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   __shared__ int is_last;
   extern __shared__ __align__(128) char dsm[];
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
-  char* stage = dsm + sizeof(TmaSmem) * kTmaWarps + (size_t)warp * kTmaStages * chunk;
+  // per stage: [128-byte header: the message's 16-byte meta][chunk]
+  const uint32_t sstride = 128 + chunk;
+  char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kTmaStages * sstride;
 
   const uint32_t P = e_local * n;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
@@ -1087,13 +1104,19 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
                                         : ((uint64_t)src * T * K + src_prefix[lo] + slot) * dmsg;
     return recv + moff;
   };
+  // lane 0: locate the message once, record (expert, source) for the stage and
+  // bulk-load the chunk AND the message's 16-byte meta onto one mbarrier, so
+  // no lane ever waits on a global load of its own
   auto issue_load = [&](int s, uint64_t it) {
     uint32_t pr;
     const char* msg = locate((uint32_t)(it / parts), pr);
     const uint32_t p = (uint32_t)(it % parts);
     const uint32_t len = tma_chunk_len(payload, chunk, p);
-    gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len);
-    gin::tma::load(stage + (size_t)s * chunk, msg + (uint64_t)p * chunk, len, &ctl->bar[s]);
+    char* sb = stage + (size_t)s * sstride;
+    ctl->dptr[s] = reinterpret_cast<char*>((uint64_t)pr);  // pair index of the stage's message
+    gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len + 16);
+    gin::tma::load(sb, msg + payload, 16, &ctl->bar[s]);
+    gin::tma::load(sb + 128, msg + (uint64_t)p * chunk, len, &ctl->bar[s]);
   };
   // Work source.  Static: warp gw takes items gw, gw+stride, ...  Dynamic
   // (L.dyn): warps grab batches of one message's parts from a device counter,
@@ -1127,31 +1150,39 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     const int s = (int)(j % kTmaStages);
     const uint64_t it = ctl->itm[s];
     if (it == kNoItem) break;
-    const uint32_t m = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
-    uint32_t pr;
-    const char* msg = locate(m, pr);
+    const uint32_t p = (uint32_t)(it % parts);
+    const uint32_t pr = (uint32_t)reinterpret_cast<uint64_t>(ctl->dptr[s]);
     const uint32_t e = rank * e_local + pr / n, src = pr % n;
-    const uint4 meta = *reinterpret_cast<const uint4*>(msg + payload);
-    const uint32_t token = meta.y, k = meta.z;
     const uint32_t len = tma_chunk_len(payload, chunk, p);
+    char* sb = stage + (size_t)s * sstride;
     gin::tma::mbar_wait(&ctl->bar[s], (uint32_t)((j / kTmaStages) & 1));
-    uint4* buf = reinterpret_cast<uint4*>(stage + (size_t)s * chunk);
+    uint4* buf = reinterpret_cast<uint4*>(sb + 128);
     {
       const uint32_t nv = len / 16;
       uint32_t i = lane;
-      for (; i + 96 < nv; i += 128) {  // 4 independent vectors per lane in flight
-        const uint4 a = buf[i], c = buf[i + 32], d = buf[i + 64], f = buf[i + 96];
-        buf[i] = transform_vec(a, L.mode, e);
-        buf[i + 32] = transform_vec(c, L.mode, e);
-        buf[i + 64] = transform_vec(d, L.mode, e);
-        buf[i + 96] = transform_vec(f, L.mode, e);
+      if (L.mode == 0) {
+        const uint32_t add = (e * 17u + 1u) & 0xFFFFu;
+        for (; i < nv; i += 32) {
+          uint4 a = buf[i];
+          a.x = u16x2_transform(a.x, add), a.y = u16x2_transform(a.y, add);
+          a.z = u16x2_transform(a.z, add), a.w = u16x2_transform(a.w, add);
+          buf[i] = a;
+        }
+      } else {
+        const float sc = 1.0f + (float)(e % 7u) / 8.0f, cc = ((float)(e % 9u) - 4.0f) / 16.0f;
+        for (; i + 32 < nv; i += 64) {  // 2 independent vectors per lane in flight
+          const uint4 a = buf[i], c = buf[i + 32];
+          buf[i] = bf16x8_transform(a, sc, cc);
+          buf[i + 32] = bf16x8_transform(c, sc, cc);
+        }
+        for (; i < nv; i += 32) buf[i] = bf16x8_transform(buf[i], sc, cc);
       }
-      for (; i < nv; i += 32) buf[i] = transform_vec(buf[i], L.mode, e);
     }
     gin::tma::fence_proxy_async_shared();
     __syncwarp();
     if (lane == 0) {
-      gin::tma::store(cbases[src] + ((uint64_t)token * K + k) * cmsg + (uint64_t)p * chunk, buf, len);
+      const uint4 meta = *reinterpret_cast<const uint4*>(sb);  // {src, token, k, tag}
+      gin::tma::store(cbases[src] + ((uint64_t)meta.y * K + meta.z) * cmsg + (uint64_t)p * chunk, buf, len);
       gin::tma::commit();
       if (j >= 1) {  // refill the previous item's stage (its store has been reading meanwhile)
         gin::tma::wait_read<1>();
@@ -1177,7 +1208,14 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       uint32_t c = 0;
       for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
         if ((rank * e_local + e_loc) % n_ctx == ctx) c += cnt[e_loc * n + src];
-      if (c) gin.release_signal_raw(src, e_local, c);
+      if (c) {
+        if (src == rank) {  // own tokens: the reducer is on this GPU
+          gin::fence_acq_rel_gpu();
+          gin::red_relaxed_sys_add(gin.sub_cell(src, rank, e_local), c);
+        } else {
+          gin.release_signal_raw(src, e_local, c);
+        }
+      }
     }
   }
   MOE_STAMP(R, 1, 3);
@@ -1521,7 +1559,7 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
 }
 static size_t combine_smem(const ginsim_cuda_moe_t m) {
   if (!kernels_of(m).tma_combine) return 0;
-  return sizeof(TmaSmem) * kCmbWarps + (size_t)kCmbWarps * kTmaStages * m->cchunk;
+  return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * (128 + m->cchunk);
 }
 static int combine_threads(const MoeKernels& k) { return k.tma_combine ? kCmbThreads : kMoeThreads; }
 
