@@ -316,6 +316,26 @@ def measure_proxy(G, rank, world, local, dist, torch, dev, stream, allgather, T,
     return res
 
 
+def measure_barrier(G, comm, rank, world, dist, torch, dev, iters=2000):
+    """BarrierSession latency (runtime.cpp:638-666), one thread per rank, p50
+    over back-to-back barriers timed with %globaltimer: the reference's
+    dissemination barrier (ceil(log2 n) rounds of signals) vs the NVLS
+    multicast barrier (one multimem.red arrival)."""
+    import numpy as np
+    out = {"workload": f"barrier latency, {world} GPUs, {iters} back-to-back barriers", "nvls_enabled": comm.nvls_enabled()}
+    ns = torch.zeros(iters, dtype=torch.int64, device=dev)
+    for mode, name in ((0, "dissemination"), (1, "nvls")):
+        if mode == 1 and not out["nvls_enabled"]:
+            continue
+        dist.barrier()
+        G.check(G.lib().ginsim_cuda_barrier_bench(G.comm_handles([comm]), 1, mode, iters, ns.data_ptr(), None))
+        torch.cuda.synchronize()
+        comm.check_device()
+        t = np.sort(ns.cpu().numpy()[100:])
+        out[name] = {"p50_ns": int(t[len(t) // 2]), "p99_ns": int(t[len(t) * 99 // 100]), "mean_ns": float(t.mean())}
+    return out
+
+
 def ctypes_stream(stream):
     return None if stream is None else stream.cuda_stream
 
@@ -415,6 +435,7 @@ def main():
     ll = None if args.no_extras else measure_ll(G, comm, rank, world, dist, torch, dev, stream)
     pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm, rank, world, dist, torch, dev)
     a2a = None if (args.no_extras or world < 2) else measure_a2a(G, comm, rank, world, dist, torch, dev, stream)
+    barrier = None if (args.no_extras or world < 2) else measure_barrier(G, comm, rank, world, dist, torch, dev)
     proxy = None
     if not args.no_extras:
         ag = allgather if world > 1 else None
@@ -529,6 +550,7 @@ def main():
         "ll": ll,
         "pingpong": pp,
         "alltoall": a2a,
+        "barrier": barrier,
         "proxy_vs_direct": proxy,
     }
     if world > 1:

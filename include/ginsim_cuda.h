@@ -263,6 +263,18 @@ int ginsim_cuda_moe_ht_ring(const ginsim_cuda_comm_t* comms_pool, uint32_t n, ui
                             uint32_t channels, uint32_t slots, uint32_t messages, uint64_t seed,
                             void* stream);
 
+/* ---- NVLink SHARP barrier ----
+ * comm_create binds one multicast granule on every rank when every device
+ * reports CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED and no two ranks share a
+ * device (GINSIM_NVLS=0 disables it).  *enabled = 1 when it is active. */
+int ginsim_cuda_nvls_enabled(ginsim_cuda_comm_t comm, int* enabled);
+/* `iters` back-to-back barriers, one thread per rank, each timed with
+ * %globaltimer into ns_out (device, iters u64, rank 0 of the launch):
+ * mode 0 = the reference's dissemination BarrierSession on reserved signal
+ * cells (runtime.cpp:651-666), mode 1 = NVLS (one multimem.red arrival). */
+int ginsim_cuda_barrier_bench(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t mode, uint32_t iters,
+                              uint64_t* ns_out, void* stream);
+
 /* ---- DeepEP-style MoE dispatch / combine (harness_moe.cpp:105-250) ---- */
 typedef struct ginsim_cuda_moe_config {
   uint32_t experts;  /* E, divisible by world */

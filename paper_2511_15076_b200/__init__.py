@@ -202,6 +202,8 @@ def _declare(L):
                                     POINTER(ctypes.c_float), P], c_int),
         "ginsim_cuda_copy_bench_ex": ([P, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, c_uint32,
                                        c_uint32, POINTER(ctypes.c_float), P], c_int),
+        "ginsim_cuda_nvls_enabled": ([P, POINTER(c_int)], c_int),
+        "ginsim_cuda_barrier_bench": ([POINTER(P), c_uint32, c_uint32, c_uint32, P, P], c_int),
         "ginsim_cuda_occupy": ([c_int, c_uint32, P, c_uint64, P], c_int),
         "ginsim_cuda_ring":([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, P], c_int),
         "ginsim_cuda_moe_ht_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, P], c_int),
@@ -391,6 +393,11 @@ class Comm:
         code = self.device_error(clear=True)
         if code:
             raise _BY_CODE.get(code, Error)(f"device-side error {code} on rank {self.rank}")
+
+    def nvls_enabled(self):
+        v = c_int()
+        check(lib().ginsim_cuda_nvls_enabled(self.h, byref(v)))
+        return bool(v.value)
 
     def proxy_stats(self):
         a, b, c, d = c_uint64(), c_uint64(), c_uint64(), c_uint64()

@@ -79,6 +79,11 @@ typedef struct GinDevCommView {
   uint64_t* counter_base;    // local [cell]
   unsigned int* error;       // local device error word
   unsigned int* workspace;   // local scratch for kernels (zeroed at init), 64 KiB
+  // NVLS barrier region (null when multicast is unavailable): the multicast
+  // mapping (multimem.* reaches every rank's copy through the NVSwitch) and
+  // this rank's own copy of the same cells.
+  uint64_t* nvls_mc;
+  uint64_t* nvls_uc;
   GinWindowView win[GIN_MAX_WINDOWS];
   GinProxyView proxy;
 } GinDevCommView;

@@ -59,6 +59,14 @@ const CuApi& cuapi() {
       throw GinError(GINSIM_E_CUDA, "driver entry point cuMemSetAccess unavailable");
     if (cudaGetDriverEntryPoint("cuMemUnmap", reinterpret_cast<void**>(&api.cuMemUnmap), cudaEnableDefault, &q) != cudaSuccess || !api.cuMemUnmap)
       throw GinError(GINSIM_E_CUDA, "driver entry point cuMemUnmap unavailable");
+    // optional (multicast): left null when absent
+    cudaGetDriverEntryPoint("cuMulticastCreate", reinterpret_cast<void**>(&api.cuMulticastCreate), cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuMulticastAddDevice", reinterpret_cast<void**>(&api.cuMulticastAddDevice), cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuMulticastBindMem", reinterpret_cast<void**>(&api.cuMulticastBindMem), cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuMulticastUnbind", reinterpret_cast<void**>(&api.cuMulticastUnbind), cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuMulticastGetGranularity", reinterpret_cast<void**>(&api.cuMulticastGetGranularity), cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuDeviceGetAttribute", reinterpret_cast<void**>(&api.cuDeviceGetAttribute), cudaEnableDefault, &q);
+    cudaGetLastError();
   });
   return api;
 }
@@ -527,6 +535,7 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
   GIN_CUDA(cudaMalloc(&c->dev_view, sizeof(GinDevCommView)));
   GIN_CUDA(cudaStreamCreateWithFlags(&c->op_stream, cudaStreamNonBlocking));
   if (cfg.backend == GIN_BACKEND_PROXY) c->proxy = proxy_start(c);
+  nvls_setup(c);  // collective; leaves nvls.on = false where multicast is unavailable
   c->sync_view();
   GIN_CUDA(cudaDeviceSynchronize());
   c->barrier();  // nobody signals a peer before every table is mapped
@@ -567,6 +576,7 @@ int ginsim_cuda_comm_destroy(ginsim_cuda_comm_t comm) {
     DeviceGuard g(c->device);
     cudaDeviceSynchronize();
     if (c->proxy) proxy_stop(c->proxy);
+    nvls_teardown(c);
     for (auto& m : c->imported) {
       cuapi().cuMemUnmap(m.ptr, m.size);
       cuapi().cuMemAddressFree(m.ptr, m.size);

@@ -62,6 +62,13 @@ struct CuApi {
   decltype(&::cuMemRelease) cuMemRelease = nullptr;
   decltype(&::cuMemSetAccess) cuMemSetAccess = nullptr;
   decltype(&::cuMemUnmap) cuMemUnmap = nullptr;
+  // NVLink SHARP multicast (optional: null when the driver lacks them)
+  decltype(&::cuMulticastCreate) cuMulticastCreate = nullptr;
+  decltype(&::cuMulticastAddDevice) cuMulticastAddDevice = nullptr;
+  decltype(&::cuMulticastBindMem) cuMulticastBindMem = nullptr;
+  decltype(&::cuMulticastUnbind) cuMulticastUnbind = nullptr;
+  decltype(&::cuMulticastGetGranularity) cuMulticastGetGranularity = nullptr;
+  decltype(&::cuDeviceGetAttribute) cuDeviceGetAttribute = nullptr;
 };
 const CuApi& cuapi();
 
@@ -130,6 +137,14 @@ struct Comm {
   std::map<CUdeviceptr, VmmAlloc> allocs;     // ginsim_cuda_mem_alloc'd regions
   std::mutex mu;
 
+  // NVLS multicast barrier region (nvls.cu): one granule bound on every rank
+  struct Nvls {
+    bool on = false, shared = false;  // shared: rank 0's handle object in this process
+    CUmemGenericAllocationHandle mc = 0, local = 0;
+    CUdeviceptr mc_va = 0, uc_va = 0;
+    uint64_t size = 0;
+  } nvls;
+
   cudaStream_t op_stream = nullptr;           // host-issued ops / cell reads
   uint64_t op_counter[8] = {};                // per-workload launch/round counters (host side)
   ProxyPtr proxy;
@@ -144,6 +159,12 @@ struct Comm {
 void check_same_device(const ginsim_cuda_comm_t* comms, uint32_t n);
 int max_coresident_ctas(const void* kernel, int threads, size_t smem, int device);
 void check_device_error(Comm* c);
+
+// NVLS multicast barrier (nvls.cu): collective setup after the signal tables,
+// teardown at comm destroy.  Disabled (nvls.on = false) without multicast
+// support, with ranks sharing a device, or with GINSIM_NVLS=0.
+void nvls_setup(Comm* c);
+void nvls_teardown(Comm* c);
 
 // Proxy agent lifecycle (proxy.cu).
 ProxyPtr proxy_start(Comm* c);

@@ -64,6 +64,17 @@ def main():
         res["dispatch_window_exact"] = bool((win == d).all())
         cwin = U.d2h(comm.window_ptr(moe.win_combine, rank), len(comb))
         res["combine_window_exact"] = bool((cwin == comb).all())
+    # BarrierSession: dissemination over signal cells and, where the box has
+    # NVLink SHARP, the multicast barrier -- both must complete every round
+    if os.environ.get("MP_BARRIER", "0") == "1":
+        ns = torch.zeros(500, dtype=torch.int64, device=dev)
+        res["nvls_enabled"] = comm.nvls_enabled()
+        for mode in (0, 1) if res["nvls_enabled"] else (0,):
+            for _ in range(2):  # rounds continue across calls
+                G.check(G.lib().ginsim_cuda_barrier_bench(G.comm_handles([comm]), 1, mode, 500, ns.data_ptr(), None))
+                torch.cuda.synchronize()
+                comm.check_device()
+            res[f"barrier_mode{mode}_p50_ns"] = int(np.sort(ns.cpu().numpy())[250])
     # put+signal ping-pong over NVLink between ranks 0 and 1 (K14)
     if world >= 2 and os.environ.get("MP_PINGPONG", "1") == "1":
         size = 1 << 22

@@ -60,6 +60,22 @@ def test_multiprocess_moe_proxy_backend(layout, tokens):
             assert r["dispatch_window_exact"] and r["combine_window_exact"], r
 
 
+def test_multiprocess_barriers_dissemination_and_nvls():
+    """BarrierSession over real GPUs: the reference's dissemination barrier and
+    the NVLS multicast barrier (when the box exposes multicast) both complete
+    1000 rounds on every rank without a device timeout."""
+    n = gpu_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = 4 if n >= 4 else 2
+    res = _torchrun(n, {"MP_TOKENS": 64, "MP_PINGPONG": 0, "MP_BARRIER": 1, "MP_ITERS": 1})
+    for r in res:
+        assert r["barrier_mode0_p50_ns"] > 0, r
+        if r["nvls_enabled"]:
+            assert r["barrier_mode1_p50_ns"] > 0, r
+    print(json.dumps(res))
+
+
 def test_multiprocess_pingpong_nvlink():
     n = gpu_count()
     if n < 2:
