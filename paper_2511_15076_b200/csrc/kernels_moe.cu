@@ -997,7 +997,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   }
 
   // Phase C/D as the LSU kernel.
-  MOE_STAMP(R, 0, 5);
+  if (R.prof) {  // puts end = the CTA's LAST warp to drain its bulk stores
+    __shared__ unsigned long long warp_end;
+    if (tid == 0) warp_end = 0;
+    __syncthreads();
+    if (lane == 0) atomicMax(&warp_end, (unsigned long long)gin::globaltimer());
+    __syncthreads();
+    if (tid == 0) R.prof[((uint64_t)0 * 1024 + blockIdx.x) * 8 + 5] = warp_end;
+  }
   arrive_last(R.ws + 0, (unsigned)(R.iteration * G), &is_last);
   if (is_last) {
     if (tid == 0) *grab_ctr = 0;  // every CTA is past Phase B
