@@ -304,7 +304,7 @@ def measure_proxy(G, rank, world, local, dist, torch, dev, stream, allgather, T,
     dmsg, cmsg = 2 * H + 16, 2 * H
     disp_us, comb_us = t[0].item() * 1e3, t[1].item() * 1e3
     res = {"workload": f"proxy backend dispatch/combine, {T} tokens/rank, hidden {H}, top-{K} of {E}, bf16, "
-                       f"{world} GPU(s), one put per expert run",
+                       f"{world} GPU(s), one copy-engine put per (expert, source) run in both phases",
            "dispatch_us_p50": disp_us, "combine_us_p50": comb_us,
            "dispatch_GBps_per_gpu": T * K * dmsg / (disp_us * 1e-6) / 1e9,
            "combine_GBps_per_gpu": T * K * cmsg / (comb_us * 1e-6) / 1e9,

@@ -46,6 +46,7 @@ struct MoeRankArgs {
   unsigned int* ws;           // per-moe arrival counters [0] dispatch [1] combine [2] slot barrier
   uint32_t* route;            // TMA dispatch scratch: hist [kMaxGrid][E], prefix [kMaxGrid][E], totals [E]
   char** dst_g;               // TMA dispatch: [T][Kp] destination pointer of every (t, k) pair
+  uint32_t* midx;             // proxy: [T][K] index of (t, k)'s result in the combine mirror window
   const uint16_t* x;          // [T][H]
   const int32_t* idx;         // [T][K]
   const void* weights;        // [T][K] u16 (mode 0) / f32 (mode 1)
@@ -67,6 +68,7 @@ struct MoeLaunch {
   uint32_t E, K, T, H, mode, layout, e_local, parts, cparts;
   uint32_t win_dispatch, win_counts, win_combine;
   uint32_t win_stage, win_cstage, coalesce;  // proxy backend: dispatch / combine staging windows
+  uint32_t win_mirror;           // proxy + coalesce: combine results in the source's send order
   uint32_t coop;                 // TMA dispatch: cooperative route tables + all-token work (large T*K)
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
@@ -319,6 +321,9 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
         const uint32_t s = run[e];
         run[e] = s + 1;  // experts of one token are distinct
         slots[(t - t0) * K + lane] = s;
+        // proxy: where (t, k)'s combine result lands in this rank's mirror
+        // window -- the send order [dst][expert prefix][slot]
+        if (PROXY) R.midx[(uint64_t)t * K + lane] = (e / e_local) * T * K + prefix_e[e] + s;
       }
       __syncwarp();
     }
@@ -475,7 +480,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
     pair_start[i] = c;
   }
   __syncthreads();
-  if (L.layout == 1) source_prefix<kMoeWarps>(cnt, src_prefix, n, e_local);
+  // (the proxy mirror needs the per-source expert prefix in both layouts)
+  if (L.layout == 1 || PROXY) source_prefix<kMoeWarps>(cnt, src_prefix, n, e_local);
   block_exclusive_scan(pair_start, P, warp_tot, &total_msgs);
   if (tid == 0) pair_start[P] = total_msgs;
   __syncthreads();
@@ -510,8 +516,16 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       k = meta[8] | (meta[9] << 8) | (meta[10] << 16) | ((uint32_t)meta[11] << 24);
     }
     const uint32_t e = rank * e_local + e_loc;
-    char* dst = (PROXY && src != rank) ? v->win[L.win_cstage].base[rank] + (uint64_t)m * cmsg
-                                       : cbases[src] + ((uint64_t)token * K + k) * cmsg;
+    char* dst;
+    if (!PROXY) {
+      dst = cbases[src] + ((uint64_t)token * K + k) * cmsg;
+    } else if (src != rank) {
+      dst = v->win[L.win_cstage].base[rank] + (uint64_t)m * cmsg;  // staged for the agent
+    } else if (L.coalesce) {  // own tokens: straight into this rank's mirror window
+      dst = v->win[L.win_mirror].base[rank] + ((uint64_t)rank * T * K + src_prefix[lo] + slot) * cmsg;
+    } else {
+      dst = cbases[src] + ((uint64_t)token * K + k) * cmsg;
+    }
     if (vec_ok) {
       const uint32_t vlo = p * vec_per_part, vhi = min(vlo + vec_per_part, nvec);
       uint32_t i = vlo + lane;
@@ -546,6 +560,17 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc) {
         if ((rank * e_local + e_loc) % n_ctx != ctx) continue;
         const uint32_t pr = e_loc * n + src;
+        if (L.coalesce) {
+          // one put per (expert, source) run: the results of one expert for one
+          // source are contiguous in the staging window (receive order) and in
+          // the source's mirror window (its send order), so the agent moves
+          // them with ONE copy-engine transfer
+          if (src != rank && cnt[pr])
+            g.put(me, world, src, L.win_mirror, ((uint64_t)rank * T * K + src_prefix[pr]) * cmsg, L.win_cstage,
+                  (uint64_t)pair_start[pr] * cmsg, (uint64_t)cnt[pr] * cmsg);
+          c += cnt[pr];
+          continue;
+        }
         for (uint32_t slot = 0; src != rank && slot < cnt[pr]; ++slot) {  // own tokens were written in place
           const uint64_t moff = L.layout == 0 ? (((uint64_t)e_loc * n + src) * T + slot) * dmsg
                                               : ((uint64_t)src * T * K + src_prefix[pr] + slot) * dmsg;
@@ -583,7 +608,16 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
     }
   }
   __syncthreads();
-  const char* crecv = v->win[L.win_combine].base[rank];
+  char* crecv = v->win[L.win_combine].base[rank];
+  // proxy + coalesce: results arrived in the mirror window (send order); the
+  // reduce gathers them through the (t, k) -> mirror index of the dispatch and
+  // also writes them to (t*K+k)*cmsg, so the combine window ends identical to
+  // the reference's (harness_moe.cpp:203-205)
+  const bool mirrored = PROXY && L.coalesce;
+  const char* mirror = mirrored ? v->win[L.win_mirror].base[rank] : nullptr;
+  auto ysrc = [&](uint32_t t, uint32_t k) -> const char* {
+    return mirrored ? mirror + (uint64_t)R.midx[(uint64_t)t * K + k] * cmsg : crecv + ((uint64_t)t * K + k) * cmsg;
+  };
   const uint64_t ritems = (uint64_t)T * parts;
   for (uint64_t it = (uint64_t)b * kMoeWarps + warp; it < ritems; it += (uint64_t)G * kMoeWarps) {
     const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
@@ -596,7 +630,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
           const uint16_t* w = reinterpret_cast<const uint16_t*>(R.weights) + (uint64_t)t * K;
           for (uint32_t k = 0; k < K; ++k) {
             const uint32_t wk = w[k];
-            const uint4 y = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+            const uint4 y = gin::ld_nc_v4(ysrc(t, k) + 16ull * i);
+            if (mirrored) gin::st_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i, y);
             const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -615,7 +650,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
           const float* w = reinterpret_cast<const float*>(R.weights) + (uint64_t)t * K;
           for (uint32_t k = 0; k < K; ++k) {
             const float wk = w[k];
-            const uint4 y = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+            const uint4 y = gin::ld_nc_v4(ysrc(t, k) + 16ull * i);
+            if (mirrored) gin::st_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i, y);
             const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -638,14 +674,18 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
         if (L.mode == 0) {
           uint32_t acc = 0;
           const uint16_t* w = reinterpret_cast<const uint16_t*>(R.weights) + (uint64_t)t * K;
-          for (uint32_t k = 0; k < K; ++k)
-            acc += (uint32_t)w[k] * reinterpret_cast<const uint16_t*>(crecv + ((uint64_t)t * K + k) * cmsg)[j];
+          for (uint32_t k = 0; k < K; ++k) {
+            const uint16_t y = reinterpret_cast<const uint16_t*>(ysrc(t, k))[j];
+            if (mirrored) reinterpret_cast<uint16_t*>(crecv + ((uint64_t)t * K + k) * cmsg)[j] = y;
+            acc += (uint32_t)w[k] * y;
+          }
           o16[j] = (uint16_t)acc;
         } else {
           float acc = 0.f;
           const float* w = reinterpret_cast<const float*>(R.weights) + (uint64_t)t * K;
           for (uint32_t k = 0; k < K; ++k) {
-            const uint16_t y = reinterpret_cast<const uint16_t*>(crecv + ((uint64_t)t * K + k) * cmsg)[j];
+            const uint16_t y = reinterpret_cast<const uint16_t*>(ysrc(t, k))[j];
+            if (mirrored) reinterpret_cast<uint16_t*>(crecv + ((uint64_t)t * K + k) * cmsg)[j] = y;
             acc = __fadd_rn(acc, __fmul_rn(w[k], __uint_as_float((uint32_t)y << 16)));
           }
           o16[j] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
@@ -1343,8 +1383,10 @@ struct ginsim_cuda_moe_s {
   Comm* comm = nullptr;
   ginsim_cuda_moe_config cfg{};
   uint32_t e_local = 0, parts = 4, G = 0, Gc = 0, Gr = 0, chunk = 0, cparts = 1, cchunk = 0;
-  uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0, win_stage = 0, win_cstage = 0;
+  uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0, win_stage = 0, win_cstage = 0, win_mirror = 0;
   bool proxy = false;
+  void* buf_mirror = nullptr;
+  uint32_t* midx = nullptr;
   void* buf_stage = nullptr;
   void* buf_cstage = nullptr;
   void* buf_dispatch = nullptr;
@@ -1401,6 +1443,11 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
     if ((rc = ginsim_cuda_window_register(comm, m->buf_stage, sbytes, &m->win_stage))) fail(rc, ginsim_cuda_last_error());
     if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_cstage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
     if ((rc = ginsim_cuda_window_register(comm, m->buf_cstage, cbytes2, &m->win_cstage))) fail(rc, ginsim_cuda_last_error());
+    // combine results in send order ([dst][expert prefix][slot]): one put per run
+    if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_mirror)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+    if ((rc = ginsim_cuda_window_register(comm, m->buf_mirror, cbytes2, &m->win_mirror))) fail(rc, ginsim_cuda_last_error());
+    DeviceGuard dgm(c->device);
+    GIN_CUDA(cudaMalloc(&m->midx, (size_t)T * K * 4));
   }
   DeviceGuard g(c->device);
   GIN_CUDA(cudaMalloc(&m->ws, 256));
@@ -1429,6 +1476,7 @@ int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
     cudaDeviceSynchronize();
     if (moe->ws) cudaFree(moe->ws);
     if (moe->route) cudaFree(moe->route);
+    if (moe->midx) cudaFree(moe->midx);
     if (moe->dst_g) cudaFree(moe->dst_g);
     if (moe->prof) cudaFree(moe->prof);
   }
@@ -1482,6 +1530,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.win_combine = moes[0]->win_combine;
   L.win_stage = moes[0]->win_stage;
   L.win_cstage = moes[0]->win_cstage;
+  L.win_mirror = moes[0]->win_mirror;
   // Proxy backend: one put descriptor per expert run (default) or per message
   // (GINSIM_PROXY_COALESCE=0, the reference's one-put-per-(t,k) pattern).
   const char* cv = std::getenv("GINSIM_PROXY_COALESCE");
@@ -1501,6 +1550,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
     L.r[i].ws = moes[i]->ws;
     L.r[i].route = moes[i]->route;
     L.r[i].dst_g = moes[i]->dst_g;
+    L.r[i].midx = moes[i]->midx;
     L.r[i].prof = moes[i]->prof;
   }
   return L;

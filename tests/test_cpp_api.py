@@ -1,0 +1,36 @@
+"""The reference-shaped C++ host API (include/ginsim/runtime.hpp) compiles
+with g++ against libginsim_b200.so and runs: host-only checks on CPU, the
+Listing-2 ring (harness_ring.cpp:18-57) on the GPU box."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIBDIR = os.path.join(ROOT, "paper_2511_15076_b200", "_lib")
+CUDA = "/usr/local/cuda"
+
+
+def _build(tmp_path):
+    exe = str(tmp_path / "ring_ref_api")
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I", f"{CUDA}/include",
+           os.path.join(ROOT, "tests", "cpp", "ring_ref_api.cpp"), "-o", exe, "-L", LIBDIR, "-lginsim_b200",
+           f"-Wl,-rpath,{LIBDIR}", "-L", f"{CUDA}/lib64", "-lcudart", "-lpthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return exe
+
+
+def test_cpp_reference_api_compiles_and_host_checks_pass(tmp_path):
+    exe = _build(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "host checks ok" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_reference_api_ring_on_gpu(tmp_path):
+    exe = _build(tmp_path)
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ring ok" in r.stdout

@@ -328,3 +328,27 @@ def test_agent_copies_progress_while_every_sm_is_held():
     if "d2d_vmm_to_peer_mapping" in rows:
         assert rows["d2d_vmm_to_peer_mapping"]["completed_while_sms_held"]
         assert rows["h2d_pinned_to_peer_mapping_8B"]["completed_while_sms_held"]
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_dissemination_barrier_emulated_and_nvls_gating(n):
+    """BarrierSession (runtime.cpp:651-666) on n emulated ranks: 300 rounds of
+    ceil(log2 n) signal exchanges complete on every rank (twice: rounds
+    continue across calls); the NVLS barrier stays off when ranks share a
+    device (multicast needs distinct devices) and asking for it is refused."""
+    cs = world(n)
+    try:
+        assert not any(c.nvls_enabled() for c in cs)
+        ns = U.malloc(8 * 300)
+        for _ in range(2):
+            G.check(G.lib().ginsim_cuda_barrier_bench(G.comm_handles(cs), n, 0, 300, ns, None))
+            U.sync()
+        t = U.d2h(ns, 8 * 300, np.uint64)
+        assert (t > 0).all()
+        for c in cs:
+            c.check_device()
+        with pytest.raises(G.UsageError):
+            G.check(G.lib().ginsim_cuda_barrier_bench(G.comm_handles(cs), n, 1, 10, ns, None))
+        U.free(ns)
+    finally:
+        close(cs)
