@@ -402,32 +402,54 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
   // Phase C: the last CTA to finish releases every expert.
   arrive_last(R.ws + 0, (unsigned)(R.iteration * G), &is_last);
   if (is_last && PROXY) {
-    // One thread per expert submits, in this order on ctx e % n_ctx: the
-    // count (inline put), the payload run (one put, or one per message when
-    // coalescing is off), then the release SignalAdd((1<<32)+count).  The
-    // agent drains each context ring in ticket order onto one stream, so the
-    // release lands after the payload (fabric.cpp:63-79).
+    // Three phases, each fully submitted before the next (CTA barrier), so on
+    // every context ring all counts precede all payload puts, which precede
+    // all releases: a release lands after its expert's payload (the agent
+    // drains a ring in ticket order onto one stream, fabric.cpp:63-79).
+    //   coalesce: every op of destination d goes on ctx d % n_ctx, and with
+    //     the compact layout all of d's experts form ONE contiguous run at
+    //     both ends (staging [dst_base][prefix][slot] == d's window
+    //     [src][prefix][slot]) -> one copy-engine transfer per destination;
+    //     with the reference layout one run per expert.
+    //   reference pattern (GINSIM_PROXY_COALESCE=0): ctx e % n_ctx and one
+    //     put per (t, k) message (harness_moe.cpp:135-167).
+    // Own experts' rows were written in place by the SMs (a same-device copy
+    // by the agent would need SMs this kernel holds): counts and releases only.
     const gin::Team world = gin::WorldTeam(n);
     gin::CoopThread me;
+    auto ctx_of = [&](uint32_t e) { return L.coalesce ? (e / e_local) % v->n_ctx : e % v->n_ctx; };
     for (uint32_t e = tid; e < E; e += kMoeThreads) {
-      const uint32_t dst = e / e_local, e_loc = e % e_local, cnt = hist_all[e];
-      const gin::Gin g(v, e % v->n_ctx);
-      g.put_value(me, world, dst, L.win_counts, ((uint64_t)e_loc * n + rank) * 4, cnt);
-      const uint64_t src0 = ((uint64_t)dst_base[dst] + prefix_e[e]) * dmsg;
-      const uint64_t dst0 = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T) * dmsg
-                                          : ((uint64_t)rank * T * K + prefix_e[e]) * dmsg;
-      const gin::Action rel = gin::SignalAction(e_loc, gin::SignalAdd((1ull << 32) + cnt));
-      if (dst == rank) {
-        // own experts: rows were written in place by the SMs (a same-device
-        // copy by the agent would need SMs this kernel holds); release only
-        g.signal(me, world, dst, e_loc, rel.op);
-      } else if (L.coalesce) {
-        g.put(me, world, dst, L.win_dispatch, dst0, L.win_stage, src0, (uint64_t)cnt * dmsg, rel);
-      } else {
-        for (uint32_t q = 0; q < cnt; ++q)
-          g.put(me, world, dst, L.win_dispatch, dst0 + q * dmsg, L.win_stage, src0 + q * dmsg, dmsg);
-        g.signal(me, world, dst, e_loc, rel.op);
+      const uint32_t dst = e / e_local, e_loc = e % e_local;
+      gin::Gin(v, ctx_of(e)).put_value(me, world, dst, L.win_counts, ((uint64_t)e_loc * n + rank) * 4, hist_all[e]);
+    }
+    __syncthreads();
+    if (L.coalesce && L.layout == 1) {
+      for (uint32_t d = tid; d < n; d += kMoeThreads) {
+        const uint32_t tot = dst_base[d + 1] - dst_base[d];
+        if (d == rank || tot == 0) continue;
+        gin::Gin(v, d % v->n_ctx).put(me, world, d, L.win_dispatch, (uint64_t)rank * T * K * dmsg, L.win_stage,
+                                       (uint64_t)dst_base[d] * dmsg, (uint64_t)tot * dmsg);
       }
+    } else {
+      for (uint32_t e = tid; e < E; e += kMoeThreads) {
+        const uint32_t dst = e / e_local, e_loc = e % e_local, cnt = hist_all[e];
+        if (dst == rank || cnt == 0) continue;
+        const gin::Gin g(v, ctx_of(e));
+        const uint64_t src0 = ((uint64_t)dst_base[dst] + prefix_e[e]) * dmsg;
+        const uint64_t dst0 = L.layout == 0 ? (((uint64_t)e_loc * n + rank) * T) * dmsg
+                                            : ((uint64_t)rank * T * K + prefix_e[e]) * dmsg;
+        if (L.coalesce) {
+          g.put(me, world, dst, L.win_dispatch, dst0, L.win_stage, src0, (uint64_t)cnt * dmsg);
+        } else {
+          for (uint32_t q = 0; q < cnt; ++q)
+            g.put(me, world, dst, L.win_dispatch, dst0 + q * dmsg, L.win_stage, src0 + q * dmsg, dmsg);
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < E; e += kMoeThreads) {
+      const uint32_t dst = e / e_local, e_loc = e % e_local;
+      gin::Gin(v, ctx_of(e)).signal(me, world, dst, e_loc, gin::SignalAdd((1ull << 32) + hist_all[e]));
     }
   } else if (is_last) {
     release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local);
@@ -482,6 +504,18 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
   __syncthreads();
   // (the proxy mirror needs the per-source expert prefix in both layouts)
   if (L.layout == 1 || PROXY) source_prefix<kMoeWarps>(cnt, src_prefix, n, e_local);
+  // proxy + coalesce: the staging window holds results source-major
+  // ([src_base[s] + src_prefix + slot]) so all of a source's results are one
+  // contiguous run at both ends (its mirror region is [rank*T*K + prefix + slot])
+  __shared__ uint32_t src_base[GIN_MAX_RANKS + 1];
+  if (PROXY) {
+    __syncthreads();
+    if (tid == 0) {
+      src_base[0] = 0;
+      for (uint32_t sidx = 0; sidx < n; ++sidx)
+        src_base[sidx + 1] = src_base[sidx] + src_prefix[(e_local - 1) * n + sidx] + cnt[(e_local - 1) * n + sidx];
+    }
+  }
   block_exclusive_scan(pair_start, P, warp_tot, &total_msgs);
   if (tid == 0) pair_start[P] = total_msgs;
   __syncthreads();
@@ -519,8 +553,9 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
     char* dst;
     if (!PROXY) {
       dst = cbases[src] + ((uint64_t)token * K + k) * cmsg;
-    } else if (src != rank) {
-      dst = v->win[L.win_cstage].base[rank] + (uint64_t)m * cmsg;  // staged for the agent
+    } else if (src != rank) {  // staged for the agent
+      dst = v->win[L.win_cstage].base[rank] +
+            (L.coalesce ? (uint64_t)src_base[src] + src_prefix[lo] + slot : (uint64_t)m) * cmsg;
     } else if (L.coalesce) {  // own tokens: straight into this rank's mirror window
       dst = v->win[L.win_mirror].base[rank] + ((uint64_t)rank * T * K + src_prefix[lo] + slot) * cmsg;
     } else {
@@ -550,7 +585,20 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
 
   // Release: the last CTA signals each (source, context) with its count.
   arrive_last(R.ws + 1, (unsigned)(R.iteration * G), &is_last);
-  if (is_last && PROXY) {
+  if (is_last && PROXY && L.coalesce) {
+    // one copy-engine transfer per source (all its results, every expert),
+    // then that source's combine flag with the total, on ctx src % n_ctx
+    const gin::Team world = gin::WorldTeam(n);
+    gin::CoopThread me;
+    for (uint32_t src = tid; src < n; src += kMoeThreads) {
+      const uint32_t tot = src_base[src + 1] - src_base[src];
+      const gin::Gin g(v, src % n_ctx);
+      if (src != rank && tot)
+        g.put(me, world, src, L.win_mirror, (uint64_t)rank * T * K * cmsg, L.win_cstage, (uint64_t)src_base[src] * cmsg,
+              (uint64_t)tot * cmsg);
+      if (tot) g.signal(me, world, src, e_local, gin::SignalAdd(tot));
+    }
+  } else if (is_last && PROXY) {  // reference pattern: one put per message, per-(source, ctx) flags
     const gin::Team world = gin::WorldTeam(n);
     gin::CoopThread me;
     for (uint32_t sc = tid; sc < n * n_ctx; sc += kMoeThreads) {
@@ -560,17 +608,6 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc) {
         if ((rank * e_local + e_loc) % n_ctx != ctx) continue;
         const uint32_t pr = e_loc * n + src;
-        if (L.coalesce) {
-          // one put per (expert, source) run: the results of one expert for one
-          // source are contiguous in the staging window (receive order) and in
-          // the source's mirror window (its send order), so the agent moves
-          // them with ONE copy-engine transfer
-          if (src != rank && cnt[pr])
-            g.put(me, world, src, L.win_mirror, ((uint64_t)rank * T * K + src_prefix[pr]) * cmsg, L.win_cstage,
-                  (uint64_t)pair_start[pr] * cmsg, (uint64_t)cnt[pr] * cmsg);
-          c += cnt[pr];
-          continue;
-        }
         for (uint32_t slot = 0; src != rank && slot < cnt[pr]; ++slot) {  // own tokens were written in place
           const uint64_t moff = L.layout == 0 ? (((uint64_t)e_loc * n + src) * T + slot) * dmsg
                                               : ((uint64_t)src * T * K + src_prefix[pr] + slot) * dmsg;

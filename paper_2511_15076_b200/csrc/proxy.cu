@@ -93,8 +93,35 @@ struct ProxyAgent {
     return e;
   }
 
+  // Stream memory operations (signals, counters, aligned inline values) are
+  // gathered and issued with one cuStreamBatchMemOp per run of consecutive
+  // memops; a copy in between flushes them first, so stream order == the
+  // ring's ticket order (the watermark rule, fabric.cpp:63-79).
+  std::vector<CUstreamBatchMemOpParams> memops;
+  static constexpr size_t kMaxBatch = 128;
+
+  void flush_memops() {
+    if (memops.empty()) return;
+    GIN_CU(cuapi().cuStreamBatchMemOp((CUstream)stream, (unsigned)memops.size(), memops.data(), 0));
+    memops.clear();
+  }
   void write64(uint64_t* dev_addr, uint64_t v) {
-    GIN_CU(cuapi().cuStreamWriteValue64((CUstream)stream, (CUdeviceptr)dev_addr, v, CU_STREAM_WRITE_VALUE_DEFAULT));
+    CUstreamBatchMemOpParams op{};
+    op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+    op.writeValue.address = (CUdeviceptr)dev_addr;
+    op.writeValue.value64 = v;
+    op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    memops.push_back(op);
+    if (memops.size() >= kMaxBatch) flush_memops();
+  }
+  void write32(void* dev_addr, uint32_t v) {
+    CUstreamBatchMemOpParams op{};
+    op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    op.writeValue.address = (CUdeviceptr)dev_addr;
+    op.writeValue.value = v;
+    op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    memops.push_back(op);
+    if (memops.size() >= kMaxBatch) flush_memops();
   }
 
   // iput / iput_signal (plugin.hpp:86-90) for one decoded descriptor.
@@ -113,13 +140,20 @@ struct ProxyAgent {
         const GinWindowView& sw = v.win[d.src_window];
         if (d.src_offset_or_value > sw.size[v.rank] || d.bytes > sw.size[v.rank] - d.src_offset_or_value)
           fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: source range exceeds capacity");
+        flush_memops();
         GIN_CUDA(cudaMemcpyAsync(dst, sw.base[v.rank] + d.src_offset_or_value, d.bytes, cudaMemcpyDefault, stream));
+        n_copies.fetch_add(1, std::memory_order_relaxed);
+      } else if (d.bytes == 4 && ((uintptr_t)dst & 3) == 0) {  // aligned inline values: a memop, no copy
+        write32(dst, (uint32_t)d.src_offset_or_value);
+      } else if (d.bytes == 8 && ((uintptr_t)dst & 7) == 0) {
+        write64(reinterpret_cast<uint64_t*>(dst), d.src_offset_or_value);
       } else {
         uint64_t* s = stage + (stage_next++ % kStage);
         *s = d.src_offset_or_value;
+        flush_memops();
         GIN_CUDA(cudaMemcpyAsync(dst, s, d.bytes, cudaMemcpyHostToDevice, stream));
+        n_copies.fetch_add(1, std::memory_order_relaxed);
       }
-      n_copies.fetch_add(1, std::memory_order_relaxed);
     }
     if (d.flags & GIN_FLAG_HAS_SIGNAL) {
       if (d.signal_id >= v.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "proxy: signal out of range");
@@ -167,7 +201,6 @@ struct ProxyAgent {
         std::memcpy(raw, slot->bytes, 64);
         __atomic_store_n(&slot->seq, t + cap, __ATOMIC_RELEASE);
         tail[ctx] = t + 1;
-        __atomic_store_n(consumed_host + ctx, t + 1, __ATOMIC_RELEASE);
         ginsim_cuda_descriptor d;
         descriptor_decode(raw, &d);  // a malformed descriptor is a protocol bug: fail the run
         if (d.flags & GIN_FLAG_HAS_COUNTER) counter_pending[d.counter_id].fetch_add(1, std::memory_order_acq_rel);
@@ -176,6 +209,8 @@ struct ProxyAgent {
         any_dev = true;
         consumed[ctx] = t + 1;
       }
+      // free the drained slots for the GPU producers once per ring batch
+      if (consumed[ctx]) __atomic_store_n(consumed_host + ctx, consumed[ctx], __ATOMIC_RELEASE);
     }
     {
       std::unique_lock<std::mutex> lk(hq_mu);
@@ -199,6 +234,7 @@ struct ProxyAgent {
         // once the copies above have completed (stream order).
         if (any_dev && consumed[ctx]) write64(c->host_view.proxy.completed + ctx, consumed[ctx]);
       }
+      flush_memops();
       pass.ev = get_event();
       GIN_CUDA(cudaEventRecord(pass.ev, stream));
       pass.stage_end = stage_next;

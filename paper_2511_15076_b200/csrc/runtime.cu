@@ -37,6 +37,8 @@ const CuApi& cuapi() {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&api.cuStreamWriteValue64), cudaEnableDefault, &q) != cudaSuccess || !api.cuStreamWriteValue64)
       throw GinError(GINSIM_E_CUDA, "driver entry point cuStreamWriteValue64 unavailable");
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", reinterpret_cast<void**>(&api.cuStreamBatchMemOp), cudaEnableDefault, &q) != cudaSuccess || !api.cuStreamBatchMemOp)
+      throw GinError(GINSIM_E_CUDA, "driver entry point cuStreamBatchMemOp unavailable");
     if (cudaGetDriverEntryPoint("cuGetErrorString", reinterpret_cast<void**>(&api.cuGetErrorString), cudaEnableDefault, &q) != cudaSuccess || !api.cuGetErrorString)
       throw GinError(GINSIM_E_CUDA, "driver entry point cuGetErrorString unavailable");
     if (cudaGetDriverEntryPoint("cuMemAddressFree", reinterpret_cast<void**>(&api.cuMemAddressFree), cudaEnableDefault, &q) != cudaSuccess || !api.cuMemAddressFree)

@@ -51,6 +51,7 @@ void cu_check(CUresult r, const char* what);
 // GPU driver; the first driver call resolves the table or fails loudly.
 struct CuApi {
   decltype(&::cuStreamWriteValue64) cuStreamWriteValue64 = nullptr;
+  decltype(&::cuStreamBatchMemOp) cuStreamBatchMemOp = nullptr;
   decltype(&::cuGetErrorString) cuGetErrorString = nullptr;
   decltype(&::cuMemAddressFree) cuMemAddressFree = nullptr;
   decltype(&::cuMemAddressReserve) cuMemAddressReserve = nullptr;
