@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--tokens", type=int, default=N_TOK)
     p.add_argument("--mode", type=int, default=1, help="0 = u16 exact, 1 = bf16")
-    p.add_argument("--layout", type=int, default=1, help="0 = reference layout, 1 = compact")
+    p.add_argument("--layout", type=int, default=1, help="0 = reference layout, 1 = compact, 2 = compact + dedup transport")
     p.add_argument("--ctas", type=int, default=0)
     p.add_argument("--engine", type=int, default=0, help="0 = auto (TMA), 1 = LSU stores, 2 = TMA")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -336,6 +336,52 @@ def measure_barrier(G, comm, rank, world, dist, torch, dev, iters=2000):
     return out
 
 
+def measure_dedup(G, comm, rank, world, dist, torch, dev, stream, T, steps=10):
+    """Labelled variant: layout 2 = the same compact receive
+    layout with a per-rank dedup transport -- one NVLink row per (token,
+    destination rank), fanned out into the expert slots by the destination.
+    Windows and cells end identical to the default path (tests); only the
+    wire traffic changes.  Per-phase device time, max over ranks."""
+    H, K, E = HIDDEN, TOPK, EXPERTS
+    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 1, 2, 0, 0))
+    x = torch.empty(T * H, dtype=torch.int16, device=dev)
+    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
+    w = torch.empty(T * K, dtype=torch.float32, device=dev)
+    out = torch.empty(T * H, dtype=torch.int16, device=dev)
+    moe.generate(1, rank, x, idx, w, stream=stream)
+    for _ in range(3):
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for i in range(steps):
+        ev[i][0].record(stream)
+        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        ev[i][1].record(stream)
+        G.Moe.combine([moe], [w], [out], stream=stream)
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    comm.check_device()
+    d = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    c = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    t = torch.tensor([d, c], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    import numpy as np
+    ih = idx.cpu().numpy().reshape(T, K) // (E // world)
+    rows_remote = sum(len(set(int(v) for v in row) - {rank}) for row in ih)
+    msgs_remote = int((ih != rank).sum())
+    disp_us = t[0].item() * 1e3
+    moe.destroy()
+    return {"workload": f"labelled variant: dedup transport (layout 2), {T} tokens/rank, hidden {H}, top-{K} of {E}, "
+                        f"bf16, {world} GPU(s)",
+            "dispatch_us": disp_us, "combine_us": t[1].item() * 1e3,
+            "remote_rows_per_rank": rows_remote, "remote_messages_per_rank": msgs_remote,
+            "wire_GBps_per_gpu": rows_remote * (2 * H + 128) / (disp_us * 1e-6) / 1e9}
+
+
 def ctypes_stream(stream):
     return None if stream is None else stream.cuda_stream
 
@@ -436,6 +482,7 @@ def main():
     pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm, rank, world, dist, torch, dev)
     a2a = None if (args.no_extras or world < 2) else measure_a2a(G, comm, rank, world, dist, torch, dev, stream)
     barrier = None if (args.no_extras or world < 2) else measure_barrier(G, comm, rank, world, dist, torch, dev)
+    dedup = None if (args.no_extras or world < 2) else measure_dedup(G, comm, rank, world, dist, torch, dev, stream, T)
     proxy = None
     if not args.no_extras:
         ag = allgather if world > 1 else None
@@ -551,6 +598,7 @@ def main():
         "pingpong": pp,
         "alltoall": a2a,
         "barrier": barrier,
+        "dedup_variant": dedup,
         "proxy_vs_direct": proxy,
     }
     if world > 1:

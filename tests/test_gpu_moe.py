@@ -385,3 +385,35 @@ def test_moe_proxy_backend_bf16_ll_shape():
             assert (run.output(r) == exp).all(), r
     finally:
         run.close()
+
+
+@pytest.mark.parametrize("n,E,K,T,H,mode", [(2, 16, 4, 40, 256, 0), (4, 64, 8, 48, 7168, 1), (8, 64, 8, 32, 7168, 0),
+                                             (8, 256, 8, 64, 7168, 1), (2, 8, 3, 33, 64, 0)])
+def test_moe_dedup_transport_matches_reference(n, E, K, T, H, mode):
+    """Layout 2: one NVLink row per (token, destination rank), fanned out into
+    the expert slots by the destination.  Dispatch windows (through the
+    compact->reference map), combine windows, expert cells and outputs equal
+    the reference's over repeated steps and a routing change."""
+    run = MoeRun(n, E, K, T, H, mode=mode, layout=2, engine=2)
+    try:
+        for seed in (1, 6):
+            run.generate(seed)
+            run.step()
+            run.step()
+            cnt = O.counts(seed, n, E, K, T)
+            for r in range(n):
+                d, comb, cells = O.moe_rank_state(seed, n, E, K, T, H, r, mode=mode)
+                win = O.compact_to_reference(run.dispatch_window(r), cnt, r, n, E // n, T, K, 2 * H + 16)
+                assert (win == d).all(), (seed, r)
+                assert (run.combine_window(r) == comb).all(), (seed, r)
+                exp, _ = O.combine(seed, E, K, H, r, T, mode=mode)
+                assert (run.output(r) == exp).all(), (seed, r)
+        for r in range(n):  # 4 steps in all: cells are 4x the per-step values (2 per seed)
+            sig, _ = run.comms[r].snapshot_cells()
+            e_local = E // n
+            c1, c6 = O.counts(1, n, E, K, T), O.counts(6, n, E, K, T)
+            for e_loc in range(e_local):
+                e = r * e_local + e_loc
+                assert sig[e_loc] == 4 * (n << 32) + 2 * int(c1[e].sum()) + 2 * int(c6[e].sum()), (r, e_loc)
+    finally:
+        run.close()

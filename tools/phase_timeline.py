@@ -20,7 +20,7 @@ import torch.distributed as dist  # noqa: E402
 
 import paper_2511_15076_b200 as G  # noqa: E402
 
-NAMES = {0: ["own_hist", "bar1+col_scan", "bar2+slots", "bar3", "puts", "release", "acquire"], 1: ["counts_scan", "transform_puts", "flag_release"],
+NAMES = {0: ["own_hist", "bar1+col_scan", "bar2+slots", "bar3", "puts", "release", "fanout(L2)/acquire"], 1: ["counts_scan", "transform_puts", "flag_release"],
          2: ["flag_acquire", "reduce"]}
 
 
@@ -49,7 +49,7 @@ def main():
     else:
         rank, world, local = 0, 1, 0
         comm = G.Comm.create_all([0], G.Config(signal_cells=512))[0]
-    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 1, 1, 0, 0))
+    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 1, int(os.environ.get("TL_LAYOUT", 1)), 0, 0))
     dev = torch.device("cuda", local)
     x = torch.empty(T * H, dtype=torch.int16, device=dev)
     idx = torch.empty(T * K, dtype=torch.int32, device=dev)
