@@ -72,6 +72,7 @@ struct MoeLaunch {
   uint32_t win_mirror;           // proxy + coalesce: combine results in the source's send order
   uint32_t win_rows;             // layout 2: per-source row staging + 128-byte row headers
   uint32_t coop;                 // TMA dispatch: cooperative route tables + all-token work (large T*K)
+  uint32_t fuse_reduce;          // TMA combine: reduce inside the send kernel (small, latency-bound T)
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
 };
@@ -1675,6 +1676,24 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     }
   }
   MOE_STAMP(R, 1, 3);
+  if (L.fuse_reduce) {
+    // small launches: the source-side reduction right here (saves the second
+    // launch); same arithmetic as moe_combine_reduce_kernel
+    if (tid == 0) gin.wait_ge_signal(e_local, R.iteration * (uint64_t)T * K);
+    __syncthreads();
+    const char* crecv = v->win[L.win_combine].base[rank];
+    const uint32_t nvec = payload / 16;
+    const uint64_t ritems = (uint64_t)T * nvec, rstride = (uint64_t)G * kTmaThreads;
+    for (uint64_t q = (uint64_t)b * kTmaThreads + tid; q < ritems; q += rstride) {
+      const uint32_t t = (uint32_t)(q / nvec), i = (uint32_t)(q % nvec);
+      uint4 y[KMAX];
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < (int)K) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+      gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
+                 reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
+    }
+  }
 }
 
 // Source side of the combine, split off the TMA send kernel so it runs at
@@ -1974,6 +1993,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   const char* dy = std::getenv("GINSIM_MOE_SCHED");
   L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
   L.coop = moes[0]->coop ? 1u : 0u;
+  L.fuse_reduce = moes[0]->coop ? 0u : 1u;
   for (uint32_t i = 0; i < n; ++i) {
     if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
@@ -2065,6 +2085,16 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   uint32_t parts = 1, chunk = 0, cparts = 1, cchunk = 0;
   if (use_tma(m)) {
     parts = (payload + 8191) / 8192;
+    if (!m->coop) {
+      // small (latency-bound) launches: split rows further so every warp of a
+      // CTA has an item (LL: one token per CTA -> 8 chunks of 1.75 KiB)
+      int sms0 = 0;
+      GIN_CUDA(cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, m->comm->device));
+      const uint32_t G0 = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sms0 / n, m->cfg.tokens));
+      const uint32_t tpc = (m->cfg.tokens + G0 - 1) / G0;
+      const uint32_t want = ((uint32_t)kTmaWarps + tpc - 1) / tpc;
+      parts = std::max(parts, std::min(want, std::max(1u, payload / 1024u)));
+    }
     chunk = ((payload + parts - 1) / parts + 15) / 16 * 16;
     m->chunk = chunk;
     cparts = (payload + 4095) / 4096;
@@ -2176,7 +2206,7 @@ int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const voi
   void* args[] = {&L, &chunk};
   const uint32_t Gc = moes[0]->Gc;
   launch_coop(k.combine, Gc, n, combine_threads(k), combine_smem(moes[0]), args, (cudaStream_t)stream);
-  if (k.reduce && !L.no_wait) {  // profiling harness: the reduce would wait on every source's flag
+  if (k.reduce && !L.no_wait && !L.fuse_reduce) {  // profiling harness: the reduce would wait on every source's flag
     GIN_CUDA(cudaLaunchKernel(k.reduce, dim3(moes[0]->Gr, n), dim3(kMoeThreads), args, 0, (cudaStream_t)stream));
   }
   moes[0]->last_ctas = Gc * n;
