@@ -1364,6 +1364,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
 
   // ---- Phase F: receive side -- fan the rows of every source out into the
   // expert slots of this rank's dispatch window
+  if (L.no_wait) return;  // profiling harness: the sender's part only
   if (tid == 0) gin.wait_ge_signal(e_local + 1, R.iteration * (uint64_t)(n - 1));
   __syncthreads();
   gin::tma::fence_proxy_async_global();  // rows/headers written by peers -> read by this CTA's bulk loads

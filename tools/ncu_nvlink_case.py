@@ -60,6 +60,12 @@ def main():
         with torch.cuda.device(r):
             G.Moe.combine([moes[r]], [bufs[r][2]], [bufs[r][3]])   # send kernel only (reduce skipped)
             torch.cuda.synchronize(r)
+    # the dedup transport (layout 2): each rank's row puts alone
+    moes2 = G.Moe.create_all(comms, G.MoeConfig(E, K, T, H, 1, 2, 0, 0))
+    for r in range(n):
+        with torch.cuda.device(r):
+            G.Moe.dispatch([moes2[r]], [bufs[r][0]], [bufs[r][1]])
+            torch.cuda.synchronize(r)
     print("profiling harness done")
 
 
