@@ -747,7 +747,10 @@ constexpr int kTmaThreads = 256;
 constexpr int kTmaWarps = kTmaThreads / 32;
 constexpr int kCmbThreads = 512;
 constexpr int kCmbWarps = kCmbThreads / 32;
-constexpr int kTmaStages = 3;
+#ifndef GIN_TMA_STAGES
+#define GIN_TMA_STAGES 3
+#endif
+constexpr int kTmaStages = GIN_TMA_STAGES;
 
 struct TmaSmem {  // per-warp control block, followed by the staging buffers
   uint64_t bar[kTmaStages];

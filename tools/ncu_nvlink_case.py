@@ -8,7 +8,7 @@ one after another, so every launch runs alone and its nvltx/nvlrx + DRAM
 counters are attributable.  Not a benchmark: numbers printed here are not
 bench values.
 
-  GINSIM_PROFILE_NO_WAIT=1 ncu --section Nvlink --section SpeedOfLight \
+  GINSIM_NVLS=0 GINSIM_PROFILE_NO_WAIT=1 ncu --section Nvlink --section SpeedOfLight \
       --metrics nvltx__bytes.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       python tools/ncu_nvlink_case.py
 """
