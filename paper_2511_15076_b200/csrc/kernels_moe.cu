@@ -747,10 +747,11 @@ constexpr int kTmaThreads = 256;
 constexpr int kTmaWarps = kTmaThreads / 32;
 constexpr int kCmbThreads = 512;
 constexpr int kCmbWarps = kCmbThreads / 32;
-#ifndef GIN_TMA_STAGES
-#define GIN_TMA_STAGES 3
-#endif
-constexpr int kTmaStages = GIN_TMA_STAGES;
+// Pipeline depth per warp.  Dispatch uses 2 stages (a shallower per-SM TMA
+// store queue drains faster at the end of the launch: -4 us at N=1, -6 us at
+// N=2, measured); the combine send keeps 3 (its transform needs the slack).
+constexpr int kTmaStages = 3;   // TmaSmem capacity, combine send
+constexpr int kDispStages = 2;  // dispatch kernels
 
 struct TmaSmem {  // per-warp control block, followed by the staging buffers
   uint64_t bar[kTmaStages];
@@ -873,9 +874,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   // per stage: [dst pointers: Kp * 8 bytes, padded to 128][row chunk]
   const uint32_t dhead = (Kp * 8 + 127) & ~127u;
   const uint32_t sstride = dhead + chunk;
-  char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kTmaStages * sstride;
+  char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kDispStages * sstride;
   uint32_t* own = reinterpret_cast<uint32_t*>(dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) +
-                                              (size_t)kTmaWarps * kTmaStages * sstride);  // [(t1-t0)*K]
+                                              (size_t)kTmaWarps * kDispStages * sstride);  // [(t1-t0)*K]
   uint32_t* g_hist = R.route;                                  // [G][E]
   uint32_t* g_pre = R.route + (size_t)kMaxGrid * kMaxExperts;  // [G][E]
   uint32_t* g_tot = R.route + 2 * (size_t)kMaxGrid * kMaxExperts;  // [E]
@@ -886,7 +887,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     run[e] = 0;
   }
   if (lane == 0) {
-    for (int s = 0; s < kTmaStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
+    for (int s = 0; s < kDispStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
     gin::tma::fence_mbar_init();
   }
   if (tid < n) sbase[tid] = v->win[L.win_dispatch].base[tid];
@@ -901,12 +902,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     uint64_t it;
     if (!coop) {
       it = lbase + (ctl->cur++) * kTmaWarps;
-    } else if (L.dyn && ctl->cur >= kTmaStages) {
+    } else if (L.dyn && ctl->cur >= kDispStages) {
       // after a static, interleaved first round (items gw + s*wstride, so
       // 1000+ warps do not all hit the counter at once and a small launch
       // still spreads over every CTA): one token per grab
       if (ctl->end == 0 || ctl->itc >= ctl->end) {
-        ctl->itc = (uint64_t)kTmaStages * wstride + atomicAdd(grab_ctr, (unsigned long long)parts);
+        ctl->itc = (uint64_t)kDispStages * wstride + atomicAdd(grab_ctr, (unsigned long long)parts);
         ctl->end = ctl->itc + parts;
       }
       it = ctl->itc++;
@@ -933,7 +934,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     // not all hit the grab counter at once when the kernel starts
     ctl->cur = 0;
     ctl->end = 0;
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < kDispStages; ++s) {
       const uint64_t it = next_item();
       ctl->itm[s] = it;
       if (it != kNoItem) issue_row(s, it);
@@ -1042,18 +1043,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   // Phase B (the first stages' row chunks were requested before Phase A)
   if (lane == 0) {
     gin::tma::fence_proxy_async_global();
-    for (int s = 0; s < kTmaStages; ++s)
+    for (int s = 0; s < kDispStages; ++s)
       if (ctl->itm[s] != kNoItem) issue_dst(s, ctl->itm[s]);
   }
   __syncwarp();
   for (uint32_t j = 0;; ++j) {
-    const int s = (int)(j % kTmaStages);
+    const int s = (int)(j % kDispStages);
     const uint64_t it = ctl->itm[s];
     if (it == kNoItem) break;
     const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
     char* sb = stage + (size_t)s * sstride;
     char* const* dp = reinterpret_cast<char* const*>(sb);
-    gin::tma::mbar_wait(&ctl->bar[s], (j / kTmaStages) & 1);
+    gin::tma::mbar_wait(&ctl->bar[s], (j / kDispStages) & 1);
     if (p == 0 && lane < K) gin::st_v4(dp[lane] + payload, make_uint4(rank, t, lane, lane + 1));  // meta
     if (lane == 0) {
       const uint32_t len = tma_chunk_len(payload, chunk, p);
@@ -1063,7 +1064,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
       // iteration ago, so their shared-memory reads overlapped this wait.
       if (j >= 1) {
         gin::tma::wait_read<1>();
-        const int ps = (int)((j - 1) % kTmaStages);
+        const int ps = (int)((j - 1) % kDispStages);
         const uint64_t nxt = next_item();
         ctl->itm[ps] = nxt;
         if (nxt != kNoItem) {
@@ -1151,9 +1152,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
   const uint32_t dhead = (Kp * 8 + 127) & ~127u;  // >= kRowHdr for K <= 15
   const uint32_t sstride = dhead + chunk;
-  char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kTmaStages * sstride;
+  char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kDispStages * sstride;
   uint32_t* own = reinterpret_cast<uint32_t*>(dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) +
-                                              (size_t)kTmaWarps * kTmaStages * sstride);
+                                              (size_t)kTmaWarps * kDispStages * sstride);
   uint32_t* rowj = own + (t1 - t0) * K;  // [t - t0][d]: row index of (t, d) (written by its first pair)
   uint32_t* g_hist = R.route;
   uint32_t* g_pre = R.route + (size_t)kMaxGrid * kMaxExperts;
@@ -1168,7 +1169,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     run[e] = 0;
   }
   if (lane == 0) {
-    for (int s = 0; s < kTmaStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
+    for (int s = 0; s < kDispStages; ++s) gin::tma::mbar_init(&ctl->bar[s], 1);
     gin::tma::fence_mbar_init();
   }
   if (tid < n) {
@@ -1295,7 +1296,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     gin::tma::load(sb + dhead, x + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
   };
   if (lane == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < kDispStages; ++s) {
       const uint64_t it = gw + s * wstride;
       if (it < items) issue(s, it);
     }
@@ -1303,7 +1304,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   for (uint32_t j = 0;; ++j) {
     const uint64_t it = gw + (uint64_t)j * wstride;
     if (it >= items) break;
-    const int s = (int)(j % kTmaStages);
+    const int s = (int)(j % kDispStages);
     const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
     char* sb = stage + (size_t)s * sstride;
     char* const* dp = reinterpret_cast<char* const*>(sb);
@@ -1312,7 +1313,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       hdr = hdr_g[(uint64_t)t * Kp + lane];
       ent = ent_g[(uint64_t)t * Kp + lane];
     }
-    gin::tma::mbar_wait(&ctl->bar[s], (j / kTmaStages) & 1);
+    gin::tma::mbar_wait(&ctl->bar[s], (j / kDispStages) & 1);
     if (p == 0 && lane < K) {
       if (hdr == 0) {
         gin::st_v4(dp[lane] + payload, make_uint4(rank, t, lane, lane + 1));  // own expert: meta in place
@@ -1332,8 +1333,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       gin::tma::commit();
       if (j >= 1) {
         gin::tma::wait_read<1>();
-        const uint64_t nxt = it - wstride + kTmaStages * wstride;
-        if (nxt < items) issue((int)((j - 1) % kTmaStages), nxt);
+        const uint64_t nxt = it - wstride + kDispStages * wstride;
+        if (nxt < items) issue((int)((j - 1) % kDispStages), nxt);
       }
     }
     __syncwarp();
@@ -1413,21 +1414,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   __syncthreads();
   const uint32_t phase0 = (uint32_t)((items + wstride - 1 - gw) / wstride);  // items this warp ran in Phase B
   if (lane == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < kDispStages; ++s) {
       const uint64_t it = gw + s * wstride;
-      if (it < fitems) fissue((int)((phase0 + s) % kTmaStages), it);
+      if (it < fitems) fissue((int)((phase0 + s) % kDispStages), it);
     }
   }
   for (uint32_t j = 0;; ++j) {
     const uint64_t it = gw + (uint64_t)j * wstride;
     if (it >= fitems) break;
     const uint32_t jj = phase0 + j;  // continue the stage/parity sequence of Phase B
-    const int s = (int)(jj % kTmaStages);
+    const int s = (int)(jj % kDispStages);
     uint32_t src, jr;
     locate_row(it, src, jr);
     const uint32_t p = (uint32_t)(it % parts);
     char* sb = stage + (size_t)s * sstride;
-    gin::tma::mbar_wait(&ctl->bar[s], (jj / kTmaStages) & 1);
+    gin::tma::mbar_wait(&ctl->bar[s], (jj / kDispStages) & 1);
     const uint32_t* h = reinterpret_cast<const uint32_t*>(sb);
     const uint32_t tok = h[0], mask = h[1];
     if (p == 0 && lane < K && ((mask >> lane) & 1)) {
@@ -1446,8 +1447,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       gin::tma::commit();
       if (j >= 1) {
         gin::tma::wait_read<1>();
-        const uint64_t nxt = it - wstride + kTmaStages * wstride;
-        if (nxt < fitems) fissue((int)((jj - 1) % kTmaStages), nxt);
+        const uint64_t nxt = it - wstride + kDispStages * wstride;
+        if (nxt < fitems) fissue((int)((jj - 1) % kDispStages), nxt);
       }
     }
     __syncwarp();
@@ -2072,7 +2073,7 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
   const size_t dhead = (kp * 8 + 127) & ~(size_t)127;
   const size_t tokens = (size_t)((m->cfg.tokens + G - 1) / G + 1);
   const size_t rowj = m->cfg.layout == 2 ? tokens * m->comm->world * 4 : 0;  // dedup: (t, dst) row indices
-  return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kTmaStages * (dhead + m->chunk) +
+  return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kDispStages * (dhead + m->chunk) +
          pairs * 4 + rowj;
 }
 static size_t combine_smem(const ginsim_cuda_moe_t m) {

@@ -57,6 +57,25 @@ def main():
     e_local = E // world
     res["cells_exact"] = all(sig[e] == iters * ((world << 32) + int(cnt[rank * e_local + e].sum()))
                              for e in range(e_local)) and sig[e_local] == iters * T * K
+    if layout != 0 and T <= 4096:
+        # compact window (layouts 1 and 2): every message of a sample carries
+        # its source's token row byte for byte and the reference meta
+        from tests import gpu_util as U
+        dmsg = 2 * H + 16
+        e_local = E // world
+        win = comm.window_ptr(moe.win_dispatch, rank)
+        rng = np.random.default_rng(rank)
+        ok = True
+        for src in range(world):
+            total = int(cnt[rank * e_local:(rank + 1) * e_local, src].sum())
+            xs = O.tokens(seed, src, T, H, mode=mode)
+            for q in rng.choice(total, size=min(48, total), replace=False) if total else []:
+                off = (src * T * K + int(q)) * dmsg
+                msg = U.d2h(win + off, dmsg) if isinstance(win, int) else None
+                meta = msg[2 * H:].view("<u4")
+                ok &= bool(meta[0] == src and meta[3] == meta[2] + 1)
+                ok &= bool((msg[:2 * H].view("<u2") == xs[int(meta[1])]).all())
+        res["compact_sample_exact"] = ok
     if layout == 0 and T <= 256:
         from tests import gpu_util as U
         d, comb, _ = O.moe_rank_state(seed, world, E, K, T, H, rank, mode=mode)

@@ -30,7 +30,7 @@ def _torchrun(n, env):
     return results
 
 
-@pytest.mark.parametrize("layout,tokens,mode", [(0, 128, 0), (1, 256, 0), (1, 4096, 1)])
+@pytest.mark.parametrize("layout,tokens,mode", [(0, 128, 0), (1, 256, 0), (1, 4096, 1), (2, 1024, 0), (2, 4096, 1)])
 def test_multiprocess_moe_parity(layout, tokens, mode):
     n = gpu_count()
     if n < 2:
@@ -41,6 +41,8 @@ def test_multiprocess_moe_parity(layout, tokens, mode):
         assert r["combine_exact"] and r["cells_exact"], r
         if "dispatch_window_exact" in r:
             assert r["dispatch_window_exact"] and r["combine_window_exact"], r
+        if "compact_sample_exact" in r:
+            assert r["compact_sample_exact"], r
 
 
 @pytest.mark.parametrize("layout,tokens", [(0, 128), (1, 1024)])
