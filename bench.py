@@ -336,14 +336,15 @@ def measure_barrier(G, comm, rank, world, dist, torch, dev, iters=2000):
     return out
 
 
-def measure_dedup(G, comm, rank, world, dist, torch, dev, stream, T, steps=10):
-    """Labelled variant: layout 2 = the same compact receive
-    layout with a per-rank dedup transport -- one NVLink row per (token,
-    destination rank), fanned out into the expert slots by the destination.
-    Windows and cells end identical to the default path (tests); only the
-    wire traffic changes.  Per-phase device time, max over ranks."""
+def measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, layout, mode, label, steps=10):
+    """Labelled variants beside the headline (same windows/cells contract,
+    tests/test_gpu_moe.py): layout 2 = the compact receive layout with a
+    per-rank dedup transport (one NVLink row per (token,
+    destination rank), fanned out into the expert slots by the destination);
+    mode 2 = fp8 dispatch (e4m3 codes + per-128 fp32 scales, SURVEY §8f f3,
+    the paper's LL format).  Per-phase device time, max over ranks."""
     H, K, E = HIDDEN, TOPK, EXPERTS
-    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 1, 2, 0, 0))
+    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, mode, layout, 0, 0))
     x = torch.empty(T * H, dtype=torch.int16, device=dev)
     idx = torch.empty(T * K, dtype=torch.int32, device=dev)
     w = torch.empty(T * K, dtype=torch.float32, device=dev)
@@ -364,22 +365,21 @@ def measure_dedup(G, comm, rank, world, dist, torch, dev, stream, T, steps=10):
         ev[i][2].record(stream)
     torch.cuda.synchronize()
     comm.check_device()
-    d = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
-    c = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    d = sorted(e[0].elapsed_time(e[1]) for e in ev)[steps // 2]
+    c = sorted(e[1].elapsed_time(e[2]) for e in ev)[steps // 2]
     t = torch.tensor([d, c], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    import numpy as np
     ih = idx.cpu().numpy().reshape(T, K) // (E // world)
     rows_remote = sum(len(set(int(v) for v in row) - {rank}) for row in ih)
     msgs_remote = int((ih != rank).sum())
+    dmsg = (H + H // 32 if mode == 2 else 2 * H) + 16
+    wire = rows_remote * (2 * H + 128) if layout == 2 else msgs_remote * dmsg
     disp_us = t[0].item() * 1e3
     moe.destroy()
-    return {"workload": f"labelled variant: dedup transport (layout 2), {T} tokens/rank, hidden {H}, top-{K} of {E}, "
-                        f"bf16, {world} GPU(s)",
-            "dispatch_us": disp_us, "combine_us": t[1].item() * 1e3,
-            "remote_rows_per_rank": rows_remote, "remote_messages_per_rank": msgs_remote,
-            "wire_GBps_per_gpu": rows_remote * (2 * H + 128) / (disp_us * 1e-6) / 1e9}
+    return {"workload": f"labelled variant: {label}, {T} tokens/rank, hidden {H}, top-{K} of {E}, {world} GPU(s)",
+            "dispatch_us_p50": disp_us, "combine_us_p50": t[1].item() * 1e3,
+            "remote_wire_bytes_per_rank": wire, "wire_GBps_per_gpu": wire / (disp_us * 1e-6) / 1e9}
 
 
 def ctypes_stream(stream):
@@ -482,7 +482,15 @@ def main():
     pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm, rank, world, dist, torch, dev)
     a2a = None if (args.no_extras or world < 2) else measure_a2a(G, comm, rank, world, dist, torch, dev, stream)
     barrier = None if (args.no_extras or world < 2) else measure_barrier(G, comm, rank, world, dist, torch, dev)
-    dedup = None if (args.no_extras or world < 2) else measure_dedup(G, comm, rank, world, dist, torch, dev, stream, T)
+    variants = None
+    if not args.no_extras:
+        variants = {"fp8_ht": measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 1, 2,
+                                              "fp8 dispatch (e4m3 + per-128 scales), compact layout"),
+                    "fp8_ll": measure_variant(G, comm, rank, world, dist, torch, dev, stream, 128, 0, 2,
+                                              "fp8 dispatch, LL shape", steps=30)}
+        if world > 1:
+            variants["dedup_ht"] = measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 2, 1,
+                                                   "dedup transport (layout 2), bf16")
     proxy = None
     if not args.no_extras:
         ag = allgather if world > 1 else None
@@ -598,7 +606,7 @@ def main():
         "pingpong": pp,
         "alltoall": a2a,
         "barrier": barrier,
-        "dedup_variant": dedup,
+        "variants": variants,
         "proxy_vs_direct": proxy,
     }
     if world > 1:

@@ -8,7 +8,7 @@ set -euo pipefail
 HERE="$(cd "$(dirname "$0")" && pwd)"
 REF="${GINSIM_REFERENCE:-/root/reference}/proj/core"
 mkdir -p "$HERE/_build"
-gcc -O2 -std=c11 -fPIC -ffp-contract=off -shared -o "$HERE/_build/libginsim_oracle.so" "$HERE/ginsim_oracle.c"
+gcc -O2 -std=c11 -fPIC -ffp-contract=off -shared -o "$HERE/_build/libginsim_oracle.so" "$HERE/ginsim_oracle.c" -lm
 if [ ! -d "$REF/src" ]; then
   echo "reference sources absent at $REF; oracle/_ref not rebuilt" >&2
   exit 0

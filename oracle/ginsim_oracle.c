@@ -12,6 +12,7 @@
  *
  * Citations are /root/reference-relative.
  */
+#include <math.h>
 #include <stddef.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -433,5 +434,143 @@ int gso_moe_bf16_rank_state(uint64_t seed, uint32_t n, uint32_t experts, uint32_
     }
   free(route);
   free(sent);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* fp8 mode (mode 2; a labelled variant outside the reference, SURVEY.md §8f
+ * f3, the paper's LL dispatch format PAPER.md:878-896): each 128-element
+ * block of a bf16 token row is sent as e4m3 codes plus one fp32 scale.
+ *   amax  = max |x_i| over the block (exact)
+ *   scale = amax / 448,  inv = 448 / amax   (fp32, single rounded; 1 if amax = 0)
+ *   q_i   = e4m3(x_i * inv)  round-to-nearest-even, saturating at +-448
+ *   deq_i = float(q_i) * scale
+ * The expert transform then runs on deq (y = bf16(deq * s_e + c_e)); the
+ * combine is the bf16 one.  Message = [q: H bytes][scales: H/128 x f32][meta]. */
+static float e4m3_value(uint8_t c) {  /* positive codes 0x00..0x7E */
+  const uint32_t e = (c >> 3) & 0xF, m = c & 7;
+  if (e == 0) return (float)m / 512.0f;                 /* subnormal: m * 2^-9 */
+  return ldexpf(1.0f + (float)m / 8.0f, (int)e - 7);
+}
+uint8_t gso_fp8_e4m3(float v) {
+  const uint8_t sign = (v < 0.0f || (v == 0.0f && signbit(v))) ? 0x80 : 0x00;
+  float a = fabsf(v);
+  if (a >= 448.0f) return (uint8_t)(sign | 0x7E);       /* satfinite */
+  uint8_t lo = 0, hi = 0x7E;                             /* largest code with value <= a */
+  while (lo < hi) {
+    const uint8_t mid = (uint8_t)((lo + hi + 1) / 2);
+    if (e4m3_value(mid) <= a) lo = mid; else hi = (uint8_t)(mid - 1);
+  }
+  uint8_t c = lo;
+  if (e4m3_value(c) != a) {
+    const float below = e4m3_value(c), above = e4m3_value((uint8_t)(c + 1));
+    const double db = (double)a - below, da = (double)above - a;
+    if (da < db || (da == db && ((c + 1) & 1) == 0)) c = (uint8_t)(c + 1);
+  }
+  return (uint8_t)(sign | c);
+}
+float gso_fp8_to_float(uint8_t c) {
+  const float v = e4m3_value((uint8_t)(c & 0x7F));
+  return (c & 0x80) ? -v : v;
+}
+/* one token row: q [H], scales [H/128] */
+void gso_fp8_quant_row(uint64_t seed, uint32_t src, uint32_t token, uint32_t hidden, uint8_t* q, float* scales) {
+  for (uint32_t b = 0; b < hidden / 128; ++b) {
+    float amax = 0.0f;
+    for (uint32_t i = 0; i < 128; ++i) {
+      const float x = fabsf(bf2f(gso_bf16_token(seed, src, token, b * 128 + i)));
+      if (x > amax) amax = x;
+    }
+    volatile float scale = amax > 0.0f ? amax / 448.0f : 1.0f;
+    volatile float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
+    scales[b] = scale;
+    for (uint32_t i = 0; i < 128; ++i) {
+      volatile float p = bf2f(gso_bf16_token(seed, src, token, b * 128 + i)) * inv;
+      q[b * 128 + i] = gso_fp8_e4m3(p);
+    }
+  }
+}
+/* expert transform of the dequantized value */
+uint16_t gso_fp8_transform(uint8_t q, float scale, uint32_t expert) {
+  volatile float s = 1.0f + (float)(expert % 7u) / 8.0f;
+  volatile float c = ((float)(expert % 9u) - 4.0f) / 16.0f;
+  volatile float deq = gso_fp8_to_float(q) * scale;
+  volatile float p = deq * s;
+  volatile float r = p + c;
+  return f2bf(r);
+}
+/* out[t][i] = bf16(sum_k w_k * y_k[i]) over the dequantized transform, fp32 in k order */
+void gso_fp8_combine_all(uint64_t seed, uint32_t experts, uint32_t top_k, uint32_t hidden, uint32_t src, uint32_t T,
+                         uint16_t* out) {
+  uint32_t ex[256];
+  uint8_t* q = (uint8_t*)malloc(hidden);
+  float* sc = (float*)malloc(sizeof(float) * (hidden / 128));
+  for (uint32_t t = 0; t < T; ++t) {
+    gso_route_token(seed, experts, top_k, src, t, ex);
+    gso_fp8_quant_row(seed, src, t, hidden, q, sc);
+    for (uint32_t i = 0; i < hidden; ++i) {
+      volatile float acc = 0.0f;
+      for (uint32_t k = 0; k < top_k; ++k) {
+        const float w = gso_bf16_weight(src, t, k);
+        const float y = bf2f(gso_fp8_transform(q[i], sc[i / 128], ex[k]));
+        volatile float prod = w * y;
+        acc = acc + prod;
+      }
+      out[(size_t)t * hidden + i] = f2bf(acc);
+    }
+  }
+  free(q);
+  free(sc);
+}
+/* fp8-mode final state, reference layout: dmsg = H + H/32 + 16, cmsg = 2H */
+int gso_moe_fp8_rank_state(uint64_t seed, uint32_t n, uint32_t experts, uint32_t top_k, uint32_t T,
+                           uint32_t hidden, uint32_t r, uint8_t* dispatch_recv, uint8_t* combine_recv) {
+  if (n == 0 || experts % n || top_k > 256 || top_k > experts || hidden % 128) return -1;
+  const uint32_t e_local = experts / n;
+  const uint64_t pay = (uint64_t)hidden + hidden / 32, dmsg = pay + 16, cmsg = 2ull * hidden;
+  uint32_t* route = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)T * top_k);
+  uint32_t* sent = (uint32_t*)calloc(experts, sizeof(uint32_t));
+  uint8_t* q = (uint8_t*)malloc(hidden);
+  float* sc = (float*)malloc(sizeof(float) * (hidden / 128));
+  for (uint32_t src = 0; src < n; ++src) {
+    memset(sent, 0, sizeof(uint32_t) * experts);
+    gso_route_table(seed, experts, top_k, src, T, route);
+    for (uint32_t t = 0; t < T; ++t) {
+      int quantized = 0;
+      for (uint32_t k = 0; k < top_k; ++k) {
+        const uint32_t e = route[(size_t)t * top_k + k];
+        const uint32_t slot = sent[e]++;
+        if (e / e_local != r) continue;
+        if (!quantized) {
+          gso_fp8_quant_row(seed, src, t, hidden, q, sc);
+          quantized = 1;
+        }
+        uint8_t* msg = dispatch_recv + (((uint64_t)(e % e_local) * n + src) * T + slot) * dmsg;
+        memcpy(msg, q, hidden);
+        for (uint32_t b = 0; b < hidden / 128; ++b) {
+          uint32_t u;
+          memcpy(&u, &sc[b], 4);
+          st32(msg + hidden + 4ull * b, u);
+        }
+        st32(msg + pay + 0, src);
+        st32(msg + pay + 4, t);
+        st32(msg + pay + 8, k);
+        st32(msg + pay + 12, k + 1);
+      }
+    }
+  }
+  gso_route_table(seed, experts, top_k, r, T, route);
+  for (uint32_t t = 0; t < T; ++t) {
+    gso_fp8_quant_row(seed, r, t, hidden, q, sc);
+    for (uint32_t k = 0; k < top_k; ++k) {
+      const uint32_t e = route[(size_t)t * top_k + k];
+      uint8_t* out = combine_recv + ((uint64_t)t * top_k + k) * cmsg;
+      for (uint32_t i = 0; i < hidden; ++i) st16(out + 2ull * i, gso_fp8_transform(q[i], sc[i / 128], e));
+    }
+  }
+  free(route);
+  free(sent);
+  free(q);
+  free(sc);
   return 0;
 }

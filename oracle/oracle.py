@@ -56,6 +56,17 @@ def lib():
         L.gso_moe_ht_plane.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, POINTER(c_uint8)]
         L.gso_bf16_round.argtypes = [ctypes.c_float]
         L.gso_bf16_round.restype = c_uint16
+        L.gso_fp8_e4m3.argtypes = [ctypes.c_float]
+        L.gso_fp8_e4m3.restype = c_uint8
+        L.gso_fp8_to_float.argtypes = [c_uint8]
+        L.gso_fp8_to_float.restype = ctypes.c_float
+        L.gso_fp8_quant_row.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, POINTER(c_uint8),
+                                        POINTER(ctypes.c_float)]
+        L.gso_fp8_combine_all.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32,
+                                          POINTER(c_uint16)]
+        L.gso_moe_fp8_rank_state.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32,
+                                             POINTER(c_uint8), POINTER(c_uint8)]
+        L.gso_moe_fp8_rank_state.restype = c_int
         _L = L
     return _L
 
@@ -83,10 +94,26 @@ def weights(src, T, K, mode=0):
     return out
 
 
+def dispatch_message_bytes(hidden, mode=0):
+    """u16/bf16: 2H payload + 16-byte meta (harness.hpp:112); fp8 (mode 2):
+    H e4m3 bytes + H/128 fp32 scales + meta."""
+    return (hidden + hidden // 32 if mode == 2 else 2 * hidden) + 16
+
+
+def fp8_quant_row(seed, src, token, hidden):
+    q = np.zeros(hidden, np.uint8)
+    sc = np.zeros(hidden // 128, np.float32)
+    lib().gso_fp8_quant_row(seed, src, token, hidden, _p(q, c_uint8), _p(sc, ctypes.c_float))
+    return q, sc
+
+
 def combine(seed, experts, top_k, hidden, src, T, mode=0):
     """Expected combine output [T][H] (u16 exact or bf16 bits) and, for bf16,
-    the fp64 reference sum."""
+    the fp64 reference sum (fp8 mode: bf16 bits of the dequantized path)."""
     out = np.zeros((T, hidden), np.uint16)
+    if mode == 2:
+        lib().gso_fp8_combine_all(seed, experts, top_k, hidden, src, T, _p(out, c_uint16))
+        return out, None
     if mode == 0:
         lib().gso_oracle_combine_all(seed, experts, top_k, hidden, src, T, _p(out, c_uint16))
         return out, None
@@ -99,11 +126,17 @@ def moe_rank_state(seed, n, experts, top_k, T, hidden, r, mode=0, n_cells=256):
     """(dispatch_recv bytes, combine_recv bytes, signal cells) of rank r after
     one moe-ll round, reference (worst-case) layout."""
     e_local = experts // n
-    dmsg, cmsg = 2 * hidden + 16, 2 * hidden
+    dmsg, cmsg = dispatch_message_bytes(hidden, mode), 2 * hidden
     d = np.zeros(e_local * n * T * dmsg, np.uint8)
     c = np.zeros(T * top_k * cmsg, np.uint8)
     cells = np.zeros(n_cells, np.uint64)
-    if mode == 0:
+    if mode == 2:
+        rc = lib().gso_moe_fp8_rank_state(seed, n, experts, top_k, T, hidden, r, _p(d, c_uint8), _p(c, c_uint8))
+        cnt = counts(seed, n, experts, top_k, T)
+        for e_loc in range(e_local):
+            cells[e_loc] = (n << 32) + int(cnt[r * e_local + e_loc].sum())
+        cells[e_local] = T * top_k
+    elif mode == 0:
         rc = lib().gso_moe_ll_rank_state(seed, n, experts, top_k, T, hidden, r, _p(d, c_uint8), _p(c, c_uint8),
                                          _p(cells, c_uint64), n_cells)
     else:

@@ -25,6 +25,7 @@
 // fence.acq_rel.sys on both sides), so one red.release.sys per expert covers
 // every warp's stores.
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -73,6 +74,8 @@ struct MoeLaunch {
   uint32_t win_rows;             // layout 2: per-source row staging + 128-byte row headers
   uint32_t coop;                 // TMA dispatch: cooperative route tables + all-token work (large T*K)
   uint32_t fuse_reduce;          // TMA combine: reduce inside the send kernel (small, latency-bound T)
+  uint64_t dmsg;                 // dispatch message bytes: payload + 16-byte meta
+  uint32_t mpay;                 // payload bytes before the meta (2H; fp8: H + H/32)
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
 };
@@ -103,6 +106,46 @@ __device__ __forceinline__ uint32_t bf16x2_pack_transform(uint32_t two, float s,
 __device__ __forceinline__ uint4 bf16x8_transform(uint4 v, float s, float c) {
   return make_uint4(bf16x2_pack_transform(v.x, s, c), bf16x2_pack_transform(v.y, s, c),
                     bf16x2_pack_transform(v.z, s, c), bf16x2_pack_transform(v.w, s, c));
+}
+
+// fp8 mode (mode 2): one 128-element block of a bf16 row per
+// warp step, 4 elements per lane: amax by warp reduction (exact), scale =
+// amax/448 and inv = 448/amax single-rounded, q = e4m3(x*inv) with RNE and
+// saturation (cvt.rn.satfinite.e4m3x2.f32) -- the oracle's gso_fp8_quant_row.
+__device__ __forceinline__ void fp8_quant_block(const uint16_t* in, uint8_t* q, float* scale_out, uint32_t lane) {
+  const uint2 raw = *reinterpret_cast<const uint2*>(in + 4 * lane);
+  float f[4] = {__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u), __uint_as_float(raw.y << 16),
+                __uint_as_float(raw.y & 0xFFFF0000u)};
+  float amax = fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float scale = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  const float inv = amax > 0.0f ? __fdiv_rn(448.0f, amax) : 1.0f;
+  const __nv_fp8x2_storage_t lo =
+      __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(f[0], inv), __fmul_rn(f[1], inv)), __NV_SATFINITE, __NV_E4M3);
+  const __nv_fp8x2_storage_t hi =
+      __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(f[2], inv), __fmul_rn(f[3], inv)), __NV_SATFINITE, __NV_E4M3);
+  *reinterpret_cast<uint32_t*>(q + 4 * lane) = (uint32_t)lo | ((uint32_t)hi << 16);
+  if (lane == 0) *scale_out = scale;
+}
+__device__ __forceinline__ float fp8_to_float(uint32_t code) {
+  const __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)code, __NV_E4M3);
+  return __half2float(__half(h));
+}
+// 8 e4m3 codes (one 16-byte bf16 output vector): deq = fp32(q)*scale, then the
+// bf16 expert transform y = bf16(deq*s + c), single-rounded ops
+__device__ __forceinline__ uint4 fp8x8_transform(uint2 codes, float scale, float s, float c) {
+  uint32_t out[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const uint32_t w = h < 2 ? codes.x : codes.y;
+    const uint32_t sh = (h & 1) * 16;
+    const float a = __fmul_rn(fp8_to_float((w >> sh) & 0xFF), scale);
+    const float b = __fmul_rn(fp8_to_float((w >> (sh + 8)) & 0xFF), scale);
+    const __nv_bfloat162 r = __floats2bfloat162_rn(__fadd_rn(__fmul_rn(a, s), c), __fadd_rn(__fmul_rn(b, s), c));
+    out[h] = *reinterpret_cast<const uint32_t*>(&r);
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
 __device__ __forceinline__ uint4 transform_vec(uint4 v, uint32_t mode, uint32_t e) {
@@ -855,7 +898,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   const uint32_t n = v->world, rank = v->rank;
   const uint32_t E = L.E, K = L.K, T = L.T, H = L.H, e_local = L.e_local;
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t dmsg = 2ull * H + 16;
+  const uint64_t dmsg = L.dmsg;
+  const bool fp8 = L.mode == 2;
   const uint32_t payload = 2u * H, parts = L.parts;
   const uint32_t Kp = (K + 1) & ~1u;  // dst_g row stride: 16-byte rows for the bulk load
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
@@ -873,7 +917,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
   // per stage: [dst pointers: Kp * 8 bytes, padded to 128][row chunk]
   const uint32_t dhead = (Kp * 8 + 127) & ~127u;
-  const uint32_t sstride = dhead + chunk;
+  // fp8: [dst row][bf16 chunk][e4m3 chunk/2][scales chunk/64, padded]
+  const uint32_t qoff = dhead + chunk, soff = qoff + chunk / 2;
+  const uint32_t sstride = fp8 ? ((soff + chunk / 64 + 15) & ~15u) : dhead + chunk;
   char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kDispStages * sstride;
   uint32_t* own = reinterpret_cast<uint32_t*>(dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) +
                                               (size_t)kTmaWarps * kDispStages * sstride);  // [(t1-t0)*K]
@@ -1055,10 +1101,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     char* sb = stage + (size_t)s * sstride;
     char* const* dp = reinterpret_cast<char* const*>(sb);
     gin::tma::mbar_wait(&ctl->bar[s], (j / kDispStages) & 1);
-    if (p == 0 && lane < K) gin::st_v4(dp[lane] + payload, make_uint4(rank, t, lane, lane + 1));  // meta
+    if (p == 0 && lane < K) gin::st_v4(dp[lane] + L.mpay, make_uint4(rank, t, lane, lane + 1));  // meta
+    if (fp8) {  // quantize the chunk in shared memory, 128 elements per warp step
+      const uint32_t len = tma_chunk_len(payload, chunk, p);
+      for (uint32_t blk = 0; blk < len / 256; ++blk)
+        fp8_quant_block(reinterpret_cast<const uint16_t*>(sb + dhead + blk * 256), reinterpret_cast<uint8_t*>(sb + qoff + blk * 128),
+                        reinterpret_cast<float*>(sb + soff) + blk, lane);
+      gin::tma::fence_proxy_async_shared();
+      __syncwarp();
+    }
     if (lane == 0) {
       const uint32_t len = tma_chunk_len(payload, chunk, p);
-      for (uint32_t k = 0; k < K; ++k) gin::tma::store(dp[k] + (uint64_t)p * chunk, sb + dhead, len);
+      if (fp8) {  // e4m3 codes at [p*chunk/2], scales at [H + p*chunk/64]
+        for (uint32_t k = 0; k < K; ++k) {
+          gin::tma::store(dp[k] + (uint64_t)p * (chunk / 2), sb + qoff, len / 2);
+          gin::tma::store(dp[k] + H + (uint64_t)p * (chunk / 64), sb + soff, len / 64);
+        }
+      } else {
+        for (uint32_t k = 0; k < K; ++k) gin::tma::store(dp[k] + (uint64_t)p * chunk, sb + dhead, len);
+      }
       gin::tma::commit();
       // Refill the stage of the PREVIOUS item: its stores were committed one
       // iteration ago, so their shared-memory reads overlapped this wait.
@@ -1486,7 +1547,8 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
   const uint32_t K = L.K, T = L.T, H = L.H, e_local = L.e_local;
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t dmsg = 2ull * H + 16, cmsg = 2ull * H;
+  const uint64_t dmsg = L.dmsg, cmsg = 2ull * H;
+  const bool fp8 = L.mode == 2;
   const uint32_t payload = 2u * H, parts = L.cparts;
   MOE_STAMP(R, 1, 0);
 
@@ -1496,8 +1558,10 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   __shared__ int is_last;
   extern __shared__ __align__(128) char dsm[];
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
-  // per stage: [128-byte header: the message's 16-byte meta][chunk]
-  const uint32_t sstride = 128 + chunk;
+  // per stage: [128-byte header: the message's 16-byte meta][chunk]; fp8:
+  // [header][e4m3 chunk/2][scales chunk/64][bf16 output chunk]
+  const uint32_t q_off = 128, s_off = 128 + chunk / 2, o_off = fp8 ? s_off + chunk / 64 : 128;
+  const uint32_t sstride = fp8 ? o_off + chunk : 128 + chunk;
   char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kTmaStages * sstride;
 
   const uint32_t P = e_local * n;
@@ -1576,9 +1640,16 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     const uint32_t len = tma_chunk_len(payload, chunk, p);
     char* sb = stage + (size_t)s * sstride;
     ctl->dptr[s] = reinterpret_cast<char*>((uint64_t)pr);  // pair index of the stage's message
-    gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len + 16);
-    gin::tma::load(sb, msg + payload, 16, &ctl->bar[s]);
-    gin::tma::load(sb + 128, msg + (uint64_t)p * chunk, len, &ctl->bar[s]);
+    if (fp8) {  // the chunk's e4m3 codes and their block scales
+      gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len / 2 + len / 64 + 16);
+      gin::tma::load(sb, msg + L.mpay, 16, &ctl->bar[s]);
+      gin::tma::load(sb + q_off, msg + (uint64_t)p * (chunk / 2), len / 2, &ctl->bar[s]);
+      gin::tma::load(sb + s_off, msg + H + (uint64_t)p * (chunk / 64), len / 64, &ctl->bar[s]);
+    } else {
+      gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len + 16);
+      gin::tma::load(sb, msg + L.mpay, 16, &ctl->bar[s]);
+      gin::tma::load(sb + 128, msg + (uint64_t)p * chunk, len, &ctl->bar[s]);
+    }
   };
   // Work source.  Static: warp gw takes items gw, gw+stride, ...  Dynamic
   // (L.dyn): warps grab batches of one message's parts from a device counter,
@@ -1618,11 +1689,16 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     const uint32_t len = tma_chunk_len(payload, chunk, p);
     char* sb = stage + (size_t)s * sstride;
     gin::tma::mbar_wait(&ctl->bar[s], (uint32_t)((j / kTmaStages) & 1));
-    uint4* buf = reinterpret_cast<uint4*>(sb + 128);
+    uint4* buf = reinterpret_cast<uint4*>(sb + o_off);
     {
       const uint32_t nv = len / 16;
       uint32_t i = lane;
-      if (L.mode == 0) {
+      if (fp8) {  // expand: 8 codes -> one 16-byte bf16 vector; scale per 128 elements
+        const float sc = 1.0f + (float)(e % 7u) / 8.0f, cc = ((float)(e % 9u) - 4.0f) / 16.0f;
+        const uint2* qin = reinterpret_cast<const uint2*>(sb + q_off);
+        const float* scl = reinterpret_cast<const float*>(sb + s_off);
+        for (; i < nv; i += 32) buf[i] = fp8x8_transform(qin[i], scl[i / 16], sc, cc);
+      } else if (L.mode == 0) {
         const uint32_t add = (e * 17u + 1u) & 0xFFFFu;
         for (; i < nv; i += 32) {
           uint4 a = buf[i];
@@ -1847,7 +1923,12 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   if (cfg->tokens == 0 || cfg->top_k == 0 || cfg->top_k > cfg->experts || cfg->top_k > 32)
     fail(GINSIM_E_USAGE, "need 1..min(experts,32) routed experts per token and at least one token");
   if (cfg->hidden == 0) fail(GINSIM_E_USAGE, "hidden must be positive");
-  if (cfg->mode > 1 || cfg->layout > 2) fail(GINSIM_E_USAGE, "mode must be 0 or 1, layout 0, 1 or 2");
+  if (cfg->mode > 2 || cfg->layout > 2) fail(GINSIM_E_USAGE, "mode must be 0, 1 or 2, layout 0, 1 or 2");
+  if (cfg->mode == 2) {
+    if (cfg->hidden % 512) fail(GINSIM_E_USAGE, "fp8 mode needs hidden % 512 == 0 (128-element scale blocks)");
+    if (cfg->layout == 2 || c->cfg.backend != GIN_BACKEND_DIRECT || cfg->engine == 1)
+      fail(GINSIM_E_USAGE, "fp8 mode runs on the direct TMA path with layout 0 or 1");
+  }
   if (cfg->layout == 2) {
     if (c->cfg.backend != GIN_BACKEND_DIRECT) fail(GINSIM_E_USAGE, "layout 2 (dedup transport) needs the direct backend");
     if (cfg->top_k > 15) fail(GINSIM_E_USAGE, "layout 2 carries at most 15 messages per row header");
@@ -1863,7 +1944,8 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   m->cfg = *cfg;
   m->e_local = e_local;
   m->parts = cfg->hidden >= 1024 ? 4 : 1;
-  const uint64_t dmsg = 2ull * cfg->hidden + 16, cmsg = 2ull * cfg->hidden;
+  const uint64_t dmsg = (cfg->mode == 2 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden) + 16;
+  const uint64_t cmsg = 2ull * cfg->hidden;
   const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
   const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
   if (cfg->layout == 2 && e_local + 2 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
@@ -1999,6 +2081,8 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
   L.coop = moes[0]->coop ? 1u : 0u;
   L.fuse_reduce = moes[0]->coop ? 0u : 1u;
+  L.mpay = cfg.mode == 2 ? cfg.hidden + cfg.hidden / 32 : 2u * cfg.hidden;
+  L.dmsg = (uint64_t)L.mpay + 16;
   for (uint32_t i = 0; i < n; ++i) {
     if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
@@ -2071,6 +2155,10 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
   // control blocks | stages of [destination row (padded to 128 B) | chunk] | own route indices
   const size_t kp = (m->cfg.top_k + 1) & ~1u;
   const size_t dhead = (kp * 8 + 127) & ~(size_t)127;
+  if (m->cfg.mode == 2) {  // + e4m3 chunk + scales per stage
+    const size_t sst = (dhead + m->chunk + m->chunk / 2 + m->chunk / 64 + 15) & ~(size_t)15;
+    return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kDispStages * sst + pairs * 4;
+  }
   const size_t tokens = (size_t)((m->cfg.tokens + G - 1) / G + 1);
   const size_t rowj = m->cfg.layout == 2 ? tokens * m->comm->world * 4 : 0;  // dedup: (t, dst) row indices
   return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kDispStages * (dhead + m->chunk) +
@@ -2078,7 +2166,9 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
 }
 static size_t combine_smem(const ginsim_cuda_moe_t m) {
   if (!kernels_of(m).tma_combine) return 0;
-  return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * (128 + m->cchunk);
+  // fp8: [hdr][e4m3 in][scales][bf16 out] per stage
+  const size_t sst = m->cfg.mode == 2 ? 128 + m->cchunk / 2 + m->cchunk / 64 + m->cchunk : 128 + m->cchunk;
+  return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * sst;
 }
 static int combine_threads(const MoeKernels& k) { return k.tma_combine ? kCmbThreads : kMoeThreads; }
 
@@ -2101,9 +2191,17 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
       parts = std::max(parts, std::min(want, std::max(1u, payload / 1024u)));
     }
     chunk = ((payload + parts - 1) / parts + 15) / 16 * 16;
-    m->chunk = chunk;
     cparts = (payload + 4095) / 4096;
     cchunk = ((payload + cparts - 1) / cparts + 15) / 16 * 16;
+    if (m->cfg.mode == 2) {
+      // fp8: chunks of whole 512-element groups, so every chunk's scale slice
+      // (chunk/64 bytes) is a 16-byte multiple at a 16-byte aligned offset
+      chunk = (chunk + 1023) / 1024 * 1024;
+      parts = (payload + chunk - 1) / chunk;
+      cchunk = 2048;  // combine stages also hold the expanded bf16 output
+      cparts = (payload + cchunk - 1) / cchunk;
+    }
+    m->chunk = chunk;
     m->cchunk = cchunk;
   }
   int sms = 0;

@@ -114,3 +114,42 @@ def test_ring_golden_states_match_oracle(golden_dir):
             # signal 0 reset every round; barrier cells count rounds
             for cell, val in c["state"][r]["signals_nonzero"]:
                 assert cell >= 256 - 64 and val == rounds
+
+
+def test_fp8_e4m3_codec_exhaustive():
+    """e4m3 (fp8 mode): every finite code round-trips; ties round to even;
+    finite overflow saturates at +-448 (cvt.rn.satfinite semantics)."""
+    L = O.lib()
+    for c in range(0x7F):
+        v = L.gso_fp8_to_float(c)
+        assert L.gso_fp8_e4m3(v) == c
+        assert L.gso_fp8_e4m3(-v) == (c | 0x80) or v == 0.0
+    for c in range(0x7E):  # midpoints between consecutive codes -> the even code
+        a, b = L.gso_fp8_to_float(c), L.gso_fp8_to_float(c + 1)
+        mid = np.float32((np.float64(a) + np.float64(b)) / 2)
+        if float(mid) == (a + b) / 2:
+            assert L.gso_fp8_e4m3(float(mid)) == (c if c % 2 == 0 else c + 1)
+    assert L.gso_fp8_e4m3(448.0) == 0x7E and L.gso_fp8_e4m3(1e6) == 0x7E and L.gso_fp8_e4m3(-1e6) == 0xFE
+
+
+def test_fp8_combine_within_stated_tolerance_of_bf16():
+    """fp8 mode moves e4m3 codes + per-128 scales instead of bf16 rows; its
+    combine output stays within the stated bound of the bf16 path:
+    |out_fp8 - out_bf16| <= 2^-4 * sum_k w_k*s_k*|x| + 2^-7 * (|out_bf16| + sum_k w_k*|y_k|)
+    (e4m3 carries 3 mantissa bits: relative error <= 2^-4 in the normal range,
+    which every scaled element reaches; the second term covers bf16 rounding)."""
+    seed, E, K, H, src, T = 3, 64, 8, 512, 1, 24
+    f8, _ = O.combine(seed, E, K, H, src, T, mode=2)
+    b16, _ = O.combine(seed, E, K, H, src, T, mode=1)
+    bf = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    x = bf(O.tokens(seed, src, T, H, mode=1))
+    route = O.route_table(seed, E, K, src, T)
+    w = O.weights(src, T, K, mode=1).astype(np.float64)
+    s = 1.0 + (route % 7) / 8.0
+    c = ((route % 9) - 4.0) / 16.0
+    wsx = np.einsum("tk,tk,th->th", w, s, np.abs(x))
+    wy = np.einsum("tk,tkh->th", w, np.abs(s[:, :, None] * x[:, None, :] + c[:, :, None]))
+    bound = 2.0 ** -4 * wsx + 2.0 ** -7 * (np.abs(bf(b16)) + wy)
+    err = np.abs(bf(f8) - bf(b16))
+    assert (err <= bound).all(), float((err / bound).max())
+    assert (f8 != b16).any()  # quantization actually happened
