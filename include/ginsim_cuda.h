@@ -281,9 +281,13 @@ typedef struct ginsim_cuda_moe_config {
   uint32_t top_k;    /* K */
   uint32_t tokens;   /* T per rank */
   uint32_t hidden;   /* elements per token (2-byte elements) */
-  uint32_t mode;     /* 0 = u16 exact (reference arithmetic), 1 = bf16 */
+  uint32_t mode;     /* 0 = u16 exact (reference arithmetic), 1 = bf16,
+                        2 = fp8 dispatch: e4m3 codes + per-128 fp32 scales (hidden % 512 == 0,
+                            direct TMA path), bf16 combine */
   uint32_t layout;   /* 0 = reference layout ((e_loc*n+src)*T+slot)*dmsg,
-                        1 = compact per-source layout (src*T*K + prefix + slot)*dmsg */
+                        1 = compact per-source layout (src*T*K + prefix + slot)*dmsg,
+                        2 = layout 1 with a per-rank dedup transport (one NVLink row per
+                            (token, destination rank), fanned out at the destination) */
   uint32_t ctas;     /* CTAs per rank (0 = as many as fit) */
   uint32_t engine;   /* data mover: 0 = auto (TMA bulk copies when messages are
                         16-byte aligned), 1 = 128-bit LSU stores, 2 = TMA */

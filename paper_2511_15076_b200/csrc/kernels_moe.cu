@@ -128,20 +128,18 @@ __device__ __forceinline__ void fp8_quant_block(const uint16_t* in, uint8_t* q, 
   *reinterpret_cast<uint32_t*>(q + 4 * lane) = (uint32_t)lo | ((uint32_t)hi << 16);
   if (lane == 0) *scale_out = scale;
 }
-__device__ __forceinline__ float fp8_to_float(uint32_t code) {
-  const __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)code, __NV_E4M3);
-  return __half2float(__half(h));
-}
 // 8 e4m3 codes (one 16-byte bf16 output vector): deq = fp32(q)*scale, then the
-// bf16 expert transform y = bf16(deq*s + c), single-rounded ops
+// bf16 expert transform y = bf16(deq*s + c), single-rounded ops.  Codes are
+// widened two at a time (cvt.rn.f16x2.e4m3x2: exact, e4m3 is a subset of f16).
 __device__ __forceinline__ uint4 fp8x8_transform(uint2 codes, float scale, float s, float c) {
   uint32_t out[4];
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     const uint32_t w = h < 2 ? codes.x : codes.y;
-    const uint32_t sh = (h & 1) * 16;
-    const float a = __fmul_rn(fp8_to_float((w >> sh) & 0xFF), scale);
-    const float b = __fmul_rn(fp8_to_float((w >> (sh + 8)) & 0xFF), scale);
+    const __nv_fp8x2_storage_t pair = (__nv_fp8x2_storage_t)((w >> ((h & 1) * 16)) & 0xFFFF);
+    const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2(pair, __NV_E4M3);
+    const float2 f = __half22float2(__half2(hr));
+    const float a = __fmul_rn(f.x, scale), b = __fmul_rn(f.y, scale);
     const __nv_bfloat162 r = __floats2bfloat162_rn(__fadd_rn(__fmul_rn(a, s), c), __fadd_rn(__fmul_rn(b, s), c));
     out[h] = *reinterpret_cast<const uint32_t*>(&r);
   }
