@@ -342,7 +342,8 @@ def measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, layout, m
     per-rank dedup transport (one NVLink row per (token,
     destination rank), fanned out into the expert slots by the destination);
     mode 2 = fp8 dispatch (e4m3 codes + per-128 fp32 scales, SURVEY §8f f3,
-    the paper's LL format).  Per-phase device time, max over ranks."""
+    the paper's LL format); mode 3 = fp8 dispatch and fp8 combine messages.
+    Per-phase device time, max over ranks."""
     H, K, E = HIDDEN, TOPK, EXPERTS
     moe = G.Moe(comm, G.MoeConfig(E, K, T, H, mode, layout, 0, 0))
     x = torch.empty(T * H, dtype=torch.int16, device=dev)
@@ -373,7 +374,7 @@ def measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, layout, m
     ih = idx.cpu().numpy().reshape(T, K) // (E // world)
     rows_remote = sum(len(set(int(v) for v in row) - {rank}) for row in ih)
     msgs_remote = int((ih != rank).sum())
-    dmsg = (H + H // 32 if mode == 2 else 2 * H) + 16
+    dmsg = (H + H // 32 if mode >= 2 else 2 * H) + 16
     wire = rows_remote * (2 * H + 128) if layout == 2 else msgs_remote * dmsg
     disp_us = t[0].item() * 1e3
     moe.destroy()
@@ -487,7 +488,9 @@ def main():
         variants = {"fp8_ht": measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 1, 2,
                                               "fp8 dispatch (e4m3 + per-128 scales), compact layout"),
                     "fp8_ll": measure_variant(G, comm, rank, world, dist, torch, dev, stream, 128, 0, 2,
-                                              "fp8 dispatch, LL shape", steps=30)}
+                                              "fp8 dispatch, LL shape", steps=30),
+                    "fp8_both_ht": measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 1, 3,
+                                                   "fp8 dispatch + fp8 combine messages, compact layout")}
         if world > 1:
             variants["dedup_ht"] = measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 2, 1,
                                                    "dedup transport (layout 2), bf16")

@@ -574,3 +574,93 @@ int gso_moe_fp8_rank_state(uint64_t seed, uint32_t n, uint32_t experts, uint32_t
   free(sc);
   return 0;
 }
+
+/* fp8 combine (mode 3 = mode 2 dispatch + fp8 combine messages): each expert
+ * output row y (bf16, the mode-2 transform) is quantized like the dispatch
+ * rows -- [e4m3: H bytes][scales: H/128 f32] per (t, k) -- and the source
+ * reduces out = bf16(sum_k w_k * (fp32(q_k) * scale_k)), fp32 in k order. */
+void gso_fp8_quant_bf16(const uint16_t* row, uint32_t hidden, uint8_t* q, float* scales) {
+  for (uint32_t b = 0; b < hidden / 128; ++b) {
+    float amax = 0.0f;
+    for (uint32_t i = 0; i < 128; ++i) {
+      const float x = fabsf(bf2f(row[b * 128 + i]));
+      if (x > amax) amax = x;
+    }
+    volatile float scale = amax > 0.0f ? amax / 448.0f : 1.0f;
+    volatile float inv = amax > 0.0f ? 448.0f / amax : 1.0f;
+    scales[b] = scale;
+    for (uint32_t i = 0; i < 128; ++i) {
+      volatile float p = bf2f(row[b * 128 + i]) * inv;
+      q[b * 128 + i] = gso_fp8_e4m3(p);
+    }
+  }
+}
+/* the combine message of (src token t, expert e): y quantized */
+static void fp8c_message(uint64_t seed, uint32_t src, uint32_t t, uint32_t hidden, uint32_t e, const uint8_t* xq,
+                         const float* xs, uint16_t* y, uint8_t* q, float* sc) {
+  for (uint32_t i = 0; i < hidden; ++i) y[i] = gso_fp8_transform(xq[i], xs[i / 128], e);
+  gso_fp8_quant_bf16(y, hidden, q, sc);
+  (void)seed;
+  (void)src;
+  (void)t;
+}
+void gso_fp8c_combine_all(uint64_t seed, uint32_t experts, uint32_t top_k, uint32_t hidden, uint32_t src, uint32_t T,
+                          uint16_t* out) {
+  uint32_t ex[256];
+  uint8_t* xq = (uint8_t*)malloc(hidden);
+  float* xs = (float*)malloc(sizeof(float) * (hidden / 128));
+  uint16_t* y = (uint16_t*)malloc(2ull * hidden);
+  uint8_t* q = (uint8_t*)malloc((size_t)top_k * hidden);
+  float* sc = (float*)malloc(sizeof(float) * top_k * (hidden / 128));
+  for (uint32_t t = 0; t < T; ++t) {
+    gso_route_token(seed, experts, top_k, src, t, ex);
+    gso_fp8_quant_row(seed, src, t, hidden, xq, xs);
+    for (uint32_t k = 0; k < top_k; ++k)
+      fp8c_message(seed, src, t, hidden, ex[k], xq, xs, y, q + (size_t)k * hidden, sc + (size_t)k * (hidden / 128));
+    for (uint32_t i = 0; i < hidden; ++i) {
+      volatile float acc = 0.0f;
+      for (uint32_t k = 0; k < top_k; ++k) {
+        const float w = gso_bf16_weight(src, t, k);
+        volatile float deq = gso_fp8_to_float(q[(size_t)k * hidden + i]) * sc[(size_t)k * (hidden / 128) + i / 128];
+        volatile float prod = w * deq;
+        acc = acc + prod;
+      }
+      out[(size_t)t * hidden + i] = f2bf(acc);
+    }
+  }
+  free(xq);
+  free(xs);
+  free(y);
+  free(q);
+  free(sc);
+}
+/* mode-3 combine window of rank r: (t*K+k) * (H + H/32) */
+void gso_fp8c_combine_window(uint64_t seed, uint32_t experts, uint32_t top_k, uint32_t hidden, uint32_t r, uint32_t T,
+                             uint8_t* combine_recv) {
+  uint32_t ex[256];
+  const uint64_t cm = (uint64_t)hidden + hidden / 32;
+  uint8_t* xq = (uint8_t*)malloc(hidden);
+  float* xs = (float*)malloc(sizeof(float) * (hidden / 128));
+  uint16_t* y = (uint16_t*)malloc(2ull * hidden);
+  uint8_t* q = (uint8_t*)malloc(hidden);
+  float* sc = (float*)malloc(sizeof(float) * (hidden / 128));
+  for (uint32_t t = 0; t < T; ++t) {
+    gso_route_token(seed, experts, top_k, r, t, ex);
+    gso_fp8_quant_row(seed, r, t, hidden, xq, xs);
+    for (uint32_t k = 0; k < top_k; ++k) {
+      fp8c_message(seed, r, t, hidden, ex[k], xq, xs, y, q, sc);
+      uint8_t* m = combine_recv + ((uint64_t)t * top_k + k) * cm;
+      memcpy(m, q, hidden);
+      for (uint32_t b = 0; b < hidden / 128; ++b) {
+        uint32_t u;
+        memcpy(&u, &sc[b], 4);
+        st32(m + hidden + 4ull * b, u);
+      }
+    }
+  }
+  free(xq);
+  free(xs);
+  free(y);
+  free(q);
+  free(sc);
+}

@@ -67,6 +67,10 @@ def lib():
         L.gso_moe_fp8_rank_state.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32,
                                              POINTER(c_uint8), POINTER(c_uint8)]
         L.gso_moe_fp8_rank_state.restype = c_int
+        L.gso_fp8c_combine_all.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32,
+                                           POINTER(c_uint16)]
+        L.gso_fp8c_combine_window.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32,
+                                              POINTER(c_uint8)]
         _L = L
     return _L
 
@@ -97,7 +101,12 @@ def weights(src, T, K, mode=0):
 def dispatch_message_bytes(hidden, mode=0):
     """u16/bf16: 2H payload + 16-byte meta (harness.hpp:112); fp8 (mode 2):
     H e4m3 bytes + H/128 fp32 scales + meta."""
-    return (hidden + hidden // 32 if mode == 2 else 2 * hidden) + 16
+    return (hidden + hidden // 32 if mode in (2, 3) else 2 * hidden) + 16
+
+
+def combine_message_bytes(hidden, mode=0):
+    """bf16/u16: 2H (harness.hpp:113); fp8 combine (mode 3): H + H/32."""
+    return hidden + hidden // 32 if mode == 3 else 2 * hidden
 
 
 def fp8_quant_row(seed, src, token, hidden):
@@ -111,6 +120,9 @@ def combine(seed, experts, top_k, hidden, src, T, mode=0):
     """Expected combine output [T][H] (u16 exact or bf16 bits) and, for bf16,
     the fp64 reference sum (fp8 mode: bf16 bits of the dequantized path)."""
     out = np.zeros((T, hidden), np.uint16)
+    if mode == 3:
+        lib().gso_fp8c_combine_all(seed, experts, top_k, hidden, src, T, _p(out, c_uint16))
+        return out, None
     if mode == 2:
         lib().gso_fp8_combine_all(seed, experts, top_k, hidden, src, T, _p(out, c_uint16))
         return out, None
@@ -126,12 +138,17 @@ def moe_rank_state(seed, n, experts, top_k, T, hidden, r, mode=0, n_cells=256):
     """(dispatch_recv bytes, combine_recv bytes, signal cells) of rank r after
     one moe-ll round, reference (worst-case) layout."""
     e_local = experts // n
-    dmsg, cmsg = dispatch_message_bytes(hidden, mode), 2 * hidden
+    dmsg, cmsg = dispatch_message_bytes(hidden, mode), combine_message_bytes(hidden, mode)
     d = np.zeros(e_local * n * T * dmsg, np.uint8)
     c = np.zeros(T * top_k * cmsg, np.uint8)
     cells = np.zeros(n_cells, np.uint64)
-    if mode == 2:
-        rc = lib().gso_moe_fp8_rank_state(seed, n, experts, top_k, T, hidden, r, _p(d, c_uint8), _p(c, c_uint8))
+    if mode in (2, 3):
+        c2 = np.zeros(T * top_k * 2 * hidden, np.uint8)
+        rc = lib().gso_moe_fp8_rank_state(seed, n, experts, top_k, T, hidden, r, _p(d, c_uint8), _p(c2, c_uint8))
+        if mode == 2:
+            c = c2
+        else:
+            lib().gso_fp8c_combine_window(seed, experts, top_k, hidden, r, T, _p(c, c_uint8))
         cnt = counts(seed, n, experts, top_k, T)
         for e_loc in range(e_local):
             cells[e_loc] = (n << 32) + int(cnt[r * e_local + e_loc].sum())

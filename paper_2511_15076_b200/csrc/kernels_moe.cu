@@ -76,6 +76,7 @@ struct MoeLaunch {
   uint32_t fuse_reduce;          // TMA combine: reduce inside the send kernel (small, latency-bound T)
   uint64_t dmsg;                 // dispatch message bytes: payload + 16-byte meta
   uint32_t mpay;                 // payload bytes before the meta (2H; fp8: H + H/32)
+  uint64_t cmsg;                 // combine message bytes (2H; fp8 combine, mode 3: H + H/32)
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
 };
@@ -807,6 +808,46 @@ __device__ __forceinline__ uint32_t tma_chunk_len(uint32_t payload, uint32_t chu
   return min(chunk, payload - p * chunk);
 }
 
+// fp8 combine (mode 3): out = bf16(sum_k w_k * fp32(q_k)*scale_k) for one
+// 16-byte output vector (8 elements) of token t, fp32 in k order.
+template <int KMAX>
+__device__ __forceinline__ uint4 reduce_fp8_vec(const char* crecv, uint64_t cmsg, uint32_t H, uint32_t t, uint32_t i,
+                                                uint32_t K, const void* weights) {
+  uint2 q[KMAX];
+  float sc[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < (int)K) {
+      const char* m = crecv + ((uint64_t)t * K + k) * cmsg;
+      q[k] = *reinterpret_cast<const uint2*>(m + 8ull * i);
+      sc[k] = *reinterpret_cast<const float*>(m + H + 4ull * (i / 16));
+    }
+  }
+  const float* w = reinterpret_cast<const float*>(weights) + (uint64_t)t * K;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < (int)K) {
+      const float wk = w[k];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint32_t word = h < 2 ? q[k].x : q[k].y;
+        const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)((word >> ((h & 1) * 16)) & 0xFFFF), __NV_E4M3);
+        const float2 f = __half22float2(__half2(hr));
+        acc[2 * h] = __fadd_rn(acc[2 * h], __fmul_rn(wk, __fmul_rn(f.x, sc[k])));
+        acc[2 * h + 1] = __fadd_rn(acc[2 * h + 1], __fmul_rn(wk, __fmul_rn(f.y, sc[k])));
+      }
+    }
+  }
+  uint32_t pk[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const __nv_bfloat162 r = __floats2bfloat162_rn(acc[2 * h], acc[2 * h + 1]);
+    pk[h] = *reinterpret_cast<const uint32_t*>(&r);
+  }
+  return make_uint4(pk[0], pk[1], pk[2], pk[3]);
+}
+
 // out = sum_k w_k * y_k for one 16-byte vector (8 elements) of token t:
 // u16 wraparound (harness_moe.cpp:227-242) or fp32 accumulate in k order
 // with single rounding per op, rounded once to bf16.
@@ -897,7 +938,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   const uint32_t E = L.E, K = L.K, T = L.T, H = L.H, e_local = L.e_local;
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t dmsg = L.dmsg;
-  const bool fp8 = L.mode == 2;
+  const bool fp8 = L.mode >= 2;
   const uint32_t payload = 2u * H, parts = L.parts;
   const uint32_t Kp = (K + 1) & ~1u;  // dst_g row stride: 16-byte rows for the bulk load
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
@@ -1545,8 +1586,8 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
   const uint32_t K = L.K, T = L.T, H = L.H, e_local = L.e_local;
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t dmsg = L.dmsg, cmsg = 2ull * H;
-  const bool fp8 = L.mode == 2;
+  const uint64_t dmsg = L.dmsg, cmsg = L.cmsg;
+  const bool fp8 = L.mode >= 2, fp8c = L.mode == 3;
   const uint32_t payload = 2u * H, parts = L.cparts;
   MOE_STAMP(R, 1, 0);
 
@@ -1558,8 +1599,10 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
   // per stage: [128-byte header: the message's 16-byte meta][chunk]; fp8:
   // [header][e4m3 chunk/2][scales chunk/64][bf16 output chunk]
+  // mode 3 adds the re-quantized output: [..][bf16 y chunk][e4m3 chunk/2][scales chunk/64]
   const uint32_t q_off = 128, s_off = 128 + chunk / 2, o_off = fp8 ? s_off + chunk / 64 : 128;
-  const uint32_t sstride = fp8 ? o_off + chunk : 128 + chunk;
+  const uint32_t oq_off = o_off + chunk, os_off = oq_off + chunk / 2;
+  const uint32_t sstride = fp8c ? os_off + chunk / 64 : (fp8 ? o_off + chunk : 128 + chunk);
   char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kTmaStages * sstride;
 
   const uint32_t P = e_local * n;
@@ -1714,11 +1757,24 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
         for (; i < nv; i += 32) buf[i] = bf16x8_transform(buf[i], sc, cc);
       }
     }
+    if (fp8c) {  // re-quantize the expert output, 128 elements per warp step
+      __syncwarp();
+      for (uint32_t blk = 0; blk < len / 256; ++blk)
+        fp8_quant_block(reinterpret_cast<const uint16_t*>(sb + o_off + blk * 256),
+                        reinterpret_cast<uint8_t*>(sb + oq_off + blk * 128), reinterpret_cast<float*>(sb + os_off) + blk,
+                        lane);
+    }
     gin::tma::fence_proxy_async_shared();
     __syncwarp();
     if (lane == 0) {
       const uint4 meta = *reinterpret_cast<const uint4*>(sb);  // {src, token, k, tag}
-      gin::tma::store(cbases[src] + ((uint64_t)meta.y * K + meta.z) * cmsg + (uint64_t)p * chunk, buf, len);
+      char* cdst = cbases[src] + ((uint64_t)meta.y * K + meta.z) * cmsg;
+      if (fp8c) {
+        gin::tma::store(cdst + (uint64_t)p * (chunk / 2), sb + oq_off, len / 2);
+        gin::tma::store(cdst + H + (uint64_t)p * (chunk / 64), sb + os_off, len / 64);
+      } else {
+        gin::tma::store(cdst + (uint64_t)p * chunk, buf, len);
+      }
       gin::tma::commit();
       if (j >= 1) {  // refill the previous item's stage (its store has been reading meanwhile)
         gin::tma::wait_read<1>();
@@ -1768,9 +1824,10 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       uint4 y[KMAX];
 #pragma unroll
       for (int k = 0; k < KMAX; ++k)
-        if (k < (int)K) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+        if (k < (int)K && !fp8c) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
       gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
-                 reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
+                 fp8c ? reduce_fp8_vec<KMAX>(crecv, cmsg, H, t, i, K, R.weights)
+                      : reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
     }
   }
 }
@@ -1781,7 +1838,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
 // 227) then the top-k weighted reduction, two 16-byte vectors per thread with
 // all 2K loads in flight before any use.  No CTA waits on another CTA of
 // this launch, so it needs no co-residency.
-template <int KMAX>
+template <int KMAX, bool FP8C>
 __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
@@ -1789,7 +1846,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
   const uint32_t rank = v->rank;
   const uint32_t K = L.K, T = L.T, H = L.H, e_local = L.e_local;
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  const uint64_t cmsg = 2ull * H;
+  const uint64_t cmsg = L.cmsg;
+  constexpr bool fp8c = FP8C;  // mode 3 (a separate instantiation keeps the bf16 path spill-free)
   const uint32_t payload = 2u * H;
   MOE_STAMP(R, 2, 0);
   if (tid == 0) gin.wait_ge_signal(e_local, R.iteration * (uint64_t)T * K);
@@ -1800,6 +1858,11 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
   const uint64_t ritems = (uint64_t)T * nvec, rstride = (uint64_t)G * kMoeThreads;
   for (uint64_t q = (uint64_t)b * kMoeThreads + tid; q < ritems; q += rstride) {
     const uint32_t t = (uint32_t)(q / nvec), i = (uint32_t)(q % nvec);
+    if (fp8c) {
+      gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
+                 reduce_fp8_vec<KMAX>(crecv, cmsg, H, t, i, K, R.weights));
+      continue;
+    }
     uint4 y[KMAX];
 #pragma unroll
     for (int k = 0; k < KMAX; ++k)
@@ -1921,8 +1984,8 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   if (cfg->tokens == 0 || cfg->top_k == 0 || cfg->top_k > cfg->experts || cfg->top_k > 32)
     fail(GINSIM_E_USAGE, "need 1..min(experts,32) routed experts per token and at least one token");
   if (cfg->hidden == 0) fail(GINSIM_E_USAGE, "hidden must be positive");
-  if (cfg->mode > 2 || cfg->layout > 2) fail(GINSIM_E_USAGE, "mode must be 0, 1 or 2, layout 0, 1 or 2");
-  if (cfg->mode == 2) {
+  if (cfg->mode > 3 || cfg->layout > 2) fail(GINSIM_E_USAGE, "mode must be 0..3, layout 0, 1 or 2");
+  if (cfg->mode >= 2) {
     if (cfg->hidden % 512) fail(GINSIM_E_USAGE, "fp8 mode needs hidden % 512 == 0 (128-element scale blocks)");
     if (cfg->layout == 2 || c->cfg.backend != GIN_BACKEND_DIRECT || cfg->engine == 1)
       fail(GINSIM_E_USAGE, "fp8 mode runs on the direct TMA path with layout 0 or 1");
@@ -1942,8 +2005,8 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   m->cfg = *cfg;
   m->e_local = e_local;
   m->parts = cfg->hidden >= 1024 ? 4 : 1;
-  const uint64_t dmsg = (cfg->mode == 2 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden) + 16;
-  const uint64_t cmsg = 2ull * cfg->hidden;
+  const uint64_t dmsg = (cfg->mode >= 2 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden) + 16;
+  const uint64_t cmsg = cfg->mode == 3 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden;
   const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
   const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
   if (cfg->layout == 2 && e_local + 2 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
@@ -2079,8 +2142,9 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
   L.coop = moes[0]->coop ? 1u : 0u;
   L.fuse_reduce = moes[0]->coop ? 0u : 1u;
-  L.mpay = cfg.mode == 2 ? cfg.hidden + cfg.hidden / 32 : 2u * cfg.hidden;
+  L.mpay = cfg.mode >= 2 ? cfg.hidden + cfg.hidden / 32 : 2u * cfg.hidden;
   L.dmsg = (uint64_t)L.mpay + 16;
+  L.cmsg = cfg.mode == 3 ? (uint64_t)cfg.hidden + cfg.hidden / 32 : 2ull * cfg.hidden;
   for (uint32_t i = 0; i < n; ++i) {
     if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
@@ -2141,7 +2205,10 @@ static MoeKernels kernels_of(const ginsim_cuda_moe_t m) {
     k.combine = (const void*)moe_combine_kernel<false>;
   } else {
     k.combine = k8 ? (const void*)moe_combine_tma_kernel<8> : (const void*)moe_combine_tma_kernel<32>;
-    k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8> : (const void*)moe_combine_reduce_kernel<32>;
+    if (m->cfg.mode == 3)
+      k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8, true> : (const void*)moe_combine_reduce_kernel<32, true>;
+    else
+      k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8, false> : (const void*)moe_combine_reduce_kernel<32, false>;
     k.tma_combine = true;
   }
   return k;
@@ -2153,7 +2220,7 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
   // control blocks | stages of [destination row (padded to 128 B) | chunk] | own route indices
   const size_t kp = (m->cfg.top_k + 1) & ~1u;
   const size_t dhead = (kp * 8 + 127) & ~(size_t)127;
-  if (m->cfg.mode == 2) {  // + e4m3 chunk + scales per stage
+  if (m->cfg.mode >= 2) {  // + e4m3 chunk + scales per stage
     const size_t sst = (dhead + m->chunk + m->chunk / 2 + m->chunk / 64 + 15) & ~(size_t)15;
     return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kDispStages * sst + pairs * 4;
   }
@@ -2165,7 +2232,9 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
 static size_t combine_smem(const ginsim_cuda_moe_t m) {
   if (!kernels_of(m).tma_combine) return 0;
   // fp8: [hdr][e4m3 in][scales][bf16 out] per stage
-  const size_t sst = m->cfg.mode == 2 ? 128 + m->cchunk / 2 + m->cchunk / 64 + m->cchunk : 128 + m->cchunk;
+  const size_t c = m->cchunk;
+  const size_t sst = m->cfg.mode == 3 ? 128 + 2 * (c / 2 + c / 64) + c
+                                      : (m->cfg.mode == 2 ? 128 + c / 2 + c / 64 + c : 128 + c);
   return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * sst;
 }
 static int combine_threads(const MoeKernels& k) { return k.tma_combine ? kCmbThreads : kMoeThreads; }
@@ -2191,7 +2260,7 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
     chunk = ((payload + parts - 1) / parts + 15) / 16 * 16;
     cparts = (payload + 4095) / 4096;
     cchunk = ((payload + cparts - 1) / cparts + 15) / 16 * 16;
-    if (m->cfg.mode == 2) {
+    if (m->cfg.mode >= 2) {
       // fp8: chunks of whole 512-element groups, so every chunk's scale slice
       // (chunk/64 bytes) is a 16-byte multiple at a 16-byte aligned offset
       chunk = (chunk + 1023) / 1024 * 1024;

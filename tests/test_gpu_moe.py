@@ -26,7 +26,7 @@ class MoeRun:
                                                           queue_depth=queue_depth))
         self.cfg = G.MoeConfig(E, K, T, H, mode, layout, ctas, engine)
         self.moes = G.Moe.create_all(self.comms, self.cfg)
-        wbytes = T * K * (2 if mode == 0 else 4)
+        wbytes = T * K * (2 if mode == 0 else 4)  # u16 weights, else fp32
         self.x = [U.malloc(T * H * 2) for _ in range(n)]
         self.idx = [U.malloc(T * K * 4) for _ in range(n)]
         self.w = [U.malloc(wbytes) for _ in range(n)]
@@ -419,15 +419,19 @@ def test_moe_dedup_transport_matches_reference(n, E, K, T, H, mode):
         run.close()
 
 
-@pytest.mark.parametrize("n,E,K,T,H,layout", [(4, 32, 8, 40, 7168, 0), (4, 64, 8, 48, 7168, 1), (2, 16, 4, 33, 512, 1),
-                                               (8, 256, 8, 64, 7168, 1)])
-def test_moe_fp8_mode_matches_oracle(n, E, K, T, H, layout):
+@pytest.mark.parametrize("mode", [2, 3])
+@pytest.mark.parametrize("n,E,K,T,H,layout,coop", [(4, 32, 8, 40, 7168, 0, 0), (4, 64, 8, 48, 7168, 1, 0),
+                                                    (2, 16, 4, 33, 512, 1, 0), (8, 256, 8, 64, 7168, 1, 0),
+                                                    (4, 64, 8, 64, 7168, 1, 1)])
+def test_moe_fp8_mode_matches_oracle(n, E, K, T, H, layout, coop, mode, monkeypatch):
     """fp8 mode (mode 2): dispatch messages = e4m3 codes +
     per-128 fp32 scales + meta, bit-exact against the oracle's quantizer;
     the expert transform runs on the dequantized values; combine windows and
     outputs bit-exact against the oracle (whose tolerance to the bf16 path is
     tests/test_oracle_golden.py::test_fp8_combine_within_stated_tolerance_of_bf16)."""
-    run = MoeRun(n, E, K, T, H, mode=2, layout=layout, engine=2)
+    if coop:  # cooperative route tables + the separate reduce kernel
+        monkeypatch.setenv("GINSIM_DISPATCH_COOP_MIN_PAIRS", "1")
+    run = MoeRun(n, E, K, T, H, mode=mode, layout=layout, engine=2)
     try:
         # (the reference layout keeps stale messages past a new routing's
         # counts, so a second routing is compared only in the compact layout)
@@ -436,13 +440,13 @@ def test_moe_fp8_mode_matches_oracle(n, E, K, T, H, layout):
             run.step()
             cnt = O.counts(seed, n, E, K, T)
             for r in range(n):
-                d, comb, _ = O.moe_rank_state(seed, n, E, K, T, H, r, mode=2)
+                d, comb, _ = O.moe_rank_state(seed, n, E, K, T, H, r, mode=mode)
                 win = run.dispatch_window(r)
                 if layout == 1:
-                    win = O.compact_to_reference(win, cnt, r, n, E // n, T, K, O.dispatch_message_bytes(H, 2))
+                    win = O.compact_to_reference(win, cnt, r, n, E // n, T, K, O.dispatch_message_bytes(H, mode))
                 assert (win == d).all(), (seed, r)
                 assert (run.combine_window(r) == comb).all(), (seed, r)
-                exp, _ = O.combine(seed, E, K, H, r, T, mode=2)
+                exp, _ = O.combine(seed, E, K, H, r, T, mode=mode)
                 assert (run.output(r) == exp).all(), (seed, r)
     finally:
         run.close()

@@ -153,3 +153,23 @@ def test_fp8_combine_within_stated_tolerance_of_bf16():
     err = np.abs(bf(f8) - bf(b16))
     assert (err <= bound).all(), float((err / bound).max())
     assert (f8 != b16).any()  # quantization actually happened
+
+
+def test_fp8_combine_messages_within_stated_tolerance_of_bf16():
+    """mode 3 (fp8 dispatch AND fp8 combine messages): two e4m3 roundings;
+    |out - out_bf16| <= 2^-4 * sum_k w_k*s_k*|x| + 2^-4 * sum_k w_k*|y_k|
+                        + 2^-7 * (|out_bf16| + sum_k w_k*|y_k|)."""
+    seed, E, K, H, src, T = 5, 64, 8, 512, 2, 24
+    f8, _ = O.combine(seed, E, K, H, src, T, mode=3)
+    b16, _ = O.combine(seed, E, K, H, src, T, mode=1)
+    bf = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    x = bf(O.tokens(seed, src, T, H, mode=1))
+    route = O.route_table(seed, E, K, src, T)
+    w = O.weights(src, T, K, mode=1).astype(np.float64)
+    s = 1.0 + (route % 7) / 8.0
+    c = ((route % 9) - 4.0) / 16.0
+    wsx = np.einsum("tk,tk,th->th", w, s, np.abs(x))
+    wy = np.einsum("tk,tkh->th", w, np.abs(s[:, :, None] * x[:, None, :] + c[:, :, None]))
+    bound = 2.0 ** -4 * wsx + 2.0 ** -4 * wy + 2.0 ** -7 * (np.abs(bf(b16)) + wy)
+    err = np.abs(bf(f8) - bf(b16))
+    assert (err <= bound).all(), float((err / bound).max())
