@@ -247,6 +247,14 @@ int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t s
                          uint32_t recv_win, uint64_t bytes_per_peer, uint32_t signal_id,
                          uint64_t expected, uint32_t ctas, void* stream);
 
+/* Ordering stress (acceptance #1, acceptance.cpp:63-118): `channels` parallel
+ * (ctx, rank -> right neighbour) channels, each `rounds` puts of `bytes` with
+ * SignalAdd(1) into a 2-slot ring; receivers acquire the signal and verify
+ * every byte, then return a credit.  VERIFICATION_FAILURE when a signal was
+ * observed before the put it follows.  Windows: 2 * channels * bytes. */
+int ginsim_cuda_ordering_stress(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t src_win, uint32_t dst_win,
+                                uint64_t bytes, uint32_t channels, uint32_t rounds, void* stream);
+
 /* Ring exchange (harness_ring.cpp:18-57) on the device: `rounds` rounds of
  * put+SignalInc to (r+1)%n, wait, verify the (rank, round) pattern, reset,
  * flush, barrier.  VERIFICATION_FAILURE through the device error word. */

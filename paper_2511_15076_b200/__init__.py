@@ -205,6 +205,7 @@ def _declare(L):
         "ginsim_cuda_nvls_enabled": ([P, POINTER(c_int)], c_int),
         "ginsim_cuda_barrier_bench": ([POINTER(P), c_uint32, c_uint32, c_uint32, P, P], c_int),
         "ginsim_cuda_occupy": ([c_int, c_uint32, P, c_uint64, P], c_int),
+        "ginsim_cuda_ordering_stress": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, P], c_int),
         "ginsim_cuda_ring":([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, P], c_int),
         "ginsim_cuda_moe_ht_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, P], c_int),
         "ginsim_cuda_moe_create": ([P, POINTER(MoeConfig), POINTER(P)], c_int),

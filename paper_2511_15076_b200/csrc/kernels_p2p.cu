@@ -169,6 +169,65 @@ __global__ void __launch_bounds__(kA2aThreads) alltoall_kernel(A2aArgs A) {
   if (blockIdx.x == 0 && threadIdx.x == 0) gin.wait_ge_signal(A.sig, A.expected);
 }
 
+// ------------------------------------------------------------------ ordering stress
+// acceptance #1 (acceptance.cpp:63-118, fabric.cpp:63-79) on the device API:
+// `channels` independent (ctx, src -> dst) channels per rank run in parallel,
+// each a stream of put + SignalAdd(1) rounds into a 2-slot ring at the right
+// neighbour; the receiving CTA acquires signal >= round+1 and checks EVERY
+// byte of that round's put (tagged with sender, channel, round), then hands
+// the slot back with a credit signal.  A put the signal did not cover shows up
+// as a stale or torn slot -> VERIFY on the device error word.
+struct OrderArgs {
+  LaneViews lv;
+  uint32_t src_win, dst_win, rounds, channels;
+  uint64_t bytes;  // per put
+};
+
+__device__ __forceinline__ uint32_t order_word(uint32_t sender, uint32_t ch, uint32_t round, uint64_t i) {
+  return (sender << 24) ^ (ch << 16) ^ (round * 2654435761u) ^ (uint32_t)(i * 40503u);
+}
+
+__global__ void ordering_stress_kernel(OrderArgs A) {
+  const GinDevCommView* v = A.lv.v[blockIdx.y];
+  const uint64_t base = A.lv.base[blockIdx.y];  // signal values reached by earlier launches
+  const uint32_t n = v->world, r = v->rank, right = (r + 1) % n, left = (r + n - 1) % n;
+  const uint32_t ch = blockIdx.x % A.channels;
+  const bool sender = blockIdx.x < A.channels;
+  gin::Gin gin(v, ch % v->n_ctx);
+  gin::CoopCta cta;
+  const gin::Team world = gin::WorldTeam(n);
+  const uint32_t words = (uint32_t)(A.bytes / 4);
+  const uint32_t data_cell = ch, credit_cell = A.channels + ch;
+  __shared__ int bad;
+  for (uint32_t round = 0; round < A.rounds; ++round) {
+    const uint64_t slot = (uint64_t)(ch * 2 + (round & 1)) * A.bytes;
+    if (sender) {
+      if (round >= 2) gin.wait_signal(cta, credit_cell, base + round - 1);  // slot free again
+      uint32_t* src = reinterpret_cast<uint32_t*>(gin.window_ptr(A.src_win, r, slot));
+      for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) src[i] = order_word(r, ch, round, i);
+      cta.sync();
+      gin.put(cta, world, right, A.dst_win, slot, A.src_win, slot, A.bytes,
+              gin::SignalAction(data_cell, gin::SignalAdd(1)));
+    } else {
+      gin.wait_signal(cta, data_cell, base + round + 1);
+      if (threadIdx.x == 0) bad = 0;
+      cta.sync();
+      const uint32_t* dst = reinterpret_cast<const uint32_t*>(gin.window_ptr(A.dst_win, r, slot));
+      for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
+        uint32_t w;
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(w) : "l"(dst + i) : "memory");
+        if (w != order_word(left, ch, round, i)) bad = 1;
+      }
+      cta.sync();
+      if (bad) {
+        if (threadIdx.x == 0) gin::raise_error(v, GIN_DEVERR_VERIFY);
+        return;
+      }
+      gin.signal(cta, world, left, credit_cell, gin::SignalAdd(1));  // hand the slot back
+    }
+  }
+}
+
 // ------------------------------------------------------------------ ring
 struct RingArgs {
   LaneViews lv;
@@ -409,6 +468,37 @@ int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t s
     GIN_CUDA(cudaLaunchCooperativeKernel((const void*)alltoall_kernel, grid, dim3(kA2aThreads), args, smem,
                                          (cudaStream_t)stream));
   }
+  GIN_API_END
+}
+
+int ginsim_cuda_ordering_stress(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t src_win, uint32_t dst_win,
+                                uint64_t bytes, uint32_t channels, uint32_t rounds, void* stream) {
+  GIN_API_BEGIN
+  check_same_device(comms, n);
+  Comm* c0 = &comms[0]->impl;
+  if (c0->world < 2) fail(GINSIM_E_USAGE, "ordering stress needs at least 2 ranks");
+  if (bytes == 0 || bytes % 4 || channels == 0 || 2 * channels > c0->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
+    fail(GINSIM_E_USAGE, "bytes must be a positive multiple of 4; 2*channels signal cells needed");
+  for (uint32_t i = 0; i < n; ++i) {
+    Comm* c = &comms[i]->impl;
+    if (src_win >= c->windows.size() || dst_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+    for (uint32_t r = 0; r < c->world; ++r)
+      if (c->windows[src_win].sizes[r] < 2ull * channels * bytes || c->windows[dst_win].sizes[r] < 2ull * channels * bytes)
+        fail(GINSIM_E_OUT_OF_BOUNDS, "windows must hold 2 * channels * bytes");
+  }
+  DeviceGuard g(c0->device);
+  OrderArgs A{};
+  A.lv = lanes(comms, n);
+  A.src_win = src_win;
+  A.dst_win = dst_win;
+  A.rounds = rounds;
+  A.channels = channels;
+  A.bytes = bytes;
+  // every launch adds `rounds` to each data and credit cell (credits: rounds on
+  // the sender side as well), so the base advances by rounds per launch
+  for (uint32_t i = 0; i < n; ++i) A.lv.base[i] = bump_host_counter(&comms[i]->impl, 5, rounds) - rounds;
+  coop_launch((const void*)ordering_stress_kernel, dim3(2 * channels, n), dim3(256), &A, (cudaStream_t)stream);
+  sync_and_check(comms, n, (cudaStream_t)stream);
   GIN_API_END
 }
 

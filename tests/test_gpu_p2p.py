@@ -352,3 +352,26 @@ def test_dissemination_barrier_emulated_and_nvls_gating(n):
         U.free(ns)
     finally:
         close(cs)
+
+
+@pytest.mark.parametrize("n,channels,rounds,nbytes,backend", [(2, 8, 200, 64 << 10, "direct"),
+                                                               (4, 6, 100, 16 << 10, "direct"),
+                                                               (8, 4, 60, 4 << 10, "direct"),
+                                                               (2, 4, 60, 16 << 10, "proxy")])
+def test_signal_orders_earlier_puts_under_concurrency(n, channels, rounds, nbytes, backend):
+    """Acceptance #1 (acceptance.cpp:63-118; fabric.cpp:63-79) on the device API:
+    many concurrent (ctx, src->dst) channels; whenever a receiver observes
+    signal >= round+1, every byte of that round's put is already visible.
+    Two launches back to back (the cells continue)."""
+    cs = world(n, backend)
+    try:
+        size = 2 * channels * nbytes
+        ws, _ = register(cs, size)
+        wd, _ = register(cs, size)
+        for _ in range(2):
+            G.check(G.lib().ginsim_cuda_ordering_stress(G.comm_handles(cs), n, ws, wd, nbytes, channels, rounds, None))
+        for c in cs:
+            c.check_device()
+            assert c.read_signal(0) == 2 * rounds
+    finally:
+        close(cs)
