@@ -15,6 +15,10 @@ Prints one JSON line on rank 0.
 """
 from __future__ import annotations
 
+import os as _os
+# every stream its own hardware queue: a proxy-agent stream aliased onto the queue of
+# a kernel that waits for the agent would stall behind it (csrc/proxy.cu)
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import argparse
 import json
 import os
@@ -303,11 +307,17 @@ def measure_proxy(G, rank, world, local, dist, torch, dev, stream, allgather, T,
     busy = (st1["busy_ns"] - st0["busy_ns"]) / max(1, st1["wall_ns"] - st0["wall_ns"])
     dmsg, cmsg = 2 * H + 16, 2 * H
     disp_us, comb_us = t[0].item() * 1e3, t[1].item() * 1e3
+    remote = int(((idx.cpu().numpy().reshape(T, K) // (E // world)) != rank).sum())
+    pipe = moe.pipelined()
     res = {"workload": f"proxy backend dispatch/combine, {T} tokens/rank, hidden {H}, top-{K} of {E}, bf16, "
-                       f"{world} GPU(s), one copy-engine put per (expert, source) run in both phases",
+                       f"{world} GPU(s), " + ("pipelined: staged chunks handed to the copy engines as they fill"
+                                             if pipe else "one copy-engine put per destination after the staging kernel"),
+           "transport": "pipeline" if pipe else "one-shot",
            "dispatch_us_p50": disp_us, "combine_us_p50": comb_us,
            "dispatch_GBps_per_gpu": T * K * dmsg / (disp_us * 1e-6) / 1e9,
            "combine_GBps_per_gpu": T * K * cmsg / (comb_us * 1e-6) / 1e9,
+           "dispatch_remote_GBps_per_gpu": remote * dmsg / (disp_us * 1e-6) / 1e9,
+           "dispatch_remote_frac_of_900": remote * dmsg / (disp_us * 1e-6) / 1e9 / 900.0,
            "descriptors_per_step": ndesc / steps, "copies_per_step": ncopy / steps,
            "descriptors_per_s": ndesc / (t[2].item() * 1e-3), "agent_thread_busy_frac": busy,
            "host_threads": 1}

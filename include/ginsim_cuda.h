@@ -229,10 +229,21 @@ int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t d
 
 /* Extended roofline probe: engine 0 = LSU 128-bit, 1 = TMA load+store with
  * `chunk`-byte stages, 2 = LSU 256-bit, 3 = copy engine (cudaMemcpyAsync over
- * the peer mapping), 4 = TMA store-only (write path alone, no reads). */
+ * the peer mapping), 4 = TMA store-only (write path alone, no reads),
+ * 5 = TMA pull (bulk-load the peer's src window, store into this rank's dst
+ * window), 6 = hybrid push (copy engine moves the last GINSIM_HYBRID_CE_PCT %
+ * on a side stream while TMA copies the rest), 7 = LSU 256-bit pull. */
 int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t dst_win, uint32_t peer,
                               uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t chunk, uint32_t iters,
                               float* ms_out, void* stream);
+
+/* Host-issued operation cost (the proxy agent's building blocks): n_ops
+ * 64-bit stream memops (kind 0, `batch` per cuStreamBatchMemOp) or copies
+ * (kind 1, cudaMemcpyAsync of `bytes` each) into `peer`'s dst window.
+ * out[0] = device microseconds per op, out[1] = host microseconds per op. */
+int ginsim_cuda_host_op_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t dst_win, uint32_t peer,
+                              uint32_t kind, uint32_t n_ops, uint32_t batch, uint64_t bytes, float* out,
+                              void* stream);
 
 /* Launches a kernel that holds every SM (ctas_per_sm x 1024 threads per SM,
  * 1..2) until *release_word (host-mapped) becomes nonzero or timeout_ms
@@ -348,6 +359,12 @@ int ginsim_cuda_moe_phase_times(ginsim_cuda_moe_t moe, uint32_t kernel, uint64_t
 
 /* Per-launch kernel count of the last dispatch/combine (for bench evidence). */
 int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t* threads);
+
+/* Transport the handle runs: 0 = direct NVLink stores, 1 = Proxy backend
+ * with one-shot staging (LSU kernels; per-message puts when
+ * GINSIM_PROXY_COALESCE=0), 2 = Proxy pipeline (chunked copy-engine puts
+ * issued while the staging kernel runs; layout 1, modes 0/1). */
+int ginsim_cuda_moe_transport(ginsim_cuda_moe_t moe, uint32_t* kind);
 
 #ifdef __cplusplus
 }

@@ -205,6 +205,8 @@ def _declare(L):
         "ginsim_cuda_nvls_enabled": ([P, POINTER(c_int)], c_int),
         "ginsim_cuda_barrier_bench": ([POINTER(P), c_uint32, c_uint32, c_uint32, P, P], c_int),
         "ginsim_cuda_occupy": ([c_int, c_uint32, P, c_uint64, P], c_int),
+        "ginsim_cuda_host_op_bench": ([P, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64,
+                                       POINTER(ctypes.c_float), P], c_int),
         "ginsim_cuda_ordering_stress": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, P], c_int),
         "ginsim_cuda_ring":([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, P], c_int),
         "ginsim_cuda_moe_ht_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, P], c_int),
@@ -216,6 +218,7 @@ def _declare(L):
         "ginsim_cuda_moe_combine": ([POINTER(P), c_uint32, POINTER(P), POINTER(P), P], c_int),
         "ginsim_cuda_moe_phase_times": ([P, c_uint32, POINTER(c_uint64), POINTER(c_uint32)], c_int),
         "ginsim_cuda_moe_last_launch": ([P, POINTER(c_uint32), POINTER(c_uint32)], c_int),
+        "ginsim_cuda_moe_transport": ([P, POINTER(c_uint32)], c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name, None)
@@ -514,6 +517,15 @@ class Moe:
         a, b = c_uint32(), c_uint32()
         check(lib().ginsim_cuda_moe_last_launch(self.h, byref(a), byref(b)))
         return a.value, b.value
+
+    def transport(self):
+        """0 direct, 1 proxy one-shot staging, 2 proxy pipeline."""
+        k = c_uint32()
+        check(lib().ginsim_cuda_moe_transport(self.h, byref(k)))
+        return k.value
+
+    def pipelined(self):
+        return self.transport() == 2
 
     def phase_times(self, kernel):
         """[ctas][8] %globaltimer stamps of the last launch of `kernel` (0 dispatch,

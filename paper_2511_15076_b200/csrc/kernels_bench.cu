@@ -4,6 +4,9 @@
 // (or the local) window, no signals.  Gives the measured NVLink write floor
 // that BASELINE's "fraction of 900 GB/s" sits next to.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <vector>
 
 #include "gin_device.cuh"
 #include "runtime_internal.h"
@@ -115,6 +118,11 @@ __global__ void __launch_bounds__(1024) occupy_kernel(const volatile uint32_t* r
   __syncthreads();
 }
 
+__global__ void spin_kernel(uint64_t ns) {
+  const uint64_t t0 = gin::globaltimer();
+  while (gin::globaltimer() - t0 < ns) __nanosleep(1000);
+}
+
 }  // namespace ginsim_b200
 
 using namespace ginsim_b200;
@@ -135,8 +143,28 @@ int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t d
     fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
   if (bytes % 16) fail(GINSIM_E_USAGE, "copy size must be a multiple of 16");
   DeviceGuard g(c->device);
-  char* dst = c->windows[dst_win].bases[peer];
-  const char* src = c->windows[src_win].bases[c->rank];
+  // engines 5/7 pull: read the peer's src window, write this rank's dst window
+  const bool pull = engine == 5 || engine == 7;
+  if (pull && (c->windows[src_win].sizes[peer] < bytes || c->windows[dst_win].sizes[c->rank] < bytes))
+    fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
+  char* dst = c->windows[dst_win].bases[pull ? c->rank : peer];
+  const char* src = c->windows[src_win].bases[pull ? peer : c->rank];
+  // engine 6: the copy engine moves the last GINSIM_HYBRID_CE_PCT percent
+  // (default 25) on a side stream while TMA copies the rest
+  uint64_t ce_bytes = 0;
+  if (engine == 6) {
+    const char* e = std::getenv("GINSIM_HYBRID_CE_PCT");
+    const uint64_t pct = std::min<uint64_t>(100, e ? std::strtoull(e, nullptr, 10) : 25);
+    ce_bytes = (bytes * pct / 100) & ~uint64_t(4095);
+  }
+  const uint64_t sm_bytes = bytes - ce_bytes;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (engine == 6) {
+    GIN_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    GIN_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    GIN_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  }
   cudaStream_t s = (cudaStream_t)stream;
   int sms = 0;
   GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
@@ -180,18 +208,38 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
   if (peer >= c->world) fail(GINSIM_E_INVALID_PEER, "peer out of range");
   if (c->windows[src_win].sizes[c->rank] < bytes || c->windows[dst_win].sizes[peer] < bytes)
     fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
-  if (bytes % 32 || engine > 4) fail(GINSIM_E_USAGE, "copy size must be a multiple of 32; engine 0..4");
+  if (bytes % 32 || engine > 7) fail(GINSIM_E_USAGE, "copy size must be a multiple of 32; engine 0..7");
   if (chunk == 0 || chunk % 16 || chunk > 16384) fail(GINSIM_E_USAGE, "chunk must be a multiple of 16 in 16..16384");
   DeviceGuard g(c->device);
-  char* dst = c->windows[dst_win].bases[peer];
-  const char* src = c->windows[src_win].bases[c->rank];
+  // engines 5/7 pull: read the peer's src window, write this rank's dst window
+  const bool pull = engine == 5 || engine == 7;
+  if (pull && (c->windows[src_win].sizes[peer] < bytes || c->windows[dst_win].sizes[c->rank] < bytes))
+    fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
+  char* dst = c->windows[dst_win].bases[pull ? c->rank : peer];
+  const char* src = c->windows[src_win].bases[pull ? peer : c->rank];
+  // engine 6: the copy engine moves the last GINSIM_HYBRID_CE_PCT percent
+  // (default 25) on a side stream while TMA copies the rest
+  uint64_t ce_bytes = 0;
+  if (engine == 6) {
+    const char* e = std::getenv("GINSIM_HYBRID_CE_PCT");
+    const uint64_t pct = std::min<uint64_t>(100, e ? std::strtoull(e, nullptr, 10) : 25);
+    ce_bytes = (bytes * pct / 100) & ~uint64_t(4095);
+  }
+  const uint64_t sm_bytes = bytes - ce_bytes;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (engine == 6) {
+    GIN_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    GIN_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    GIN_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  }
   cudaStream_t s = (cudaStream_t)stream;
   int sms = 0;
   GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const uint32_t G = ctas ? ctas : (uint32_t)sms;
   const size_t smem_ld = 1024 + (size_t)(kCopyThreads / 32) * kCopyStages * chunk;
   const size_t smem_st = (size_t)(kCopyThreads / 32) * chunk;
-  if (engine == 1) {
+  if (engine == 1 || engine == 5 || engine == 6) {
     if (smem_ld > 227 * 1024) fail(GINSIM_E_USAGE, "chunk too large for 4 stages x 8 warps");
     GIN_CUDA(cudaFuncSetAttribute((const void*)tma_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ld));
   }
@@ -206,7 +254,17 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
       case 1: tma_copy_kernel<<<G, kCopyThreads, smem_ld, s>>>(dst, src, bytes, chunk); break;
       case 2: lsu256_copy_kernel<<<G, kCopyThreads, 0, s>>>(dst, src, bytes); break;
       case 3: GIN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s)); break;
-      default: tma_store_only_kernel<<<G, kCopyThreads, smem_st, s>>>(dst, bytes, chunk); break;
+      case 4: tma_store_only_kernel<<<G, kCopyThreads, smem_st, s>>>(dst, bytes, chunk); break;
+      case 5: tma_copy_kernel<<<G, kCopyThreads, smem_ld, s>>>(dst, src, bytes, chunk); break;
+      case 6:
+        GIN_CUDA(cudaEventRecord(fork, s));
+        GIN_CUDA(cudaStreamWaitEvent(side, fork, 0));
+        if (ce_bytes) GIN_CUDA(cudaMemcpyAsync(dst + sm_bytes, src + sm_bytes, ce_bytes, cudaMemcpyDefault, side));
+        if (sm_bytes) tma_copy_kernel<<<G, kCopyThreads, smem_ld, s>>>(dst, src, sm_bytes, chunk);
+        GIN_CUDA(cudaEventRecord(join, side));
+        GIN_CUDA(cudaStreamWaitEvent(s, join, 0));
+        break;
+      default: lsu256_copy_kernel<<<G, kCopyThreads, 0, s>>>(dst, src, bytes); break;
     }
   };
   launch();
@@ -221,6 +279,77 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
   *ms_out = ms / (float)std::max(1u, iters);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (side) {
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    cudaStreamDestroy(side);
+  }
+  GIN_API_END
+}
+
+// Host-issued operation cost (the proxy agent's building blocks): n_ops
+// stream memops (kind 0: 64-bit writes, batched `batch` per
+// cuStreamBatchMemOp) or copies (kind 1: cudaMemcpyAsync of `bytes` each)
+// into `peer`'s dst window.  out[0] = device us per op (events), out[1] =
+// host us per op spent issuing.
+int ginsim_cuda_host_op_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t dst_win, uint32_t peer,
+                              uint32_t kind, uint32_t n_ops, uint32_t batch, uint64_t bytes, float* out,
+                              void* stream) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  if (src_win >= c->windows.size() || dst_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+  if (peer >= c->world || kind > 1 || n_ops == 0 || batch == 0 || batch > 256) fail(GINSIM_E_USAGE, "bad probe arguments");
+  const uint64_t span = kind == 0 ? 8ull * n_ops : bytes * n_ops;
+  if (c->windows[dst_win].sizes[peer] < span || c->windows[src_win].sizes[c->rank] < span)
+    fail(GINSIM_E_OUT_OF_BOUNDS, "probe exceeds window capacity");
+  DeviceGuard g(c->device);
+  char* dst = c->windows[dst_win].bases[peer];
+  const char* src = c->windows[src_win].bases[c->rank];
+  cudaStream_t s = (cudaStream_t)stream, own = nullptr;
+  if (!s) {  // stream memops need an explicit stream
+    GIN_CUDA(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+    s = own;
+  }
+  std::vector<CUstreamBatchMemOpParams> ops;
+  auto issue = [&](uint64_t v) {
+    if (kind == 0) {
+      for (uint32_t i = 0; i < n_ops; i += batch) {
+        ops.clear();
+        for (uint32_t j = i; j < std::min(n_ops, i + batch); ++j) {
+          CUstreamBatchMemOpParams op{};
+          op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+          op.writeValue.address = (CUdeviceptr)(dst + 8ull * j);
+          op.writeValue.value64 = v + j;
+          op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+          ops.push_back(op);
+        }
+        GIN_CU(cuapi().cuStreamBatchMemOp((CUstream)s, (unsigned)ops.size(), ops.data(), 0));
+      }
+    } else {
+      for (uint32_t j = 0; j < n_ops; ++j)
+        GIN_CUDA(cudaMemcpyAsync(dst + bytes * j, src + bytes * j, bytes, cudaMemcpyDefault, s));
+    }
+  };
+  issue(1);
+  GIN_CUDA(cudaStreamSynchronize(s));
+  cudaEvent_t e0, e1;
+  GIN_CUDA(cudaEventCreate(&e0));
+  GIN_CUDA(cudaEventCreate(&e1));
+  // a short spin kernel first so the whole sequence is queued before it runs
+  spin_kernel<<<1, 32, 0, s>>>(2000000ull);
+  GIN_CUDA(cudaEventRecord(e0, s));
+  const auto h0 = std::chrono::steady_clock::now();
+  issue(1000);
+  const auto h1 = std::chrono::steady_clock::now();
+  GIN_CUDA(cudaEventRecord(e1, s));
+  GIN_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  GIN_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  out[0] = ms * 1000.f / (float)n_ops;
+  out[1] = (float)std::chrono::duration<double, std::micro>(h1 - h0).count() / (float)n_ops;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (own) cudaStreamDestroy(own);
   GIN_API_END
 }
 

@@ -39,6 +39,7 @@
 #include "moe_lsu.cuh"
 #include "moe_tma.cuh"
 #include "moe_dedup.cuh"
+#include "moe_pipe.cuh"
 #include "moe_gen.cuh"
 
 
@@ -51,6 +52,8 @@ struct ginsim_cuda_moe_s {
   uint32_t e_local = 0, parts = 4, G = 0, Gc = 0, Gr = 0, chunk = 0, cparts = 1, cchunk = 0;
   uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0, win_stage = 0, win_cstage = 0, win_mirror = 0;
   bool proxy = false;
+  bool pipe = false;              // Proxy pipeline (moe_pipe.cuh): chunked copy-engine puts, layout 1
+  uint32_t* pipe_buf = nullptr;   // R.pipe
   void* buf_mirror = nullptr;
   uint32_t* midx = nullptr;
   uint32_t win_rows = 0;
@@ -107,7 +110,7 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
   if (cfg->layout == 2 && e_local + 2 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
     fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag and rows cell exceed the signal table");
-  const uint64_t nbytes = ((uint64_t)e_local * n + n) * 4;  // counts [e_loc][src] + row counts [src] (layout 2)
+  const uint64_t nbytes = ((uint64_t)e_local * n + n) * 4;  // counts [src][e_loc] + row counts [src] (layout 2)
   const uint64_t cbytes = T * K * cmsg;
   if (ginsim_cuda_mem_alloc(comm, dbytes, &m->buf_dispatch)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
   if (ginsim_cuda_mem_alloc(comm, nbytes, &m->buf_counts)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
@@ -117,6 +120,17 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   if ((rc = ginsim_cuda_window_register(comm, m->buf_counts, nbytes, &m->win_counts))) fail(rc, ginsim_cuda_last_error());
   if ((rc = ginsim_cuda_window_register(comm, m->buf_combine, cbytes, &m->win_combine))) fail(rc, ginsim_cuda_last_error());
   m->proxy = c->cfg.backend == GIN_BACKEND_PROXY;
+  {
+    // Proxy backend, compact layout, 16-byte rows, one put per run: the
+    // pipelined transport (GINSIM_PROXY_PIPE=0 keeps the one-shot LSU staging
+    // kernels; GINSIM_PROXY_COALESCE=0 the reference's one put per message)
+    const char* pv = std::getenv("GINSIM_PROXY_PIPE");
+    const char* cv = std::getenv("GINSIM_PROXY_COALESCE");
+    m->pipe = m->proxy && cfg->layout == 1 && cfg->mode <= 1 && (2u * cfg->hidden) % 16u == 0 &&
+              !(pv && pv[0] == '0') && !(cv && cv[0] == '0');
+    if (m->pipe && e_local + 2 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
+      fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag and rows cell exceed the signal table");
+  }
   if (cfg->layout == 2) {
     // row staging: [src][j] rows of 2H bytes, then [src][j] 128-byte headers
     const uint64_t rbytes = n * T * (2ull * cfg->hidden + 128);
@@ -130,7 +144,9 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
     // registered windows the host agent copies from (the reference's staging
     // windows, harness_moe.cpp:122-130).  Separate windows, so a combine never
     // overwrites rows the agent may still be copying out for the dispatch.
-    const uint64_t sbytes = T * K * dmsg, cbytes2 = n * T * K * cmsg;
+    // (pipeline: the counts staged for the count puts follow the rows)
+    const uint64_t sbytes = T * K * dmsg + (m->pipe ? ((uint64_t)cfg->experts * 4 + 15) / 16 * 16 : 0);
+    const uint64_t cbytes2 = n * T * K * cmsg;
     if (ginsim_cuda_mem_alloc(comm, sbytes, &m->buf_stage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
     if ((rc = ginsim_cuda_window_register(comm, m->buf_stage, sbytes, &m->win_stage))) fail(rc, ginsim_cuda_last_error());
     if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_cstage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
@@ -140,6 +156,7 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
     if ((rc = ginsim_cuda_window_register(comm, m->buf_mirror, cbytes2, &m->win_mirror))) fail(rc, ginsim_cuda_last_error());
     DeviceGuard dgm(c->device);
     GIN_CUDA(cudaMalloc(&m->midx, (size_t)T * K * 4));
+    if (m->pipe) GIN_CUDA(cudaMalloc(&m->pipe_buf, ((size_t)T * K + kPipeCtrWords) * 4));
   }
   DeviceGuard g(c->device);
   GIN_CUDA(cudaMalloc(&m->ws, 256));
@@ -169,6 +186,7 @@ int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
     if (moe->ws) cudaFree(moe->ws);
     if (moe->route) cudaFree(moe->route);
     if (moe->midx) cudaFree(moe->midx);
+    if (moe->pipe_buf) cudaFree(moe->pipe_buf);
     if (moe->aux_g) cudaFree(moe->aux_g);
     if (moe->dst_g) cudaFree(moe->dst_g);
     if (moe->prof) cudaFree(moe->prof);
@@ -237,7 +255,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   const char* dy = std::getenv("GINSIM_MOE_SCHED");
   L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
   L.coop = moes[0]->coop ? 1u : 0u;
-  L.fuse_reduce = moes[0]->coop ? 0u : 1u;
+  L.fuse_reduce = (moes[0]->coop || moes[0]->pipe) ? 0u : 1u;
   L.mpay = cfg.mode >= 2 ? cfg.hidden + cfg.hidden / 32 : 2u * cfg.hidden;
   L.dmsg = (uint64_t)L.mpay + 16;
   L.cmsg = cfg.mode == 3 ? (uint64_t)cfg.hidden + cfg.hidden / 32 : 2ull * cfg.hidden;
@@ -250,6 +268,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
     L.r[i].dst_g = moes[i]->dst_g;
     L.r[i].midx = moes[i]->midx;
     L.r[i].aux_g = moes[i]->aux_g;
+    L.r[i].pipe = moes[i]->pipe_buf;
     L.r[i].prof = moes[i]->prof;
   }
   return L;
@@ -264,7 +283,8 @@ struct MoeKernels {
   const void* dispatch;
   const void* combine;   // cooperative: expert side (+ fused reduce when reduce == nullptr)
   const void* reduce;    // optional separate source-side reduction
-  int threads;           // of dispatch / combine
+  int threads;           // of dispatch
+  int cthreads;          // of combine
   bool tma_dispatch, tma_combine;
 };
 
@@ -279,16 +299,24 @@ static MoeKernels kernels_of(const ginsim_cuda_moe_t m) {
   const bool k8 = m->cfg.top_k <= 8;
   const uint32_t e = engine_of(m);
   MoeKernels k{};
+  if (m->pipe) {
+    k.dispatch = (const void*)moe_dispatch_pipe_kernel;
+    k.combine = (const void*)moe_combine_pipe_kernel;
+    k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8, false, true>
+                  : (const void*)moe_combine_reduce_kernel<32, false, true>;
+    k.threads = k.cthreads = kPipeThreads;
+    return k;
+  }
   if (e == 1 && m->proxy) {
     k.dispatch = k8 ? (const void*)moe_dispatch_kernel<8, true> : (const void*)moe_dispatch_kernel<32, true>;
     k.combine = (const void*)moe_combine_kernel<true>;
-    k.threads = kMoeThreads;
+    k.threads = k.cthreads = kMoeThreads;
     return k;
   }
   if (e == 1) {
     k.dispatch = k8 ? (const void*)moe_dispatch_kernel<8, false> : (const void*)moe_dispatch_kernel<32, false>;
     k.combine = (const void*)moe_combine_kernel<false>;
-    k.threads = kMoeThreads;
+    k.threads = k.cthreads = kMoeThreads;
     return k;
   }
   if (m->cfg.layout == 2)
@@ -299,12 +327,16 @@ static MoeKernels kernels_of(const ginsim_cuda_moe_t m) {
   k.tma_dispatch = true;
   if (e == 3) {
     k.combine = (const void*)moe_combine_kernel<false>;
+    k.cthreads = kMoeThreads;
   } else {
+    k.cthreads = kCmbThreads;
     k.combine = k8 ? (const void*)moe_combine_tma_kernel<8> : (const void*)moe_combine_tma_kernel<32>;
     if (m->cfg.mode == 3)
-      k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8, true> : (const void*)moe_combine_reduce_kernel<32, true>;
+      k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8, true, false>
+                    : (const void*)moe_combine_reduce_kernel<32, true, false>;
     else
-      k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8, false> : (const void*)moe_combine_reduce_kernel<32, false>;
+      k.reduce = k8 ? (const void*)moe_combine_reduce_kernel<8, false, false>
+                    : (const void*)moe_combine_reduce_kernel<32, false, false>;
     k.tma_combine = true;
   }
   return k;
@@ -333,7 +365,7 @@ static size_t combine_smem(const ginsim_cuda_moe_t m) {
                                       : (m->cfg.mode == 2 ? 128 + c / 2 + c / 64 + c : 128 + c);
   return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * sst;
 }
-static int combine_threads(const MoeKernels& k) { return k.tma_combine ? kCmbThreads : kMoeThreads; }
+static int combine_threads(const MoeKernels& k) { return k.cthreads; }
 
 static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   ginsim_cuda_moe_t m = moes[0];
@@ -394,7 +426,10 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   const int div = m->proxy ? 2 : 1;
   const uint32_t Gd = pick(std::max(1, cap_d / div)), Gc = pick(std::max(1, cap_c / div));
   uint32_t Gr = 0;
-  if (k.reduce) Gr = std::max<uint32_t>(1, (uint32_t)max_coresident_ctas(k.reduce, kMoeThreads, 0, m->comm->device) / n);
+  // (the reduce waits on the combine flag, which on the Proxy backend follows
+  // agent copies: emulated ranks' same-device copies need free SMs)
+  if (k.reduce)
+    Gr = std::max<uint32_t>(1, (uint32_t)max_coresident_ctas(k.reduce, kMoeThreads, 0, m->comm->device) / n / div);
   if (!use_tma(m) || !k.tma_combine) {
     // LSU combine: (message, part) work items sized to the warp count
     const uint32_t nvec = payload % 16u == 0 ? payload / 16u : 0u;
@@ -488,6 +523,11 @@ int ginsim_cuda_moe_phase_times(ginsim_cuda_moe_t moe, uint32_t kernel, uint64_t
   GIN_CUDA(cudaMemcpy(out, moe->prof + (uint64_t)kernel * 1024 * 8, 1024 * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   if (ctas) *ctas = kernel == 0 ? moe->G : (kernel == 1 ? moe->Gc : moe->Gr);
   GIN_API_END
+}
+
+int ginsim_cuda_moe_transport(ginsim_cuda_moe_t moe, uint32_t* kind) {
+  if (kind) *kind = moe->pipe ? 2u : (moe->proxy ? 1u : 0u);
+  return GINSIM_OK;
 }
 
 int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t* threads) {

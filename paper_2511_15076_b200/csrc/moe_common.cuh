@@ -17,6 +17,7 @@ struct MoeRankArgs {
   char** dst_g;               // TMA dispatch: [T][Kp] destination pointer of every (t, k) pair
   uint32_t* midx;             // proxy: [T][K] index of (t, k)'s result in the combine mirror window
   uint64_t* aux_g;            // layout 2: [2][T][Kp] row-header address and (slot, e_loc) per pair
+  uint32_t* pipe;             // proxy pipeline: [T*K] staging position -> pair, then chunk counters
   const uint16_t* x;          // [T][H]
   const int32_t* idx;         // [T][K]
   const void* weights;        // [T][K] u16 (mode 0) / f32 (mode 1)
@@ -179,6 +180,15 @@ __device__ __forceinline__ bool arrive_last(unsigned int* ctr, unsigned int targ
 // fences (one MEMBAR per warp instruction) and adds (1<<32)+count to their
 // cells with relaxed reductions -- a release pattern per lane, one .sys fence
 // per destination instead of one per expert.
+// Count window: cnt[src][e_loc] u32 (source-major, so one source's counts
+// for a destination's experts are one contiguous run -- a single put on the
+// Proxy backend), then the dedup row counts [src] at e_local*n.  Kernels scan
+// (e_loc, src) pairs in e_loc-major order (harness_moe.cpp:174-179): pair i
+// = e_loc*n + src lives at count_index(i).
+__device__ __forceinline__ uint32_t count_index(uint32_t i, uint32_t n, uint32_t e_local) {
+  return (i % n) * e_local + i / n;
+}
+
 __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDevCommView* v, uint32_t win_counts,
                                                 const uint32_t* hist, uint32_t n, uint32_t rank, uint32_t e_local) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -188,7 +198,7 @@ __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDe
     // one fence between them releases both the puts (by cumulativity) and
     // the counts; for own experts the acquirer is on this GPU (GPU scope)
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
-      gin::st_relaxed_sys32(cb + (uint64_t)e_loc * n + rank, hist[d * e_local + e_loc]);
+      gin::st_relaxed_sys32(cb + (uint64_t)rank * e_local + e_loc, hist[d * e_local + e_loc]);
     if (d == rank) gin::fence_acq_rel_gpu(); else gin::fence_acq_rel_sys();
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_loc), (1ull << 32) + hist[d * e_local + e_loc]);

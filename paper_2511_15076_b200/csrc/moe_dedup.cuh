@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     for (uint32_t d = warp; d < n; d += kTmaWarps) {
       uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[L.win_counts].base[d]);
       for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
-        gin::st_relaxed_sys32(cb + (uint64_t)e_loc * n + rank, hist_all[d * e_local + e_loc]);
+        gin::st_relaxed_sys32(cb + (uint64_t)rank * e_local + e_loc, hist_all[d * e_local + e_loc]);
       if (lane == 0) gin::st_relaxed_sys32(cb + (uint64_t)e_local * n + rank, hist_all[E + d]);
       if (d == rank) {
         gin::fence_acq_rel_gpu();
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   gin::tma::fence_proxy_async_global();  // rows/headers written by peers -> read by this CTA's bulk loads
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
   const uint32_t P = e_local * n;
-  for (uint32_t i = tid; i < P; i += kTmaThreads) cntv[i] = gin::ld_acquire_sys32(counts + i);
+  for (uint32_t i = tid; i < P; i += kTmaThreads) cntv[i] = gin::ld_acquire_sys32(counts + count_index(i, n, e_local));
   if (tid <= n) rcnt[tid] = 0;
   __syncthreads();
   if (tid < n) rcnt[tid] = tid == rank ? 0u : gin::ld_acquire_sys32(counts + P + tid);

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
     auto ctx_of = [&](uint32_t e) { return L.coalesce ? (e / e_local) % v->n_ctx : e % v->n_ctx; };
     for (uint32_t e = tid; e < E; e += kMoeThreads) {
       const uint32_t dst = e / e_local, e_loc = e % e_local;
-      gin::Gin(v, ctx_of(e)).put_value(me, world, dst, L.win_counts, ((uint64_t)e_loc * n + rank) * 4, hist_all[e]);
+      gin::Gin(v, ctx_of(e)).put_value(me, world, dst, L.win_counts, ((uint64_t)rank * e_local + e_loc) * 4, hist_all[e]);
     }
     __syncthreads();
     if (L.coalesce && L.layout != 0) {
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
   const uint32_t P = e_local * n;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
   for (uint32_t i = tid; i < P; i += kMoeThreads) {
-    const uint32_t c = gin::ld_acquire_sys32(counts + i);
+    const uint32_t c = gin::ld_acquire_sys32(counts + count_index(i, n, e_local));
     cnt[i] = c;
     pair_start[i] = c;
   }

@@ -21,6 +21,67 @@ __device__ __forceinline__ void rank_grid_barrier(unsigned int* ctr, unsigned in
   __syncthreads();
 }
 
+// Cooperative route tables (Phase A of the TMA dispatch kernels): CTA b
+// histograms its own pairs [t0*K, t0*K + nq) into smem (own[] keeps their
+// experts) and a global row hist[b][E]; after a grid barrier warp w of CTA b
+// scans expert e = b + w*G down the G rows (exclusive prefix = the slots
+// taken by earlier CTAs, total = the expert's count); after a second barrier
+// the CTA loads its prefix row into run[] and the totals into hist_all[].
+template <int THREADS>
+__device__ __forceinline__ void coop_route_tables(const MoeRankArgs& R, uint32_t E, uint32_t K, uint32_t t0,
+                                                  uint32_t nq, uint32_t* own, uint32_t* hist_all, uint32_t* run,
+                                                  unsigned int* bar0, unsigned int* bar1, unsigned int bar_target) {
+  constexpr int WARPS = THREADS / 32;
+  const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* g_hist = R.route;                                  // [G][E]
+  uint32_t* g_pre = R.route + (size_t)kMaxGrid * kMaxExperts;  // [G][E]
+  uint32_t* g_tot = R.route + 2 * (size_t)kMaxGrid * kMaxExperts;  // [E]
+  // A0: own routes -> smem + own histogram -> global row
+  for (uint32_t q = tid; q < nq; q += THREADS) {
+    const uint32_t e = (uint32_t)__ldg(R.idx + (uint64_t)t0 * K + q);
+    own[q] = e;
+    atomicAdd(&hist_all[e], 1u);
+  }
+  __syncthreads();
+  for (uint32_t e = tid; e < E; e += THREADS) g_hist[(size_t)b * E + e] = hist_all[e];
+  MOE_STAMP(R, 0, 1);
+  rank_grid_barrier(bar0, bar_target);
+  // A1: column scans, one warp per expert e = b + w*G
+  for (uint32_t e = b + warp * G; e < E; e += WARPS * G) {
+    uint32_t carry = 0;
+    auto scan_chunk = [&](uint32_t c0, uint32_t x) {
+      uint32_t incl = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      if (c0 + lane < G) g_pre[(size_t)(c0 + lane) * E + e] = carry + incl - x;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    };
+    uint32_t pre[8];  // the first 256 rows' loads in flight together
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t bb = c * 32 + lane;
+      pre[c] = bb < G ? __ldcg(g_hist + (size_t)bb * E + e) : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if ((uint32_t)c * 32 < G) scan_chunk(c * 32, pre[c]);
+    for (uint32_t c0 = 256; c0 < G; c0 += 32)
+      scan_chunk(c0, c0 + lane < G ? __ldcg(g_hist + (size_t)(c0 + lane) * E + e) : 0u);
+    if (lane == 0) g_tot[e] = carry;
+  }
+  MOE_STAMP(R, 0, 2);
+  rank_grid_barrier(bar1, bar_target);
+  // A2: this CTA's prefix row and the totals; reference slot numbers
+  for (uint32_t e = tid; e < E; e += THREADS) {
+    run[e] = __ldcg(g_pre + (size_t)b * E + e);
+    hist_all[e] = __ldcg(g_tot + e);
+  }
+  __syncthreads();
+}
+
 // Dispatch over the TMA engine.
 //  Phase A (route tables, cooperative): CTA b histograms only its own token
 //    range into a global row hist[b][E]; after a grid barrier, warp w of CTA
@@ -73,9 +134,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kDispStages * sstride;
   uint32_t* own = reinterpret_cast<uint32_t*>(dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) +
                                               (size_t)kTmaWarps * kDispStages * sstride);  // [(t1-t0)*K]
-  uint32_t* g_hist = R.route;                                  // [G][E]
-  uint32_t* g_pre = R.route + (size_t)kMaxGrid * kMaxExperts;  // [G][E]
-  uint32_t* g_tot = R.route + 2 * (size_t)kMaxGrid * kMaxExperts;  // [E]
   char** dst_g = R.dst_g;                                      // [T][Kp]
 
   for (uint32_t e = tid; e < E; e += kTmaThreads) {
@@ -143,51 +201,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     histogram_pass<kTmaThreads>(R.idx, T * K, t0 * K, nq, hist_all, run, own);
     __syncthreads();
   } else {
-  // A0: own routes -> smem + own histogram -> global row
-  for (uint32_t q = tid; q < nq; q += kTmaThreads) {
-    const uint32_t e = (uint32_t)__ldg(R.idx + (uint64_t)t0 * K + q);
-    own[q] = e;
-    atomicAdd(&hist_all[e], 1u);
+    coop_route_tables<kTmaThreads>(R, E, K, t0, nq, own, hist_all, run, R.ws + 3, R.ws + 4, bar_target);
   }
-  __syncthreads();
-  for (uint32_t e = tid; e < E; e += kTmaThreads) g_hist[(size_t)b * E + e] = hist_all[e];
-  MOE_STAMP(R, 0, 1);
-  rank_grid_barrier(R.ws + 3, bar_target);
-  // A1: column scans, one warp per expert e = b + w*G
-  for (uint32_t e = b + warp * G; e < E; e += kTmaWarps * G) {
-    uint32_t carry = 0;
-    auto scan_chunk = [&](uint32_t c0, uint32_t x) {
-      uint32_t incl = x;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-      }
-      if (c0 + lane < G) g_pre[(size_t)(c0 + lane) * E + e] = carry + incl - x;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    };
-    uint32_t pre[8];  // the first 256 rows' loads in flight together
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t bb = c * 32 + lane;
-      pre[c] = bb < G ? __ldcg(g_hist + (size_t)bb * E + e) : 0u;
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if ((uint32_t)c * 32 < G) scan_chunk(c * 32, pre[c]);
-    for (uint32_t c0 = 256; c0 < G; c0 += 32)
-      scan_chunk(c0, c0 + lane < G ? __ldcg(g_hist + (size_t)(c0 + lane) * E + e) : 0u);
-    if (lane == 0) g_tot[e] = carry;
-  }
-  MOE_STAMP(R, 0, 2);
-  rank_grid_barrier(R.ws + 4, bar_target);
-  // A2: this CTA's prefix row and the totals; reference slot numbers
-  for (uint32_t e = tid; e < E; e += kTmaThreads) {
-    run[e] = __ldcg(g_pre + (size_t)b * E + e);
-    hist_all[e] = __ldcg(g_tot + e);
-  }
-  __syncthreads();
-  }  // coop
   if (L.layout != 0) {  // per-destination exclusive prefix of the expert totals, one warp per destination
     for (uint32_t d = warp; d < n; d += kTmaWarps) {
       uint32_t carry = 0;
@@ -348,7 +363,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   const uint32_t P = e_local * n;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
   for (uint32_t i = tid; i < P; i += kTmaThreads) {
-    const uint32_t c = gin::ld_acquire_sys32(counts + i);
+    const uint32_t c = gin::ld_acquire_sys32(counts + count_index(i, n, e_local));
     cnt[i] = c;
     pair_start[i] = c;
   }
@@ -577,8 +592,11 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
 // buffers): acquire the combine flag (>= T*K per iteration, harness_moe.cpp:
 // 227) then the top-k weighted reduction, two 16-byte vectors per thread with
 // all 2K loads in flight before any use.  No CTA waits on another CTA of
-// this launch, so it needs no co-residency.
-template <int KMAX, bool FP8C>
+// this launch, so it needs no co-residency.  MIRROR (Proxy pipeline): the
+// results arrived in the mirror window in send order; y is gathered through
+// the dispatch's (t, k) -> mirror index and also written to (t*K+k)*cmsg, so
+// the combine window ends as the reference's (harness_moe.cpp:203-205).
+template <int KMAX, bool FP8C, bool MIRROR>
 __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
   const GinDevCommView* v = R.view;
@@ -604,9 +622,19 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
       continue;
     }
     uint4 y[KMAX];
+    if (MIRROR) {
+      const char* mirror = v->win[L.win_mirror].base[rank];
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-      if (k < (int)K) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+      for (int k = 0; k < KMAX; ++k)
+        if (k < (int)K) y[k] = gin::ld_nc_v4(mirror + (uint64_t)__ldg(R.midx + (uint64_t)t * K + k) * cmsg + 16ull * i);
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < (int)K) gin::st_v4(const_cast<char*>(crecv) + ((uint64_t)t * K + k) * cmsg + 16ull * i, y[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < (int)K) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+    }
     gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
                reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
   }

@@ -9,7 +9,14 @@
 //     (proxy_backend.hpp:67-68, cpp:64-113), decode (descriptor.cpp), and post
 //     through the plugin's iput / iput_signal analogue: cudaMemcpyAsync for
 //     the payload (peer VMM mapping, copy engine) followed, in stream order,
-//     by cuStreamWriteValue64 stores for the signal and counter cells.
+//     by cuStreamWriteValue64 stores for the signal and counter cells.  Up to
+//     4 CUDA streams, context c on stream c % streams (the reference's
+//     per-context channel): ops of a context are ordered, contexts progress
+//     independently, so copies toward different peers overlap each other's
+//     per-op overheads.  Ranks emulated on one device share the device's
+//     hardware queues (CUDA_DEVICE_MAX_CONNECTIONS, default 8): a stream
+//     aliased onto the queue of a spinning MoE kernel would stall the agent
+//     behind it, so each of their agents keeps a single stream.
 //
 // Signals without SM atomics: rank d's cell id is the sum over sources s of a
 // sub-cell [s][id] that only s writes (gin_types.h).  The agent is the single
@@ -22,6 +29,7 @@
 #include <sched.h>
 #include <time.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 
@@ -41,7 +49,7 @@ struct ProxyAgent {
   std::vector<GinRingSlot*> slots;       // pinned host, device-mapped
   uint64_t* consumed_host = nullptr;     // pinned host, device-mapped: [ctx] tickets consumed
   std::vector<uint64_t> tail;            // next ticket to consume per ctx
-  cudaStream_t stream = nullptr;
+  std::vector<cudaStream_t> streams;     // context c -> streams[c % size]
   std::thread th;
   std::atomic<bool> stop{false};
 
@@ -56,7 +64,7 @@ struct ProxyAgent {
 
   // completion tracking: one event per pass with work
   struct Pass {
-    cudaEvent_t ev;
+    std::vector<cudaEvent_t> evs;        // one per context stream with work
     std::vector<uint64_t> host_done;     // per ctx host tickets complete after this pass
     std::vector<uint32_t> counters;      // counter ids completed by this pass
     uint32_t stage_end;
@@ -97,37 +105,46 @@ struct ProxyAgent {
   // gathered and issued with one cuStreamBatchMemOp per run of consecutive
   // memops; a copy in between flushes them first, so stream order == the
   // ring's ticket order (the watermark rule, fabric.cpp:63-79).
-  std::vector<CUstreamBatchMemOpParams> memops;
+  // (A memop costs ~1.2-1.4 us of stream time on B200 even batched,
+  // tools/host_op_probe.py, so workloads should need few of them.)
+  std::vector<std::vector<CUstreamBatchMemOpParams>> memops;  // per ctx
+  std::vector<uint8_t> touched;                               // ctx used in this pass
   static constexpr size_t kMaxBatch = 128;
 
-  void flush_memops() {
-    if (memops.empty()) return;
-    GIN_CU(cuapi().cuStreamBatchMemOp((CUstream)stream, (unsigned)memops.size(), memops.data(), 0));
-    memops.clear();
+  cudaStream_t stream_of(uint32_t ctx) const { return streams[ctx % streams.size()]; }
+  void flush_memops(uint32_t ctx) {
+    auto& m = memops[ctx];
+    if (m.empty()) return;
+    GIN_CU(cuapi().cuStreamBatchMemOp((CUstream)stream_of(ctx), (unsigned)m.size(), m.data(), 0));
+    m.clear();
   }
-  void write64(uint64_t* dev_addr, uint64_t v) {
+  void write64(uint32_t ctx, uint64_t* dev_addr, uint64_t v) {
     CUstreamBatchMemOpParams op{};
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
     op.writeValue.address = (CUdeviceptr)dev_addr;
     op.writeValue.value64 = v;
     op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
-    memops.push_back(op);
-    if (memops.size() >= kMaxBatch) flush_memops();
+    memops[ctx].push_back(op);
+    touched[ctx] = 1;
+    if (memops[ctx].size() >= kMaxBatch) flush_memops(ctx);
   }
-  void write32(void* dev_addr, uint32_t v) {
+  void write32(uint32_t ctx, void* dev_addr, uint32_t v) {
     CUstreamBatchMemOpParams op{};
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
     op.writeValue.address = (CUdeviceptr)dev_addr;
     op.writeValue.value = v;
     op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
-    memops.push_back(op);
-    if (memops.size() >= kMaxBatch) flush_memops();
+    memops[ctx].push_back(op);
+    touched[ctx] = 1;
+    if (memops[ctx].size() >= kMaxBatch) flush_memops(ctx);
   }
 
   // iput / iput_signal (plugin.hpp:86-90) for one decoded descriptor.
   void post(uint32_t ctx, const ginsim_cuda_descriptor& d, Pass& pass) {
     const GinDevCommView& v = c->host_view;
     const uint32_t peer = d.peer;  // team 0 = world: team-relative == world rank
+    cudaStream_t stream = stream_of(ctx);
+    touched[ctx] = 1;
     if (peer >= v.world) fail(GINSIM_E_INVALID_PEER, "proxy: descriptor peer out of range");
     if (d.opcode != GIN_OP_SIGNAL_ONLY && d.bytes > 0) {
       if (d.dst_window >= v.n_windows) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown destination window");
@@ -140,17 +157,17 @@ struct ProxyAgent {
         const GinWindowView& sw = v.win[d.src_window];
         if (d.src_offset_or_value > sw.size[v.rank] || d.bytes > sw.size[v.rank] - d.src_offset_or_value)
           fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: source range exceeds capacity");
-        flush_memops();
+        flush_memops(ctx);
         GIN_CUDA(cudaMemcpyAsync(dst, sw.base[v.rank] + d.src_offset_or_value, d.bytes, cudaMemcpyDefault, stream));
         n_copies.fetch_add(1, std::memory_order_relaxed);
       } else if (d.bytes == 4 && ((uintptr_t)dst & 3) == 0) {  // aligned inline values: a memop, no copy
-        write32(dst, (uint32_t)d.src_offset_or_value);
+        write32(ctx, dst, (uint32_t)d.src_offset_or_value);
       } else if (d.bytes == 8 && ((uintptr_t)dst & 7) == 0) {
-        write64(reinterpret_cast<uint64_t*>(dst), d.src_offset_or_value);
+        write64(ctx, reinterpret_cast<uint64_t*>(dst), d.src_offset_or_value);
       } else {
         uint64_t* s = stage + (stage_next++ % kStage);
         *s = d.src_offset_or_value;
-        flush_memops();
+        flush_memops(ctx);
         GIN_CUDA(cudaMemcpyAsync(dst, s, d.bytes, cudaMemcpyHostToDevice, stream));
         n_copies.fetch_add(1, std::memory_order_relaxed);
       }
@@ -159,29 +176,31 @@ struct ProxyAgent {
       if (d.signal_id >= v.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "proxy: signal out of range");
       uint64_t& val = sig_value[(size_t)peer * v.signal_cells + d.signal_id];
       val += (d.flags & GIN_FLAG_SIGNAL_IS_ADD) ? d.signal_operand : 1ull;
-      write64(v.signals[peer] + (uint64_t)v.rank * v.signal_cells + d.signal_id, val);
+      write64(ctx, v.signals[peer] + (uint64_t)v.rank * v.signal_cells + d.signal_id, val);
     }
     if (d.flags & GIN_FLAG_HAS_COUNTER) {
       if (d.counter_id >= v.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "proxy: counter out of range");
       ctr_value[d.counter_id] += 1;
-      write64(v.counters + d.counter_id, ctr_value[d.counter_id]);
+      write64(ctx, v.counters + d.counter_id, ctr_value[d.counter_id]);
       pass.counters.push_back(d.counter_id);
     }
-    (void)ctx;
   }
 
   void retire_completed(bool block) {
     while (!inflight.empty()) {
       Pass& p = inflight.front();
-      cudaError_t q = block ? cudaEventSynchronize(p.ev) : cudaEventQuery(p.ev);
-      if (q == cudaErrorNotReady) return;
-      GIN_CUDA(q);
+      while (!p.evs.empty()) {
+        cudaError_t q = block ? cudaEventSynchronize(p.evs.back()) : cudaEventQuery(p.evs.back());
+        if (q == cudaErrorNotReady) return;
+        GIN_CUDA(q);
+        free_events.push_back(p.evs.back());
+        p.evs.pop_back();
+      }
       for (uint32_t i = 0; i < n_ctx; ++i) {
         if (p.host_done[i] > host_completed[i].load(std::memory_order_relaxed))
           host_completed[i].store(p.host_done[i], std::memory_order_release);
       }
       for (uint32_t id : p.counters) counter_pending[id].fetch_sub(1, std::memory_order_acq_rel);
-      free_events.push_back(p.ev);
       inflight.pop_front();
     }
   }
@@ -232,11 +251,14 @@ struct ProxyAgent {
         if (!pass.host_done[ctx]) pass.host_done[ctx] = host_taken[ctx];
         // device-visible flush word: every ticket consumed so far is complete
         // once the copies above have completed (stream order).
-        if (any_dev && consumed[ctx]) write64(c->host_view.proxy.completed + ctx, consumed[ctx]);
+        if (any_dev && consumed[ctx]) write64(ctx, c->host_view.proxy.completed + ctx, consumed[ctx]);
+        if (!touched[ctx]) continue;
+        flush_memops(ctx);
+        cudaEvent_t ev = get_event();
+        GIN_CUDA(cudaEventRecord(ev, stream_of(ctx)));
+        pass.evs.push_back(ev);
+        touched[ctx] = 0;
       }
-      flush_memops();
-      pass.ev = get_event();
-      GIN_CUDA(cudaEventRecord(pass.ev, stream));
       pass.stage_end = stage_next;
       inflight.push_back(std::move(pass));
       n_desc.fetch_add(work, std::memory_order_relaxed);
@@ -286,7 +308,17 @@ ProxyPtr proxy_start(Comm* c) {
   p->n_ctx = c->cfg.n_contexts;
   p->cap = c->cfg.queue_depth;
   DeviceGuard g(c->device);
-  GIN_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  p->streams.assign(c->shares_device ? 1u : std::min<uint32_t>(p->n_ctx, 4u), nullptr);
+  for (auto& st : p->streams) GIN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  p->memops.assign(p->n_ctx, {});
+  p->touched.assign(p->n_ctx, 0);
+  // events are created up front: the agent must never call into the runtime
+  // for anything but issuing work once kernels that wait on it are running
+  for (int i = 0; i < 256; ++i) {
+    cudaEvent_t e;
+    GIN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->free_events.push_back(e);
+  }
   p->slots.resize(p->n_ctx);
   p->tail.assign(p->n_ctx, 0);
   p->host_submitted.assign(p->n_ctx, 0);
@@ -330,13 +362,14 @@ void proxy_stop(ProxyPtr& p) {
   p->stop.store(true, std::memory_order_release);
   if (p->th.joinable()) p->th.join();
   DeviceGuard g(p->c->device);
-  cudaStreamSynchronize(p->stream);
-  for (auto& f : p->inflight) cudaEventDestroy(f.ev);
+  for (auto st : p->streams) cudaStreamSynchronize(st);
+  for (auto& f : p->inflight)
+    for (auto e : f.evs) cudaEventDestroy(e);
   for (auto e : p->free_events) cudaEventDestroy(e);
   for (auto s : p->slots) cudaFreeHost(s);
   if (p->consumed_host) cudaFreeHost(p->consumed_host);
   if (p->stage) cudaFreeHost(p->stage);
-  cudaStreamDestroy(p->stream);
+  for (auto st : p->streams) cudaStreamDestroy(st);
   p.reset();
 }
 

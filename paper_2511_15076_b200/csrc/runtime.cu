@@ -533,6 +533,7 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
   for (uint32_t r = 0; r < world; ++r) {
     v.signals[r] = r == rank ? reinterpret_cast<uint64_t*>(c->signal_alloc.ptr)
                              : reinterpret_cast<uint64_t*>(c->map_blob(blobs[r]));
+    if (r != rank && blobs[r].pid == mine.pid && blobs[r].device == device) c->shares_device = true;
   }
   GIN_CUDA(cudaMalloc(&c->dev_view, sizeof(GinDevCommView)));
   GIN_CUDA(cudaStreamCreateWithFlags(&c->op_stream, cudaStreamNonBlocking));

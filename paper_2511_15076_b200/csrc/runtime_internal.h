@@ -147,6 +147,7 @@ struct Comm {
   } nvls;
 
   cudaStream_t op_stream = nullptr;           // host-issued ops / cell reads
+  bool shares_device = false;                 // another rank of this comm runs on this device in this process
   uint64_t op_counter[8] = {};                // per-workload launch/round counters (host side)
   ProxyPtr proxy;
 

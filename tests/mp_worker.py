@@ -1,6 +1,10 @@
 """One rank of a multi-process (torchrun) parity run: real GPUs, one process
 per GPU, NVLink peer mappings imported through POSIX-FD handles.
 Launched by tests/test_gpu_multi.py; prints one JSON line per rank."""
+import os as _os
+# every stream its own hardware queue: a proxy-agent stream aliased onto the queue of
+# a kernel that waits for the agent would stall behind it (csrc/proxy.cu)
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import json
 import os
 import sys
