@@ -177,6 +177,11 @@ int ginsim_cuda_snapshot_cells(ginsim_cuda_comm_t comm, uint64_t* signals, uint6
  * clear != 0 resets it. */
 int ginsim_cuda_device_error(ginsim_cuda_comm_t comm, uint32_t* code, int clear);
 /* Proxy agent statistics: descriptors consumed, memcpy calls issued. */
+/* Diagnostics (GINSIM_PROXY_TRACE=1 at comm creation): per agent copy
+ * {bytes, ctx, host issue us, device start us, device duration us} since the
+ * first traced copy, 5 doubles per record; clears the trace. */
+int ginsim_cuda_proxy_trace(ginsim_cuda_comm_t comm, double* out, uint32_t max_records, uint32_t* n_out);
+
 int ginsim_cuda_proxy_stats(ginsim_cuda_comm_t comm, uint64_t* descriptors, uint64_t* copies,
                             uint64_t* busy_ns, uint64_t* wall_ns);
 

@@ -193,6 +193,7 @@ def _declare(L):
         "ginsim_cuda_snapshot_cells": ([P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
         "ginsim_cuda_device_error": ([P, POINTER(c_uint32), c_int], c_int),
         "ginsim_cuda_proxy_stats": ([P, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64)], c_int),
+        "ginsim_cuda_proxy_trace": ([P, POINTER(ctypes.c_double), c_uint32, POINTER(c_uint32)], c_int),
         "ginsim_cuda_descriptor_encode": ([POINTER(Descriptor), POINTER(c_uint8)], c_int),
         "ginsim_cuda_descriptor_decode": ([POINTER(c_uint8), POINTER(Descriptor)], c_int),
         "ginsim_cuda_pingpong": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32,
@@ -402,6 +403,14 @@ class Comm:
         v = c_int()
         check(lib().ginsim_cuda_nvls_enabled(self.h, byref(v)))
         return bool(v.value)
+
+    def proxy_trace(self, max_records=4096):
+        """[(bytes, ctx, host_issue_us, dev_start_us, dev_us)] of the agent's copies
+        since the last call (GINSIM_PROXY_TRACE=1 at creation)."""
+        buf = (ctypes.c_double * (5 * max_records))()
+        n = c_uint32()
+        check(lib().ginsim_cuda_proxy_trace(self.h, buf, max_records, byref(n)))
+        return [tuple(buf[5 * i:5 * i + 5]) for i in range(n.value)]
 
     def proxy_stats(self):
         a, b, c, d = c_uint64(), c_uint64(), c_uint64(), c_uint64()

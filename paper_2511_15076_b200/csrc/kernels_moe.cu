@@ -255,6 +255,11 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   const char* dy = std::getenv("GINSIM_MOE_SCHED");
   L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
   L.coop = moes[0]->coop ? 1u : 0u;
+  const char* sc = std::getenv("GINSIM_PIPE_STAGE_CTAS");
+  // own-expert rows are a plain HBM copy; on 48 CTAs it keeps pace with the
+  // copy engines without starving them of HBM (tools/proxy_phases.py, N=2:
+  // dispatch 412 us vs 439 us on every CTA)
+  L.stage_ctas = sc ? (uint32_t)std::strtoul(sc, nullptr, 10) : 48u;
   L.fuse_reduce = (moes[0]->coop || moes[0]->pipe) ? 0u : 1u;
   L.mpay = cfg.mode >= 2 ? cfg.hidden + cfg.hidden / 32 : 2u * cfg.hidden;
   L.dmsg = (uint64_t)L.mpay + 16;

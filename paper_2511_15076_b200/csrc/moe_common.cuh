@@ -48,6 +48,7 @@ struct MoeLaunch {
   uint64_t cmsg;                 // combine message bytes (2H; fp8 combine, mode 3: H + H/32)
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
+  uint32_t stage_ctas;           // Proxy pipeline: CTAs that stage (the rest leave the copy engines the HBM)
 };
 
 // ------------------------------------------------------------------ helpers

@@ -124,14 +124,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
   extern __shared__ uint32_t own[];  // [(t1-t0)*K] experts of this CTA's pairs
   uint32_t* inv = R.pipe;
   uint32_t* ctr = R.pipe + TK;
-  unsigned long long* grab = reinterpret_cast<unsigned long long*>(R.ws + 24);
+  unsigned long long* grab = reinterpret_cast<unsigned long long*>(R.ws + 32);  // [2]
   char* stg = v->win[L.win_stage].base[rank];
   const uint64_t cnt_off = TK * dmsg;  // staged counts [E] after the rows
 
   if (tid == 0) pipe_flush_all(v);
   if (b == 0) {  // published to the grid by the route-table barriers
     for (uint32_t i = tid; i < kPipeCombineCtr; i += kPipeThreads) ctr[i] = 0;
-    if (tid == 0) *grab = 0;
+    if (tid == 0) grab[0] = grab[1] = 0;
   }
   for (uint32_t e = tid; e < E; e += kPipeThreads) {
     hist_all[e] = 0;
@@ -217,10 +217,18 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
   // Phase B: messages in staging order, one warp each, from a grab counter
   const char* x = reinterpret_cast<const char*>(R.x);
   char* own_win = v->win[L.win_dispatch].base[rank] + (uint64_t)rank * TK * dmsg;
-  while (true) {
+  // remote messages on every CTA; own ones (a plain HBM copy that would only
+  // compete with the copy engines for HBM) on the first L.stage_ctas
+  const uint32_t remote_end = pbase[n - 1];
+  for (bool own_phase = false;;) {
     uint32_t m = 0;
-    if (lane == 0) m = (uint32_t)atomicAdd(grab, 1ull);
+    if (lane == 0) m = (uint32_t)atomicAdd(grab + (own_phase ? 1 : 0), 1ull) + (own_phase ? remote_end : 0u);
     m = __shfl_sync(0xffffffffu, m, 0);
+    if (!own_phase && m >= remote_end) {
+      if (b >= L.stage_ctas) break;
+      own_phase = true;
+      continue;
+    }
     if (m >= (uint32_t)TK) break;
     uint32_t j = 0;
     while (m >= pbase[j + 1]) ++j;
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLa
   __shared__ uint32_t pbase[GIN_MAX_RANKS + 1], pch[GIN_MAX_RANKS];
   __shared__ int is_last;
   uint32_t* ctr = R.pipe + TK + kPipeCombineCtr;
-  unsigned long long* grab = reinterpret_cast<unsigned long long*>(R.ws + 28);
+  unsigned long long* grab = reinterpret_cast<unsigned long long*>(R.ws + 36);  // [2]
 
   if (tid == 0) pipe_flush_all(v);
   if (b == 0) {
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLa
     // signalled it once this step, and none signals it again before this
     // rank's combine results reach it
     if (tid == 0) {
-      *grab = 0;
+      grab[0] = grab[1] = 0;
       if (!L.no_wait) gin::Gin(v, 0).reset_signal(e_local + 1);
     }
   }
@@ -312,11 +320,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLa
   const char* recv = v->win[L.win_dispatch].base[rank];
   char* cst = v->win[L.win_cstage].base[rank];
   char* own_mirror = v->win[L.win_mirror].base[rank] + (uint64_t)rank * TK * cmsg;
-  const uint32_t total = pbase[n];
-  while (true) {
+  const uint32_t total = pbase[n], remote_end = pbase[n - 1];
+  for (bool own_phase = false;;) {
     uint32_t m = 0;
-    if (lane == 0) m = (uint32_t)atomicAdd(grab, 1ull);
+    if (lane == 0) m = (uint32_t)atomicAdd(grab + (own_phase ? 1 : 0), 1ull) + (own_phase ? remote_end : 0u);
     m = __shfl_sync(0xffffffffu, m, 0);
+    if (!own_phase && m >= remote_end) {
+      if (b >= L.stage_ctas) break;
+      own_phase = true;
+      continue;
+    }
     if (m >= total) break;
     uint32_t j = 0;
     while (m >= pbase[j + 1]) ++j;

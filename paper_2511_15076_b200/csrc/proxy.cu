@@ -81,6 +81,16 @@ struct ProxyAgent {
   std::vector<std::atomic<uint32_t>> counter_pending;
 
   std::atomic<uint64_t> n_desc{0}, n_copies{0}, busy_ns{0};
+
+  // GINSIM_PROXY_TRACE=1: timing events around every copy (diagnostics)
+  struct CopyTrace {
+    uint64_t bytes, issue_ns;
+    uint32_t ctx;
+    cudaEvent_t e0, e1;
+  };
+  bool trace = false;
+  std::mutex trace_mu;
+  std::vector<CopyTrace> traces;
   uint64_t t_start = 0;
   std::string failure;
   std::atomic<bool> failed{false};
@@ -158,7 +168,19 @@ struct ProxyAgent {
         if (d.src_offset_or_value > sw.size[v.rank] || d.bytes > sw.size[v.rank] - d.src_offset_or_value)
           fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: source range exceeds capacity");
         flush_memops(ctx);
+        CopyTrace tr{};
+        if (trace) {
+          tr = CopyTrace{d.bytes, now_ns(), ctx, nullptr, nullptr};
+          GIN_CUDA(cudaEventCreate(&tr.e0));
+          GIN_CUDA(cudaEventCreate(&tr.e1));
+          GIN_CUDA(cudaEventRecord(tr.e0, stream));
+        }
         GIN_CUDA(cudaMemcpyAsync(dst, sw.base[v.rank] + d.src_offset_or_value, d.bytes, cudaMemcpyDefault, stream));
+        if (trace) {
+          GIN_CUDA(cudaEventRecord(tr.e1, stream));
+          std::lock_guard<std::mutex> lk(trace_mu);
+          if (traces.size() < 65536) traces.push_back(tr);
+        }
         n_copies.fetch_add(1, std::memory_order_relaxed);
       } else if (d.bytes == 4 && ((uintptr_t)dst & 3) == 0) {  // aligned inline values: a memop, no copy
         write32(ctx, dst, (uint32_t)d.src_offset_or_value);
@@ -349,6 +371,8 @@ ProxyPtr proxy_start(Comm* c) {
   GIN_CUDA(cudaHostAlloc(&st, sizeof(uint64_t) * ProxyAgent::kStage, cudaHostAllocPortable));
   p->stage = static_cast<uint64_t*>(st);
   p->sig_value.assign((size_t)c->world * c->cfg.signal_cells, 0);
+  const char* tv = std::getenv("GINSIM_PROXY_TRACE");
+  p->trace = tv && tv[0] == '1';
   p->ctr_value.assign(c->cfg.counter_cells, 0);
   ProxyAgent* raw = p.get();
   p->th = std::thread([raw] { raw->main(); });
@@ -403,6 +427,33 @@ void proxy_host_flush(Comm* c, uint32_t ctx) {
 
 bool proxy_counter_pending(Comm* c, uint32_t id) {
   return c->proxy && c->proxy->counter_pending[id].load(std::memory_order_acquire) != 0;
+}
+
+// Copy trace (GINSIM_PROXY_TRACE=1): per copy {bytes, ctx, host issue ns,
+// device start us, device duration us} relative to the first traced copy;
+// returns the number of records written (the trace is then cleared).
+uint32_t proxy_trace(Comm* c, double* out, uint32_t max_records) {
+  ProxyAgent* p = c->proxy.get();
+  std::lock_guard<std::mutex> lk(p->trace_mu);
+  const uint32_t nrec = std::min<uint32_t>(max_records, (uint32_t)p->traces.size());
+  for (uint32_t i = 0; i < nrec; ++i) {
+    auto& t = p->traces[i];
+    GIN_CUDA(cudaEventSynchronize(t.e1));
+    float st = 0, du = 0;
+    GIN_CUDA(cudaEventElapsedTime(&st, p->traces[0].e0, t.e0));
+    GIN_CUDA(cudaEventElapsedTime(&du, t.e0, t.e1));
+    out[i * 5 + 0] = (double)t.bytes;
+    out[i * 5 + 1] = t.ctx;
+    out[i * 5 + 2] = (double)(t.issue_ns - p->traces[0].issue_ns) / 1e3;
+    out[i * 5 + 3] = st * 1e3;
+    out[i * 5 + 4] = du * 1e3;
+  }
+  for (auto& t : p->traces) {
+    cudaEventDestroy(t.e0);
+    cudaEventDestroy(t.e1);
+  }
+  p->traces.clear();
+  return nrec;
 }
 
 void proxy_stats(Comm* c, uint64_t* descs, uint64_t* copies, uint64_t* busy, uint64_t* wall) {

@@ -935,6 +935,15 @@ int ginsim_cuda_device_error(ginsim_cuda_comm_t comm, uint32_t* code, int clear)
   GIN_API_END
 }
 
+int ginsim_cuda_proxy_trace(ginsim_cuda_comm_t comm, double* out, uint32_t max_records, uint32_t* n_out) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  if (!c->proxy) fail(GINSIM_E_BACKEND_MISMATCH, "proxy_trace on a direct-backend comm");
+  DeviceGuard g(c->device);
+  *n_out = proxy_trace(c, out, max_records);
+  GIN_API_END
+}
+
 int ginsim_cuda_proxy_stats(ginsim_cuda_comm_t comm, uint64_t* descriptors, uint64_t* copies, uint64_t* busy_ns,
                             uint64_t* wall_ns) {
   GIN_API_BEGIN

@@ -175,6 +175,7 @@ void proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]);
 void proxy_host_flush(Comm* c, uint32_t ctx);
 bool proxy_counter_pending(Comm* c, uint32_t id);
 void proxy_stats(Comm* c, uint64_t* descs, uint64_t* copies, uint64_t* busy_ns, uint64_t* wall_ns);
+uint32_t proxy_trace(Comm* c, double* out, uint32_t max_records);
 
 // Descriptor codec (descriptor.cpp).
 int descriptor_check(const ginsim_cuda_descriptor* d);
