@@ -387,6 +387,37 @@ def test_moe_proxy_backend_bf16_ll_shape():
         run.close()
 
 
+@pytest.mark.parametrize("n,E,K,T,H,mode,stage_ctas", [(2, 16, 8, 512, 7168, 0, "48"), (4, 32, 8, 256, 7168, 1, "1"),
+                                                        (3, 24, 5, 200, 4096, 1, "48")])
+def test_moe_proxy_pipeline_multi_chunk(n, E, K, T, H, mode, stage_ctas, monkeypatch):
+    """Proxy pipeline (moe_pipe.cuh) with several copy-engine chunks per peer,
+    own-expert rows on few CTAs, a routing change between steps: dispatch
+    windows (through the compact map), combine windows, expert cells and the
+    combine flag equal the reference's; the rows cell is back to 0."""
+    monkeypatch.setenv("GINSIM_PIPE_STAGE_CTAS", stage_ctas)
+    run = MoeRun(n, E, K, T, H, mode=mode, layout=1, backend="proxy")
+    try:
+        assert run.moes[0].transport() == 2
+        for step, seed in enumerate((1, 6, 6)):
+            run.generate(seed)
+            run.step()
+            cnt = O.counts(seed, n, E, K, T)
+            e_local = E // n
+            for r in range(n):
+                d, comb, cells = O.moe_rank_state(seed, n, E, K, T, H, r, mode=mode)
+                win = O.compact_to_reference(run.dispatch_window(r), cnt, r, n, e_local, T, K, 2 * H + 16)
+                assert (win == d).all(), (step, r)
+                assert (run.combine_window(r) == comb).all(), (step, r)
+                exp, _ = O.combine(seed, E, K, H, r, T, mode=mode)
+                assert (run.output(r) == exp).all(), (step, r)
+                sig, _ = run.comms[r].snapshot_cells()
+                assert int(sig[e_local + 1]) == 0, (step, r)
+                if step == 0:
+                    assert [int(v) for v in sig[:e_local + 1]] == [int(v) for v in cells[:e_local + 1]], r
+    finally:
+        run.close()
+
+
 @pytest.mark.parametrize("n,E,K,T,H,mode", [(2, 16, 4, 40, 256, 0), (4, 64, 8, 48, 7168, 1), (8, 64, 8, 32, 7168, 0),
                                              (8, 256, 8, 64, 7168, 1), (2, 8, 3, 33, 64, 0)])
 def test_moe_dedup_transport_matches_reference(n, E, K, T, H, mode):
