@@ -608,7 +608,11 @@ def main():
                    "parallelism": f"ep{world}", "l2": "inputs larger than L2 (470 MB of messages per phase per rank)"},
         "us_per_step": ms_per_step * 1e3, "dispatch_us": d_mean * 1e3, "combine_us": c_mean * 1e3,
         "per_gpu_GBps": value / world,
-        "roofline": {"bound": "hbm", "kernel": f"moe_{dom}_kernel", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm",
+                     "kernel": ({"dispatch": "moe_dispatch_tma_kernel",
+                                 "combine": "moe_combine_tma_kernel + moe_combine_reduce_kernel"}[dom]
+                                if args.engine in (0, 2) else f"moe_{dom}_kernel"),
+                     "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": dom_bytes},
         "clocks": clk,
@@ -628,7 +632,10 @@ def main():
                           "dispatch_remote_GBps_per_gpu": rem_disp / (d_mean * 1e-3) / 1e9,
                           "combine_remote_GBps_per_gpu": remote_msgs * cmsg / (c_mean * 1e-3) / 1e9,
                           "frac_of_900": rem_disp / (d_mean * 1e-3) / 1e9 / 900.0,
-                          "frac_of_measured_770": rem_disp / (d_mean * 1e-3) / 1e9 / 770.0}
+                          "frac_of_measured_770": rem_disp / (d_mean * 1e-3) / 1e9 / 770.0,
+                          "frac_of_sm_write_ceiling_705": rem_disp / (d_mean * 1e-3) / 1e9 / 705.0,
+                          "note": "N>1 the step is NVLink-bound: the HBM roofline above is not the binding one; "
+                                  "combine_remote_GBps includes the reduce kernel's time"}
     if world == 1 and not args.no_cpu_baseline:
         try:
             r = run_reference(args, 3, 0)

@@ -364,10 +364,10 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
 }
 static size_t combine_smem(const ginsim_cuda_moe_t m) {
   if (!kernels_of(m).tma_combine) return 0;
-  // fp8: [hdr][e4m3 in][scales][bf16 out] per stage
-  const size_t c = m->cchunk;
-  const size_t sst = m->cfg.mode == 3 ? 128 + 2 * (c / 2 + c / 64) + c
-                                      : (m->cfg.mode == 2 ? 128 + c / 2 + c / 64 + c : 128 + c);
+  // per stage (moe_combine_tma_kernel): mode 3 [hdr][e4m3][scales in][scales out],
+  // mode 2 [hdr][scales][bf16 out (codes loaded into its back half)], else [hdr][chunk]
+  const size_t c = m->cchunk, scb = (c / 64 + 15) / 16 * 16;
+  const size_t sst = m->cfg.mode == 3 ? 128 + c / 2 + 2 * scb : (m->cfg.mode == 2 ? 128 + scb + c : 128 + c);
   return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * sst;
 }
 static int combine_threads(const MoeKernels& k) { return k.cthreads; }
@@ -398,7 +398,9 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
       // (chunk/64 bytes) is a 16-byte multiple at a 16-byte aligned offset
       chunk = (chunk + 1023) / 1024 * 1024;
       parts = (payload + chunk - 1) / chunk;
-      cchunk = 2048;  // combine stages also hold the expanded bf16 output
+      // combine: mode 2 expands 4 KiB of bf16 output per stage (its codes
+      // load into the buffer's back half); mode 3 re-quantizes 6 KiB in place
+      cchunk = m->cfg.mode == 3 ? 6144 : 4096;
       cparts = (payload + cchunk - 1) / cchunk;
     }
     m->chunk = chunk;

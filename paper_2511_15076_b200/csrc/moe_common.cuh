@@ -117,6 +117,46 @@ __device__ __forceinline__ uint4 fp8x8_transform(uint2 codes, float scale, float
   return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
+// Mode-2 combine: a lane holds at most this many 8-code vectors of a chunk
+// (chunk <= 4096 payload bytes = 256 vectors over 32 lanes).
+constexpr int kFp8MaxVec = 8;
+
+// Mode-3 combine, one lane's 16 elements of a 128-element block (8 lanes per
+// block): the same arithmetic as fp8x8_transform + fp8_quant_block -- y =
+// bf16(deq*s + c), block amax over the bf16 values, scale = amax/448 and
+// codes = e4m3(y * (448/amax)), all single-rounded -- kept in registers; the
+// codes overwrite the lane's own 16 input codes.
+__device__ __forceinline__ void fp8_requant16(uint4* cp, uint4 codes, float scale_in, float s, float c,
+                                              float* scale_out, uint32_t sub8) {
+  const uint4 y0 = fp8x8_transform(make_uint2(codes.x, codes.y), scale_in, s, c);
+  const uint4 y1 = fp8x8_transform(make_uint2(codes.z, codes.w), scale_in, s, c);
+  const uint32_t w[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+  float f[16];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    f[2 * h] = __uint_as_float(w[h] << 16);
+    f[2 * h + 1] = __uint_as_float(w[h] & 0xFFFF0000u);
+  }
+  float amax = 0.0f;
+#pragma unroll
+  for (int h = 0; h < 16; ++h) amax = fmaxf(amax, fabsf(f[h]));
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float scale = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  const float inv = amax > 0.0f ? __fdiv_rn(448.0f, amax) : 1.0f;
+  uint32_t q[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+        make_float2(__fmul_rn(f[4 * h], inv), __fmul_rn(f[4 * h + 1], inv)), __NV_SATFINITE, __NV_E4M3);
+    const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+        make_float2(__fmul_rn(f[4 * h + 2], inv), __fmul_rn(f[4 * h + 3], inv)), __NV_SATFINITE, __NV_E4M3);
+    q[h] = (uint32_t)lo | ((uint32_t)hi << 16);
+  }
+  *cp = make_uint4(q[0], q[1], q[2], q[3]);
+  if (sub8 == 0) *scale_out = scale;
+}
+
 __device__ __forceinline__ uint4 transform_vec(uint4 v, uint32_t mode, uint32_t e) {
   if (mode == 0) {
     const uint32_t add = (e * 17u + 1u) & 0xFFFFu;

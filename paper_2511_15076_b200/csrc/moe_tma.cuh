@@ -352,12 +352,18 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   __shared__ int is_last;
   extern __shared__ __align__(128) char dsm[];
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
-  // per stage: [128-byte header: the message's 16-byte meta][chunk]; fp8:
-  // [header][e4m3 chunk/2][scales chunk/64][bf16 output chunk]
-  // mode 3 adds the re-quantized output: [..][bf16 y chunk][e4m3 chunk/2][scales chunk/64]
-  const uint32_t q_off = 128, s_off = 128 + chunk / 2, o_off = fp8 ? s_off + chunk / 64 : 128;
-  const uint32_t oq_off = o_off + chunk, os_off = oq_off + chunk / 2;
-  const uint32_t sstride = fp8c ? os_off + chunk / 64 : (fp8 ? o_off + chunk : 128 + chunk);
+  // per stage: [128-byte header: the message's 16-byte meta][chunk]
+  //   mode 2: [header][scales chunk/64][bf16 output chunk], the e4m3 codes
+  //     bulk-loaded into the back half of the output buffer (every lane holds
+  //     its codes in registers before any output is written)
+  //   mode 3: [header][e4m3 chunk/2][scales in chunk/64][scales out chunk/64],
+  //     re-quantized in place in registers (no bf16 staging)
+  const uint32_t sc_bytes = ((chunk / 64) + 15) & ~15u;
+  const uint32_t q_off = fp8c ? 128 : 128 + sc_bytes + chunk / 2;  // e4m3 codes
+  const uint32_t s_off = fp8c ? 128 + chunk / 2 : 128;             // scales in
+  const uint32_t o_off = fp8c ? 0 : (fp8 ? 128 + sc_bytes : 128);  // bf16 output (modes 0-2)
+  const uint32_t os_off = 128 + chunk / 2 + sc_bytes;              // scales out (mode 3)
+  const uint32_t sstride = fp8c ? os_off + sc_bytes : (fp8 ? o_off + chunk : 128 + chunk);
   char* stage = dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)warp * kTmaStages * sstride;
 
   const uint32_t P = e_local * n;
@@ -489,11 +495,29 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     {
       const uint32_t nv = len / 16;
       uint32_t i = lane;
-      if (fp8) {  // expand: 8 codes -> one 16-byte bf16 vector; scale per 128 elements
+      if (fp8c) {  // dequant -> transform -> bf16 -> re-quantize, 8 lanes per 128-element block
+        const float sc = 1.0f + (float)(e % 7u) / 8.0f, cc = ((float)(e % 9u) - 4.0f) / 16.0f;
+        const float* scl = reinterpret_cast<const float*>(sb + s_off);
+        float* sco = reinterpret_cast<float*>(sb + os_off);
+        const uint32_t grp = lane >> 3, sub8 = lane & 7;
+        for (uint32_t blk0 = 0; blk0 < len / 256; blk0 += 4) {  // len is a multiple of 1024: 4 blocks per step
+          const uint32_t blk = blk0 + grp;
+          uint4* cp = reinterpret_cast<uint4*>(sb + q_off + blk * 128 + sub8 * 16);
+          const uint4 codes = *cp;
+          fp8_requant16(cp, codes, scl[blk], sc, cc, sco + blk, sub8);
+        }
+      } else if (fp8) {  // expand: 8 codes -> one 16-byte bf16 vector; scale per 128 elements
         const float sc = 1.0f + (float)(e % 7u) / 8.0f, cc = ((float)(e % 9u) - 4.0f) / 16.0f;
         const uint2* qin = reinterpret_cast<const uint2*>(sb + q_off);
         const float* scl = reinterpret_cast<const float*>(sb + s_off);
-        for (; i < nv; i += 32) buf[i] = fp8x8_transform(qin[i], scl[i / 16], sc, cc);
+        uint2 q[kFp8MaxVec];  // the codes share the output buffer: read them all first
+#pragma unroll
+        for (int m = 0; m < kFp8MaxVec; ++m)
+          if (i + 32 * m < nv) q[m] = qin[i + 32 * m];
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < kFp8MaxVec; ++m)
+          if (i + 32 * m < nv) buf[i + 32 * m] = fp8x8_transform(q[m], scl[(i + 32 * m) / 16], sc, cc);
       } else if (L.mode == 0) {
         const uint32_t add = (e * 17u + 1u) & 0xFFFFu;
         for (; i < nv; i += 32) {
@@ -512,20 +536,13 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
         for (; i < nv; i += 32) buf[i] = bf16x8_transform(buf[i], sc, cc);
       }
     }
-    if (fp8c) {  // re-quantize the expert output, 128 elements per warp step
-      __syncwarp();
-      for (uint32_t blk = 0; blk < len / 256; ++blk)
-        fp8_quant_block(reinterpret_cast<const uint16_t*>(sb + o_off + blk * 256),
-                        reinterpret_cast<uint8_t*>(sb + oq_off + blk * 128), reinterpret_cast<float*>(sb + os_off) + blk,
-                        lane);
-    }
     gin::tma::fence_proxy_async_shared();
     __syncwarp();
     if (lane == 0) {
       const uint4 meta = *reinterpret_cast<const uint4*>(sb);  // {src, token, k, tag}
       char* cdst = cbases[src] + ((uint64_t)meta.y * K + meta.z) * cmsg;
       if (fp8c) {
-        gin::tma::store(cdst + (uint64_t)p * (chunk / 2), sb + oq_off, len / 2);
+        gin::tma::store(cdst + (uint64_t)p * (chunk / 2), sb + q_off, len / 2);
         gin::tma::store(cdst + H + (uint64_t)p * (chunk / 64), sb + os_off, len / 64);
       } else {
         gin::tma::store(cdst + (uint64_t)p * chunk, buf, len);

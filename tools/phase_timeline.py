@@ -49,7 +49,7 @@ def main():
     else:
         rank, world, local = 0, 1, 0
         comm = G.Comm.create_all([0], G.Config(signal_cells=512))[0]
-    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 1, int(os.environ.get("TL_LAYOUT", 1)), 0, 0))
+    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, int(os.environ.get("TL_MODE", 1)), int(os.environ.get("TL_LAYOUT", 1)), 0, 0))
     dev = torch.device("cuda", local)
     x = torch.empty(T * H, dtype=torch.int16, device=dev)
     idx = torch.empty(T * K, dtype=torch.int32, device=dev)
