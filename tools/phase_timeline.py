@@ -63,6 +63,8 @@ def main():
     res = {"rank": rank, "world": world, "tokens": T}
     for kern in (0, 1, 2):
         st = moe.phase_times(kern).astype(np.int64)
+        if not (st[:, 0] > 0).all():  # kernel not launched (LL: reduce fused into the send)
+            continue
         summ, nz = summarize(st)
         phases = {}
         for a, b in zip(nz[:-1], nz[1:]):
@@ -85,6 +87,8 @@ def print_logs(paths):
             d = json.loads(line)
             print(f"rank {d['rank']}/{d['world']}")
             for k in ("dispatch", "combine_send", "combine_reduce"):
+                if k not in d:
+                    continue
                 head = {a: (round(b, 1) if isinstance(b, float) else b) for a, b in d[k].items() if a != "phases"}
                 print("  ", k, head)
                 for p, v in d[k]["phases"].items():
