@@ -13,9 +13,10 @@
 //
 // Wire protocol per (source, destination) and step, all on the destination's
 // context ring (ordered onto one stream by the agent, fabric.cpp:63-79):
-//   k chunk puts  ->  one put of the source's e_local counts (the count
-//   window is source-major)  ->  SignalAdd(1) on the destination's rows cell
-//   (e_local + 1).
+//   one put of the source's e_local counts (the count window is
+//   source-major; issued right after the route tables, so the copy engine
+//   moves it while the first chunk stages)  ->  k chunk puts  ->
+//   SignalAdd(1) on the destination's rows cell (e_local + 1).
 // The destination acquires the rows cell (>= n: its combine kernel resets the
 // cell, so the signal table ends as the reference's) and then releases every
 // (local expert, source) cell on the source's behalf by (1<<32)+count --
@@ -202,17 +203,24 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
   rank_grid_barrier(R.ws + 22, bar_target);
   MOE_STAMP(R, 0, 4);
 
-  // counts put + rows release of rotated peer j (one thread)
+  // rows release of rotated peer j (one thread), after every chunk put and
+  // the counts put on the same ring
   auto finish_peer = [&](uint32_t j) {
     const uint32_t d = (rank + 1 + j) % n;
-    const gin::Gin g(v, d % n_ctx);
     gin::CoopThread me;
-    const gin::Team world = gin::WorldTeam(n);
-    g.put(me, world, d, L.win_counts, (uint64_t)rank * e_local * 4, L.win_stage, cnt_off + (uint64_t)d * e_local * 4,
-          (uint64_t)e_local * 4);
-    g.signal(me, world, d, e_local + 1, gin::SignalAdd(1));
+    gin::Gin(v, d % n_ctx).signal(me, gin::WorldTeam(n), d, e_local + 1, gin::SignalAdd(1));
   };
-  if (b == 0 && tid + 1 < n && pbase[tid + 1] == pbase[tid]) finish_peer(tid);  // no messages for that peer
+  if (b == 0 && tid + 1 < n) {
+    // counts first: the copy engine moves them while the first chunk stages
+    const uint32_t d = (rank + 1 + tid) % n;
+    gin::CoopThread me;
+    gin::Gin(v, d % n_ctx).put(me, gin::WorldTeam(n), d, L.win_counts, (uint64_t)rank * e_local * 4, L.win_stage,
+                               cnt_off + (uint64_t)d * e_local * 4, (uint64_t)e_local * 4);
+    if (pbase[tid + 1] == pbase[tid]) {  // no messages for that peer
+      gin::fence_acq_rel_gpu();
+      finish_peer(tid);
+    }
+  }
 
   // Phase B: messages in staging order, one warp each, from a grab counter
   const char* x = reinterpret_cast<const char*>(R.x);
