@@ -143,28 +143,8 @@ int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t d
     fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
   if (bytes % 16) fail(GINSIM_E_USAGE, "copy size must be a multiple of 16");
   DeviceGuard g(c->device);
-  // engines 5/7 pull: read the peer's src window, write this rank's dst window
-  const bool pull = engine == 5 || engine == 7;
-  if (pull && (c->windows[src_win].sizes[peer] < bytes || c->windows[dst_win].sizes[c->rank] < bytes))
-    fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
-  char* dst = c->windows[dst_win].bases[pull ? c->rank : peer];
-  const char* src = c->windows[src_win].bases[pull ? peer : c->rank];
-  // engine 6: the copy engine moves the last GINSIM_HYBRID_CE_PCT percent
-  // (default 25) on a side stream while TMA copies the rest
-  uint64_t ce_bytes = 0;
-  if (engine == 6) {
-    const char* e = std::getenv("GINSIM_HYBRID_CE_PCT");
-    const uint64_t pct = std::min<uint64_t>(100, e ? std::strtoull(e, nullptr, 10) : 25);
-    ce_bytes = (bytes * pct / 100) & ~uint64_t(4095);
-  }
-  const uint64_t sm_bytes = bytes - ce_bytes;
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  if (engine == 6) {
-    GIN_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    GIN_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    GIN_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-  }
+  char* dst = c->windows[dst_win].bases[peer];
+  const char* src = c->windows[src_win].bases[c->rank];
   cudaStream_t s = (cudaStream_t)stream;
   int sms = 0;
   GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
@@ -208,7 +188,7 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
   if (peer >= c->world) fail(GINSIM_E_INVALID_PEER, "peer out of range");
   if (c->windows[src_win].sizes[c->rank] < bytes || c->windows[dst_win].sizes[peer] < bytes)
     fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
-  if (bytes % 32 || engine > 7) fail(GINSIM_E_USAGE, "copy size must be a multiple of 32; engine 0..7");
+  if (bytes % 32 || engine > 8) fail(GINSIM_E_USAGE, "copy size must be a multiple of 32; engine 0..8");
   if (chunk == 0 || chunk % 16 || chunk > 16384) fail(GINSIM_E_USAGE, "chunk must be a multiple of 16 in 16..16384");
   DeviceGuard g(c->device);
   // engines 5/7 pull: read the peer's src window, write this rank's dst window
@@ -228,6 +208,22 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
   const uint64_t sm_bytes = bytes - ce_bytes;
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // engine 8: copy engine toward EVERY other rank at once, one stream per peer
+  // (bytes / (world-1) each, from disjoint slices): do peer copies overlap?
+  std::vector<cudaStream_t> ps;
+  std::vector<cudaEvent_t> pj;
+  if (engine == 8) {
+    if (c->world < 2) fail(GINSIM_E_USAGE, "engine 8 needs peers");
+    for (uint32_t q = 0; q + 1 < c->world; ++q) {
+      cudaStream_t st;
+      cudaEvent_t ev;
+      GIN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      GIN_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ps.push_back(st);
+      pj.push_back(ev);
+    }
+    GIN_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  }
   if (engine == 6) {
     GIN_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     GIN_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -264,6 +260,19 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
         GIN_CUDA(cudaEventRecord(join, side));
         GIN_CUDA(cudaStreamWaitEvent(s, join, 0));
         break;
+      case 8: {
+        GIN_CUDA(cudaEventRecord(fork, s));
+        const uint64_t per = (bytes / (c->world - 1)) & ~uint64_t(4095);
+        for (uint32_t q = 0, i = 0; q < c->world; ++q) {
+          if (q == c->rank) continue;
+          GIN_CUDA(cudaStreamWaitEvent(ps[i], fork, 0));
+          GIN_CUDA(cudaMemcpyAsync(c->windows[dst_win].bases[q] + per * i, src + per * i, per, cudaMemcpyDefault, ps[i]));
+          GIN_CUDA(cudaEventRecord(pj[i], ps[i]));
+          GIN_CUDA(cudaStreamWaitEvent(s, pj[i], 0));
+          ++i;
+        }
+        break;
+      }
       default: lsu256_copy_kernel<<<G, kCopyThreads, 0, s>>>(dst, src, bytes); break;
     }
   };
@@ -284,6 +293,9 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
     cudaEventDestroy(join);
     cudaStreamDestroy(side);
   }
+  for (auto st : ps) cudaStreamDestroy(st);
+  for (auto ev : pj) cudaEventDestroy(ev);
+  if (engine == 8) cudaEventDestroy(fork);
   GIN_API_END
 }
 

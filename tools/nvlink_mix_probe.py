@@ -41,7 +41,12 @@ def main():
              ("tma_pull", 5, 148, 4096, None), ("tma_pull_296", 5, 296, 4096, None),
              ("tma_pull_6k", 5, 148, 6144, None), ("lsu256_pull", 7, 296, 4096, None),
              ("lsu256_pull_592", 7, 592, 4096, None)]
-    for pct in (10, 20, 30, 40, 60):
+    if world > 2:
+        cases.append(("ce_all_peers", 8, 0, 4096, None))
+        cases.append(("tma_push_one_peer", 1, 148, 4096, None))
+    if os.environ.get("MIX_ONLY_CE"):
+        cases = [c for c in cases if c[1] in (1, 3, 8)]
+    for pct in (() if os.environ.get("MIX_ONLY_CE") else (10, 20, 30, 40, 60)):
         cases.append((f"hybrid_ce{pct}", 6, 148, 4096, pct))
         cases.append((f"hybrid_ce{pct}_64cta", 6, 64, 4096, pct))
     for name, eng, ctas, chunk, pct in cases:
