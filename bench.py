@@ -217,6 +217,10 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
             rows.append({"size_bytes": sz, "iters": iters, "p50_ns": p50, "p99_ns": int(t[min(iters - 1, iters * 99 // 100)]),
                          "mean_ns": float(t.mean()), "one_way_ns": p50 / 2,
                          "GBps_per_direction": (2 * sz / (p50 * 1e-9) / 1e9) if sz else None})
+    if rows:  # each size against the 0-byte round-trip floor and, for bandwidth, against 900 GB/s
+        for r in rows:
+            r["x_rtt_floor"] = r["p50_ns"] / rows[0]["p50_ns"]
+            r["frac_of_900"] = r["GBps_per_direction"] / 900.0 if r["GBps_per_direction"] else None
     return {"rows": rows, "target_us": 5.0, "floor_ns": rows[0]["p50_ns"] if rows else None,
             "csv_schema": "size_bytes,iters,p50_ns,p99_ns,mean_ns,backend=direct,transport=nvlink"}
 
