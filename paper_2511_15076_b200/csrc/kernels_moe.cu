@@ -71,6 +71,7 @@ struct ginsim_cuda_moe_s {
   uint64_t* prof = nullptr;  // GINSIM_PROFILE_PHASES=1: [3][1024][8] %globaltimer stamps
   uint64_t iteration_dispatch = 0, iteration_combine = 0;
   uint32_t last_ctas = 0;
+  uint32_t fanout = 0;  // layout 2: fan-out CTAs (fixed with the grid at the first launch)
 };
 
 extern "C" {
@@ -108,9 +109,10 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   const uint64_t cmsg = cfg->mode == 3 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden;
   const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
   const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
-  if (cfg->layout == 2 && e_local + 2 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
-    fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag and rows cell exceed the signal table");
-  const uint64_t nbytes = ((uint64_t)e_local * n + n) * 4;  // counts [src][e_loc] + row counts [src] (layout 2)
+  if (cfg->layout == 2 && e_local + 3 + kDedupChunks > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
+    fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag, rows, chunk and bounds cells exceed the signal table");
+  // counts [src][e_loc] + row counts [src] + row bounds [src][chunks + 1] (layout 2)
+  const uint64_t nbytes = ((uint64_t)e_local * n + n + n * (kDedupChunks + 1)) * 4;
   const uint64_t cbytes = T * K * cmsg;
   if (ginsim_cuda_mem_alloc(comm, dbytes, &m->buf_dispatch)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
   if (ginsim_cuda_mem_alloc(comm, nbytes, &m->buf_counts)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
@@ -260,6 +262,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   // copy engines without starving them of HBM (tools/proxy_phases.py, N=2:
   // dispatch 412 us vs 439 us on every CTA)
   L.stage_ctas = sc ? (uint32_t)std::strtoul(sc, nullptr, 10) : 48u;
+  L.fanout_ctas = moes[0]->fanout;
   L.fuse_reduce = (moes[0]->coop || moes[0]->pipe) ? 0u : 1u;
   L.mpay = cfg.mode >= 2 ? cfg.hidden + cfg.hidden / 32 : 2u * cfg.hidden;
   L.dmsg = (uint64_t)L.mpay + 16;
@@ -445,7 +448,19 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
       parts = std::max(1u, std::min(want, nvec / 32u));
     }
   }
+  // layout 2: two thirds of the CTAs fan received rows out while the rest
+  // put (48 of 148 CTAs keep NVLink busy; N=4 HT dispatch 318 us vs 373 us
+  // sequential, tools/phase_timeline.py TL_LAYOUT=2; at N=2 the rows are few
+  // and the sequential order is 3% faster).  GINSIM_DEDUP_FANOUT_CTAS
+  // overrides; 0 = every CTA puts, then fans out.
+  uint32_t fanout = 0;
+  if (m->cfg.layout == 2) {
+    const char* fo = std::getenv("GINSIM_DEDUP_FANOUT_CTAS");
+    fanout = fo ? (uint32_t)std::strtoul(fo, nullptr, 10) : (Gd >= 4 && m->comm->world > 2 ? 2 * Gd / 3 : 0u);
+    if (fanout >= Gd) fanout = Gd - 1;
+  }
   for (uint32_t i = 0; i < n; ++i) {
+    moes[i]->fanout = fanout;
     moes[i]->G = Gd;
     moes[i]->Gc = Gc;
     moes[i]->Gr = Gr;
@@ -476,6 +491,7 @@ int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const vo
   plan(moes, n);
   const MoeKernels k = kernels_of(moes[0]);
   L.parts = moes[0]->parts;
+  L.fanout_ctas = moes[0]->fanout;
   const uint32_t G = moes[0]->G;
   uint32_t chunk = moes[0]->chunk;
   const size_t smem = dispatch_smem(moes[0], G);

@@ -49,6 +49,7 @@ struct MoeLaunch {
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
   uint32_t stage_ctas;           // Proxy pipeline: CTAs that stage (the rest leave the copy engines the HBM)
+  uint32_t fanout_ctas;          // layout 2: CTAs that fan received rows out while the others put (0 = all, in turn)
 };
 
 // ------------------------------------------------------------------ helpers

@@ -16,16 +16,28 @@ namespace ginsim_b200 {
 // top-8 of 256 a token has 4.63 distinct remote ranks instead of 7.0 remote
 // messages, at 2 ranks one row instead of ~4 messages.
 //
-// Sender phases as moe_dispatch_tma_kernel (cooperative route tables with the
-// n destination "row" bins appended to the E expert bins), then
-//   C: per remote destination: counts + row count (relaxed) + fence.sys + one
-//      release of the destination's rows cell; own experts released as usual.
-//   F: every rank acquires the rows cell (n-1 sources), then fans the rows
-//      out through the same TMA pipeline (bulk load header + row chunk, bulk
-//      store to each listed slot), the last CTA releases the experts'
-//      (1<<32)+count on behalf of each source (own GPU: GPU scope).
+// Phases (cooperative route tables as moe_dispatch_tma_kernel with the n
+// destination "row" bins appended to the E expert bins):
+//   A': CTA 0 publishes, per remote destination, the row boundaries of the
+//      kDedupChunks token chunks (chunk c = the tokens of CTAs [c*G/C,
+//      (c+1)*G/C), so its first row is that CTA's exclusive row prefix) into
+//      the destination's count window, then releases its J-ready cell.
+//   B: sender CTAs (b < G - Gf) put one row per (token, destination rank);
+//      a sender warp that leaves a token chunk drains its bulk stores and
+//      counts itself out of the chunk; the last one releases that chunk's
+//      cell (e_local + 2 + c) at every destination.
+//   C: per remote destination: counts + row count + one release of its rows
+//      cell; own experts released as usual.
+//   F: fan-out CTAs (b >= G - Gf; all CTAs after C when Gf = 0) walk the
+//      (source, chunk) segments in order, acquire each segment's chunk cell
+//      and fan its rows out (bulk load header + row chunk, bulk store to each
+//      listed message position) while the senders are still putting -- the
+//      HBM-bound fan-out overlaps the NVLink-bound row puts.  The last
+//      fan-out CTA acquires the rows cells (counts) and releases the
+//      experts' (1<<32)+count on behalf of each source (GPU scope).
 //   D: acquire every local expert as before.
 constexpr uint32_t kRowHdr = 128;
+constexpr uint32_t kDedupChunks = 4;
 
 template <int KMAX>
 __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeLaunch L, uint32_t chunk) {
@@ -45,7 +57,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
 
   __shared__ uint32_t hist_all[kMaxExperts + GIN_MAX_RANKS], run[kMaxExperts + GIN_MAX_RANKS];
   __shared__ uint32_t prefix_e[kMaxExperts];
-  __shared__ uint32_t cntv[kMaxExperts], src_prefix[kMaxExperts], rcnt[GIN_MAX_RANKS + 1];
+  __shared__ uint32_t seg[GIN_MAX_RANKS * kDedupChunks + 1];  // fan-out: first row item of each (source, chunk)
+  __shared__ uint32_t segj[GIN_MAX_RANKS * kDedupChunks];     // first row index (j) of the segment
   __shared__ char* sbase[GIN_MAX_RANKS];
   __shared__ char* rbase[GIN_MAX_RANKS];
   __shared__ int is_last;
@@ -64,6 +77,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   uint64_t* hdr_g = R.aux_g;              // [T][Kp] header address of the (t, dst) row (remote pairs)
   uint64_t* ent_g = R.aux_g + (size_t)T * Kp;  // [T][Kp] slot | e_loc << 32
   const uint64_t rows_bytes = (uint64_t)n * T * payload;  // row region of the row window, headers follow
+  // sender / fan-out split (L.fanout_ctas = Gf; 0 = every CTA does both, in turn)
+  const uint32_t Gf = L.fanout_ctas, Gs = G - Gf;
+  const bool sender = Gf == 0 || b < Gs, fanner = Gf == 0 || b >= Gs;
+  const uint32_t C = kDedupChunks;
+  auto chunk_t0 = [&](uint32_t c) { return (uint32_t)((uint64_t)(c * G / C) * T / G); };
+  const uint32_t P = e_local * n;
+  uint32_t* jwin = reinterpret_cast<uint32_t*>(v->win[L.win_counts].base[rank]) + P + n;  // [src][C+1] row bounds
 
   for (uint32_t e = tid; e < EB; e += kTmaThreads) {
     hist_all[e] = 0;
@@ -130,6 +150,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     }
   }
   __syncthreads();
+  if (b == 0) {
+    // A': row boundaries of every token chunk, per remote destination, then
+    // its J-ready cell (fence: the bounds before the release)
+    for (uint32_t i = tid; i < n * (C + 1); i += kTmaThreads) {
+      const uint32_t d = i / (C + 1), c = i % (C + 1);
+      if (d == rank) continue;
+      const uint32_t j = c == C ? hist_all[E + d] : __ldcg(g_pre + (size_t)(c * G / C) * EB + E + d);
+      gin::st_relaxed_sys32(reinterpret_cast<uint32_t*>(v->win[L.win_counts].base[d]) + P + n + rank * (C + 1) + c, j);
+    }
+    __syncthreads();
+    if (tid < n && tid != rank) {
+      gin::fence_acq_rel_sys();
+      gin::red_relaxed_sys_add(gin.sub_cell(tid, rank, e_local + 2 + C), 1ull);
+    }
+  }
   if (warp == 0) {
     for (uint32_t c0 = 0; c0 < nq; c0 += 32) {
       const uint32_t q = c0 + lane;
@@ -157,7 +192,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       if (valid) {
         const uint32_t t = t0 + q / K, slot = base + before, e_loc = e % e_local;
         const uint64_t pi = (uint64_t)t * Kp + k;
-        ent_g[pi] = (uint64_t)slot | ((uint64_t)e_loc << 32);
+        ent_g[pi] = (uint64_t)(prefix_e[e] + slot) | ((uint64_t)e_loc << 32);  // position in src's region
         if (d == rank) {
           dst_g[pi] = sbase[d] + ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
           hdr_g[pi] = 0;
@@ -186,8 +221,27 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   // ---- Phase B: one bulk store per (token, destination rank) for remote
   // rows, one per message for own experts
   const char* x = reinterpret_cast<const char*>(R.x);
-  const uint64_t items = (uint64_t)T * parts;
-  const uint64_t gw = (uint64_t)b * kTmaWarps + warp, wstride = (uint64_t)G * kTmaWarps;
+  const uint64_t items = sender ? (uint64_t)T * parts : 0;
+  const uint64_t gw = (uint64_t)b * kTmaWarps + warp, wstride = (uint64_t)Gs * kTmaWarps;
+  // a token chunk is done once every sender warp holding one of its items has
+  // drained its bulk stores; monotone per-chunk arrival counters (ws[48+c])
+  auto chunk_of = [&](uint32_t t) {
+    uint32_t c = 0;
+    while (c + 1 < C && chunk_t0(c + 1) <= t) ++c;
+    return c;
+  };
+  auto chunk_done = [&](uint32_t c) {  // lane 0, once this warp's items of chunk c completed
+    gin::fence_acq_rel_sys();
+    const uint64_t len = (uint64_t)(chunk_t0(c + 1 < C ? c + 1 : C) - chunk_t0(c)) * parts;
+    const unsigned warps_c = (unsigned)(len < wstride ? len : wstride);
+    const unsigned prev = atomicAdd(R.ws + 48 + c, 1u);
+    if (prev + 1 == (unsigned)R.iteration * warps_c) {
+      gin::fence_acq_rel_sys();  // every sender warp's rows of the chunk, then the releases
+      for (uint32_t d = 0; d < n; ++d)
+        if (d != rank) gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_local + 2 + c), 1ull);
+    }
+  };
+  uint32_t cur_chunk = 0xFFFFFFFFu;
   auto issue = [&](int s, uint64_t it) {
     const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
     const uint32_t len = tma_chunk_len(payload, chunk, p);
@@ -232,6 +286,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       for (uint32_t k = 0; k < K; ++k)
         if (dp[k]) gin::tma::store(dp[k] + (uint64_t)p * chunk, sb + dhead, len);
       gin::tma::commit();
+      // first item of a new token chunk: once every older group completed
+      // (this item's stores stay in flight), count this warp out of the old one
+      const uint32_t c = chunk_of(t);
+      if (cur_chunk != 0xFFFFFFFFu && c != cur_chunk) {
+        gin::tma::wait_done<1>();
+        chunk_done(cur_chunk);
+      }
+      cur_chunk = c;
       if (j >= 1) {
         gin::tma::wait_read<1>();
         const uint64_t nxt = it - wstride + kDispStages * wstride;
@@ -242,14 +304,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   }
   if (lane == 0) {
     gin::tma::wait_all();
+    if (cur_chunk != 0xFFFFFFFFu) chunk_done(cur_chunk);
     gin::tma::fence_proxy_async_global();
   }
   MOE_STAMP(R, 0, 5);
 
-  // ---- Phase C: per remote destination: counts + row count, one fence, one
-  // release of its rows cell; own experts as usual (GPU scope)
-  arrive_last(R.ws + 0, bar_target, &is_last);
-  if (is_last) {
+  // ---- Phase C (senders): per remote destination: counts + row count, one
+  // fence, one release of its rows cell; own experts as usual (GPU scope)
+  if (sender) arrive_last(R.ws + 0, (unsigned)(R.iteration * Gs), &is_last);
+  if (sender && is_last) {
     for (uint32_t d = warp; d < n; d += kTmaWarps) {
       uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[L.win_counts].base[d]);
       for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
@@ -268,43 +331,56 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   MOE_STAMP(R, 0, 6);
 
   // ---- Phase F: receive side -- fan the rows of every source out into the
-  // expert slots of this rank's dispatch window
+  // expert slots of this rank's dispatch window, chunk by chunk as they land
   if (L.no_wait) return;  // profiling harness: the sender's part only
-  if (tid == 0) gin.wait_ge_signal(e_local + 1, R.iteration * (uint64_t)(n - 1));
-  __syncthreads();
-  gin::tma::fence_proxy_async_global();  // rows/headers written by peers -> read by this CTA's bulk loads
-  const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
-  const uint32_t P = e_local * n;
-  for (uint32_t i = tid; i < P; i += kTmaThreads) cntv[i] = gin::ld_acquire_sys32(counts + count_index(i, n, e_local));
-  if (tid <= n) rcnt[tid] = 0;
-  __syncthreads();
-  if (tid < n) rcnt[tid] = tid == rank ? 0u : gin::ld_acquire_sys32(counts + P + tid);
-  source_prefix<kTmaWarps>(cntv, src_prefix, n, e_local);
-  __syncthreads();
-  if (tid == 0) {  // rcnt -> exclusive prefix over sources (row order: source-major)
-    uint32_t acc = 0;
-    for (uint32_t s2 = 0; s2 < n; ++s2) {
-      const uint32_t c = rcnt[s2];
-      rcnt[s2] = acc;
-      acc += c;
+  const uint32_t GF = Gf ? Gf : G, fb = Gf ? b - Gs : b;  // fan-out CTA count / index
+  if (fanner) {
+    if (tid == 0) {  // every source's row bounds
+      for (uint32_t s2 = 0; s2 < n; ++s2)
+        if (s2 != rank) gin.wait_ge(gin.sub_cell(rank, s2, e_local + 2 + C), R.iteration);
     }
-    rcnt[n] = acc;
+    __syncthreads();
+    if (tid == 0) {  // segments chunk-major (the order they land in), sources rotated
+      uint32_t acc = 0, i = 0;
+      for (uint32_t c = 0; c < C; ++c) {
+        for (uint32_t jj = 1; jj < n; ++jj, ++i) {
+          const uint32_t s2 = (rank + jj) % n;
+          const uint32_t j0 = gin::ld_acquire_sys32(jwin + s2 * (C + 1) + c);
+          const uint32_t j1 = gin::ld_acquire_sys32(jwin + s2 * (C + 1) + c + 1);
+          seg[i] = acc;
+          segj[i] = j0;
+          acc += (j1 - j0) * parts;
+        }
+      }
+      seg[i] = acc;
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  const uint32_t nseg = (n - 1) * C;
   const char* rows = v->win[L.win_rows].base[rank];
   char* mywin = v->win[L.win_dispatch].base[rank];
-  const uint64_t fitems = (uint64_t)rcnt[n] * parts;
-  auto locate_row = [&](uint64_t it, uint32_t& src, uint32_t& jr) {
-    const uint32_t r = (uint32_t)(it / parts);
-    uint32_t s2 = 0;
-    while (s2 + 1 < n && rcnt[s2 + 1] <= r) ++s2;
-    while (s2 < n && rcnt[s2 + 1] == rcnt[s2]) ++s2;  // skip sources with no rows
-    src = s2;
-    jr = r - rcnt[s2];
+  const uint64_t fitems = fanner ? seg[nseg] : 0;
+  const uint64_t gwf = (uint64_t)fb * kTmaWarps + warp, fstride = (uint64_t)GF * kTmaWarps;
+  auto locate_row = [&](uint64_t it, uint32_t& si, uint32_t& src, uint32_t& jr) {
+    uint32_t lo = 0, hi = nseg;  // last segment whose first item <= it
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (seg[mid] <= it) lo = mid; else hi = mid;
+    }
+    while (lo + 1 < nseg && seg[lo + 1] == seg[lo]) ++lo;  // skip empty segments
+    si = lo;
+    src = (rank + 1 + lo % (n - 1)) % n;
+    jr = segj[lo] + (uint32_t)((it - seg[lo]) / parts);
   };
+  uint32_t ready_seg = 0xFFFFFFFFu;  // lane 0: highest segment acquired so far (items ascend)
   auto fissue = [&](int s, uint64_t it) {
-    uint32_t src, jr;
-    locate_row(it, src, jr);
+    uint32_t si, src, jr;
+    locate_row(it, si, src, jr);
+    if (ready_seg == 0xFFFFFFFFu || si > ready_seg) {
+      gin.wait_ge(gin.sub_cell(rank, src, e_local + 2 + si / (n - 1)), R.iteration);
+      gin::tma::fence_proxy_async_global();  // rows written by the peer -> this warp's bulk loads
+      ready_seg = si;
+    }
     const uint32_t p = (uint32_t)(it % parts);
     const uint32_t len = tma_chunk_len(payload, chunk, p);
     char* sb = stage + (size_t)s * sstride;
@@ -312,43 +388,40 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     gin::tma::load(sb, rows + rows_bytes + ((uint64_t)src * T + jr) * kRowHdr, kRowHdr, &ctl->bar[s]);
     gin::tma::load(sb + dhead, rows + ((uint64_t)src * T + jr) * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
   };
-  __syncthreads();
-  const uint32_t phase0 = (uint32_t)((items + wstride - 1 - gw) / wstride);  // items this warp ran in Phase B
+  const uint32_t phase0 = items > gw ? (uint32_t)((items - gw + wstride - 1) / wstride) : 0u;  // items run in B
   if (lane == 0) {
     for (int s = 0; s < kDispStages; ++s) {
-      const uint64_t it = gw + s * wstride;
+      const uint64_t it = gwf + s * fstride;
       if (it < fitems) fissue((int)((phase0 + s) % kDispStages), it);
     }
   }
   for (uint32_t j = 0;; ++j) {
-    const uint64_t it = gw + (uint64_t)j * wstride;
+    const uint64_t it = gwf + (uint64_t)j * fstride;
     if (it >= fitems) break;
     const uint32_t jj = phase0 + j;  // continue the stage/parity sequence of Phase B
     const int s = (int)(jj % kDispStages);
-    uint32_t src, jr;
-    locate_row(it, src, jr);
+    uint32_t si, src, jr;
+    locate_row(it, si, src, jr);
     const uint32_t p = (uint32_t)(it % parts);
     char* sb = stage + (size_t)s * sstride;
     gin::tma::mbar_wait(&ctl->bar[s], (jj / kDispStages) & 1);
     const uint32_t* h = reinterpret_cast<const uint32_t*>(sb);
     const uint32_t tok = h[0], mask = h[1];
     if (p == 0 && lane < K && ((mask >> lane) & 1)) {
-      const uint32_t slot = h[2 + 2 * lane], e_loc = h[3 + 2 * lane] & 0xFFFFu;
-      char* m = mywin + ((uint64_t)src * T * K + src_prefix[e_loc * n + src] + slot) * dmsg;
+      char* m = mywin + ((uint64_t)src * T * K + h[2 + 2 * lane]) * dmsg;
       gin::st_v4(m + payload, make_uint4(src, tok, lane, lane + 1));
     }
     if (lane == 0) {
       const uint32_t len = tma_chunk_len(payload, chunk, p);
       for (uint32_t k = 0; k < K; ++k) {
         if (!((mask >> k) & 1)) continue;
-        const uint32_t slot = h[2 + 2 * k], e_loc = h[3 + 2 * k] & 0xFFFFu;
-        char* m = mywin + ((uint64_t)src * T * K + src_prefix[e_loc * n + src] + slot) * dmsg;
+        char* m = mywin + ((uint64_t)src * T * K + h[2 + 2 * k]) * dmsg;
         gin::tma::store(m + (uint64_t)p * chunk, sb + dhead, len);
       }
       gin::tma::commit();
       if (j >= 1) {
         gin::tma::wait_read<1>();
-        const uint64_t nxt = it - wstride + kDispStages * wstride;
+        const uint64_t nxt = it - fstride + kDispStages * fstride;
         if (nxt < fitems) fissue((int)((jj - 1) % kDispStages), nxt);
       }
     }
@@ -358,14 +431,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     gin::tma::wait_all();
     gin::tma::fence_proxy_async_global();
   }
-  // the last CTA releases every (local expert, remote source) pair on the
-  // source's behalf: this GPU is the only reader (GPU scope)
-  arrive_last(R.ws + 12, bar_target, &is_last);
-  if (is_last) {
+  // the last fan-out CTA releases every (local expert, remote source) pair on
+  // the source's behalf once its counts are in: this GPU is the only reader
+  if (fanner) arrive_last(R.ws + 12, (unsigned)(R.iteration * GF), &is_last);
+  if (fanner && is_last) {
+    if (tid == 0) gin.wait_ge_signal(e_local + 1, R.iteration * (uint64_t)(n - 1));
+    __syncthreads();
+    const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
     gin::fence_acq_rel_gpu();
     for (uint32_t i = tid; i < P; i += kTmaThreads) {
       const uint32_t e_loc = i / n, src = i % n;
-      if (src != rank) gin::red_relaxed_sys_add(gin.sub_cell(rank, src, e_loc), (1ull << 32) + cntv[i]);
+      if (src != rank)
+        gin::red_relaxed_sys_add(gin.sub_cell(rank, src, e_loc),
+                                 (1ull << 32) + gin::ld_acquire_sys32(counts + count_index(i, n, e_local)));
     }
   }
   MOE_STAMP(R, 0, 7);

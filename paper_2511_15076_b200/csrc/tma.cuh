@@ -68,6 +68,12 @@ __device__ __forceinline__ void wait_read() {
 }
 // Wait until every committed group has fully completed its writes.
 __device__ __forceinline__ void wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Full completion (writes performed, not just source reads) of every group
+// but the newest N.
+template <int N>
+__device__ __forceinline__ void wait_done() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 
 }  // namespace tma
 }  // namespace gin
