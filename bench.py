@@ -208,7 +208,7 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
     for sz in [0, 8, 64, 512, 4096, 32768, 262144, 1 << 20, 4 << 20]:
         iters = 1000 if sz <= 65536 else 200
         if rank in (0, 1):
-            G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, iters, 100, 0, 512,
+            G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, iters, 100, 401, 512,
                                                  rtt.data_ptr(), None))
         dist.barrier()
         if rank == 0:
@@ -234,12 +234,13 @@ def measure_a2a(G, comm, rank, world, dist, torch, dev, stream):
     cap = world * sizes[-1]
     sb, rb = comm.mem_alloc(cap), comm.mem_alloc(cap)
     ws, wr = comm.window_register(sb, cap), comm.window_register(rb, cap)
-    sid = 400  # above the MoE cells, below the barrier slots
+    sid = 400  # above the MoE cells, below the barrier slots (the ping-pong uses 401/402)
     h = G.comm_handles([comm])
     rows = []
     for M in sizes:
         iters = 50 if M <= (1 << 20) else 10
         base = comm.read_signal(sid)
+        dist.barrier()  # every rank holds its base before any rank's first put of this size
         k = 0
 
         def once():

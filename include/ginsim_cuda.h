@@ -218,7 +218,9 @@ int ginsim_cuda_descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* 
  * puts `bytes` with SignalInc to rank 1 and waits for the echo, `iters`
  * timed iterations after `warmup`; a single persistent CTA per rank times
  * every round trip with %globaltimer into rtt_ns_out (device, iters u64,
- * written by rank 0).  window `send_win` / `recv_win` of >= bytes. */
+ * written by rank 0).  window `send_win` / `recv_win` of >= bytes.  Cells
+ * signal_id (rounds) and signal_id+1 (a launch handshake, so no ping can
+ * precede the peer's host read of the round cell) are the ping-pong's own. */
 int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1,
                          uint32_t send_win, uint32_t recv_win, uint64_t bytes, uint32_t iters,
                          uint32_t warmup, uint32_t signal_id, uint32_t threads, uint64_t* rtt_ns_out,

@@ -28,6 +28,8 @@ struct PingArgs {
   LaneViews lv;
   uint32_t peer0, peer1, send_win, recv_win, sig, iters, warmup, ctas;
   uint64_t bytes;
+  uint64_t ready[GIN_MAX_RANKS];   // handshake count (cell sig+1) each lane waits for
+  uint64_t arrive0[GIN_MAX_RANKS]; // multi-CTA rounds: arrivals on workspace word 0 before this call
   uint64_t* rtt;  // device, iters entries (written by peer0's lane)
 };
 
@@ -44,6 +46,12 @@ __global__ void pingpong_kernel(PingArgs A) {
   if (me != A.peer0 && me != A.peer1) return;
   const bool initiator = me == A.peer0;
   const uint32_t other = initiator ? A.peer1 : A.peer0;
+  // Handshake on cell sig+1: each side announces its launch and waits for the
+  // other's, so no ping reaches a rank before its host read of the cell the
+  // rounds are counted from (the race a slow responder would otherwise lose).
+  if (blockIdx.x == 0 && threadIdx.x == 0) gin.release_signal_raw(other, A.sig + 1, 1);
+  if (threadIdx.x == 0) gin.wait_ge_signal(A.sig + 1, A.ready[blockIdx.y]);
+  __syncthreads();
   const uint32_t total = A.warmup + A.iters;
   const uint64_t chunk = ((A.bytes + A.ctas - 1) / A.ctas + 15) & ~15ull;
   const uint64_t lo = std::min<uint64_t>(A.bytes, chunk * blockIdx.x);
@@ -62,7 +70,7 @@ __global__ void pingpong_kernel(PingArgs A) {
     if (threadIdx.x == 0) {
       gin::fence_acq_rel_sys();
       const unsigned prev = atomicAdd(ws, 1u);
-      last = prev + 1 == round * A.ctas;
+      last = prev + 1 == (unsigned)(A.arrive0[blockIdx.y] + (uint64_t)round * A.ctas);
       if (last) {
         gin::fence_acq_rel_sys();
         gin.release_signal_raw(other, A.sig, 1);
@@ -73,19 +81,19 @@ __global__ void pingpong_kernel(PingArgs A) {
     if (threadIdx.x == 0) gin.wait_ge_signal(A.sig, want);
     cta.sync();
   };
-  // ws counts rounds across calls: continue from the host-provided offset.
-  const uint32_t round0 = (uint32_t)(base >> 32);
-  const uint64_t sig0 = base & 0xFFFFFFFFull;
+  // ws counts CTA arrivals across calls (whose CTA counts differ with the
+  // message size): round i of this call is complete at arrive0 + i*ctas
+  const uint64_t sig0 = base;
   for (uint32_t i = 1; i <= total; ++i) {
     if (initiator) {
       const uint64_t t0 = gin::globaltimer();
-      send(round0 + i);
+      send(i);
       wait(sig0 + i);
       const uint64_t t1 = gin::globaltimer();
       if (blockIdx.x == 0 && threadIdx.x == 0 && i > A.warmup) A.rtt[i - 1 - A.warmup] = t1 - t0;
     } else {
       wait(sig0 + i);
-      send(round0 + i);
+      send(i);
     }
   }
 }
@@ -376,7 +384,7 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
   check_same_device(comms, n);
   Comm* c0 = &comms[0]->impl;
   if (peer0 == peer1 || peer0 >= c0->world || peer1 >= c0->world) fail(GINSIM_E_INVALID_PEER, "ping-pong needs two distinct ranks");
-  if (signal_id >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range");
+  if (signal_id + 1 >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range (uses signal_id and signal_id+1)");
   if (iters == 0) fail(GINSIM_E_USAGE, "bench iterations must be positive");
   DeviceGuard g(c0->device);
   PingArgs A{};
@@ -403,9 +411,11 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
     uint64_t cur = 0;
     if (int rc = ginsim_cuda_read_signal(comms[i], signal_id, &cur)) fail(rc, ginsim_cuda_last_error());
     // the arrival counter only advances on multi-CTA launches
-    const uint64_t adv = A.ctas > 1 ? (uint64_t)(warmup + iters) : 0;
-    const uint64_t rounds_before = bump_host_counter(c, 0, adv) - adv;
-    A.lv.base[i] = (rounds_before << 32) | (cur & 0xFFFFFFFFull);
+    const uint64_t adv = A.ctas > 1 ? (uint64_t)(warmup + iters) * A.ctas : 0;
+    A.arrive0[i] = bump_host_counter(c, 0, adv) - adv;
+    A.lv.base[i] = cur;
+    // handshake cell sig+1 (dedicated to ping-pong): one arrival per call
+    A.ready[i] = bump_host_counter(c, 6, 1);
   }
   const uint32_t thr = threads ? threads : 512;
   coop_launch((const void*)pingpong_kernel, dim3(A.ctas, n), dim3(thr), &A, (cudaStream_t)stream);

@@ -237,6 +237,7 @@ def test_pingpong_payload_and_counts():
         # a second call continues from the cell values (no reset needed)
         G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles(cs), 2, 0, 1, ws, wr, 1 << 20, 10, 1, 0, 512, rtt, None))
         assert cs[0].read_signal(0) == 66
+        assert cs[0].read_signal(1) == 2 and cs[1].read_signal(1) == 2  # one launch handshake per call
         U.free(rtt)
     finally:
         close(cs)
