@@ -208,7 +208,7 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
     for sz in [0, 8, 64, 512, 4096, 32768, 262144, 1 << 20, 4 << 20]:
         iters = 1000 if sz <= 65536 else 200
         if rank in (0, 1):
-            G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, iters, 100, 401, 512,
+            G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, iters, 100, 4001, 512,
                                                  rtt.data_ptr(), None))
         dist.barrier()
         if rank == 0:
@@ -234,7 +234,9 @@ def measure_a2a(G, comm, rank, world, dist, torch, dev, stream):
     cap = world * sizes[-1]
     sb, rb = comm.mem_alloc(cap), comm.mem_alloc(cap)
     ws, wr = comm.window_register(sb, cap), comm.window_register(rb, cap)
-    sid = 400  # above the MoE cells, below the barrier slots (the ping-pong uses 401/402)
+    # (every MoE handle on this comm owns e_local + 7 cells from 0 up; the
+    # headline, LL and variant handles stay far below)
+    sid = 4000  # below the barrier slots; the ping-pong uses 4001/4002
     h = G.comm_handles([comm])
     rows = []
     for M in sizes:
@@ -422,10 +424,10 @@ def main():
             out = [None] * world
             dist.all_gather_object(out, blob)
             return out
-        comm = G.Comm.create(rank, world, local, allgather, G.Config(signal_cells=512))
+        comm = G.Comm.create(rank, world, local, allgather, G.Config(signal_cells=4096))
     else:
         allgather = None
-        comm = G.Comm.create_all([local], G.Config(signal_cells=512))[0]
+        comm = G.Comm.create_all([local], G.Config(signal_cells=4096))[0]
 
     T, H, K, E = args.tokens, HIDDEN, TOPK, EXPERTS
     cfg = G.MoeConfig(E, K, T, H, args.mode, args.layout, args.ctas, args.engine)

@@ -72,6 +72,7 @@ struct ginsim_cuda_moe_s {
   uint64_t iteration_dispatch = 0, iteration_combine = 0;
   uint32_t last_ctas = 0;
   uint32_t fanout = 0;  // layout 2: fan-out CTAs (fixed with the grid at the first launch)
+  uint32_t cell0 = 0;   // this handle's signal cells: [cell0, cell0 + e_local + 3 + kDedupChunks)
 };
 
 extern "C" {
@@ -98,19 +99,32 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
     if (cfg->engine == 1) fail(GINSIM_E_USAGE, "layout 2 runs on the TMA engine");
   }
   const uint32_t e_local = cfg->experts / c->world;
-  if (e_local + 1 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
-    fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag exceed the signal table");
+  // Every handle owns its signal cells (expert cells, combine flag, rows,
+  // chunk and bounds cells): the waits count per-handle iterations, so two
+  // handles on one comm must never share a cell.  Handles take consecutive
+  // ranges in creation order (identical on every rank: creation is
+  // collective); the first handle of a comm starts at cell 0, as the
+  // reference's state has it.
+  const uint32_t span = e_local + 3 + kDedupChunks;
+  uint32_t cell0;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    cell0 = c->moe_cells_next;
+    if ((uint64_t)cell0 + span > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
+      fail(GINSIM_E_USAGE, "signal table has no room for this MoE handle's " + std::to_string(span) +
+                               " cells (raise Config.signal_cells)");
+    c->moe_cells_next = cell0 + span;
+  }
   auto m = std::make_unique<ginsim_cuda_moe_s>();
   m->comm = c;
   m->cfg = *cfg;
   m->e_local = e_local;
+  m->cell0 = cell0;
   m->parts = cfg->hidden >= 1024 ? 4 : 1;
   const uint64_t dmsg = (cfg->mode >= 2 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden) + 16;
   const uint64_t cmsg = cfg->mode == 3 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden;
   const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
   const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
-  if (cfg->layout == 2 && e_local + 3 + kDedupChunks > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
-    fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag, rows, chunk and bounds cells exceed the signal table");
   // counts [src][e_loc] + row counts [src] + row bounds [src][chunks + 1] (layout 2)
   const uint64_t nbytes = ((uint64_t)e_local * n + n + n * (kDedupChunks + 1)) * 4;
   const uint64_t cbytes = T * K * cmsg;
@@ -130,8 +144,6 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
     const char* cv = std::getenv("GINSIM_PROXY_COALESCE");
     m->pipe = m->proxy && cfg->layout == 1 && cfg->mode <= 1 && (2u * cfg->hidden) % 16u == 0 &&
               !(pv && pv[0] == '0') && !(cv && cv[0] == '0');
-    if (m->pipe && e_local + 2 > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
-      fail(GINSIM_E_USAGE, "per-expert signals plus the combine flag and rows cell exceed the signal table");
   }
   if (cfg->layout == 2) {
     // row staging: [src][j] rows of 2H bytes, then [src][j] 128-byte headers
@@ -245,6 +257,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.win_cstage = moes[0]->win_cstage;
   L.win_mirror = moes[0]->win_mirror;
   L.win_rows = moes[0]->win_rows;
+  L.cell0 = moes[0]->cell0;
   // Proxy backend: one put descriptor per expert run (default) or per message
   // (GINSIM_PROXY_COALESCE=0, the reference's one-put-per-(t,k) pattern).
   const char* cv = std::getenv("GINSIM_PROXY_COALESCE");
@@ -268,7 +281,8 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   L.dmsg = (uint64_t)L.mpay + 16;
   L.cmsg = cfg.mode == 3 ? (uint64_t)cfg.hidden + cfg.hidden / 32 : 2ull * cfg.hidden;
   for (uint32_t i = 0; i < n; ++i) {
-    if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch)
+    if (std::memcmp(&moes[i]->cfg, &cfg, sizeof(cfg)) != 0 || moes[i]->win_dispatch != L.win_dispatch ||
+        moes[i]->cell0 != L.cell0)
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
     L.r[i].view = moes[i]->comm->dev_view;
     L.r[i].ws = moes[i]->ws;

@@ -50,6 +50,7 @@ struct MoeLaunch {
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
   uint32_t stage_ctas;           // Proxy pipeline: CTAs that stage (the rest leave the copy engines the HBM)
   uint32_t fanout_ctas;          // layout 2: CTAs that fan received rows out while the others put (0 = all, in turn)
+  uint32_t cell0;                // first signal cell of this handle: expert cells, combine flag, rows/chunk cells
 };
 
 // ------------------------------------------------------------------ helpers
@@ -232,7 +233,8 @@ __device__ __forceinline__ uint32_t count_index(uint32_t i, uint32_t n, uint32_t
 }
 
 __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDevCommView* v, uint32_t win_counts,
-                                                const uint32_t* hist, uint32_t n, uint32_t rank, uint32_t e_local) {
+                                                const uint32_t* hist, uint32_t n, uint32_t rank, uint32_t e_local,
+                                                uint32_t cell0) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (uint32_t d = warp; d < n; d += nw) {
     uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[win_counts].base[d]);
@@ -243,7 +245,7 @@ __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDe
       gin::st_relaxed_sys32(cb + (uint64_t)rank * e_local + e_loc, hist[d * e_local + e_loc]);
     if (d == rank) gin::fence_acq_rel_gpu(); else gin::fence_acq_rel_sys();
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
-      gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_loc), (1ull << 32) + hist[d * e_local + e_loc]);
+      gin::red_relaxed_sys_add(gin.sub_cell(d, rank, cell0 + e_loc), (1ull << 32) + hist[d * e_local + e_loc]);
   }
 }
 

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     __syncthreads();
     if (tid < n && tid != rank) {
       gin::fence_acq_rel_sys();
-      gin::red_relaxed_sys_add(gin.sub_cell(tid, rank, e_local + 2 + C), 1ull);
+      gin::red_relaxed_sys_add(gin.sub_cell(tid, rank, L.cell0 + e_local + 2 + C), 1ull);
     }
   }
   if (warp == 0) {
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     if (prev + 1 == (unsigned)R.iteration * warps_c) {
       gin::fence_acq_rel_sys();  // every sender warp's rows of the chunk, then the releases
       for (uint32_t d = 0; d < n; ++d)
-        if (d != rank) gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_local + 2 + c), 1ull);
+        if (d != rank) gin::red_relaxed_sys_add(gin.sub_cell(d, rank, L.cell0 + e_local + 2 + c), 1ull);
     }
   };
   uint32_t cur_chunk = 0xFFFFFFFFu;
@@ -321,10 +321,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       if (d == rank) {
         gin::fence_acq_rel_gpu();
         for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
-          gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_loc), (1ull << 32) + hist_all[d * e_local + e_loc]);
+          gin::red_relaxed_sys_add(gin.sub_cell(d, rank, L.cell0 + e_loc), (1ull << 32) + hist_all[d * e_local + e_loc]);
       } else {
         gin::fence_acq_rel_sys();
-        if (lane == 0) gin::red_relaxed_sys_add(gin.sub_cell(d, rank, e_local + 1), 1ull);
+        if (lane == 0) gin::red_relaxed_sys_add(gin.sub_cell(d, rank, L.cell0 + e_local + 1), 1ull);
       }
     }
   }
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   if (fanner) {
     if (tid == 0) {  // every source's row bounds
       for (uint32_t s2 = 0; s2 < n; ++s2)
-        if (s2 != rank) gin.wait_ge(gin.sub_cell(rank, s2, e_local + 2 + C), R.iteration);
+        if (s2 != rank) gin.wait_ge(gin.sub_cell(rank, s2, L.cell0 + e_local + 2 + C), R.iteration);
     }
     __syncthreads();
     if (tid == 0) {  // segments chunk-major (the order they land in), sources rotated
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     uint32_t si, src, jr;
     locate_row(it, si, src, jr);
     if (ready_seg == 0xFFFFFFFFu || si > ready_seg) {
-      gin.wait_ge(gin.sub_cell(rank, src, e_local + 2 + si / (n - 1)), R.iteration);
+      gin.wait_ge(gin.sub_cell(rank, src, L.cell0 + e_local + 2 + si / (n - 1)), R.iteration);
       gin::tma::fence_proxy_async_global();  // rows written by the peer -> this warp's bulk loads
       ready_seg = si;
     }
@@ -435,21 +435,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   // the source's behalf once its counts are in: this GPU is the only reader
   if (fanner) arrive_last(R.ws + 12, (unsigned)(R.iteration * GF), &is_last);
   if (fanner && is_last) {
-    if (tid == 0) gin.wait_ge_signal(e_local + 1, R.iteration * (uint64_t)(n - 1));
+    if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local + 1, R.iteration * (uint64_t)(n - 1));
     __syncthreads();
     const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
     gin::fence_acq_rel_gpu();
     for (uint32_t i = tid; i < P; i += kTmaThreads) {
       const uint32_t e_loc = i / n, src = i % n;
       if (src != rank)
-        gin::red_relaxed_sys_add(gin.sub_cell(rank, src, e_loc),
+        gin::red_relaxed_sys_add(gin.sub_cell(rank, src, L.cell0 + e_loc),
                                  (1ull << 32) + gin::ld_acquire_sys32(counts + count_index(i, n, e_local)));
     }
   }
   MOE_STAMP(R, 0, 7);
   if (tid == 0 && !L.no_wait) {
     const uint64_t want = R.iteration * ((uint64_t)n << 32);
-    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(e_loc, want);
+    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(L.cell0 + e_loc, want);
   }
 }
 

@@ -198,10 +198,10 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
     __syncthreads();
     for (uint32_t e = tid; e < E; e += kMoeThreads) {
       const uint32_t dst = e / e_local, e_loc = e % e_local;
-      gin::Gin(v, ctx_of(e)).signal(me, world, dst, e_loc, gin::SignalAdd((1ull << 32) + hist_all[e]));
+      gin::Gin(v, ctx_of(e)).signal(me, world, dst, L.cell0 + e_loc, gin::SignalAdd((1ull << 32) + hist_all[e]));
     }
   } else if (is_last) {
-    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local);
+    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0);
   }
   // Phase D: return once every local expert has been released by every source.
   if (tid == 0) {
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
     for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) {
       const uint64_t t_start = gin::globaltimer();
       uint32_t spins = 0;
-      while (gin.read_signal(e_loc) < want) {
+      while (gin.read_signal(L.cell0 + e_loc) < want) {
         if (++spins > 32) __nanosleep(64);
         if ((spins & 1023) == 0 && gin::globaltimer() - t_start > v->timeout_ns) {
           gin::raise_error(v, GIN_DEVERR_TIMEOUT);
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       if (src != rank && tot)
         g.put(me, world, src, L.win_mirror, (uint64_t)rank * T * K * cmsg, L.win_cstage, (uint64_t)src_base[src] * cmsg,
               (uint64_t)tot * cmsg);
-      if (tot) g.signal(me, world, src, e_local, gin::SignalAdd(tot));
+      if (tot) g.signal(me, world, src, L.cell0 + e_local, gin::SignalAdd(tot));
     }
   } else if (is_last && PROXY) {  // reference pattern: one put per message, per-(source, ctx) flags
     const gin::Team world = gin::WorldTeam(n);
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
         }
         c += cnt[pr];
       }
-      if (c) g.signal(me, world, src, e_local, gin::SignalAdd(c));
+      if (c) g.signal(me, world, src, L.cell0 + e_local, gin::SignalAdd(c));
     }
   } else if (is_last) {
     for (uint32_t sc = tid; sc < n * n_ctx; sc += kMoeThreads) {
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
       uint32_t c = 0;
       for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc)
         if ((rank * e_local + e_loc) % n_ctx == ctx) c += cnt[e_loc * n + src];
-      if (c) gin.release_signal_raw(src, e_local, c);
+      if (c) gin.release_signal_raw(src, L.cell0 + e_local, c);
     }
   }
 
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
     const uint64_t want = R.iteration * (uint64_t)T * K;
     const uint64_t t_start = gin::globaltimer();
     uint32_t spins = 0;
-    while (gin.read_signal(e_local) < want) {
+    while (gin.read_signal(L.cell0 + e_local) < want) {
       if (++spins > 32) __nanosleep(64);
       if ((spins & 1023) == 0 && gin::globaltimer() - t_start > v->timeout_ns) {
         gin::raise_error(v, GIN_DEVERR_TIMEOUT);

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
   auto finish_peer = [&](uint32_t j) {
     const uint32_t d = (rank + 1 + j) % n;
     gin::CoopThread me;
-    gin::Gin(v, d % n_ctx).signal(me, gin::WorldTeam(n), d, e_local + 1, gin::SignalAdd(1));
+    gin::Gin(v, d % n_ctx).signal(me, gin::WorldTeam(n), d, L.cell0 + e_local + 1, gin::SignalAdd(1));
   };
   if (b == 0 && tid + 1 < n) {
     // counts first: the copy engine moves them while the first chunk stages
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
   arrive_last(R.ws + 0, bar_target, &is_last);
   if (is_last && tid == 0) {
     gin::fence_acq_rel_gpu();
-    gin::red_relaxed_sys_add(gin.sub_cell(rank, rank, e_local + 1), 1ull);
+    gin::red_relaxed_sys_add(gin.sub_cell(rank, rank, L.cell0 + e_local + 1), 1ull);
   }
   MOE_STAMP(R, 0, 6);
   if (L.no_wait) return;
@@ -266,12 +266,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
   // the source's behalf; this GPU is the only reader of these cells
   const uint32_t P = e_local * n;
   if ((uint64_t)b * kPipeThreads < P) {
-    if (tid == 0) gin.wait_ge_signal(e_local + 1, (uint64_t)n);
+    if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local + 1, (uint64_t)n);
     __syncthreads();
     const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
     for (uint32_t i = b * kPipeThreads + tid; i < P; i += G * kPipeThreads) {
       const uint32_t src = i / e_local, e_loc = i % e_local;
-      gin::red_relaxed_sys_add(gin.sub_cell(rank, src, e_loc), (1ull << 32) + gin::ld_acquire_sys32(counts + i));
+      gin::red_relaxed_sys_add(gin.sub_cell(rank, src, L.cell0 + e_loc), (1ull << 32) + gin::ld_acquire_sys32(counts + i));
     }
   }
   MOE_STAMP(R, 0, 7);
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLa
     // rank's combine results reach it
     if (tid == 0) {
       grab[0] = grab[1] = 0;
-      if (!L.no_wait) gin::Gin(v, 0).reset_signal(e_local + 1);
+      if (!L.no_wait) gin::Gin(v, 0).reset_signal(L.cell0 + e_local + 1);
     }
   }
   const uint32_t P = e_local * n;
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLa
       pipe_chunk_done(ctr, n, j, q, tot, pch[j], lane,
                       [&] {
                         gin::CoopThread me;
-                        gin::Gin(v, s % n_ctx).signal(me, gin::WorldTeam(n), s, e_local, gin::SignalAdd(tot));
+                        gin::Gin(v, s % n_ctx).signal(me, gin::WorldTeam(n), s, L.cell0 + e_local, gin::SignalAdd(tot));
                       },
                       gin::Gin(v, s % n_ctx), s, L.win_mirror, (uint64_t)rank * TK * cmsg, L.win_cstage,
                       (uint64_t)pbase[j] * cmsg, cmsg);
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLa
     const uint32_t own_tot = pbase[n] - pbase[n - 1];
     gin::fence_acq_rel_gpu();
     gin::CoopThread me;
-    if (own_tot) gin::Gin(v, rank % n_ctx).signal(me, gin::WorldTeam(n), rank, e_local, gin::SignalAdd(own_tot));
+    if (own_tot) gin::Gin(v, rank % n_ctx).signal(me, gin::WorldTeam(n), rank, L.cell0 + e_local, gin::SignalAdd(own_tot));
   }
   MOE_STAMP(R, 1, 3);
 }

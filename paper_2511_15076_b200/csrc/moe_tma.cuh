@@ -318,13 +318,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   arrive_last(R.ws + 0, (unsigned)(R.iteration * G), &is_last);
   if (is_last) {
     if (tid == 0) *grab_ctr = 0;  // every CTA is past Phase B
-    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local);
+    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0);
   }
   MOE_STAMP(R, 0, 6);
   if (tid == 0) {
     const uint64_t want = R.iteration * ((uint64_t)n << 32);
     if (!L.no_wait)
-      for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(e_loc, want);
+      for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(L.cell0 + e_loc, want);
   }
   MOE_STAMP(R, 0, 7);
 }
@@ -575,9 +575,9 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       if (c) {
         if (src == rank) {  // own tokens: the reducer is on this GPU
           gin::fence_acq_rel_gpu();
-          gin::red_relaxed_sys_add(gin.sub_cell(src, rank, e_local), c);
+          gin::red_relaxed_sys_add(gin.sub_cell(src, rank, L.cell0 + e_local), c);
         } else {
-          gin.release_signal_raw(src, e_local, c);
+          gin.release_signal_raw(src, L.cell0 + e_local, c);
         }
       }
     }
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   if (L.fuse_reduce) {
     // small launches: the source-side reduction right here (saves the second
     // launch); same arithmetic as moe_combine_reduce_kernel
-    if (tid == 0) gin.wait_ge_signal(e_local, R.iteration * (uint64_t)T * K);
+    if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, R.iteration * (uint64_t)T * K);
     __syncthreads();
     const char* crecv = v->win[L.win_combine].base[rank];
     const uint32_t nvec = payload / 16;
@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
   constexpr bool fp8c = FP8C;  // mode 3 (a separate instantiation keeps the bf16 path spill-free)
   const uint32_t payload = 2u * H;
   MOE_STAMP(R, 2, 0);
-  if (tid == 0) gin.wait_ge_signal(e_local, R.iteration * (uint64_t)T * K);
+  if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, R.iteration * (uint64_t)T * K);
   __syncthreads();
   MOE_STAMP(R, 2, 1);
   const char* crecv = v->win[L.win_combine].base[rank];

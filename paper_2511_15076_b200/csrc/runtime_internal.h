@@ -148,6 +148,7 @@ struct Comm {
 
   cudaStream_t op_stream = nullptr;           // host-issued ops / cell reads
   bool shares_device = false;                 // another rank of this comm runs on this device in this process
+  uint32_t moe_cells_next = 0;                // next free signal cell for a MoE handle (ranges are never reused)
   uint64_t op_counter[8] = {};                // per-workload launch/round counters (host side)
   ProxyPtr proxy;
 

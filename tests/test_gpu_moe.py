@@ -312,6 +312,46 @@ def test_moe_ht_config_compact_properties():
         run.close()
 
 
+def test_two_handles_share_a_comm():
+    """Two MoE handles (different shapes and layouts) on the same comms,
+    stepped alternately: each owns its signal cells, so neither's waits are
+    satisfied by the other's releases; every output equals the oracle's."""
+    n = 2
+    U.set_device(0)
+    comms = G.Comm.create_all([0] * n, G.Config(signal_cells=512, timeout_ms=20000))
+    shapes = [(16, 4, 40, 256, 1), (32, 8, 24, 512, 0)]  # E, K, T, H, layout
+    runs = []
+    try:
+        for E, K, T, H, layout in shapes:
+            moes = G.Moe.create_all(comms, G.MoeConfig(E, K, T, H, 0, layout, 0, 0))
+            bufs = [[U.malloc(T * H * 2), U.malloc(T * K * 4), U.malloc(T * K * 2), U.malloc(T * H * 2)]
+                    for _ in range(n)]
+            runs.append((moes, bufs, (E, K, T, H)))
+        for step, seed in enumerate((3, 3, 8, 8)):
+            for moes, bufs, (E, K, T, H) in runs:
+                for r, m in enumerate(moes):
+                    m.generate(seed, r, bufs[r][0], bufs[r][1], bufs[r][2])
+                U.sync()
+                G.Moe.dispatch(moes, [b[0] for b in bufs], [b[1] for b in bufs])
+                G.Moe.combine(moes, [b[2] for b in bufs], [b[3] for b in bufs])
+                U.sync()
+                for c in comms:
+                    c.check_device()
+                for r in range(n):
+                    exp, _ = O.combine(seed, E, K, H, r, T)
+                    got = U.d2h(bufs[r][3], T * H * 2, np.uint16).reshape(T, H)
+                    assert (got == exp).all(), (step, E, r)
+    finally:
+        for moes, bufs, _ in runs:
+            for b in bufs:
+                for p in b:
+                    U.free(p)
+            for m in moes:
+                m.destroy()
+        for c in comms:
+            c.destroy()
+
+
 @pytest.mark.parametrize("coalesce", ["1", "0"])
 @pytest.mark.parametrize("layout", [0, 1])
 def test_moe_proxy_backend_matches_reference_final_state(coalesce, layout, monkeypatch):
