@@ -1,7 +1,8 @@
-"""Debug: multi-process ping-pong with the launch handshake."""
-import os, sys, time
+"""Multi-process put+signal ping-pong p50 for a few sizes (ranks 0 and 1)."""
+import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import numpy as np
 import torch
 import torch.distributed as dist
 import paper_2511_15076_b200 as G
@@ -13,19 +14,18 @@ def ag(blob):
     out = [None] * world
     dist.all_gather_object(out, blob)
     return out
-comm = G.Comm.create(rank, world, local, ag, G.Config(signal_cells=512, timeout_ms=5000))
+cells = int(os.environ.get("CELLS", "4096"))
+sig = int(os.environ.get("SIG", "4001"))
+comm = G.Comm.create(rank, world, local, ag, G.Config(signal_cells=cells))
 sz = 1 << 20
 sb, rb = comm.mem_alloc(sz), comm.mem_alloc(sz)
 ws, wr = comm.window_register(sb, sz), comm.window_register(rb, sz)
 rtt = torch.zeros(1000, dtype=torch.int64, device=torch.device("cuda", local))
-sig = int(os.environ.get("SIG", "401"))
-for s in [8, 64, 4096]:
-    print(rank, "before", s, comm.read_signal(sig), comm.read_signal(sig + 1), flush=True)
-    try:
-        G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, s, 50, 5, sig, 512, rtt.data_ptr(), None))
-    except Exception as e:
-        print(rank, "ERR", e, flush=True)
-    print(rank, "after", s, comm.read_signal(sig), comm.read_signal(sig + 1), flush=True)
+for s in (0, 8, 4096):
+    G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, s, 1000, 100, sig, 512, rtt.data_ptr(), None))
     dist.barrier()
+    if rank == 0:
+        t = np.sort(rtt.cpu().numpy())
+        print(f"lib {os.environ.get('GINSIM_LIB', 'new')[-12:]} cells {cells} sig {sig} bytes {s} p50 {int(t[500])}", flush=True)
 comm.destroy()
 dist.destroy_process_group()
