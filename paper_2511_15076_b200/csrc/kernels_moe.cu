@@ -396,7 +396,9 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   const uint32_t payload = 2u * m->cfg.hidden;
   uint32_t parts = 1, chunk = 0, cparts = 1, cchunk = 0;
   if (use_tma(m)) {
-    parts = (payload + 8191) / 8192;
+    const char* dc = std::getenv("GINSIM_DISPATCH_CHUNK");  // tuning knob (bytes, multiple of 16)
+    const uint32_t dchunk = dc ? std::max(16u, (uint32_t)std::strtoul(dc, nullptr, 10)) : 8192u;
+    parts = (payload + dchunk - 1) / dchunk;
     if (!m->coop) {
       // small (latency-bound) launches: split rows further so every warp of a
       // CTA has an item (LL: one token per CTA -> 8 chunks of 1.75 KiB)

@@ -55,7 +55,7 @@ def main():
     idx = torch.empty(T * K, dtype=torch.int32, device=dev)
     w = torch.empty(T * K, dtype=torch.float32, device=dev)
     out = torch.empty(T * H, dtype=torch.int16, device=dev)
-    moe.generate(1, rank, x, idx, w)
+    moe.generate(1, (rank + int(os.environ.get("TL_SHIFT", 0))) % world, x, idx, w)
     for _ in range(4):
         G.Moe.dispatch([moe], [x], [idx])
         G.Moe.combine([moe], [w], [out])
