@@ -21,11 +21,12 @@ sz = 1 << 20
 sb, rb = comm.mem_alloc(sz), comm.mem_alloc(sz)
 ws, wr = comm.window_register(sb, sz), comm.window_register(rb, sz)
 rtt = torch.zeros(1000, dtype=torch.int64, device=torch.device("cuda", local))
+warm = int(os.environ.get("WARMUP", "100"))
 for s in (0, 8, 4096):
-    G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, s, 1000, 100, sig, 512, rtt.data_ptr(), None))
+    G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, s, 1000, warm, sig, 512, rtt.data_ptr(), None))
     dist.barrier()
     if rank == 0:
         t = np.sort(rtt.cpu().numpy())
-        print(f"lib {os.environ.get('GINSIM_LIB', 'new')[-12:]} cells {cells} sig {sig} bytes {s} p50 {int(t[500])}", flush=True)
+        print(f"lib {os.environ.get('GINSIM_LIB', 'new')[-12:]} warmup {warm} cells {cells} sig {sig} bytes {s} p50 {int(t[500])}", flush=True)
 comm.destroy()
 dist.destroy_process_group()
