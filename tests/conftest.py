@@ -5,6 +5,12 @@ import sys
 
 import pytest
 
+# Emulated ranks put one proxy agent stream (plus an op stream) per rank on
+# one device; with more streams than hardware queues an agent stream can alias
+# onto the queue of the MoE kernel it must feed (csrc/proxy.cu).  Before any
+# CUDA context exists:
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -428,7 +428,7 @@ def test_moe_proxy_backend_bf16_ll_shape():
 
 
 @pytest.mark.parametrize("n,E,K,T,H,mode,stage_ctas", [(2, 16, 8, 512, 7168, 0, "48"), (4, 32, 8, 256, 7168, 1, "1"),
-                                                        (3, 24, 5, 200, 4096, 1, "48")])
+                                                        (3, 24, 5, 200, 4096, 1, "48"), (8, 64, 8, 160, 7168, 1, "48")])
 def test_moe_proxy_pipeline_multi_chunk(n, E, K, T, H, mode, stage_ctas, monkeypatch):
     """Proxy pipeline (moe_pipe.cuh) with several copy-engine chunks per peer,
     own-expert rows on few CTAs, a routing change between steps: dispatch
