@@ -53,6 +53,19 @@ struct MoeLaunch {
   uint32_t cell0;                // first signal cell of this handle: expert cells, combine flag, rows/chunk cells
 };
 
+// Per-handle launch counters in device memory (ws words 56..59: [0]
+// dispatch, [1] combine).  A dispatch/combine launch's iteration is the
+// stored value + 1 (read by every CTA at its start); the CTA that completes
+// the launch's grid-wide arrival -- after every CTA has read it -- stores it
+// back.  The host therefore passes no per-launch value, and a step captured
+// in a CUDA graph advances on every replay.
+__device__ __forceinline__ uint64_t* moe_iter_ptr(const MoeRankArgs& R, int kind) {
+  return reinterpret_cast<uint64_t*>(R.ws + 56) + kind;
+}
+__device__ __forceinline__ uint64_t moe_iteration(const MoeRankArgs& R, int kind, bool next) {
+  return *reinterpret_cast<volatile uint64_t*>(moe_iter_ptr(R, kind)) + (next ? 1u : 0u);
+}
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t u16x2_transform(uint32_t two, uint32_t add) {
   // two u16 lanes: y = 3x + (17e+1), each lane mod 2^16

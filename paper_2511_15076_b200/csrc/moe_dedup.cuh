@@ -42,6 +42,7 @@ constexpr uint32_t kDedupChunks = 4;
 template <int KMAX>
 __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeLaunch L, uint32_t chunk) {
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 0, true);
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
   const uint32_t n = v->world, rank = v->rank;
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   const uint32_t payload = 2u * H, parts = L.parts;
   const uint32_t Kp = (K + 1) & ~1u;
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
-  const unsigned int bar_target = (unsigned int)(R.iteration * G);
+  const unsigned int bar_target = (unsigned int)(iteration * G);
   MOE_STAMP(R, 0, 0);
 
   __shared__ uint32_t hist_all[kMaxExperts + GIN_MAX_RANKS], run[kMaxExperts + GIN_MAX_RANKS];
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     const uint64_t len = (uint64_t)(chunk_t0(c + 1 < C ? c + 1 : C) - chunk_t0(c)) * parts;
     const unsigned warps_c = (unsigned)(len < wstride ? len : wstride);
     const unsigned prev = atomicAdd(R.ws + 48 + c, 1u);
-    if (prev + 1 == (unsigned)R.iteration * warps_c) {
+    if (prev + 1 == (unsigned)iteration * warps_c) {
       gin::fence_acq_rel_sys();  // every sender warp's rows of the chunk, then the releases
       for (uint32_t d = 0; d < n; ++d)
         if (d != rank) gin::red_relaxed_sys_add(gin.sub_cell(d, rank, L.cell0 + e_local + 2 + c), 1ull);
@@ -311,7 +312,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
 
   // ---- Phase C (senders): per remote destination: counts + row count, one
   // fence, one release of its rows cell; own experts as usual (GPU scope)
-  if (sender) arrive_last(R.ws + 0, (unsigned)(R.iteration * Gs), &is_last);
+  if (sender) arrive_last(R.ws + 0, (unsigned)(iteration * Gs), &is_last);
+  if (sender && is_last && tid == 0) *moe_iter_ptr(R, 0) = iteration;  // all CTAs read it before Phase A's barriers
   if (sender && is_last) {
     for (uint32_t d = warp; d < n; d += kTmaWarps) {
       uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[L.win_counts].base[d]);
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   if (fanner) {
     if (tid == 0) {  // every source's row bounds
       for (uint32_t s2 = 0; s2 < n; ++s2)
-        if (s2 != rank) gin.wait_ge(gin.sub_cell(rank, s2, L.cell0 + e_local + 2 + C), R.iteration);
+        if (s2 != rank) gin.wait_ge(gin.sub_cell(rank, s2, L.cell0 + e_local + 2 + C), iteration);
     }
     __syncthreads();
     if (tid == 0) {  // segments chunk-major (the order they land in), sources rotated
@@ -377,7 +379,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     uint32_t si, src, jr;
     locate_row(it, si, src, jr);
     if (ready_seg == 0xFFFFFFFFu || si > ready_seg) {
-      gin.wait_ge(gin.sub_cell(rank, src, L.cell0 + e_local + 2 + si / (n - 1)), R.iteration);
+      gin.wait_ge(gin.sub_cell(rank, src, L.cell0 + e_local + 2 + si / (n - 1)), iteration);
       gin::tma::fence_proxy_async_global();  // rows written by the peer -> this warp's bulk loads
       ready_seg = si;
     }
@@ -433,9 +435,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   }
   // the last fan-out CTA releases every (local expert, remote source) pair on
   // the source's behalf once its counts are in: this GPU is the only reader
-  if (fanner) arrive_last(R.ws + 12, (unsigned)(R.iteration * GF), &is_last);
+  if (fanner) arrive_last(R.ws + 12, (unsigned)(iteration * GF), &is_last);
   if (fanner && is_last) {
-    if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local + 1, R.iteration * (uint64_t)(n - 1));
+    if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local + 1, iteration * (uint64_t)(n - 1));
     __syncthreads();
     const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
     gin::fence_acq_rel_gpu();
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   }
   MOE_STAMP(R, 0, 7);
   if (tid == 0 && !L.no_wait) {
-    const uint64_t want = R.iteration * ((uint64_t)n << 32);
+    const uint64_t want = iteration * ((uint64_t)n << 32);
     for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(L.cell0 + e_loc, want);
   }
 }

@@ -13,6 +13,7 @@ namespace ginsim_b200 {
 template <int KMAX, bool PROXY>
 __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 0, true);
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
   const uint32_t n = v->world, rank = v->rank;
@@ -149,7 +150,8 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
   }
 
   // Phase C: the last CTA to finish releases every expert.
-  arrive_last(R.ws + 0, (unsigned)(R.iteration * G), &is_last);
+  arrive_last(R.ws + 0, (unsigned)(iteration * G), &is_last);
+  if (is_last && tid == 0) *moe_iter_ptr(R, 0) = iteration;  // every CTA has read it (arrival)
   if (is_last && PROXY) {
     // Three phases, each fully submitted before the next (CTA barrier), so on
     // every context ring all counts precede all payload puts, which precede
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
   }
   // Phase D: return once every local expert has been released by every source.
   if (tid == 0) {
-    const uint64_t want = R.iteration * ((uint64_t)n << 32);
+    const uint64_t want = iteration * ((uint64_t)n << 32);
     for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) {
       const uint64_t t_start = gin::globaltimer();
       uint32_t spins = 0;
@@ -228,6 +230,7 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
 template <bool PROXY>
 __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 1, true);
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
   const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
@@ -333,7 +336,8 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
   }
 
   // Release: the last CTA signals each (source, context) with its count.
-  arrive_last(R.ws + 1, (unsigned)(R.iteration * G), &is_last);
+  arrive_last(R.ws + 1, (unsigned)(iteration * G), &is_last);
+  if (is_last && tid == 0) *moe_iter_ptr(R, 1) = iteration;  // every CTA has read it (arrival)
   if (is_last && PROXY && L.coalesce) {
     // one copy-engine transfer per source (all its results, every expert),
     // then that source's combine flag with the total, on ctx src % n_ctx
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
 
   // Source side: acquire all T*K outputs, then reduce with the top-k weights.
   if (tid == 0) {
-    const uint64_t want = R.iteration * (uint64_t)T * K;
+    const uint64_t want = iteration * (uint64_t)T * K;
     const uint64_t t_start = gin::globaltimer();
     uint32_t spins = 0;
     while (gin.read_signal(L.cell0 + e_local) < want) {

@@ -108,6 +108,7 @@ __device__ __forceinline__ void pipe_chunk_done(uint32_t* ctr, uint32_t n, uint3
 
 __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 0, true);
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
   const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
   const uint64_t dmsg = L.dmsg, TK = (uint64_t)T * K;
   const uint32_t payload = 2u * H;
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
-  const unsigned int bar_target = (unsigned int)(R.iteration * G);
+  const unsigned int bar_target = (unsigned int)(iteration * G);
   MOE_STAMP(R, 0, 0);
 
   __shared__ uint32_t hist_all[kMaxExperts], run[kMaxExperts], prefix_e[kMaxExperts];
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
 
   // Phase C: own experts' rows are in place -> own rows cell (GPU scope)
   arrive_last(R.ws + 0, bar_target, &is_last);
+  if (is_last && tid == 0) *moe_iter_ptr(R, 0) = iteration;  // every CTA has read it (arrival)
   if (is_last && tid == 0) {
     gin::fence_acq_rel_gpu();
     gin::red_relaxed_sys_add(gin.sub_cell(rank, rank, L.cell0 + e_local + 1), 1ull);
@@ -279,13 +281,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_dispatch_pipe_kernel(MoeL
 
 __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 1, true);
   const GinDevCommView* v = R.view;
   const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
   const uint32_t K = L.K, T = L.T, H = L.H, e_local = L.e_local;
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const uint64_t dmsg = L.dmsg, cmsg = L.cmsg, TK = (uint64_t)T * K;
   const uint32_t payload = 2u * H;
-  const unsigned int bar_target = (unsigned int)(R.iteration * G);
+  const unsigned int bar_target = (unsigned int)(iteration * G);
   MOE_STAMP(R, 1, 0);
 
   __shared__ uint32_t cnt[kMaxExperts], src_prefix[kMaxExperts];
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) moe_combine_pipe_kernel(MoeLa
   // own results are in place: this rank's share of its own combine flag,
   // through the agent like every other source's (one writer per sub-cell)
   arrive_last(R.ws + 1, bar_target, &is_last);
+  if (is_last && tid == 0) *moe_iter_ptr(R, 1) = iteration;  // every CTA has read it (arrival)
   if (is_last && tid == 0) {
     const uint32_t own_tot = pbase[n] - pbase[n - 1];
     gin::fence_acq_rel_gpu();

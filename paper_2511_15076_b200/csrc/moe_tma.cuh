@@ -104,6 +104,7 @@ __device__ __forceinline__ void coop_route_tables(const MoeRankArgs& R, uint32_t
 template <int KMAX>
 __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLaunch L, uint32_t chunk) {
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 0, true);
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
   const uint32_t n = v->world, rank = v->rank;
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   const uint32_t payload = 2u * H, parts = L.parts;
   const uint32_t Kp = (K + 1) & ~1u;  // dst_g row stride: 16-byte rows for the bulk load
   const uint32_t t0 = (uint32_t)((uint64_t)b * T / G), t1 = (uint32_t)((uint64_t)(b + 1) * T / G);
-  const unsigned int bar_target = (unsigned int)(R.iteration * G);
+  const unsigned int bar_target = (unsigned int)(iteration * G);
   // coop: route tables built cooperatively + work over all tokens (large T*K);
   // local: every CTA histograms the whole (small) route table and moves only
   // its own tokens -- no grid barrier on the latency-bound LL path
@@ -315,14 +316,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     __syncthreads();
     if (tid == 0) R.prof[((uint64_t)0 * 1024 + blockIdx.x) * 8 + 5] = warp_end;
   }
-  arrive_last(R.ws + 0, (unsigned)(R.iteration * G), &is_last);
+  arrive_last(R.ws + 0, (unsigned)(iteration * G), &is_last);
   if (is_last) {
     if (tid == 0) *grab_ctr = 0;  // every CTA is past Phase B
+    if (tid == 0) *moe_iter_ptr(R, 0) = iteration;  // every CTA has read it (arrival)
     release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0);
   }
   MOE_STAMP(R, 0, 6);
   if (tid == 0) {
-    const uint64_t want = R.iteration * ((uint64_t)n << 32);
+    const uint64_t want = iteration * ((uint64_t)n << 32);
     if (!L.no_wait)
       for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(L.cell0 + e_loc, want);
   }
@@ -336,6 +338,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   constexpr int kTmaThreads = kCmbThreads;
   constexpr int kTmaWarps = kCmbThreads / 32;
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 1, true);
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
   const uint32_t n = v->world, rank = v->rank, n_ctx = v->n_ctx;
@@ -564,9 +567,10 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   }
   MOE_STAMP(R, 1, 2);
 
-  arrive_last(R.ws + 1, (unsigned)(R.iteration * G), &is_last);
+  arrive_last(R.ws + 1, (unsigned)(iteration * G), &is_last);
   if (is_last) {
     if (tid == 0) *grab_ctr = 0;  // every CTA is past its loop: ready for the next launch
+    if (tid == 0) *moe_iter_ptr(R, 1) = iteration;  // every CTA has read it (arrival)
     for (uint32_t sc = tid; sc < n * n_ctx; sc += kTmaThreads) {
       const uint32_t src = sc / n_ctx, ctx = sc % n_ctx;
       uint32_t c = 0;
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   if (L.fuse_reduce) {
     // small launches: the source-side reduction right here (saves the second
     // launch); same arithmetic as moe_combine_reduce_kernel
-    if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, R.iteration * (uint64_t)T * K);
+    if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, iteration * (uint64_t)T * K);
     __syncthreads();
     const char* crecv = v->win[L.win_combine].base[rank];
     const uint32_t nvec = payload / 16;
@@ -616,6 +620,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
 template <int KMAX, bool FP8C, bool MIRROR>
 __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeLaunch L, uint32_t /*chunk*/) {
   const MoeRankArgs& R = L.r[blockIdx.y];
+  const uint64_t iteration = moe_iteration(R, 1, false);
   const GinDevCommView* v = R.view;
   gin::Gin gin(v, 0);
   const uint32_t rank = v->rank;
@@ -625,7 +630,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
   constexpr bool fp8c = FP8C;  // mode 3 (a separate instantiation keeps the bf16 path spill-free)
   const uint32_t payload = 2u * H;
   MOE_STAMP(R, 2, 0);
-  if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, R.iteration * (uint64_t)T * K);
+  if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, iteration * (uint64_t)T * K);
   __syncthreads();
   MOE_STAMP(R, 2, 1);
   const char* crecv = v->win[L.win_combine].base[rank];

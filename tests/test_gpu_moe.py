@@ -312,6 +312,44 @@ def test_moe_ht_config_compact_properties():
         run.close()
 
 
+def test_moe_step_replays_in_a_cuda_graph():
+    """dispatch + combine captured once in a CUDA graph and replayed: the
+    kernels take their iteration from per-handle device counters, so every
+    replay is a full step -- outputs equal the oracle's and the expert cells
+    and combine flag advance by one step's values per replay."""
+    import torch
+    n, E, K, T, H, seed = 2, 16, 4, 64, 256, 4
+    run = MoeRun(n, E, K, T, H, layout=1)
+    try:
+        run.generate(seed)
+        run.step()  # plans the grids (attributes and occupancy are not capturable calls)
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            G.Moe.dispatch(run.moes, run.x, run.idx, stream=s)
+            G.Moe.combine(run.moes, run.w, run.out, stream=s)
+        e_local = E // n
+        cnt = O.counts(seed, n, E, K, T)
+        for rep in range(3):
+            for r in range(n):
+                U.memset(run.out[r], 0, T * H * 2)
+            g.replay()
+            torch.cuda.synchronize()
+            for c in run.comms:
+                c.check_device()
+            steps = 2 + rep
+            for r in range(n):
+                exp, _ = O.combine(seed, E, K, H, r, T)
+                assert (run.output(r) == exp).all(), (rep, r)
+                sig, _ = run.comms[r].snapshot_cells()
+                for e_loc in range(e_local):
+                    e = r * e_local + e_loc
+                    assert sig[e_loc] == steps * ((n << 32) + int(cnt[e].sum())), (rep, r, e_loc)
+                assert sig[e_local] == steps * T * K, (rep, r)
+    finally:
+        run.close()
+
+
 def test_two_handles_share_a_comm():
     """Two MoE handles (different shapes and layouts) on the same comms,
     stepped alternately: each owns its signal cells, so neither's waits are
