@@ -110,8 +110,6 @@ def main():
         for sz in [8, 64, 512, 4096, 32768, 262144, 1 << 20, 1 << 22]:
             iters = 1000 if sz <= 65536 else 200
             if rank in (0, 1):
-                if os.environ.get("MP_VERBOSE") == "1":
-                    print(f"rank {rank} pingpong {sz} cells {comm.read_signal(401)} {comm.read_signal(402)}", flush=True)
                 G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, iters, 100, 401, 512,
                                                      rtt.data_ptr(), None))
             dist.barrier()
