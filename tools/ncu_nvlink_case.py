@@ -26,8 +26,8 @@ import paper_2511_15076_b200 as G  # noqa: E402
 
 def main():
     assert os.environ.get("GINSIM_PROFILE_NO_WAIT") == "1", "set GINSIM_PROFILE_NO_WAIT=1"
-    n = 2
-    comms = G.Comm.create_all([0, 1], G.Config(signal_cells=512))
+    n = int(os.environ.get("NVL_N", "2"))  # GPUs driven by this one process
+    comms = G.Comm.create_all(list(range(n)), G.Config(signal_cells=512))
     size = 256 << 20
     srcs = [c.mem_alloc(size) for c in comms]
     dsts = [c.mem_alloc(size) for c in comms]
