@@ -74,19 +74,25 @@ __device__ __forceinline__ uint32_t u16x2_transform(uint32_t two, uint32_t add) 
   return lo | (hi << 16);
 }
 
+// 8 bf16 lanes: y = bf16(fp32(x)*s + c), single-rounded mul and add, packed
+// back two at a time (cvt.rn.bf16x2.f32) -- same rounding as bf16x2_transform.
+// The pair's multiply goes through the sm_100 packed fp32 pipe (FMUL2: each
+// lane an IEEE rn multiply).  The add stays scalar: ptxas 12.9 contracts a
+// mul.rn.f32x2 + add.rn.f32x2 pair into FFMA2 (single rounding -- measured in
+// SASS), which would break bit-exactness; a scalar FADD after FMUL2 is kept.
+__device__ __forceinline__ float2 mul_add2_rn(float2 v, float s, float c) {
+  const float2 m = __fmul2_rn(v, make_float2(s, s));
+  return make_float2(__fadd_rn(m.x, c), __fadd_rn(m.y, c));
+}
 __device__ __forceinline__ uint32_t bf16x2_transform(uint32_t two, float s, float c) {
-  const float a = __uint_as_float(two << 16), b = __uint_as_float(two & 0xFFFF0000u);
-  const __nv_bfloat16 ya = __float2bfloat16_rn(__fadd_rn(__fmul_rn(a, s), c));
-  const __nv_bfloat16 yb = __float2bfloat16_rn(__fadd_rn(__fmul_rn(b, s), c));
+  const float2 y = mul_add2_rn(make_float2(__uint_as_float(two << 16), __uint_as_float(two & 0xFFFF0000u)), s, c);
+  const __nv_bfloat16 ya = __float2bfloat16_rn(y.x), yb = __float2bfloat16_rn(y.y);
   return (uint32_t)__bfloat16_as_ushort(ya) | ((uint32_t)__bfloat16_as_ushort(yb) << 16);
 }
 
-// 8 bf16 lanes: y = bf16(fp32(x)*s + c), single-rounded mul and add, packed
-// back two at a time (cvt.rn.bf16x2.f32) -- same rounding as bf16x2_transform.
 __device__ __forceinline__ uint32_t bf16x2_pack_transform(uint32_t two, float s, float c) {
-  const float a = __fadd_rn(__fmul_rn(__uint_as_float(two << 16), s), c);
-  const float b = __fadd_rn(__fmul_rn(__uint_as_float(two & 0xFFFF0000u), s), c);
-  const __nv_bfloat162 r = __floats2bfloat162_rn(a, b);  // .x = a (low half), .y = b
+  const float2 y = mul_add2_rn(make_float2(__uint_as_float(two << 16), __uint_as_float(two & 0xFFFF0000u)), s, c);
+  const __nv_bfloat162 r = __floats2bfloat162_rn(y.x, y.y);  // .x = low half, .y = high half
   return *reinterpret_cast<const uint32_t*>(&r);
 }
 __device__ __forceinline__ uint4 bf16x8_transform(uint4 v, float s, float c) {
@@ -125,8 +131,8 @@ __device__ __forceinline__ uint4 fp8x8_transform(uint2 codes, float scale, float
     const __nv_fp8x2_storage_t pair = (__nv_fp8x2_storage_t)((w >> ((h & 1) * 16)) & 0xFFFF);
     const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2(pair, __NV_E4M3);
     const float2 f = __half22float2(__half2(hr));
-    const float a = __fmul_rn(f.x, scale), b = __fmul_rn(f.y, scale);
-    const __nv_bfloat162 r = __floats2bfloat162_rn(__fadd_rn(__fmul_rn(a, s), c), __fadd_rn(__fmul_rn(b, s), c));
+    const float2 y = mul_add2_rn(__fmul2_rn(f, make_float2(scale, scale)), s, c);
+    const __nv_bfloat162 r = __floats2bfloat162_rn(y.x, y.y);
     out[h] = *reinterpret_cast<const uint32_t*>(&r);
   }
   return make_uint4(out[0], out[1], out[2], out[3]);
@@ -162,10 +168,11 @@ __device__ __forceinline__ void fp8_requant16(uint4* cp, uint4 codes, float scal
   uint32_t q[4];
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
-        make_float2(__fmul_rn(f[4 * h], inv), __fmul_rn(f[4 * h + 1], inv)), __NV_SATFINITE, __NV_E4M3);
-    const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-        make_float2(__fmul_rn(f[4 * h + 2], inv), __fmul_rn(f[4 * h + 3], inv)), __NV_SATFINITE, __NV_E4M3);
+    const float2 iv = make_float2(inv, inv);
+    const __nv_fp8x2_storage_t lo =
+        __nv_cvt_float2_to_fp8x2(__fmul2_rn(make_float2(f[4 * h], f[4 * h + 1]), iv), __NV_SATFINITE, __NV_E4M3);
+    const __nv_fp8x2_storage_t hi =
+        __nv_cvt_float2_to_fp8x2(__fmul2_rn(make_float2(f[4 * h + 2], f[4 * h + 3]), iv), __NV_SATFINITE, __NV_E4M3);
     q[h] = (uint32_t)lo | ((uint32_t)hi << 16);
   }
   *cp = make_uint4(q[0], q[1], q[2], q[3]);
