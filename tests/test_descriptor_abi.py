@@ -180,3 +180,20 @@ def test_header_codes_mirror_reference_errors():
              "FlowControlViolation", "ChildFailure", "UsageError"]
     codes = [getattr(G, n).code for n in names]
     assert codes == list(range(1, 24))
+
+
+def test_no_contracted_packed_fma_in_the_library():
+    """The expert transform and the fp8 (re)quantizers are mul-then-add with two
+    roundings, like the oracle (`oracle/ginsim_oracle.c`) and the reference's
+    `proj/core/src/harness_moe.cpp` data functions.  ptxas 12.9 contracts an `f32x2` mul + add
+    pair into one FFMA2 even with explicit `.rn`, so the kernels keep the adds
+    scalar.  This guards that: the shipped SASS must contain no FFMA2."""
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", G.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    assert "FMUL2" in sass  # the packed multiply pipe is in use
+    assert "FFMA2" not in sass
