@@ -113,10 +113,11 @@ __device__ __forceinline__ void fp8_quant_block(const uint16_t* in, uint8_t* q, 
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   const float scale = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
   const float inv = amax > 0.0f ? __fdiv_rn(448.0f, amax) : 1.0f;
+  const float2 iv = make_float2(inv, inv);
   const __nv_fp8x2_storage_t lo =
-      __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(f[0], inv), __fmul_rn(f[1], inv)), __NV_SATFINITE, __NV_E4M3);
+      __nv_cvt_float2_to_fp8x2(__fmul2_rn(make_float2(f[0], f[1]), iv), __NV_SATFINITE, __NV_E4M3);
   const __nv_fp8x2_storage_t hi =
-      __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(f[2], inv), __fmul_rn(f[3], inv)), __NV_SATFINITE, __NV_E4M3);
+      __nv_cvt_float2_to_fp8x2(__fmul2_rn(make_float2(f[2], f[3]), iv), __NV_SATFINITE, __NV_E4M3);
   *reinterpret_cast<uint32_t*>(q + 4 * lane) = (uint32_t)lo | ((uint32_t)hi << 16);
   if (lane == 0) *scale_out = scale;
 }
