@@ -1,16 +1,25 @@
 #!/usr/bin/env python3
 """bench.py — DeepEP-style MoE dispatch+combine over the B200 GIN path.
 
-Workload (BASELINE.json configs[3]): high-throughput dispatch/combine with
-4096 tokens per rank, hidden 7168, top-8 of 256 experts, bf16 payloads, one
-rank per GPU (N = --gpus; at N=1 every expert is local and the path is
-HBM-bound; at N>1 the remote share crosses NVLink 5 peer mappings).
-A step = one dispatch (route + NVLink puts + per-expert releases) and one
-combine (expert transform fused into the return puts + flag wait + top-k
-weighted reduce) over one batch of synthetic tokens already in HBM.
+Workload (BASELINE.json configs[3], the metric's "at 8xB200" config):
+high-throughput dispatch/combine, 8 ranks x 4096 tokens per rank, hidden 7168,
+top-8 of 256 experts, in the reference's own u16 arithmetic (so both arms
+compute the identical function, bit for bit).
+  * --gpus 1: the 8 ranks are emulated on the one GPU (every rank's windows in
+    its HBM, one cooperative launch per phase with blockIdx.y = rank), so the
+    whole 8-rank protocol runs and the path is HBM-bound.
+  * --gpus N (torchrun): one rank per GPU, N ranks x 4096 tokens; the remote
+    share crosses NVLink 5 peer mappings.
+A step = one dispatch (route + puts + per-expert releases) and one combine
+(expert transform fused into the return puts + flag wait + top-k weighted
+reduce) over one batch of synthetic tokens already in HBM.  After the timed
+region the measured state is checked against the CPU oracle (outputs and
+every window record); `e2e` repeats the step through the public API with
+host buffers and the copies inside the timed region.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-For N>1 the driver launches it under torch.distributed.run (one rank per GPU).
+--impl reference runs the unmodified reference (oracle/_ref) on the same
+workload (a bounded token sample per step, stated in the line) on the host.
 Prints one JSON line on rank 0.
 """
 from __future__ import annotations
@@ -42,7 +51,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--tokens", type=int, default=N_TOK)
-    p.add_argument("--mode", type=int, default=1, help="0 = u16 exact, 1 = bf16")
+    p.add_argument("--mode", type=int, default=0, help="0 = u16 exact (the reference's arithmetic), 1 = bf16")
+    p.add_argument("--ranks", type=int, default=0, help="ranks per process (0 = 8 emulated at --gpus 1, else 1)")
+    p.add_argument("--no-verify", action="store_true", help="skip the post-run parity check against the oracle")
     p.add_argument("--layout", type=int, default=1, help="0 = reference layout, 1 = compact, 2 = compact + dedup transport")
     p.add_argument("--ctas", type=int, default=0)
     p.add_argument("--engine", type=int, default=0, help="0 = auto (TMA), 1 = LSU stores, 2 = TMA")
@@ -106,50 +117,115 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+# --------------------------------------------------------------------- workload (both arms)
+UNIT = "GB/s (dispatch+combine message bytes, all ranks)"
+
+
+def ranks_per_process(args, world):
+    """Ranks this process drives: at N=1 the BASELINE 8-rank HT config runs as 8
+    emulated ranks on the one GPU (one cooperative launch, blockIdx.y = rank);
+    under torchrun one rank per GPU."""
+    if args.ranks:
+        return args.ranks
+    return 8 if world == 1 else 1
+
+
+def workload(R, T, H=HIDDEN, K=TOPK, E=EXPERTS, mode=0):
+    arith = {0: "u16 reference arithmetic", 1: "bf16"}.get(mode, f"mode {mode}")
+    return f"DeepEP HT dispatch+combine: {R} ranks x {T} tokens/rank, hidden {H}, top-{K} of {E} experts, {arith}"
+
+
+def step_bytes(R, T, H=HIDDEN, K=TOPK):
+    """Algorithmic bytes of one step: every (token, k) message once each way."""
+    return R * T * K * ((2 * H + 16) + 2 * H)
+
+
 # --------------------------------------------------------------------- reference arm
-def ref_sample_bytes(n, T, K=TOPK, H=HIDDEN):
-    return n * T * K * ((2 * H + 16) + 2 * H)
+def mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
 
 
-def run_reference(args, steps, warmup):
-    """The reference's own CPU implementation (oracle/_ref = ginsim compiled from
-    /root/reference) on a bounded sample of the workload: run_moe_ll with 8
-    in-process ranks (2 host threads each), T=128 tokens/rank, hidden 7168,
-    top-8 of 256.  Metric: dispatch+combine bytes moved per second."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(R, T_max, steps, warmup, budget_s):
+    """The reference's own CPU implementation (oracle/_ref: ginsim compiled
+    from /root/reference by oracle/build_ref.sh) through its public harness
+    run_moe_ll (harness_moe.cpp:252) with R in-process ranks (2 host threads
+    each), hidden 7168, top-8 of 256, seed 1.  Each step is one run_moe_ll
+    call on a bounded sample of T_ref tokens per rank: the reference sizes
+    its receive windows for the worst case (T*(E+K)*(dmsg+cmsg) bytes per
+    rank, harness_moe.cpp:122-125), so T_ref is the largest power of two
+    <= T_max that fits 60% of MemAvailable and the time budget (from an
+    untimed calibration run at 128 tokens).  Throughput counts the same
+    message bytes as the GPU arm."""
     from oracle import oracle as O
     if not O.ref_available():
         return None
-    n_ref, t_ref = 8, 128
-    times = []
-    for i in range(warmup + steps):
-        j = O.ref_run("moe-ll", "--ranks", n_ref, "--experts", EXPERTS, "--topk", TOPK, "--tokens", t_ref,
-                      "--hidden", HIDDEN, "--seed", 1, "--backend", "direct")
-        if i >= warmup:
-            times.append(j["best_s"])
-    t = statistics.median(times)
-    gbs = ref_sample_bytes(n_ref, t_ref) / t / 1e9
-    return {"value": gbs, "s_per_sample": t, "cores": 2 * n_ref,
-            "sample": f"reference run_moe_ll (harness_moe.cpp:252), 8 in-process ranks x 2 threads, T=128/rank, "
-                      f"hidden 7168, top-8 of 256, verification included; median of {len(times)}"}
+    H, K, E = HIDDEN, TOPK, EXPERTS
+    per_token = R * (E + K) * ((2 * H + 16) + 2 * H)
+    mem = mem_available()
+
+    def once(T):
+        j = O.ref_run("moe-ll", "--ranks", R, "--experts", E, "--topk", K, "--tokens", T, "--hidden", H,
+                      "--seed", 1, "--backend", "direct", timeout=1800)
+        return j["best_s"]
+
+    t0 = min(128, T_max)
+    probe = once(t0)  # calibration (counts as the first warm-up run)
+    runs_left = steps + max(0, warmup - 1)
+    s_tok = probe / t0
+    T = T_max
+    while T > t0 and (T * per_token > 0.6 * mem or runs_left * s_tok * T > budget_s):
+        T //= 2
+    for _ in range(max(0, warmup - 1)):
+        once(T)
+    times = [once(T) for _ in range(steps)]
+    mean = sum(times) / len(times)
+    return {"value": step_bytes(R, T) / mean / 1e9, "s_per_step": mean, "tokens": T, "cores": min(2 * R, os.cpu_count() or 1),
+            "mem_available_gb": round(mem / 2**30, 1), "calibration_s": probe,
+            "sample": f"reference run_moe_ll (harness_moe.cpp:252) per step: {R} in-process ranks x 2 host threads, "
+                      f"{T} tokens/rank (largest power of two <= {T_max} fitting 60% of MemAvailable "
+                      f"{mem / 2**30:.0f} GiB and a {budget_s:.0f} s budget), hidden {H}, top-{K} of {E}, "
+                      f"u16, verification included; mean of {len(times)} after {warmup} warm-up"}
 
 
 def reference_main(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    r = run_reference(args, max(1, min(args.steps, 5)), min(1, args.warmup))
+    R = world * ranks_per_process(args, world)
+    budget = float(os.environ.get("GINSIM_REF_BUDGET_S", "240"))
+    r = run_reference(R, args.tokens, args.steps, args.warmup, budget)
     if r is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
         return
-    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s (dispatch+combine bytes, all ranks)",
-            "n_gpus": 0, "steps": max(1, min(args.steps, 5)), "warmup": min(1, args.warmup),
-            "ms_per_step": r["s_per_sample"] * 1e3, "higher_is_better": True, "scaling": "weak",
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["s_per_step"] * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-            "config": {"workload": "DeepEP dispatch/combine sample: 8 ranks x 128 tokens, hidden 7168, top-8/256",
-                       "requested_gpus": args.gpus},
-            "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["cores"], "kind": "reference",
+            "config": {"workload": workload(R, args.tokens), "ranks": R, "tokens_per_rank": args.tokens,
+                       "sample_tokens_per_rank": r["tokens"], "hidden": HIDDEN, "top_k": TOPK, "experts": EXPERTS,
+                       "device": "host CPU only (the reference has no GPU code)"},
+            "host": {"nproc": os.cpu_count(), "cpu_model": cpu_model(), "mem_available_gb": r["mem_available_gb"]},
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
                              "sample": r["sample"]},
-            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
@@ -438,6 +514,52 @@ def ctypes_stream(stream):
     return None if stream is None else stream.cuda_stream
 
 
+# --------------------------------------------------------------------- parity self-check
+def verify_step(G, torch, comms, moes, outs, seed, R_total, T, H, K, E, mode, layout, stream):
+    """Checker (after the timed region; never timed): every output token of
+    every local rank against the CPU oracle's combine (oracle/ginsim_oracle.c,
+    pinned to the reference), and every dispatch-window message and
+    combine-window record against the oracle's expected record digests
+    (device digests: ginsim_cuda_digest).  Bit-exact in u16 mode; bf16 mode
+    compares with the fp32-sequential oracle bit for bit as well."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    dev = outs[0].device
+    dmsg, cmsg = 2 * H + 16, 2 * H
+    slots = (R_total * T * K) if layout == 1 else (E // R_total) * R_total * T
+    got = []
+    for c, m, o in zip(comms, moes, outs):
+        dd = torch.empty(slots, dtype=torch.int64, device=dev)
+        cd = torch.empty(T * K, dtype=torch.int64, device=dev)
+        G.digest(c.window_ptr(m.win_dispatch, c.rank), dmsg, slots, dd, stream=stream)
+        G.digest(c.window_ptr(m.win_combine, c.rank), cmsg, T * K, cd, stream=stream)
+        got.append((dd, cd, o))
+    torch.cuda.synchronize()
+
+    def expect(r):
+        exp, _ = O.combine(seed, E, K, H, r, T, mode=mode)
+        d, v, cdig = O.window_digests(seed, R_total, E, K, T, H, r, mode=mode, layout=layout)
+        return exp, d, v, cdig
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(comms), os.cpu_count() or 1))) as ex:
+        exps = list(ex.map(expect, [c.rank for c in comms]))
+    ok_out = ok_disp = ok_comb = True
+    msgs = 0
+    for (dd, cd, o), (exp, d, v, cdig) in zip(got, exps):
+        out = o.view(torch.int16).cpu().numpy().view("<u2").reshape(T, H)
+        ok_out &= bool((out == exp).all())
+        dh = dd.cpu().numpy().view("<u8")
+        ok_disp &= bool((dh[v] == d[v]).all())
+        msgs += int(v.sum())
+        ok_comb &= bool((cd.cpu().numpy().view("<u8") == cdig).all())
+    return {"outputs": ok_out, "dispatch_windows": ok_disp, "combine_windows": ok_comb,
+            "ranks_checked": [c.rank for c in comms], "tokens_checked_per_rank": T,
+            "dispatch_messages_checked": msgs, "combine_records_checked": len(comms) * T * K,
+            "oracle": "oracle/ginsim_oracle.c (restatement pinned to the reference); records compared by digest",
+            "exact": True}
+
+
 # --------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -451,6 +573,12 @@ def main():
     import paper_2511_15076_b200 as G
 
     torch.cuda.set_device(local)
+    R = ranks_per_process(args, world)
+    if world > 1 and R != 1:
+        raise SystemExit("bench.py: one rank per GPU under torchrun (--ranks applies to --gpus 1)")
+    R_total = world * R
+    cfg_comm = G.Config(signal_cells=4096)
+    allgather = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
@@ -458,44 +586,43 @@ def main():
             out = [None] * world
             dist.all_gather_object(out, blob)
             return out
-        comm = G.Comm.create(rank, world, local, allgather, G.Config(signal_cells=4096))
+        comms = [G.Comm.create(rank, world, local, allgather, cfg_comm)]
     else:
-        allgather = None
-        comm = G.Comm.create_all([local], G.Config(signal_cells=4096))[0]
+        comms = G.Comm.create_all([local] * R, cfg_comm)
 
     T, H, K, E = args.tokens, HIDDEN, TOPK, EXPERTS
+    seed = 1
     cfg = G.MoeConfig(E, K, T, H, args.mode, args.layout, args.ctas, args.engine)
-    moe = G.Moe(comm, cfg)
+    moes = G.Moe.create_all(comms, cfg) if R > 1 else [G.Moe(comms[0], cfg)]
     dev = torch.device("cuda", local)
-    x = torch.empty(T * H, dtype=torch.int16, device=dev)
-    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
-    w = torch.empty(T * K, dtype=torch.float32 if args.mode == 1 else torch.int16, device=dev)
-    out = torch.empty(T * H, dtype=torch.int16, device=dev)
+    wdt = torch.float32 if args.mode == 1 else torch.int16
+    xs = [torch.empty(T * H, dtype=torch.int16, device=dev) for _ in comms]
+    idxs = [torch.empty(T * K, dtype=torch.int32, device=dev) for _ in comms]
+    ws = [torch.empty(T * K, dtype=wdt, device=dev) for _ in comms]
+    outs = [torch.empty(T * H, dtype=torch.int16, device=dev) for _ in comms]
     stream = torch.cuda.Stream(device=dev)
-    moe.generate(1, rank, x, idx, w, stream=stream)
+    for c, m, x, i, w in zip(comms, moes, xs, idxs, ws):
+        m.generate(seed, c.rank, x, i, w, stream=stream)
     torch.cuda.synchronize()
 
-    def step():
-        G.Moe.dispatch([moe], [x], [idx], stream=stream)
-        G.Moe.combine([moe], [w], [out], stream=stream)
+    def step(xb=xs, ib=idxs, wb=ws, ob=outs):
+        G.Moe.dispatch(moes, xb, ib, stream=stream)
+        G.Moe.combine(moes, wb, ob, stream=stream)
 
-    # algorithmic bytes (per rank): dispatch messages + combine messages
-    from numpy import array  # noqa: F401  (torch-only path below)
-    idx_host = idx.cpu().numpy().reshape(T, K)
-    e_local = E // world
-    remote_msgs = int(((idx_host // e_local) != rank).sum())
+    e_local = E // R_total
+    remote_msgs = 0
+    for c, i in zip(comms, idxs):
+        remote_msgs += int(((i.cpu().numpy().reshape(T, K) // e_local) != c.rank).sum())
     dmsg, cmsg = 2 * H + 16, 2 * H
-    disp_bytes = T * K * dmsg
-    comb_bytes = T * K * cmsg
-    step_bytes_rank = disp_bytes + comb_bytes
-    remote_bytes_rank = remote_msgs * (dmsg + cmsg)
+    bytes_step = step_bytes(R_total, T)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    comm.check_device()
+    for c in comms:
+        c.check_device()
 
-    # --- device-timed region: K steps, events around each kernel ---------------
+    # --- device-timed region: K steps, events around each launch ---------------
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local)
@@ -508,16 +635,17 @@ def main():
     start.record(stream)
     for i in range(args.steps):
         ev[i][0].record(stream)
-        G.Moe.dispatch([moe], [x], [idx], stream=stream)
+        G.Moe.dispatch(moes, xs, idxs, stream=stream)
         ev[i][1].record(stream)
-        G.Moe.combine([moe], [w], [out], stream=stream)
+        G.Moe.combine(moes, ws, outs, stream=stream)
         ev[i][2].record(stream)
     end.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
-    comm.check_device()
+    for c in comms:
+        c.check_device()
     total_ms = start.elapsed_time(end)
     d_ms = [e[0].elapsed_time(e[1]) for e in ev]
     c_ms = [e[1].elapsed_time(e[2]) for e in ev]
@@ -526,44 +654,62 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, d_mean, c_mean = t.tolist()
     ms_per_step = total_ms / args.steps
-    agg_bytes = step_bytes_rank * world
-    value = agg_bytes / (ms_per_step * 1e-3) / 1e9
+    value = bytes_step / (ms_per_step * 1e-3) / 1e9
 
-    # --- secondary configs on the same ranks: LL latency and put+signal RTT ---
-    ll = None if args.no_extras else measure_ll(G, comm, rank, world, dist, torch, dev, stream)
-    pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm, rank, world, dist, torch, dev)
-    a2a = None if (args.no_extras or world < 2) else measure_a2a(G, comm, rank, world, dist, torch, dev, stream)
-    barrier = None if (args.no_extras or world < 2) else measure_barrier(G, comm, rank, world, dist, torch, dev)
+    # --- parity self-check of the measured state (checker, untimed) ------------
+    parity = None
+    if not args.no_verify and args.mode in (0, 1) and args.layout in (0, 1):
+        try:
+            parity = verify_step(G, torch, comms, moes, outs, seed, R_total, T, H, K, E, args.mode, args.layout, stream)
+        except Exception as e:  # noqa: BLE001
+            parity = {"error": str(e)[:300]}
+        if world > 1:
+            okv = all(parity.get(k) is True for k in ("outputs", "dispatch_windows", "combine_windows"))
+            f = torch.tensor([1.0 if okv else 0.0], device=dev)
+            dist.all_reduce(f, op=dist.ReduceOp.MIN)
+            parity["all_ranks_ok"] = bool(f.item() == 1.0)
+
+    # --- secondary configs on a single-rank comm: LL latency, RTT, variants ----
+    if R > 1:
+        comm_x = G.Comm.create_all([local], cfg_comm)[0]
+    else:
+        comm_x = comms[0]
+    ll = None if args.no_extras else measure_ll(G, comm_x, rank, world, dist, torch, dev, stream)
+    pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm_x, rank, world, dist, torch, dev)
+    a2a = None if (args.no_extras or world < 2) else measure_a2a(G, comm_x, rank, world, dist, torch, dev, stream)
+    barrier = None if (args.no_extras or world < 2) else measure_barrier(G, comm_x, rank, world, dist, torch, dev)
     variants = None
     if not args.no_extras:
-        variants = {"fp8_ht": measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 1, 2,
+        variants = {"bf16_ht": measure_variant(G, comm_x, rank, world, dist, torch, dev, stream, T, 1, 1,
+                                               "bf16 payloads and arithmetic, compact layout"),
+                    "fp8_ht": measure_variant(G, comm_x, rank, world, dist, torch, dev, stream, T, 1, 2,
                                               "fp8 dispatch (e4m3 + per-128 scales), compact layout"),
-                    "fp8_ll": measure_variant(G, comm, rank, world, dist, torch, dev, stream, 128, 0, 2,
+                    "fp8_ll": measure_variant(G, comm_x, rank, world, dist, torch, dev, stream, 128, 0, 2,
                                               "fp8 dispatch, LL shape", steps=30),
-                    "fp8_both_ht": measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 1, 3,
+                    "fp8_both_ht": measure_variant(G, comm_x, rank, world, dist, torch, dev, stream, T, 1, 3,
                                                    "fp8 dispatch + fp8 combine messages, compact layout")}
         if world > 1:
-            variants["dedup_ht"] = measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, 2, 1,
+            variants["dedup_ht"] = measure_variant(G, comm_x, rank, world, dist, torch, dev, stream, T, 2, 1,
                                                    "dedup transport (layout 2), bf16")
     proxy = None
     if not args.no_extras:
-        ag = allgather if world > 1 else None
-        proxy = {"ll": measure_proxy(G, rank, world, local, dist, torch, dev, stream, ag, 128, 10),
-                 "ht": measure_proxy(G, rank, world, local, dist, torch, dev, stream, ag, T, 3)}
+        proxy = {"ll": measure_proxy(G, rank, world, local, dist, torch, dev, stream, allgather, 128, 10),
+                 "ht": measure_proxy(G, rank, world, local, dist, torch, dev, stream, allgather, T, 3)}
 
     # --- e2e: host buffers through the public API, copies inside the region ---
-    # Every step copies its inputs (x, topk_idx, weights) from pinned host
-    # memory and reads its output back.  The copies run on their own streams
-    # and are double-buffered, so step i+1's H2D and step i-1's D2H overlap
-    # step i's dispatch/combine (what a serving loop does); the region spans
-    # the first H2D to the last D2H.
+    # Every step copies every local rank's inputs (x, topk_idx, weights) from
+    # pinned host memory and reads every output back.  The copies run on their
+    # own streams and are double-buffered, so step i+1's H2D and step i-1's D2H
+    # overlap step i's dispatch/combine (what a serving loop does); the region
+    # spans the first H2D to the last D2H.
     e2e = None
     if not args.no_e2e:
-        xh = x.cpu().pin_memory()
-        ih = idx.cpu().pin_memory()
-        wh = w.cpu().pin_memory()
-        ohs = [torch.empty_like(out, device="cpu").pin_memory() for _ in range(2)]
-        xs, idxs, wss, outs = [x, x.clone()], [idx, idx.clone()], [w, w.clone()], [out, out.clone()]
+        xh = [x.cpu().pin_memory() for x in xs]
+        ih = [i.cpu().pin_memory() for i in idxs]
+        wh = [w.cpu().pin_memory() for w in ws]
+        ohs = [[torch.empty_like(o, device="cpu").pin_memory() for o in outs] for _ in range(2)]
+        bufs = [(xs, idxs, ws, outs), ([x.clone() for x in xs], [i.clone() for i in idxs], [w.clone() for w in ws],
+                                       [o.clone() for o in outs])]
         h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         e_steps = max(4, args.steps)
 
@@ -575,22 +721,24 @@ def main():
                 s_ev.record(h2d_s)
             for i in range(nsteps):
                 b = i % 2
+                bx, bi, bw, bo = bufs[b]
                 with torch.cuda.stream(h2d_s):
                     if i >= 2:
                         h2d_s.wait_event(comp_done[i - 2])   # buffer b free again
-                    xs[b].copy_(xh, non_blocking=True)
-                    idxs[b].copy_(ih, non_blocking=True)
-                    wss[b].copy_(wh, non_blocking=True)
+                    for j in range(len(comms)):
+                        bx[j].copy_(xh[j], non_blocking=True)
+                        bi[j].copy_(ih[j], non_blocking=True)
+                        bw[j].copy_(wh[j], non_blocking=True)
                     h2d_done[i].record(h2d_s)
                 stream.wait_event(h2d_done[i])
                 if i >= 2:
-                    stream.wait_event(d2h_done[i - 2])       # out[b] read back
-                G.Moe.dispatch([moe], [xs[b]], [idxs[b]], stream=stream)
-                G.Moe.combine([moe], [wss[b]], [outs[b]], stream=stream)
+                    stream.wait_event(d2h_done[i - 2])       # outputs of buffer b read back
+                step(bx, bi, bw, bo)
                 comp_done[i].record(stream)
                 with torch.cuda.stream(d2h_s):
                     d2h_s.wait_event(comp_done[i])
-                    ohs[b].copy_(outs[b], non_blocking=True)
+                    for j in range(len(comms)):
+                        ohs[b][j].copy_(bo[j], non_blocking=True)
                     d2h_done[i].record(d2h_s)
             if e_ev is not None:
                 stream.wait_event(d2h_done[-1])
@@ -606,11 +754,13 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = te.item() / e_steps
-        ok = bool((ohs[(e_steps - 1) % 2] == out.cpu()).all())
-        e2e = {"value": agg_bytes / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms, "steps": e_steps,
-               "h2d_bytes_per_step": int(xh.numel() * 2 + ih.numel() * 4 + wh.numel() * wh.element_size()),
-               "d2h_bytes_per_step": int(ohs[0].numel() * 2), "pipelined": "double-buffered H2D/D2H streams",
-               "output_matches_device_path": ok}
+        last = (e_steps - 1) % 2
+        ok = all(bool((ohs[last][j] == outs[j].cpu()).all()) for j in range(len(comms)))
+        e2e = {"value": bytes_step / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms, "steps": e_steps,
+               "h2d_bytes_per_step": int(sum(x.numel() * 2 + i.numel() * 4 + w.numel() * w.element_size()
+                                             for x, i, w in zip(xh, ih, wh))) * world,
+               "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in ohs[0])) * world,
+               "pipelined": "double-buffered H2D/D2H streams", "output_matches_device_path": ok}
 
     if rank != 0:
         if world > 1:
@@ -619,14 +769,16 @@ def main():
         return
 
     peak, peak_kind = load_peaks()
-    # dominant kernel and its algorithmic HBM bytes per launch
-    # Per-launch algorithmic HBM bytes.  Symmetric traffic: every message this
-    # rank writes lands in some rank's HBM and, on average, as many land here.
+    # dominant kernel and its algorithmic HBM bytes per launch:
+    # one launch covers the R ranks of this process.  Symmetric traffic: every
+    # message a rank writes lands in some rank's HBM and, on average, as many
+    # land in it.
     #   dispatch: read T rows (2H) + idx, write T*K messages (dmsg)
     #   combine (send + reduce kernels): read T*K messages, write T*K combine
     #   rows (cmsg), read them back, write T output rows (+ weights)
-    disp_hbm = T * H * 2 + T * K * 4 + T * K * dmsg
-    comb_hbm = T * K * dmsg + 2 * T * K * cmsg + T * H * 2 + T * K * 4
+    wb = 4 if args.mode == 1 else 2
+    disp_hbm = R * (T * H * 2 + T * K * 4 + T * K * dmsg)
+    comb_hbm = R * (T * K * dmsg + 2 * T * K * cmsg + T * H * 2 + T * K * wb)
     dom = "dispatch" if d_mean >= c_mean else "combine"
     dom_ms = max(d_mean, c_mean)
     dom_bytes = disp_hbm if dom == "dispatch" else comb_hbm
@@ -635,20 +787,26 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        traffic = tr.get("dispatch") if dom == "dispatch" else tr.get("combine", 0) + tr.get("reduce", 0)
+        key = f"R{R}"
+        tr = tr.get(key, tr)
+        traffic = tr.get("dispatch") if dom == "dispatch" else (tr.get("combine", 0) + tr.get("reduce", 0)) or None
     except Exception:  # noqa: BLE001
         pass
     line = {
-        "metric": METRIC, "value": value, "unit": "GB/s (dispatch+combine bytes, all GPUs)",
+        "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if args.mode == 1 else "u16", "data": "synthetic",
-        "config": {"workload": f"DeepEP HT dispatch+combine, {T} tokens/rank, hidden {H}, top-{K} of {E} experts, "
-                               f"{world} rank(s) x 1 GPU", "tokens_per_rank": T, "hidden": H, "top_k": K,
-                   "experts": E, "layout": "compact" if args.layout == 1 else "reference",
-                   "parallelism": f"ep{world}", "l2": "inputs larger than L2 (470 MB of messages per phase per rank)"},
+        "config": {"workload": workload(R_total, T, mode=args.mode), "ranks": R_total, "tokens_per_rank": T,
+                   "hidden": H, "top_k": K, "experts": E,
+                   "placement": (f"{R} ranks emulated on 1 GPU (one cooperative launch per phase)" if R > 1
+                                 else f"1 rank per GPU x {world}"),
+                   "layout": {0: "reference", 1: "compact", 2: "compact + dedup"}[args.layout],
+                   "parallelism": f"ep{R_total}",
+                   "l2": f"inputs larger than L2 ({R * T * K * dmsg / 1e6:.0f} MB of messages per phase per GPU)"},
         "us_per_step": ms_per_step * 1e3, "dispatch_us": d_mean * 1e3, "combine_us": c_mean * 1e3,
         "per_gpu_GBps": value / world,
+        "parity": parity,
         "roofline": {"bound": "hbm",
                      "kernel": ({"dispatch": "moe_dispatch_tma_kernel",
                                  "combine": "moe_combine_tma_kernel + moe_combine_reduce_kernel"}[dom]
@@ -657,7 +815,7 @@ def main():
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": dom_bytes},
         "clocks": clk,
-        # dispatch + combine-send + reduce kernels per step (2 with the LSU engines)
+        # dispatch + combine-send + reduce kernels per step (one launch covers every emulated rank)
         "gpu_launches": (3 if args.engine in (0, 2) else 2) * args.steps,
         "e2e": e2e,
         "ll": ll,
@@ -679,12 +837,12 @@ def main():
                                   "combine_remote_GBps includes the reduce kernel's time"}
     if world == 1 and not args.no_cpu_baseline:
         try:
-            r = run_reference(args, 3, 0)
+            r = run_reference(R_total, T, 2, 1, float(os.environ.get("GINSIM_CPU_BASELINE_BUDGET_S", "20")))
         except Exception as e:  # noqa: BLE001
             r = None
             line["cpu_baseline_error"] = str(e)[:200]
         if r:
-            line["cpu_baseline"] = {"value": r["value"], "unit": "GB/s", "cores": r["cores"], "kind": "reference",
+            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
                                     "sample": r["sample"]}
     print(json.dumps(line))
     if world > 1:

@@ -301,6 +301,17 @@ int ginsim_cuda_nvls_enabled(ginsim_cuda_comm_t comm, int* enabled);
 int ginsim_cuda_barrier_bench(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t mode, uint32_t iters,
                               uint64_t* ns_out, void* stream);
 
+/* ---- verification utility ----
+ * Per-record digests of `count` consecutive records of `record_bytes` at the
+ * device pointer `records` into out[count] (device memory):
+ *   digest(rec) = sum_i mix64(w_i + i * 0xD1B54A32D192ED03) mod 2^64
+ * over the record's little-endian u64 words (tail zero-padded), mix64 =
+ * harness_moe.cpp:17-22.  The large-shape analogue of the reference's
+ * in-program message verification (harness_moe.cpp:184-200, :227-242): the
+ * CPU checker computes the digests it expects and compares arrays, so a
+ * 3.76 GB window is verified without copying it to the host. */
+int ginsim_cuda_digest(const void* records, uint64_t record_bytes, uint64_t count, uint64_t* out, void* stream);
+
 /* ---- DeepEP-style MoE dispatch / combine (harness_moe.cpp:105-250) ---- */
 typedef struct ginsim_cuda_moe_config {
   uint32_t experts;  /* E, divisible by world */

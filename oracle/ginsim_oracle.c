@@ -664,3 +664,118 @@ void gso_fp8c_combine_window(uint64_t seed, uint32_t experts, uint32_t top_k, ui
   free(q);
   free(sc);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Record digests for the large-shape checks (bench self-check, the 8-rank
+ * T=4096 GPU test).  Same definition as the device utility
+ * (paper_2511_15076_b200/csrc/verify.cu, include/ginsim_cuda.h
+ * ginsim_cuda_digest):  digest = sum_i mix64(w_i + i*0xD1B54A32D192ED03)
+ * over the record's little-endian u64 words, tail zero-padded. */
+static uint64_t dg_word(uint64_t w, uint64_t i) { return gso_mix64(w + i * 0xD1B54A32D192ED03ull); }
+
+uint64_t gso_digest(const uint8_t* p, uint64_t bytes) {
+  uint64_t acc = 0, j = 0;
+  for (; 8 * j + 8 <= bytes; ++j) {
+    uint64_t w;
+    memcpy(&w, p + 8 * j, 8);  /* little-endian host */
+    acc += dg_word(w, j);
+  }
+  if (8 * j < bytes) {
+    uint64_t w = 0;
+    for (uint32_t b = 0; 8 * j + b < bytes; ++b) w |= (uint64_t)p[8 * j + b] << (8 * b);
+    acc += dg_word(w, j);
+  }
+  return acc;
+}
+
+/* Digests of every record rank r holds after one moe-ll step
+ * (proj/core/src/harness_moe.cpp:105-250), mode 0 (u16, the reference's
+ * arithmetic) or 1 (bf16):
+ *   disp[s], valid[s]: dispatch window slot s (layout 0: ((e_loc*n+src)*T+slot),
+ *     harness_moe.cpp:135-137; layout 1: src*T*K + prefix(e_loc) + slot, the
+ *     compact per-source layout); valid[s] = 1 where a message lands.  Slots:
+ *     layout 0 e_local*n*T, layout 1 n*T*K.
+ *   comb[t*K+k]: combine window record (token*K+k)*cmsg of rank r
+ *     (harness_moe.cpp:203-205), the expert transform of r's own token.
+ * Payload digests are computed once per token (its K messages share the row;
+ * only the 16-byte meta differs) when 2*hidden is a multiple of 8. */
+int gso_moe_window_digests(uint64_t seed, uint32_t n, uint32_t experts, uint32_t top_k, uint32_t T,
+                           uint32_t hidden, uint32_t mode, uint32_t layout, uint32_t r, uint64_t* disp,
+                           uint8_t* valid, uint64_t* comb) {
+  if (n == 0 || experts % n || top_k > 256 || top_k > experts || mode > 1 || layout > 1) return -1;
+  const uint32_t e_local = experts / n;
+  const uint64_t dmsg = 2ull * hidden + 16, cmsg = 2ull * hidden;
+  const uint64_t slots = layout == 0 ? (uint64_t)e_local * n * T : (uint64_t)n * T * top_k;
+  const int split = (2ull * hidden) % 8 == 0;
+  const uint64_t pw = 2ull * hidden / 8;  /* payload words when split */
+  uint32_t* route = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)T * top_k);
+  uint32_t* sent = (uint32_t*)calloc(e_local, sizeof(uint32_t));
+  uint32_t* pre = (uint32_t*)calloc(e_local + 1, sizeof(uint32_t));
+  uint16_t* row = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)hidden + 16);
+  uint8_t* msg = (uint8_t*)malloc(dmsg);
+  memset(valid, 0, slots);
+  memset(disp, 0, slots * sizeof(uint64_t));
+  for (uint32_t src = 0; src < n; ++src) {
+    gso_route_table(seed, experts, top_k, src, T, route);
+    memset(sent, 0, sizeof(uint32_t) * e_local);
+    for (size_t j = 0; j < (size_t)T * top_k; ++j)
+      if (route[j] / e_local == r) sent[route[j] % e_local]++;
+    pre[0] = 0;
+    for (uint32_t e = 0; e < e_local; ++e) pre[e + 1] = pre[e] + sent[e];
+    memset(sent, 0, sizeof(uint32_t) * e_local);
+    for (uint32_t t = 0; t < T; ++t) {
+      const uint32_t* ex = route + (size_t)t * top_k;
+      int mine = 0;
+      for (uint32_t k = 0; k < top_k; ++k) mine |= ex[k] / e_local == r;
+      if (!mine) continue;
+      for (uint32_t i = 0; i < hidden; ++i)
+        row[i] = mode == 0 ? gso_token_element(seed, src, t, i) : gso_bf16_token(seed, src, t, i);
+      uint64_t pd = 0;
+      if (split)
+        for (uint64_t j = 0; j < pw; ++j) {
+          uint64_t w;
+          memcpy(&w, (const uint8_t*)row + 8 * j, 8);
+          pd += dg_word(w, j);
+        }
+      for (uint32_t k = 0; k < top_k; ++k) {
+        const uint32_t e = ex[k];
+        if (e / e_local != r) continue;
+        const uint32_t e_loc = e % e_local, slot = sent[e_loc]++;
+        const uint64_t s = layout == 0 ? ((uint64_t)e_loc * n + src) * T + slot
+                                       : (uint64_t)src * T * top_k + pre[e_loc] + slot;
+        uint64_t d;
+        if (split) {
+          d = pd + dg_word((uint64_t)src | ((uint64_t)t << 32), pw) + dg_word((uint64_t)k | ((uint64_t)(k + 1) << 32), pw + 1);
+        } else {
+          for (uint32_t i = 0; i < hidden; ++i) st16(msg + 2ull * i, row[i]);
+          st32(msg + 2ull * hidden + 0, src);
+          st32(msg + 2ull * hidden + 4, t);
+          st32(msg + 2ull * hidden + 8, k);
+          st32(msg + 2ull * hidden + 12, k + 1);
+          d = gso_digest(msg, dmsg);
+        }
+        disp[s] = d;
+        valid[s] = 1;
+      }
+    }
+  }
+  /* combine records: r's own tokens, transformed by the expert each went to */
+  gso_route_table(seed, experts, top_k, r, T, route);
+  for (uint32_t t = 0; t < T; ++t) {
+    uint16_t* x = row;
+    for (uint32_t i = 0; i < hidden; ++i)
+      x[i] = mode == 0 ? gso_token_element(seed, r, t, i) : gso_bf16_token(seed, r, t, i);
+    for (uint32_t k = 0; k < top_k; ++k) {
+      const uint32_t e = route[(size_t)t * top_k + k];
+      for (uint32_t i = 0; i < hidden; ++i)
+        st16(msg + 2ull * i, mode == 0 ? gso_expert_transform(x[i], e) : gso_bf16_transform(x[i], e));
+      comb[(size_t)t * top_k + k] = gso_digest(msg, cmsg);
+    }
+  }
+  free(route);
+  free(sent);
+  free(pre);
+  free(row);
+  free(msg);
+  return 0;
+}

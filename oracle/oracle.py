@@ -251,3 +251,31 @@ def ref_run(*args, timeout=900):
     if r.returncode != 0:
         raise RuntimeError(f"reference driver failed: {r.stdout} {r.stderr}")
     return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+# ---------------------------------------------------------------- digests
+def digest(buf):
+    """gso_digest of a byte buffer (the device utility ginsim_cuda_digest's definition)."""
+    a = np.ascontiguousarray(np.frombuffer(bytes(buf), np.uint8) if not isinstance(buf, np.ndarray) else buf.view(np.uint8))
+    L = lib()
+    L.gso_digest.restype = c_uint64
+    L.gso_digest.argtypes = [POINTER(c_uint8), c_uint64]
+    return int(L.gso_digest(_p(a, c_uint8), a.nbytes))
+
+
+def window_digests(seed, n, E, K, T, H, r, mode=0, layout=1):
+    """Expected per-record digests of rank r after one step: (dispatch slot
+    digests, valid mask, combine record digests[T*K]).  Slots: layout 0
+    e_local*n*T (harness_moe.cpp:135-137), layout 1 n*T*K (compact)."""
+    L = lib()
+    L.gso_moe_window_digests.restype = c_int
+    L.gso_moe_window_digests.argtypes = [c_uint64, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32,
+                                         c_uint32, c_uint32, POINTER(c_uint64), POINTER(c_uint8), POINTER(c_uint64)]
+    slots = (E // n) * n * T if layout == 0 else n * T * K
+    d = np.zeros(slots, np.uint64)
+    v = np.zeros(slots, np.uint8)
+    c = np.zeros(T * K, np.uint64)
+    rc = L.gso_moe_window_digests(seed, n, E, K, T, H, mode, layout, r, _p(d, c_uint64), _p(v, c_uint8), _p(c, c_uint64))
+    if rc != 0:
+        raise ValueError(f"gso_moe_window_digests rc={rc}")
+    return d, v.astype(bool), c

@@ -220,6 +220,7 @@ def _declare(L):
         "ginsim_cuda_moe_phase_times": ([P, c_uint32, POINTER(c_uint64), POINTER(c_uint32)], c_int),
         "ginsim_cuda_moe_last_launch": ([P, POINTER(c_uint32), POINTER(c_uint32)], c_int),
         "ginsim_cuda_moe_transport": ([P, POINTER(c_uint32)], c_int),
+        "ginsim_cuda_digest": ([P, c_uint64, c_uint64, P, P], c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name, None)
@@ -464,6 +465,13 @@ class Gin:
 def pool_select(channel_id: int, n_contexts: int = 4):
     """runtime.hpp:51-58: flat channel id -> (comm index, context index)."""
     return channel_id // n_contexts, channel_id % n_contexts
+
+
+def digest(records, record_bytes, count, out, stream=None):
+    """Per-record digests of `count` records at device pointer `records` into
+    the device buffer `out` (count u64): the checker compares them with the
+    CPU oracle's (ginsim_cuda_digest, include/ginsim_cuda.h)."""
+    check(lib().ginsim_cuda_digest(_ptr(records), record_bytes, count, _ptr(out), _stream(stream)))
 
 
 def descriptor_encode(d: Descriptor) -> bytes:
