@@ -246,6 +246,26 @@ class DevComm {
       if (w->id() == id) return *w;
     throw UnknownWindow("window " + std::to_string(id) + " was never registered");
   }
+  // B200 addition (no reference counterpart): release a window on this rank;
+  // the id is reused by the next window_register (ginsim_cuda.h).
+  void window_deregister(WindowId id) {
+    check(ginsim_cuda_window_deregister(c_, id));
+    windows_.erase(std::remove_if(windows_.begin(), windows_.end(), [&](const auto& w) { return w->id() == id; }),
+                   windows_.end());
+  }
+
+  // Sub-teams (runtime.hpp:145-148, runtime.cpp:329-343).  World is id 0.
+  const Team& register_team(Team team) {
+    check(ginsim_cuda_register_team(c_, team.id, team.members.data(), static_cast<uint32_t>(team.members.size())));
+    teams_.push_back(std::make_unique<Team>(std::move(team)));
+    return *teams_.back();
+  }
+  const Team& team(TeamId id) const {
+    if (id == 0) return world_team_;
+    for (auto& t : teams_)
+      if (t->id == id) return *t;
+    throw UsageError("team " + std::to_string(id) + " not registered");
+  }
 
   uint64_t read_signal(SignalId id) const {
     uint64_t v = 0;
@@ -290,6 +310,7 @@ class DevComm {
   int device_ = 0;
   BackendKind backend_ = BackendKind::Direct;
   Team world_team_;
+  std::vector<std::unique_ptr<Team>> teams_;
   std::vector<std::unique_ptr<Window>> windows_;
 };
 

@@ -136,9 +136,31 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
  * harness_launch.cpp:16-63).  ptrs[r]/bytes[r] as for window_register. */
 int ginsim_cuda_window_register_all(const ginsim_cuda_comm_t* comms, uint32_t n, void* const* ptrs,
                                     const uint64_t* bytes, uint32_t* window_id);
+/* Releases window `window_id` on this rank (no reference counterpart: the
+ * reference never deregisters; SURVEY.md §8(b) lists it for GPU memory
+ * lifetime).  Local, not collective: waits for this rank's device work, then
+ * unmaps the peer regions imported for the window and frees the id, which the
+ * next window_register reuses (lowest free id first), so ranks that register
+ * and deregister in the same order keep agreeing on ids.  Every rank must
+ * deregister before any rank registers a window into the freed id.  The local
+ * bytes stay owned by the caller (free them with ginsim_cuda_mem_free after
+ * every rank has deregistered).  UNKNOWN_WINDOW if not registered. */
+int ginsim_cuda_window_deregister(ginsim_cuda_comm_t comm, uint32_t window_id);
 /* Window::size_of (types.hpp:105) and the peer mapping of rank's region. */
 int ginsim_cuda_window_size(ginsim_cuda_comm_t comm, uint32_t window_id, uint32_t rank, uint64_t* bytes);
 int ginsim_cuda_window_ptr(ginsim_cuda_comm_t comm, uint32_t window_id, uint32_t rank, void** ptr);
+
+/* ---------------------------------------------------------------- teams
+ * DevComm::register_team / team (runtime.hpp:145-148, runtime.cpp:329-343).
+ * Local.  The world team (id 0, identity) is always present.  members[i] is
+ * the world rank of team rank i.  USAGE on an empty team, a duplicate id or a
+ * full table (16 teams); INVALID_PEER for a member outside the world.  The
+ * device API's gin::Gin::team(id) returns the registered team; on the Proxy
+ * backend descriptors carry (team id, team-relative peer) and the host agent
+ * resolves the world rank (proxy_backend.cpp:72). */
+int ginsim_cuda_register_team(ginsim_cuda_comm_t comm, uint32_t team_id, const uint32_t* members, uint32_t n);
+/* members[] receives up to 8 world ranks; USAGE if the id is not registered. */
+int ginsim_cuda_team(ginsim_cuda_comm_t comm, uint32_t team_id, uint32_t* members, uint32_t* n);
 
 /* ---------------------------------------------------------------- host ops
  * Host-issued one-sided ops (Gin, runtime.hpp:260-306), executed on the GPU
@@ -185,6 +207,72 @@ int ginsim_cuda_proxy_trace(ginsim_cuda_comm_t comm, double* out, uint32_t max_r
 int ginsim_cuda_proxy_stats(ginsim_cuda_comm_t comm, uint64_t* descriptors, uint64_t* copies,
                             uint64_t* busy_ns, uint64_t* wall_ns);
 
+/* ---------------------------------------------------------------- plugin boundary
+ * FabricPlugin (proj/core/include/ginsim/plugin.hpp:64-144, plugin.cpp:18-172)
+ * and DirectContext (direct_backend.hpp:17-63, direct_backend.cpp:7-57), so a
+ * host runtime written against the reference's plugin interface drives the
+ * GPU backends.  The semantics must match the comm's backend (0 direct,
+ * 1 proxy); a call of the other semantics raises BACKEND_MISMATCH.
+ * Memory-region handles are the window ids (reg_mr is idempotent). */
+typedef struct ginsim_cuda_plugin_s* ginsim_cuda_plugin_t;
+typedef struct ginsim_cuda_direct_ctx_s* ginsim_cuda_direct_ctx_t;
+
+/* PutSource (plugin.hpp:39-46): a registered window range, or <= 8 inline
+ * little-endian bytes carried in the descriptor. */
+typedef struct ginsim_cuda_put_source {
+  uint32_t is_inline;
+  uint32_t mr;          /* source window (when !is_inline) */
+  uint64_t offset;      /* in the source window */
+  uint64_t inline_value;
+} ginsim_cuda_put_source;
+
+/* ResolvedOp (direct_backend.hpp:17-27): team translation already applied. */
+typedef struct ginsim_cuda_resolved_op {
+  uint32_t opcode;      /* 1 PUT, 2 PUT_INLINE, 3 SIGNAL_ONLY */
+  uint32_t peer;        /* world rank */
+  uint32_t dst_window;
+  uint32_t src_window;  /* 0xFFFFFFFF inline */
+  uint64_t dst_offset;
+  uint64_t src_offset_or_value;
+  uint64_t bytes;
+  ginsim_cuda_action action;
+} ginsim_cuda_resolved_op;
+
+int ginsim_cuda_plugin_create(ginsim_cuda_comm_t comm, uint32_t semantics, ginsim_cuda_plugin_t* out);
+int ginsim_cuda_plugin_destroy(ginsim_cuda_plugin_t plugin);
+/* reg_mr (plugin.hpp:78): idempotent; UNKNOWN_WINDOW if the window is not registered. */
+int ginsim_cuda_plugin_reg_mr(ginsim_cuda_plugin_t plugin, uint32_t window_id, uint32_t* mr);
+int ginsim_cuda_plugin_is_registered(ginsim_cuda_plugin_t plugin, uint32_t window_id, int* registered);
+/* iput / iput_signal (plugin.hpp:86-90), proxy semantics: the op goes to the
+ * comm's host agent (copy engine + stream-memop signal/counter after the
+ * copy); *request is unique until retired.  iput with a remote signal in
+ * `action` is GENERIC ("use iput_signal"); UNKNOWN_WINDOW for an unregistered
+ * mr; OUT_OF_BOUNDS / INVALID_PEER / INVALID_CONTEXT as submit_op. */
+int ginsim_cuda_plugin_iput(ginsim_cuda_plugin_t plugin, const ginsim_cuda_put_source* src, uint32_t dst_mr,
+                            uint64_t dst_offset, uint64_t bytes, uint32_t peer, uint32_t ctx,
+                            const ginsim_cuda_action* action, uint64_t* request);
+int ginsim_cuda_plugin_iput_signal(ginsim_cuda_plugin_t plugin, const ginsim_cuda_put_source* src, uint32_t dst_mr,
+                                   uint64_t dst_offset, uint64_t bytes, uint32_t peer, uint32_t ctx,
+                                   uint32_t signal_id, uint32_t signal_add, uint64_t operand,
+                                   const ginsim_cuda_action* action, uint64_t* request);
+/* test (plugin.hpp:93): *done = 1 once the request's put has completed
+ * (idempotent); UNKNOWN_HANDLE for an unknown or retired id. */
+int ginsim_cuda_plugin_test(ginsim_cuda_plugin_t plugin, uint64_t request, int* done);
+/* retire (plugin.hpp:97): releases a completed request and returns its
+ * completion action; UNKNOWN_HANDLE if unknown/retired, GENERIC before completion. */
+int ginsim_cuda_plugin_retire(ginsim_cuda_plugin_t plugin, uint64_t request, ginsim_cuda_action* action);
+int ginsim_cuda_plugin_outstanding(ginsim_cuda_plugin_t plugin, uint64_t* requests);
+/* create_context (plugin.hpp:105), direct semantics: the posting object of
+ * context ctx (one CUDA stream); INVALID_CONTEXT when ctx >= n_contexts. */
+int ginsim_cuda_plugin_create_context(ginsim_cuda_plugin_t plugin, uint32_t ctx, ginsim_cuda_direct_ctx_t* out);
+/* DirectContext::post / poll / outstanding (direct_backend.cpp:11-57): post
+ * launches the op on the context's stream (NVLink stores, red.release.sys
+ * signal, counter bump on the device); poll retires the ops the stream has
+ * executed (*retired = how many); outstanding = posted minus retired. */
+int ginsim_cuda_direct_post(ginsim_cuda_direct_ctx_t ctx, const ginsim_cuda_resolved_op* op);
+int ginsim_cuda_direct_poll(ginsim_cuda_direct_ctx_t ctx, uint64_t* retired);
+int ginsim_cuda_direct_outstanding(ginsim_cuda_direct_ctx_t ctx, uint64_t* outstanding);
+
 /* ---------------------------------------------------------------- descriptor codec
  * proj/core/src/descriptor.cpp:148-199 (encode_descriptor / decode_descriptor),
  * 64-byte little-endian layout of descriptor.hpp:13-27. */
@@ -225,6 +313,15 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
                          uint32_t send_win, uint32_t recv_win, uint64_t bytes, uint32_t iters,
                          uint32_t warmup, uint32_t signal_id, uint32_t threads, uint64_t* rtt_ns_out,
                          void* stream);
+
+/* Raw NVLink round-trip floor: one thread per rank flips
+ * a flag word in the peer's signal table and polls its own -- no put, no API.
+ * mode 0 = st.release.sys / ld.acquire.sys, mode 1 = relaxed .sys (no
+ * ordering).  rtt_ns_out as for ping-pong (iters u64, written by peer0).
+ * Cells signal_id (the flag) and signal_id+1 (a launch handshake) must be
+ * dedicated to it. */
+int ginsim_cuda_rtt_floor(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1, uint32_t mode,
+                          uint32_t iters, uint32_t warmup, uint32_t signal_id, uint64_t* rtt_ns_out, void* stream);
 
 /* Roofline probe: copy `bytes` from this rank's src window into `peer`'s dst
  * window (peer == own rank: local HBM copy) `iters` times with the put path's
@@ -278,6 +375,14 @@ int ginsim_cuda_ordering_stress(const ginsim_cuda_comm_t* comms, uint32_t n, uin
  * flush, barrier.  VERIFICATION_FAILURE through the device error word. */
 int ginsim_cuda_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_win,
                      uint32_t recv_win, uint64_t bytes, uint32_t rounds, void* stream);
+
+/* The same ring over a registered team (team_id 0 = world): team rank i puts
+ * to team rank (i+1) % |team| with SignalInc on `signal_id` and syncs a
+ * BarrierSession over the team; non-members return at once.  The device
+ * validates the op (submit_op, runtime.cpp:474-507): an out-of-range
+ * signal_id raises INVALID_SIGNAL, an unregistered team RANK_OUT_OF_RANGE. */
+int ginsim_cuda_team_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t team_id, uint32_t send_win,
+                          uint32_t recv_win, uint64_t bytes, uint32_t rounds, uint32_t signal_id, void* stream);
 
 /* moe-ht circular-buffer flow control (harness_moe.cpp:283-382) on the
  * device: `channels` channels, `slots`-deep rings of 256-byte stamped slots,
@@ -340,7 +445,14 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
 /* moe_create for every rank of an in-process group from one caller thread. */
 int ginsim_cuda_moe_create_all(const ginsim_cuda_comm_t* comms, uint32_t n, const ginsim_cuda_moe_config* cfg,
                                ginsim_cuda_moe_t* out);
+/* Waits for the rank's device work (and, on the Proxy backend, for the agent
+ * to drain every submitted descriptor), deregisters and frees the handle's
+ * windows and scratch, and returns its signal-cell range for reuse by a later
+ * moe_create (which zeroes the range between two barriers). */
 int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe);
+/* The handle's signal cells: [first, first + span) = local expert cells
+ * (e_local), the combine flag, the rows cell and the dedup chunk cells. */
+int ginsim_cuda_moe_cells(ginsim_cuda_moe_t moe, uint32_t* first, uint32_t* span);
 int ginsim_cuda_moe_windows(ginsim_cuda_moe_t moe, uint32_t* dispatch_win, uint32_t* count_win,
                             uint32_t* combine_win);
 

@@ -220,7 +220,17 @@ def _declare(L):
         "ginsim_cuda_moe_phase_times": ([P, c_uint32, POINTER(c_uint64), POINTER(c_uint32)], c_int),
         "ginsim_cuda_moe_last_launch": ([P, POINTER(c_uint32), POINTER(c_uint32)], c_int),
         "ginsim_cuda_moe_transport": ([P, POINTER(c_uint32)], c_int),
+        "ginsim_cuda_moe_cells": ([P, POINTER(c_uint32), POINTER(c_uint32)], c_int),
         "ginsim_cuda_digest": ([P, c_uint64, c_uint64, P, P], c_int),
+        "ginsim_cuda_window_deregister": ([P, c_uint32], c_int),
+        "ginsim_cuda_plugin_create": ([P, c_uint32, POINTER(P)], c_int),
+        "ginsim_cuda_plugin_destroy": ([P], c_int),
+        "ginsim_cuda_rtt_floor": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, P,
+                                   P], c_int),
+        "ginsim_cuda_team_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, P],
+                                  c_int),
+        "ginsim_cuda_register_team": ([P, c_uint32, POINTER(c_uint32), c_uint32], c_int),
+        "ginsim_cuda_team": ([P, c_uint32, POINTER(c_uint32), POINTER(c_uint32)], c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name, None)
@@ -344,6 +354,21 @@ class Comm:
         for c in comms:
             c.n_windows = max(c.n_windows, wid.value + 1)
         return wid.value
+
+    def window_deregister(self, win):
+        """Release window `win` on this rank (local; ids are reused lowest-first)."""
+        check(lib().ginsim_cuda_window_deregister(self.h, win))
+
+    # -- teams (runtime.hpp:145-148)
+    def register_team(self, team_id, members):
+        m = (c_uint32 * len(members))(*members)
+        check(lib().ginsim_cuda_register_team(self.h, team_id, m, len(members)))
+
+    def team(self, team_id):
+        m = (c_uint32 * 8)()
+        n = c_uint32()
+        check(lib().ginsim_cuda_team(self.h, team_id, m, byref(n)))
+        return list(m[:n.value])
 
     def window_size(self, win, rank):
         v = c_uint64()
@@ -529,6 +554,12 @@ class Moe:
         n = len(moes)
         check(lib().ginsim_cuda_moe_combine(_arr([m.h.value for m in moes]), n, _arr([_ptr(w) for w in ws]),
                                             _arr([_ptr(o) for o in outs]), _stream(stream)))
+
+    def cells(self):
+        """(first, span) of the signal cells this handle owns."""
+        a, b = c_uint32(), c_uint32()
+        check(lib().ginsim_cuda_moe_cells(self.h, byref(a), byref(b)))
+        return a.value, b.value
 
     def last_launch(self):
         a, b = c_uint32(), c_uint32()

@@ -71,6 +71,18 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
                : "l"(p));
   return v;
 }
+// Coherent (weak, non-.nc) 128-bit load that skips L1 allocation: for data
+// other GPUs write into this rank's windows while the reading kernel runs,
+// read after the acquire of the flag that publishes it (.nc is only valid for
+// data that is read-only for the kernel's whole lifetime).
+__device__ __forceinline__ uint4 ld_na_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ uint4 ld_v4(const void* p) {
   uint4 v;
   asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -149,16 +161,29 @@ __device__ __host__ inline Action WithCounter(Action a, uint32_t id) {
   return a;
 }
 
-// Team: an ordered subset of world ranks (types.hpp:75-84).  World = identity.
+// Team: an ordered subset of world ranks (types.hpp:75-84).  World = id 0,
+// identity.  Sub-teams used on the Proxy backend must be registered on the
+// comm (ginsim_cuda_register_team, runtime.cpp:329-343): the descriptor
+// carries (team id, team-relative peer) and the host agent resolves it
+// (proxy_backend.cpp:72).
 struct Team {
+  uint32_t id;
   uint32_t n;
   uint8_t members[GIN_MAX_RANKS];
   __device__ __host__ uint32_t world_rank(uint32_t team_rank) const { return members[team_rank]; }
 };
 __device__ __host__ inline Team WorldTeam(uint32_t world) {
   Team t;
+  t.id = 0;
   t.n = world;
   for (uint32_t i = 0; i < GIN_MAX_RANKS; ++i) t.members[i] = (uint8_t)i;
+  return t;
+}
+__device__ __host__ inline Team TeamFromView(const GinTeamView& tv) {
+  Team t;
+  t.id = tv.id;
+  t.n = tv.n;
+  for (uint32_t i = 0; i < GIN_MAX_RANKS; ++i) t.members[i] = tv.members[i];
   return t;
 }
 
@@ -186,7 +211,16 @@ __device__ __forceinline__ void coop_copy(const Coop& c, char* dst, const char* 
       st_v4(d + i + 3 * n, f);
     }
     for (; i < nv; i += n) st_v4(d + i, ld_v4(s + i));
-    for (uint64_t j = (nv << 4) + r; j < bytes; j += n) dst[j] = src[j];
+    uint64_t j = nv << 4;
+    if (j + 8 <= bytes) {  // an 8-byte tail word in one store (small puts: one NVLink write)
+      if (r == 0) *reinterpret_cast<uint64_t*>(dst + j) = *reinterpret_cast<const uint64_t*>(src + j);
+      j += 8;
+    }
+    for (j += r; j < bytes; j += n) dst[j] = src[j];
+  } else if ((((uintptr_t)dst | (uintptr_t)src) & 7) == 0) {
+    uint64_t j = 8ull * r;
+    for (; j + 8 <= bytes; j += 8ull * n) *reinterpret_cast<uint64_t*>(dst + j) = *reinterpret_cast<const uint64_t*>(src + j);
+    for (uint64_t k = (bytes & ~7ull) + r; k < bytes; k += n) dst[k] = src[k];
   } else {
     for (uint64_t j = r; j < bytes; j += n) dst[j] = src[j];
   }
@@ -213,6 +247,7 @@ class Gin {
   __device__ void put(const Coop& c, const Team& team, uint32_t peer, uint32_t dst_win,
                       uint64_t dst_off, uint32_t src_win, uint64_t src_off, uint64_t bytes,
                       Action a = NoAction()) const {
+    if (!check_op(team, peer, a)) return;
     const uint32_t p = team.world_rank(peer);
     if (!check_range(dst_win, p, dst_off, bytes) || !check_range(src_win, v_->rank, src_off, bytes)) return;
     if (v_->backend == GIN_BACKEND_PROXY) {
@@ -239,6 +274,7 @@ class Gin {
   __device__ void put_value_raw(const Coop& c, const Team& team, uint32_t peer, uint32_t dst_win,
                                 uint64_t dst_off, uint64_t le_value, uint32_t width,
                                 Action a = NoAction()) const {
+    if (!check_op(team, peer, a)) return;
     const uint32_t p = team.world_rank(peer);
     if (width == 0 || width > 8) {
       if (c.rank() == 0) raise_error(v_, GIN_DEVERR_OUT_OF_BOUNDS);
@@ -283,6 +319,7 @@ class Gin {
     Action a = extra;
     a.signal_id = (int32_t)id;
     a.op = op;
+    if (!check_op(team, peer, a)) return;
     const uint32_t p = team.world_rank(peer);
     if (v_->backend == GIN_BACKEND_PROXY) {
       c.sync();
@@ -316,6 +353,10 @@ class Gin {
 
   // --- completion state (ID-addressed cells) -------------
   __device__ uint64_t read_signal(uint32_t id) const {
+    if (id >= v_->signal_cells) {
+      raise_error(v_, GIN_DEVERR_INVALID_SIGNAL);
+      return ~0ull;  // waits on an invalid cell end at once (the error word is set)
+    }
     uint64_t s = 0;
     for (uint32_t src = 0; src < v_->world; ++src) s += ld_acquire_sys(sub_cell(v_->rank, src, id));
     return s - ld_relaxed_sys(v_->signal_base + id);
@@ -335,14 +376,49 @@ class Gin {
     }
     c.sync();
   }
+  // Point-to-point waits for latency-critical handoffs with one known sender:
+  // the raw value of the sub-cell `src` writes for cell `id` (its running sum
+  // of signals to this rank, never reset by reset_signal), polled with ONE
+  // acquire load per iteration and no backoff.  read_signal/wait_signal sum
+  // every source's sub-cell instead.
+  __device__ uint64_t read_signal_from(uint32_t src, uint32_t id) const {
+    if (id >= v_->signal_cells || src >= v_->world) {
+      raise_error(v_, id >= v_->signal_cells ? GIN_DEVERR_INVALID_SIGNAL : GIN_DEVERR_INVALID_PEER);
+      return ~0ull;
+    }
+    return ld_acquire_sys(sub_cell(v_->rank, src, id));
+  }
+  __device__ void wait_signal_from(uint32_t src, uint32_t id, uint64_t raw_target) const {
+    if (id >= v_->signal_cells || src >= v_->world) {
+      raise_error(v_, id >= v_->signal_cells ? GIN_DEVERR_INVALID_SIGNAL : GIN_DEVERR_INVALID_PEER);
+      return;
+    }
+    const uint64_t* p = sub_cell(v_->rank, src, id);
+    const uint64_t t0 = globaltimer();
+    for (uint32_t spins = 1; ld_acquire_sys(p) < raw_target; ++spins) {
+      if ((spins & 4095) == 0 && expired(t0, 256)) {
+        raise_error(v_, GIN_DEVERR_TIMEOUT);
+        break;
+      }
+    }
+  }
+
   // Reset sets the cell to 0 (runtime.cpp:414-418); only the owner may call
   // it, and only when no signal to the cell is in flight.
   __device__ void reset_signal(uint32_t id) const {
+    if (id >= v_->signal_cells) {
+      raise_error(v_, GIN_DEVERR_INVALID_SIGNAL);
+      return;
+    }
     uint64_t s = 0;
     for (uint32_t src = 0; src < v_->world; ++src) s += ld_acquire_sys(sub_cell(v_->rank, src, id));
     st_relaxed_sys(v_->signal_base + id, s);
   }
   __device__ uint64_t read_counter(uint32_t id) const {
+    if (id >= v_->counter_cells) {
+      raise_error(v_, GIN_DEVERR_INVALID_COUNTER);
+      return ~0ull;
+    }
     return ld_acquire_sys(v_->counters + id) - ld_relaxed_sys(v_->counter_base + id);
   }
   template <class Coop>
@@ -361,6 +437,10 @@ class Gin {
     c.sync();
   }
   __device__ void reset_counter(uint32_t id) const {
+    if (id >= v_->counter_cells) {
+      raise_error(v_, GIN_DEVERR_INVALID_COUNTER);
+      return;
+    }
     st_relaxed_sys(v_->counter_base + id, ld_acquire_sys(v_->counters + id));
   }
 
@@ -409,10 +489,34 @@ class Gin {
     return globaltimer() - t0 > v_->timeout_ns;
   }
 
+  // A registered team of this comm by id (DevComm::team, runtime.cpp:338-343);
+  // an unknown id yields an empty team (every op on it raises RankOutOfRange).
+  __device__ Team team(uint32_t id) const {
+    for (uint32_t i = 0; i < GIN_MAX_TEAMS; ++i)
+      if (v_->teams[i].n && v_->teams[i].id == id) return TeamFromView(v_->teams[i]);
+    Team t = WorldTeam(v_->world);
+    t.id = id;
+    t.n = 0;
+    return t;
+  }
+
  private:
+  // submit_op validation (runtime.cpp:474-507): team-relative peer in range
+  // (team_translate -> RankOutOfRange, types.cpp:14-20), world rank in range,
+  // signal and counter ids inside their tables.
+  __device__ bool check_op(const Team& team, uint32_t peer, const Action& a) const {
+    unsigned code = 0;
+    if (peer >= team.n) code = GIN_DEVERR_RANK_OUT_OF_RANGE;
+    else if (team.members[peer] >= v_->world) code = GIN_DEVERR_INVALID_PEER;
+    else if (a.signal_id >= 0 && (uint32_t)a.signal_id >= v_->signal_cells) code = GIN_DEVERR_INVALID_SIGNAL;
+    else if (a.counter_id >= 0 && (uint32_t)a.counter_id >= v_->counter_cells) code = GIN_DEVERR_INVALID_COUNTER;
+    if (code) raise_error(v_, code);
+    return code == 0;
+  }
+
   __device__ bool check_range(uint32_t w, uint32_t r, uint64_t off, uint64_t len) const {
-    if (w >= v_->n_windows || r >= v_->world) {
-      raise_error(v_, w >= v_->n_windows ? GIN_DEVERR_UNKNOWN_WINDOW : GIN_DEVERR_INVALID_PEER);
+    if (w >= GIN_MAX_WINDOWS || !((v_->win_live >> w) & 1ull) || r >= v_->world) {
+      raise_error(v_, r >= v_->world ? GIN_DEVERR_INVALID_PEER : GIN_DEVERR_UNKNOWN_WINDOW);
       return false;
     }
     const uint64_t cap = v_->win[w].size[r];
@@ -461,7 +565,9 @@ class Gin {
       flags |= GIN_FLAG_HAS_COUNTER;
       ctr_id = (uint32_t)a.counter_id;
     }
-    const uint16_t team_id = 0;
+    // (team id, team-relative peer) as the reference's descriptor carries them;
+    // the agent resolves the world rank (proxy_backend.cpp:72)
+    const uint16_t team_id = (uint16_t)team.id;
     w[0] = (uint64_t)opcode | ((uint64_t)flags << 8) | ((uint64_t)team_id << 16) | ((uint64_t)peer << 32);
     w[1] = (uint64_t)dst_win | ((uint64_t)src_win << 32);
     w[2] = dst_off;
@@ -470,7 +576,6 @@ class Gin {
     w[5] = (uint64_t)sig_id | ((uint64_t)ctr_id << 32);
     w[6] = operand;
     w[7] = 0;
-    (void)team;
     const GinProxyView& px = v_->proxy;
     const unsigned long long ticket = atomicAdd(&px.tickets[ctx_], 1ull);
     GinRingSlot* slot = px.slots[ctx_] + (ticket & px.mask);

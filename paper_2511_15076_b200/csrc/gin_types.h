@@ -11,8 +11,9 @@
 #include <stdint.h>
 
 #define GIN_MAX_RANKS 8
-#define GIN_MAX_WINDOWS 32
+#define GIN_MAX_WINDOWS 64
 #define GIN_MAX_CONTEXTS 16
+#define GIN_MAX_TEAMS 16
 // proj/core/include/ginsim/runtime.hpp:62-63: top 8 slots x 8 steps of the
 // signal table are reserved for BarrierSession.
 #define GIN_BARRIER_SLOTS 8
@@ -35,6 +36,7 @@
 #define GIN_DEVERR_TIMEOUT 19        // ginsim::Timeout
 #define GIN_DEVERR_OUT_OF_BOUNDS 3   // ginsim::OutOfBounds
 #define GIN_DEVERR_INVALID_PEER 15   // ginsim::InvalidPeer
+#define GIN_DEVERR_RANK_OUT_OF_RANGE 5  // ginsim::RankOutOfRange (team_translate, types.cpp:14-20)
 #define GIN_DEVERR_INVALID_SIGNAL 16
 #define GIN_DEVERR_INVALID_COUNTER 17
 #define GIN_DEVERR_UNKNOWN_WINDOW 4
@@ -46,6 +48,15 @@ typedef struct GinWindowView {
   char* base[GIN_MAX_RANKS];      // every rank's region, mapped into this rank
   uint64_t size[GIN_MAX_RANKS];   // per-rank capacity (asymmetric allowed)
 } GinWindowView;
+
+// A registered team (proj/core/include/ginsim/types.hpp:75-84,
+// runtime.cpp:329-343): team-relative rank i is world rank members[i].
+// Slot 0 is the world team (id 0); n == 0 marks a free slot.
+typedef struct GinTeamView {
+  uint32_t id;
+  uint32_t n;
+  uint8_t members[GIN_MAX_RANKS];
+} GinTeamView;
 
 // One proxy descriptor ring per context (proj/core/include/ginsim/
 // proxy_backend.hpp:23-53): slots live in pinned host memory mapped into the
@@ -84,6 +95,8 @@ typedef struct GinDevCommView {
   // this rank's own copy of the same cells.
   uint64_t* nvls_mc;
   uint64_t* nvls_uc;
+  uint64_t win_live;              // bit w: window id w is registered (ids are reused after deregister)
   GinWindowView win[GIN_MAX_WINDOWS];
+  GinTeamView teams[GIN_MAX_TEAMS];
   GinProxyView proxy;
 } GinDevCommView;

@@ -137,7 +137,7 @@ int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t d
                            void* stream) {
   GIN_API_BEGIN
   Comm* c = &comm->impl;
-  if (src_win >= c->windows.size() || dst_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+  if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
   if (peer >= c->world) fail(GINSIM_E_INVALID_PEER, "peer out of range");
   if (c->windows[src_win].sizes[c->rank] < bytes || c->windows[dst_win].sizes[peer] < bytes)
     fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
@@ -184,7 +184,7 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
                               float* ms_out, void* stream) {
   GIN_API_BEGIN
   Comm* c = &comm->impl;
-  if (src_win >= c->windows.size() || dst_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+  if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
   if (peer >= c->world) fail(GINSIM_E_INVALID_PEER, "peer out of range");
   if (c->windows[src_win].sizes[c->rank] < bytes || c->windows[dst_win].sizes[peer] < bytes)
     fail(GINSIM_E_OUT_OF_BOUNDS, "copy exceeds window capacity");
@@ -309,7 +309,7 @@ int ginsim_cuda_host_op_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
                               void* stream) {
   GIN_API_BEGIN
   Comm* c = &comm->impl;
-  if (src_win >= c->windows.size() || dst_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+  if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
   if (peer >= c->world || kind > 1 || n_ops == 0 || batch == 0 || batch > 256) fail(GINSIM_E_USAGE, "bad probe arguments");
   const uint64_t span = kind == 0 ? 8ull * n_ops : bytes * n_ops;
   if (c->windows[dst_win].sizes[peer] < span || c->windows[src_win].sizes[c->rank] < span)

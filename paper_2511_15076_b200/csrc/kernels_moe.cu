@@ -48,6 +48,7 @@ using namespace ginsim_b200;
 
 struct ginsim_cuda_moe_s {
   Comm* comm = nullptr;
+  ginsim_cuda_comm_t comm_handle = nullptr;
   ginsim_cuda_moe_config cfg{};
   uint32_t e_local = 0, parts = 4, G = 0, Gc = 0, Gr = 0, chunk = 0, cparts = 1, cchunk = 0;
   uint32_t win_dispatch = 0, win_counts = 0, win_combine = 0, win_stage = 0, win_cstage = 0, win_mirror = 0;
@@ -73,6 +74,8 @@ struct ginsim_cuda_moe_s {
   uint32_t last_ctas = 0;
   uint32_t fanout = 0;  // layout 2: fan-out CTAs (fixed with the grid at the first launch)
   uint32_t cell0 = 0;   // this handle's signal cells: [cell0, cell0 + e_local + 3 + kDedupChunks)
+  uint32_t cell_span = 0;
+  uint64_t* cell_acc = nullptr;  // [e_local] counts consumed so far per local expert cell (wait targets)
 };
 
 extern "C" {
@@ -105,21 +108,50 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   // ranges in creation order (identical on every rank: creation is
   // collective); the first handle of a comm starts at cell 0, as the
   // reference's state has it.
+  // A range released by moe_destroy is reused (first fit, in the same order
+  // on every rank); its cells are reset to zero first -- every rank zeroes
+  // the sub-cells of its own table and its proxy agent's running values,
+  // between two barriers, so no stale release of the previous handle can
+  // satisfy a wait of the new one.
   const uint32_t span = e_local + 3 + kDedupChunks;
-  uint32_t cell0;
+  uint32_t cell0 = UINT32_MAX;
   {
     std::lock_guard<std::mutex> lk(c->mu);
-    cell0 = c->moe_cells_next;
-    if ((uint64_t)cell0 + span > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
-      fail(GINSIM_E_USAGE, "signal table has no room for this MoE handle's " + std::to_string(span) +
-                               " cells (raise Config.signal_cells)");
-    c->moe_cells_next = cell0 + span;
+    for (size_t i = 0; i < c->moe_cells_free.size(); ++i) {
+      auto& fr = c->moe_cells_free[i];
+      if (fr.second < span) continue;
+      cell0 = fr.first;
+      fr.first += span;
+      fr.second -= span;
+      if (fr.second == 0) c->moe_cells_free.erase(c->moe_cells_free.begin() + (long)i);
+      break;
+    }
+    if (cell0 == UINT32_MAX) {
+      cell0 = c->moe_cells_next;
+      if ((uint64_t)cell0 + span > c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
+        fail(GINSIM_E_USAGE, "signal table has no room for this MoE handle's " + std::to_string(span) +
+                                 " cells (raise Config.signal_cells or destroy unused handles)");
+      c->moe_cells_next = cell0 + span;
+    }
+  }
+  {
+    c->barrier();  // every rank has destroyed (and synchronised) the previous owner of the range
+    if (c->proxy) proxy_reset_cells(c, cell0, span);
+    DeviceGuard g(c->device);
+    for (uint32_t src = 0; src < c->world; ++src)
+      GIN_CUDA(cudaMemset(c->host_view.signals[c->rank] + (uint64_t)src * c->cfg.signal_cells + cell0, 0, span * 8ull));
+    GIN_CUDA(cudaMemset(c->host_view.signal_base + cell0, 0, span * 8ull));
+    GIN_CUDA(cudaDeviceSynchronize());
+    // (the window registrations below are collective: no rank signals into
+    //  the range before every rank has reset it)
   }
   auto m = std::make_unique<ginsim_cuda_moe_s>();
   m->comm = c;
+  m->comm_handle = comm;
   m->cfg = *cfg;
   m->e_local = e_local;
   m->cell0 = cell0;
+  m->cell_span = span;
   m->parts = cfg->hidden >= 1024 ? 4 : 1;
   const uint64_t dmsg = (cfg->mode >= 2 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden) + 16;
   const uint64_t cmsg = cfg->mode == 3 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden;
@@ -174,6 +206,8 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   }
   DeviceGuard g(c->device);
   GIN_CUDA(cudaMalloc(&m->ws, 256));
+  GIN_CUDA(cudaMalloc(&m->cell_acc, (size_t)e_local * 8));
+  GIN_CUDA(cudaMemset(m->cell_acc, 0, (size_t)e_local * 8));
   GIN_CUDA(cudaMalloc(&m->route, (2 * (size_t)kMaxGrid + 1) * kMaxExperts * 4));
   GIN_CUDA(cudaMalloc(&m->dst_g, (size_t)cfg->tokens * ((cfg->top_k + 1) & ~1u) * sizeof(char*)));
   GIN_CUDA(cudaMemset(m->ws, 0, 256));
@@ -194,10 +228,14 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
 int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
   GIN_API_BEGIN
   if (!moe) return GINSIM_OK;
+  Comm* c = moe->comm;
+  ginsim_cuda_comm_t ch = moe->comm_handle;
   {
-    DeviceGuard g(moe->comm->device);
-    cudaDeviceSynchronize();
+    DeviceGuard g(c->device);
+    GIN_CUDA(cudaDeviceSynchronize());
+    if (c->proxy) proxy_quiesce(c);  // no descriptor of this handle left in a ring
     if (moe->ws) cudaFree(moe->ws);
+    if (moe->cell_acc) cudaFree(moe->cell_acc);
     if (moe->route) cudaFree(moe->route);
     if (moe->midx) cudaFree(moe->midx);
     if (moe->pipe_buf) cudaFree(moe->pipe_buf);
@@ -205,10 +243,31 @@ int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
     if (moe->dst_g) cudaFree(moe->dst_g);
     if (moe->prof) cudaFree(moe->prof);
   }
-  // window memory stays mapped until the comm is destroyed (windows are
-  // never deregistered in the reference either).
+  // Windows and their VMM memory go back (local deregistration: peers'
+  // imports of this rank's memory keep it alive until they deregister too).
+  const std::pair<uint32_t, void*> owned[] = {
+      {moe->win_dispatch, moe->buf_dispatch}, {moe->win_counts, moe->buf_counts}, {moe->win_combine, moe->buf_combine},
+      {moe->win_rows, moe->buf_rows},         {moe->win_stage, moe->buf_stage},   {moe->win_cstage, moe->buf_cstage},
+      {moe->win_mirror, moe->buf_mirror}};
+  for (const auto& o : owned) {
+    if (!o.second) continue;
+    int rc = ginsim_cuda_window_deregister(ch, o.first);
+    if (rc) fail(rc, ginsim_cuda_last_error());
+    rc = ginsim_cuda_mem_free(ch, o.second);
+    if (rc) fail(rc, ginsim_cuda_last_error());
+  }
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->moe_cells_free.emplace_back(moe->cell0, moe->cell_span);
+  }
   delete moe;
   GIN_API_END
+}
+
+int ginsim_cuda_moe_cells(ginsim_cuda_moe_t moe, uint32_t* first, uint32_t* span) {
+  if (first) *first = moe->cell0;
+  if (span) *span = moe->cell_span;
+  return GINSIM_OK;
 }
 
 int ginsim_cuda_moe_windows(ginsim_cuda_moe_t moe, uint32_t* d, uint32_t* c, uint32_t* cb) {
@@ -286,6 +345,7 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
       fail(GINSIM_E_USAGE, "moe handles in one launch must share a config");
     L.r[i].view = moes[i]->comm->dev_view;
     L.r[i].ws = moes[i]->ws;
+    L.r[i].cell_acc = moes[i]->cell_acc;
     L.r[i].route = moes[i]->route;
     L.r[i].dst_g = moes[i]->dst_g;
     L.r[i].midx = moes[i]->midx;

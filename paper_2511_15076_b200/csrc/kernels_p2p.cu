@@ -29,6 +29,7 @@ struct PingArgs {
   uint32_t peer0, peer1, send_win, recv_win, sig, iters, warmup, ctas;
   uint64_t bytes;
   uint64_t ready[GIN_MAX_RANKS];   // handshake count (cell sig+1) each lane waits for
+  uint64_t raw0[GIN_MAX_RANKS];    // raw sub-cell (this rank, other, sig) at launch: rounds are counted from it
   uint64_t arrive0[GIN_MAX_RANKS]; // multi-CTA rounds: arrivals on workspace word 0 before this call
   uint64_t* rtt;  // device, iters entries (written by peer0's lane)
 };
@@ -77,13 +78,15 @@ __global__ void pingpong_kernel(PingArgs A) {
       }
     }
   };
+  // one sender per cell: poll its raw sub-cell (one acquire load, no backoff)
   auto wait = [&](uint64_t want) {
-    if (threadIdx.x == 0) gin.wait_ge_signal(A.sig, want);
+    if (threadIdx.x == 0) gin.wait_signal_from(other, A.sig, want);
     cta.sync();
   };
   // ws counts CTA arrivals across calls (whose CTA counts differ with the
   // message size): round i of this call is complete at arrive0 + i*ctas
-  const uint64_t sig0 = base;
+  (void)base;
+  const uint64_t sig0 = A.raw0[blockIdx.y];
   for (uint32_t i = 1; i <= total; ++i) {
     if (initiator) {
       const uint64_t t0 = gin::globaltimer();
@@ -94,6 +97,65 @@ __global__ void pingpong_kernel(PingArgs A) {
     } else {
       wait(sig0 + i);
       send(i);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ raw round-trip floor
+// The NVLink round trip with no API in the way: one
+// thread per rank, a flag word in the peer's signal table written with a
+// single store and polled with a single load.  mode 0: st.release.sys /
+// ld.acquire.sys (what a put+signal's signal costs at minimum); mode 1:
+// st.relaxed.sys / ld.relaxed.sys (no ordering at all: the fabric floor).
+struct FloorArgs {
+  const GinDevCommView* v[GIN_MAX_RANKS];
+  uint32_t peer0, peer1, sig, iters, warmup, mode;
+  uint64_t* rtt;
+};
+
+__global__ void rtt_floor_kernel(FloorArgs A) {
+  const GinDevCommView* v = A.v[blockIdx.y];
+  if (threadIdx.x != 0) return;
+  gin::Gin gin(v, 0);
+  const uint32_t me = v->rank;
+  if (me != A.peer0 && me != A.peer1) return;
+  const bool initiator = me == A.peer0;
+  const uint32_t other = initiator ? A.peer1 : A.peer0;
+  uint64_t* mine = gin.sub_cell(me, other, A.sig);    // written by the peer
+  uint64_t* theirs = gin.sub_cell(other, me, A.sig);  // written by me
+  // Launch handshake on cell sig+1: read the flag's current value, then
+  // announce this launch and wait for the peer's announcement -- the peer
+  // writes the flag only after that, so b_mine precedes its first write.
+  const uint64_t b_mine = gin::ld_acquire_sys(mine);
+  const uint64_t b_theirs = gin::ld_relaxed_sys(theirs);  // my writes continue from earlier calls
+  const uint64_t hs0 = gin::ld_acquire_sys(gin.sub_cell(me, other, A.sig + 1));
+  gin::red_release_sys_add(gin.sub_cell(other, me, A.sig + 1), 1);
+  gin.wait_signal_from(other, A.sig + 1, hs0 + 1);
+  const uint64_t t_start = gin::globaltimer();
+  auto wait = [&](uint64_t want) {
+    for (uint32_t s = 1;; ++s) {
+      const uint64_t x = A.mode == 0 ? gin::ld_acquire_sys(mine) : gin::ld_relaxed_sys(mine);
+      if (x >= want) return;
+      if ((s & 4095) == 0 && gin::globaltimer() - t_start > v->timeout_ns) {
+        gin::raise_error(v, GIN_DEVERR_TIMEOUT);
+        return;
+      }
+    }
+  };
+  auto post = [&](uint64_t x) {
+    if (A.mode == 0) gin::st_release_sys(theirs, x);
+    else gin::st_relaxed_sys(theirs, x);
+  };
+  for (uint32_t i = 1; i <= A.warmup + A.iters; ++i) {
+    if (initiator) {
+      const uint64_t t0 = gin::globaltimer();
+      post(b_theirs + i);
+      wait(b_mine + i);
+      const uint64_t t1 = gin::globaltimer();
+      if (i > A.warmup) A.rtt[i - 1 - A.warmup] = t1 - t0;
+    } else {
+      wait(b_mine + i);
+      post(b_theirs + i);
     }
   }
 }
@@ -240,6 +302,7 @@ __global__ void ordering_stress_kernel(OrderArgs A) {
 struct RingArgs {
   LaneViews lv;
   uint32_t send_win, recv_win, rounds;
+  uint32_t team_id, sig, slot;
   uint64_t bytes;
 };
 
@@ -247,33 +310,50 @@ __device__ __forceinline__ uint8_t ring_byte(uint32_t sender, uint32_t round, ui
   return (uint8_t)(sender * 131u + round * 31u + i * 7u + 1u);
 }
 
+// harness_ring.cpp:18-57 over a team (world = id 0): team rank i puts to team
+// rank (i+1) % |team| at recv[world_rank(i) * S] with SignalInc on `sig`,
+// waits, verifies its predecessor's (world rank, round) pattern, resets,
+// flushes and syncs a BarrierSession over the team (barrier slot `slot`).
+// Ranks outside the team return at once.  Puts and signals name team-relative
+// peers, so the Proxy backend's descriptors carry (team id, team rank) and
+// the agent resolves them (proxy_backend.cpp:72).
 __global__ void ring_kernel(RingArgs A) {
   const GinDevCommView* v = A.lv.v[blockIdx.y];
   gin::Gin gin(v, 0);
   gin::CoopCta cta;
-  const gin::Team world = gin::WorldTeam(v->world);
-  const uint32_t n = v->world, r = v->rank, peer = (r + 1) % n, pred = (r + n - 1) % n;
+  const gin::Team team = gin.team(A.team_id);
+  uint32_t me = team.n;
+  for (uint32_t i = 0; i < team.n; ++i)
+    if (team.members[i] == v->rank) me = i;
+  if (team.n == 0) {
+    if (threadIdx.x == 0) gin::raise_error(v, GIN_DEVERR_RANK_OUT_OF_RANGE);
+    return;
+  }
+  if (me == team.n) return;  // not a member
+  const uint32_t n = team.n, r = v->rank, peer = (me + 1) % n, pred_w = team.world_rank((me + n - 1) % n);
+  const uint32_t peer_w = team.world_rank(peer);
   const uint64_t S = A.bytes;
-  gin::BarrierSession barrier(gin, world, 0, A.lv.base[blockIdx.y]);
+  gin::BarrierSession barrier(gin, team, A.slot, A.lv.base[blockIdx.y]);
   __shared__ int bad;
   for (uint32_t round = 0; round < A.rounds; ++round) {
-    char* send = gin.window_ptr(A.send_win, r, (uint64_t)peer * S);
+    char* send = gin.window_ptr(A.send_win, r, (uint64_t)peer_w * S);
     for (uint64_t i = threadIdx.x; i < S; i += blockDim.x) send[i] = (char)ring_byte(r, round, i);
     cta.sync();
-    gin.put(cta, world, peer, A.recv_win, (uint64_t)r * S, A.send_win, (uint64_t)peer * S, S,
-            gin::SignalAction(0, gin::SignalInc()));
-    gin.wait_signal(cta, 0, 1);
+    gin.put(cta, team, peer, A.recv_win, (uint64_t)r * S, A.send_win, (uint64_t)peer_w * S, S,
+            gin::SignalAction(A.sig, gin::SignalInc()));
+    gin.wait_signal(cta, A.sig, 1);
+    if (*reinterpret_cast<volatile unsigned int*>(v->error)) return;  // e.g. an invalid signal id
     if (threadIdx.x == 0) bad = 0;
     cta.sync();
-    const char* recv = gin.window_ptr(A.recv_win, r, (uint64_t)pred * S);
+    const char* recv = gin.window_ptr(A.recv_win, r, (uint64_t)pred_w * S);
     for (uint64_t i = threadIdx.x; i < S; i += blockDim.x)
-      if ((uint8_t)recv[i] != ring_byte(pred, round, i)) bad = 1;
+      if ((uint8_t)recv[i] != ring_byte(pred_w, round, i)) bad = 1;
     cta.sync();
     if (bad) {
       if (threadIdx.x == 0) gin::raise_error(v, GIN_DEVERR_VERIFY);
       return;
     }
-    if (threadIdx.x == 0) gin.reset_signal(0);
+    if (threadIdx.x == 0) gin.reset_signal(A.sig);
     gin.flush(cta);     // sources reusable before the next round overwrites them
     barrier.sync(cta);  // no peer may signal round+1 before everyone reset
   }
@@ -403,7 +483,7 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
     Comm* c = &comms[i]->impl;
     if (c->rank != peer0 && c->rank != peer1) continue;
     for (uint32_t w : {send_win, recv_win}) {
-      if (w >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "ping-pong window not registered");
+      if (!c->window_live(w)) fail(GINSIM_E_UNKNOWN_WINDOW, "ping-pong window not registered");
     }
     if (c->windows[send_win].sizes[c->rank] < bytes) fail(GINSIM_E_OUT_OF_BOUNDS, "send window smaller than message");
     const uint32_t other = c->rank == peer0 ? peer1 : peer0;
@@ -414,11 +494,41 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
     const uint64_t adv = A.ctas > 1 ? (uint64_t)(warmup + iters) * A.ctas : 0;
     A.arrive0[i] = bump_host_counter(c, 0, adv) - adv;
     A.lv.base[i] = cur;
+    // raw sub-cell the peer's pings land in (read before the launch; the
+    // handshake keeps the peer from pinging before this kernel runs)
+    GIN_CUDA(cudaMemcpy(&A.raw0[i], c->host_view.signals[c->rank] + (uint64_t)other * c->cfg.signal_cells + signal_id, 8,
+                        cudaMemcpyDeviceToHost));
     // handshake cell sig+1 (dedicated to ping-pong): one arrival per call
     A.ready[i] = bump_host_counter(c, 6, 1);
   }
-  const uint32_t thr = threads ? threads : 512;
+  // small messages: one warp (the CTA barrier before the release is then a
+  // warp barrier); large ones spread the copy over 512 threads per CTA
+  const uint32_t thr = threads ? threads : (bytes <= 4096 ? 32 : 512);
   coop_launch((const void*)pingpong_kernel, dim3(A.ctas, n), dim3(thr), &A, (cudaStream_t)stream);
+  sync_and_check(comms, n, (cudaStream_t)stream);
+  GIN_API_END
+}
+
+int ginsim_cuda_rtt_floor(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1, uint32_t mode,
+                          uint32_t iters, uint32_t warmup, uint32_t signal_id, uint64_t* rtt_ns_out, void* stream) {
+  GIN_API_BEGIN
+  check_same_device(comms, n);
+  Comm* c0 = &comms[0]->impl;
+  if (peer0 == peer1 || peer0 >= c0->world || peer1 >= c0->world) fail(GINSIM_E_INVALID_PEER, "needs two distinct ranks");
+  if (signal_id + 1 >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range (uses signal_id and signal_id+1)");
+  if (mode > 1) fail(GINSIM_E_USAGE, "mode: 0 release/acquire, 1 relaxed");
+  if (iters == 0) fail(GINSIM_E_USAGE, "iterations must be positive");
+  DeviceGuard g(c0->device);
+  FloorArgs A{};
+  A.peer0 = peer0;
+  A.peer1 = peer1;
+  A.sig = signal_id;
+  A.iters = iters;
+  A.warmup = warmup;
+  A.mode = mode;
+  A.rtt = rtt_ns_out;
+  for (uint32_t i = 0; i < n; ++i) A.v[i] = comms[i]->impl.dev_view;
+  coop_launch((const void*)rtt_floor_kernel, dim3(1, n), dim3(32), &A, (cudaStream_t)stream);
   sync_and_check(comms, n, (cudaStream_t)stream);
   GIN_API_END
 }
@@ -434,7 +544,7 @@ int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t s
   if (signal_id >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range");
   for (uint32_t i = 0; i < n; ++i) {
     Comm* c = &comms[i]->impl;
-    if (send_win >= c->windows.size() || recv_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+    if (!c->window_live(send_win) || !c->window_live(recv_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
     for (uint32_t r = 0; r < world; ++r) {
       if (c->windows[recv_win].sizes[r] < (uint64_t)world * bytes_per_peer ||
           c->windows[send_win].sizes[r] < (uint64_t)world * bytes_per_peer)
@@ -491,7 +601,7 @@ int ginsim_cuda_ordering_stress(const ginsim_cuda_comm_t* comms, uint32_t n, uin
     fail(GINSIM_E_USAGE, "bytes must be a positive multiple of 4; 2*channels signal cells needed");
   for (uint32_t i = 0; i < n; ++i) {
     Comm* c = &comms[i]->impl;
-    if (src_win >= c->windows.size() || dst_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+    if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
     for (uint32_t r = 0; r < c->world; ++r)
       if (c->windows[src_win].sizes[r] < 2ull * channels * bytes || c->windows[dst_win].sizes[r] < 2ull * channels * bytes)
         fail(GINSIM_E_OUT_OF_BOUNDS, "windows must hold 2 * channels * bytes");
@@ -512,15 +622,14 @@ int ginsim_cuda_ordering_stress(const ginsim_cuda_comm_t* comms, uint32_t n, uin
   GIN_API_END
 }
 
-int ginsim_cuda_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_win, uint32_t recv_win, uint64_t bytes,
-                     uint32_t rounds, void* stream) {
-  GIN_API_BEGIN
+static void ring_launch(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t team_id, uint32_t send_win,
+                        uint32_t recv_win, uint64_t bytes, uint32_t rounds, uint32_t sig, void* stream) {
   check_same_device(comms, n);
   Comm* c0 = &comms[0]->impl;
   if (c0->world < 2) fail(GINSIM_E_USAGE, "ring exchange needs at least 2 ranks");
   for (uint32_t i = 0; i < n; ++i) {
     Comm* c = &comms[i]->impl;
-    if (send_win >= c->windows.size() || recv_win >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+    if (!c->window_live(send_win) || !c->window_live(recv_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
     for (uint32_t r = 0; r < c->world; ++r)
       if (c->windows[send_win].sizes[r] < c->world * bytes || c->windows[recv_win].sizes[r] < c->world * bytes)
         fail(GINSIM_E_OUT_OF_BOUNDS, "ring windows must hold world * bytes");
@@ -532,9 +641,36 @@ int ginsim_cuda_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_
   A.recv_win = recv_win;
   A.rounds = rounds;
   A.bytes = bytes;
-  for (uint32_t i = 0; i < n; ++i) A.lv.base[i] = bump_host_counter(&comms[i]->impl, 2, rounds) - rounds;
+  A.team_id = team_id;
+  A.sig = sig;
+  // World rings sync on barrier slot 0, sub-team rings on slot 1.  The round
+  // count a BarrierSession continues from is read from the slot's first cell
+  // (one signal per completed round; quiescent between launches), so a
+  // launch that failed part-way (e.g. a device-side validation error) does
+  // not desynchronise later ones.
+  A.slot = team_id == 0 ? 0 : 1;
+  for (uint32_t i = 0; i < n; ++i) {
+    Comm* c = &comms[i]->impl;
+    const uint32_t cell = c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS + A.slot * GIN_BARRIER_STEPS;
+    uint64_t done = 0;
+    if (int rc = ginsim_cuda_read_signal(comms[i], cell, &done)) fail(rc, ginsim_cuda_last_error());
+    A.lv.base[i] = done;
+  }
   coop_launch((const void*)ring_kernel, dim3(1, n), dim3(512), &A, (cudaStream_t)stream);
   sync_and_check(comms, n, (cudaStream_t)stream);
+}
+
+int ginsim_cuda_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t send_win, uint32_t recv_win, uint64_t bytes,
+                     uint32_t rounds, void* stream) {
+  GIN_API_BEGIN
+  ring_launch(comms, n, 0, send_win, recv_win, bytes, rounds, 0, stream);
+  GIN_API_END
+}
+
+int ginsim_cuda_team_ring(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t team_id, uint32_t send_win,
+                          uint32_t recv_win, uint64_t bytes, uint32_t rounds, uint32_t signal_id, void* stream) {
+  GIN_API_BEGIN
+  ring_launch(comms, n, team_id, send_win, recv_win, bytes, rounds, signal_id, stream);
   GIN_API_END
 }
 
@@ -552,7 +688,7 @@ int ginsim_cuda_moe_ht_ring(const ginsim_cuda_comm_t* pool, uint32_t n, uint32_t
     for (uint32_t p = 0; p < n_pool; ++p) {
       Comm* c = &pool[r * n_pool + p]->impl;
       if (c->device != c0->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
-      if (c->windows.size() < 2) fail(GINSIM_E_UNKNOWN_WINDOW, "each pool comm needs recv and stage windows");
+      if (!c->window_live(0) || !c->window_live(1)) fail(GINSIM_E_UNKNOWN_WINDOW, "each pool comm needs recv and stage windows");
       if (c->windows[0].sizes[c->rank] < (uint64_t)n_ctx * slots * 256) fail(GINSIM_E_OUT_OF_BOUNDS, "recv window too small");
       A.pool[r][p] = c->dev_view;
     }

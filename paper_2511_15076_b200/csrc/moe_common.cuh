@@ -23,6 +23,7 @@ struct MoeRankArgs {
   const void* weights;        // [T][K] u16 (mode 0) / f32 (mode 1)
   uint16_t* out;              // [T][H]
   uint64_t iteration;         // 1-based
+  uint64_t* cell_acc;         // [e_local] counts consumed by earlier iterations per local expert cell
   uint64_t* prof;             // optional per-CTA %globaltimer stamps [3 kernels][1024 CTAs][8]
 };
 
@@ -64,6 +65,23 @@ __device__ __forceinline__ uint64_t* moe_iter_ptr(const MoeRankArgs& R, int kind
 }
 __device__ __forceinline__ uint64_t moe_iteration(const MoeRankArgs& R, int kind, bool next) {
   return *reinterpret_cast<volatile uint64_t*>(moe_iter_ptr(R, kind)) + (next ? 1u : 0u);
+}
+
+// Acquire local expert e_loc's dispatch cell for `iteration` (one thread).
+// The cell accumulates (n<<32) + count per source per iteration
+// (harness_moe.cpp:163-167) and is never reset, so once the counts of all
+// iterations sum past 2^32 they carry into the arrival field, and a bare
+// "cell >= it*(n<<32)" would pass before every source has released.  The
+// target therefore adds the counts consumed by earlier iterations
+// (cell_acc): cell >= it*(n<<32) + acc holds only when all n sources of this
+// iteration have released (one iteration's counts stay below 2^32), and the
+// value read after the wait advances acc exactly (modular arithmetic).
+__device__ __forceinline__ void acquire_expert_cell(const gin::Gin& gin, const MoeRankArgs& R, uint32_t cell,
+                                                    uint32_t e_loc, uint64_t iteration, uint32_t n) {
+  const uint64_t arrivals = iteration * ((uint64_t)n << 32);
+  const uint64_t acc = R.cell_acc[e_loc];
+  gin.wait_ge_signal(cell, arrivals + acc);
+  R.cell_acc[e_loc] = gin.read_signal(cell) - arrivals;
 }
 
 // ------------------------------------------------------------------ helpers

@@ -449,10 +449,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     }
   }
   MOE_STAMP(R, 0, 7);
-  if (tid == 0 && !L.no_wait) {
-    const uint64_t want = iteration * ((uint64_t)n << 32);
-    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(L.cell0 + e_loc, want);
-  }
+  if (tid == 0 && !L.no_wait)
+    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) acquire_expert_cell(gin, R, L.cell0 + e_loc, e_loc, iteration, n);
 }
 
 }  // namespace ginsim_b200

@@ -206,20 +206,8 @@ __global__ void __launch_bounds__(kMoeThreads, KMAX <= 8 ? 2 : 1) moe_dispatch_k
     release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0);
   }
   // Phase D: return once every local expert has been released by every source.
-  if (tid == 0) {
-    const uint64_t want = iteration * ((uint64_t)n << 32);
-    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) {
-      const uint64_t t_start = gin::globaltimer();
-      uint32_t spins = 0;
-      while (gin.read_signal(L.cell0 + e_loc) < want) {
-        if (++spins > 32) __nanosleep(64);
-        if ((spins & 1023) == 0 && gin::globaltimer() - t_start > v->timeout_ns) {
-          gin::raise_error(v, GIN_DEVERR_TIMEOUT);
-          break;
-        }
-      }
-    }
-  }
+  if (tid == 0)
+    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) acquire_expert_cell(gin, R, L.cell0 + e_loc, e_loc, iteration, n);
 }
 
 // ------------------------------------------------------------------ combine
@@ -420,7 +408,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
           const uint16_t* w = reinterpret_cast<const uint16_t*>(R.weights) + (uint64_t)t * K;
           for (uint32_t k = 0; k < K; ++k) {
             const uint32_t wk = w[k];
-            const uint4 y = gin::ld_nc_v4(ysrc(t, k) + 16ull * i);
+            const uint4 y = gin::ld_na_v4(ysrc(t, k) + 16ull * i);
             if (mirrored) gin::st_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i, y);
             const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
@@ -440,7 +428,7 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_kernel(MoeLaunch L
           const float* w = reinterpret_cast<const float*>(R.weights) + (uint64_t)t * K;
           for (uint32_t k = 0; k < K; ++k) {
             const float wk = w[k];
-            const uint4 y = gin::ld_nc_v4(ysrc(t, k) + 16ull * i);
+            const uint4 y = gin::ld_na_v4(ysrc(t, k) + 16ull * i);
             if (mirrored) gin::st_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i, y);
             const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll

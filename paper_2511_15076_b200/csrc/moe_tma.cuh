@@ -323,11 +323,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0);
   }
   MOE_STAMP(R, 0, 6);
-  if (tid == 0) {
-    const uint64_t want = iteration * ((uint64_t)n << 32);
-    if (!L.no_wait)
-      for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) gin.wait_ge_signal(L.cell0 + e_loc, want);
-  }
+  if (tid == 0 && !L.no_wait)
+    for (uint32_t e_loc = b; e_loc < e_local; e_loc += G) acquire_expert_cell(gin, R, L.cell0 + e_loc, e_loc, iteration, n);
   MOE_STAMP(R, 0, 7);
 }
 
@@ -600,7 +597,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       uint4 y[KMAX];
 #pragma unroll
       for (int k = 0; k < KMAX; ++k)
-        if (k < (int)K && !fp8c) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+        if (k < (int)K && !fp8c) y[k] = gin::ld_na_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
       gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
                  fp8c ? reduce_fp8_vec<KMAX>(crecv, cmsg, H, t, i, K, R.weights)
                       : reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
@@ -648,14 +645,14 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
       const char* mirror = v->win[L.win_mirror].base[rank];
 #pragma unroll
       for (int k = 0; k < KMAX; ++k)
-        if (k < (int)K) y[k] = gin::ld_nc_v4(mirror + (uint64_t)__ldg(R.midx + (uint64_t)t * K + k) * cmsg + 16ull * i);
+        if (k < (int)K) y[k] = gin::ld_na_v4(mirror + (uint64_t)__ldg(R.midx + (uint64_t)t * K + k) * cmsg + 16ull * i);
 #pragma unroll
       for (int k = 0; k < KMAX; ++k)
         if (k < (int)K) gin::st_v4(const_cast<char*>(crecv) + ((uint64_t)t * K + k) * cmsg + 16ull * i, y[k]);
     } else {
 #pragma unroll
       for (int k = 0; k < KMAX; ++k)
-        if (k < (int)K) y[k] = gin::ld_nc_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+        if (k < (int)K) y[k] = gin::ld_na_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
     }
     gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
                reduce_vec<KMAX>(y, K, L.mode, R.weights, t));

@@ -238,7 +238,9 @@ int ginsim_cuda_barrier_bench(const ginsim_cuda_comm_t* comms, uint32_t n, uint3
   BarArgs A{};
   A.mode = mode;
   A.iters = iters;
-  A.slot = 0;
+  // barrier slot 2: slot 0 is the world ring's, slot 1 the team ring's; every
+  // slot's round count lives in its own host counter
+  A.slot = 2;
   A.ns = ns_out;
   for (uint32_t i = 0; i < n; ++i) {
     Comm* c = &comms[i]->impl;

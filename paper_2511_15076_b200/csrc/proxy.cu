@@ -9,11 +9,16 @@
 //     (proxy_backend.hpp:67-68, cpp:64-113), decode (descriptor.cpp), and post
 //     through the plugin's iput / iput_signal analogue: cudaMemcpyAsync for
 //     the payload (peer VMM mapping, copy engine) followed, in stream order,
-//     by cuStreamWriteValue64 stores for the signal and counter cells.  Up to
-//     4 CUDA streams, context c on stream c % streams (the reference's
-//     per-context channel): ops of a context are ordered, contexts progress
-//     independently, so copies toward different peers overlap each other's
-//     per-op overheads.  Ranks emulated on one device share the device's
+//     by cuStreamWriteValue64 stores for the signal cells.  Up to 4 CUDA
+//     streams, peer p on stream p % streams: every op toward one peer (any
+//     context) is ordered on one stream -- stronger than the reference's
+//     per-(ctx, peer) channel order -- and copies toward different peers
+//     overlap each other's per-op overheads.  Because one stream owns each
+//     peer's signal sub-cells, the running values the agent writes land in
+//     issue order and a cell never moves backwards.  Local counters (and the
+//     device-visible flush words) are written once per pass on stream 0 after
+//     it has waited for every other stream the pass used, so they too have a
+//     single in-order writer.  Ranks emulated on one device share the device's
 //     hardware queues (CUDA_DEVICE_MAX_CONNECTIONS, default 8): a stream
 //     aliased onto the queue of a spinning MoE kernel would stall the agent
 //     behind it, so each of their agents keeps a single stream.
@@ -25,7 +30,8 @@
 // signal is ordered after every earlier put of the channel (fabric.cpp:63-79)
 // and no kernel is launched, so a persistent user kernel that occupies every
 // SM can never starve the agent.  Counters (local completion,
-// proxy_backend.cpp:95-110) are written the same way after the copy.
+// proxy_backend.cpp:95-110) are written at the end of the pass whose copies
+// completed them.
 #include <sched.h>
 #include <time.h>
 
@@ -49,11 +55,12 @@ struct ProxyAgent {
   std::vector<GinRingSlot*> slots;       // pinned host, device-mapped
   uint64_t* consumed_host = nullptr;     // pinned host, device-mapped: [ctx] tickets consumed
   std::vector<uint64_t> tail;            // next ticket to consume per ctx
-  std::vector<cudaStream_t> streams;     // context c -> streams[c % size]
+  std::vector<cudaStream_t> streams;     // peer p -> streams[p % size]
   std::thread th;
   std::atomic<bool> stop{false};
 
   // running cell values this agent owns
+  std::mutex sig_mu;                     // sig_value: agent thread vs proxy_reset_cells
   std::vector<uint64_t> sig_value;       // [peer][cell] sub-cell (peer, my rank)
   std::vector<uint64_t> ctr_value;       // [cell]
 
@@ -117,57 +124,81 @@ struct ProxyAgent {
   // ring's ticket order (the watermark rule, fabric.cpp:63-79).
   // (A memop costs ~1.2-1.4 us of stream time on B200 even batched,
   // tools/host_op_probe.py, so workloads should need few of them.)
-  std::vector<std::vector<CUstreamBatchMemOpParams>> memops;  // per ctx
-  std::vector<uint8_t> touched;                               // ctx used in this pass
+  std::vector<std::vector<CUstreamBatchMemOpParams>> memops;  // per stream
+  std::vector<uint8_t> touched;                               // stream used in this pass
+  std::vector<uint8_t> ctr_touched;                           // counter completed in this pass
   static constexpr size_t kMaxBatch = 128;
 
-  cudaStream_t stream_of(uint32_t ctx) const { return streams[ctx % streams.size()]; }
-  void flush_memops(uint32_t ctx) {
-    auto& m = memops[ctx];
+  // Copy streams 0..S-1 (peer p on p % S); memop queue S is the completion
+  // stream when there are several copy streams, else stream 0 doubles as it.
+  cudaStream_t comp_stream = nullptr;
+  uint32_t stream_index(uint32_t peer) const { return peer % (uint32_t)streams.size(); }
+  uint32_t completion_index() const { return comp_stream ? (uint32_t)streams.size() : 0u; }
+  cudaStream_t completion_stream() const { return comp_stream ? comp_stream : streams[0]; }
+  cudaStream_t stream_at(uint32_t si) const { return si < streams.size() ? streams[si] : comp_stream; }
+  void flush_memops(uint32_t si) {
+    auto& m = memops[si];
     if (m.empty()) return;
-    GIN_CU(cuapi().cuStreamBatchMemOp((CUstream)stream_of(ctx), (unsigned)m.size(), m.data(), 0));
+    GIN_CU(cuapi().cuStreamBatchMemOp((CUstream)stream_at(si), (unsigned)m.size(), m.data(), 0));
     m.clear();
   }
-  void write64(uint32_t ctx, uint64_t* dev_addr, uint64_t v) {
+  void write64(uint32_t si, uint64_t* dev_addr, uint64_t v) {
     CUstreamBatchMemOpParams op{};
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
     op.writeValue.address = (CUdeviceptr)dev_addr;
     op.writeValue.value64 = v;
     op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
-    memops[ctx].push_back(op);
-    touched[ctx] = 1;
-    if (memops[ctx].size() >= kMaxBatch) flush_memops(ctx);
+    memops[si].push_back(op);
+    touched[si] = 1;
+    if (memops[si].size() >= kMaxBatch) flush_memops(si);
   }
-  void write32(uint32_t ctx, void* dev_addr, uint32_t v) {
+  void write32(uint32_t si, void* dev_addr, uint32_t v) {
     CUstreamBatchMemOpParams op{};
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
     op.writeValue.address = (CUdeviceptr)dev_addr;
     op.writeValue.value = v;
     op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
-    memops[ctx].push_back(op);
-    touched[ctx] = 1;
-    if (memops[ctx].size() >= kMaxBatch) flush_memops(ctx);
+    memops[si].push_back(op);
+    touched[si] = 1;
+    if (memops[si].size() >= kMaxBatch) flush_memops(si);
+  }
+
+  // Team-relative peer -> world rank (proxy_backend.cpp:72 hooks_.resolve_peer,
+  // runtime.cpp:571 / types.cpp:14-20 team_translate).
+  uint32_t resolve_peer(uint32_t team, uint32_t peer) const {
+    const GinDevCommView& v = c->host_view;
+    for (uint32_t i = 0; i < GIN_MAX_TEAMS; ++i) {
+      const GinTeamView& t = v.teams[i];
+      if (t.n == 0 || t.id != team) continue;
+      if (peer >= t.n)
+        fail(GINSIM_E_RANK_OUT_OF_RANGE, "proxy: team rank " + std::to_string(peer) + " out of range for team of " +
+                                             std::to_string(t.n));
+      return t.members[peer];
+    }
+    fail(GINSIM_E_USAGE, "proxy: team " + std::to_string(team) + " not registered");
   }
 
   // iput / iput_signal (plugin.hpp:86-90) for one decoded descriptor.
   void post(uint32_t ctx, const ginsim_cuda_descriptor& d, Pass& pass) {
+    (void)ctx;
     const GinDevCommView& v = c->host_view;
-    const uint32_t peer = d.peer;  // team 0 = world: team-relative == world rank
-    cudaStream_t stream = stream_of(ctx);
-    touched[ctx] = 1;
+    const uint32_t peer = resolve_peer(d.team, d.peer);
     if (peer >= v.world) fail(GINSIM_E_INVALID_PEER, "proxy: descriptor peer out of range");
+    const uint32_t si = stream_index(peer);
+    cudaStream_t stream = streams[si];
+    touched[si] = 1;
     if (d.opcode != GIN_OP_SIGNAL_ONLY && d.bytes > 0) {
-      if (d.dst_window >= v.n_windows) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown destination window");
+      if (d.dst_window >= GIN_MAX_WINDOWS || !((v.win_live >> d.dst_window) & 1ull)) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown destination window");
       const GinWindowView& dw = v.win[d.dst_window];
       if (d.dst_offset > dw.size[peer] || d.bytes > dw.size[peer] - d.dst_offset)
         fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: destination range exceeds capacity");
       char* dst = dw.base[peer] + d.dst_offset;
       if (d.opcode == GIN_OP_PUT) {
-        if (d.src_window >= v.n_windows) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown source window");
+        if (d.src_window >= GIN_MAX_WINDOWS || !((v.win_live >> d.src_window) & 1ull)) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown source window");
         const GinWindowView& sw = v.win[d.src_window];
         if (d.src_offset_or_value > sw.size[v.rank] || d.bytes > sw.size[v.rank] - d.src_offset_or_value)
           fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: source range exceeds capacity");
-        flush_memops(ctx);
+        flush_memops(si);
         CopyTrace tr{};
         if (trace) {
           tr = CopyTrace{d.bytes, now_ns(), ctx, nullptr, nullptr};
@@ -183,27 +214,32 @@ struct ProxyAgent {
         }
         n_copies.fetch_add(1, std::memory_order_relaxed);
       } else if (d.bytes == 4 && ((uintptr_t)dst & 3) == 0) {  // aligned inline values: a memop, no copy
-        write32(ctx, dst, (uint32_t)d.src_offset_or_value);
+        write32(si, dst, (uint32_t)d.src_offset_or_value);
       } else if (d.bytes == 8 && ((uintptr_t)dst & 7) == 0) {
-        write64(ctx, reinterpret_cast<uint64_t*>(dst), d.src_offset_or_value);
+        write64(si, reinterpret_cast<uint64_t*>(dst), d.src_offset_or_value);
       } else {
         uint64_t* s = stage + (stage_next++ % kStage);
         *s = d.src_offset_or_value;
-        flush_memops(ctx);
+        flush_memops(si);
         GIN_CUDA(cudaMemcpyAsync(dst, s, d.bytes, cudaMemcpyHostToDevice, stream));
         n_copies.fetch_add(1, std::memory_order_relaxed);
       }
     }
     if (d.flags & GIN_FLAG_HAS_SIGNAL) {
       if (d.signal_id >= v.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "proxy: signal out of range");
-      uint64_t& val = sig_value[(size_t)peer * v.signal_cells + d.signal_id];
-      val += (d.flags & GIN_FLAG_SIGNAL_IS_ADD) ? d.signal_operand : 1ull;
-      write64(ctx, v.signals[peer] + (uint64_t)v.rank * v.signal_cells + d.signal_id, val);
+      uint64_t val;
+      {
+        std::lock_guard<std::mutex> lk(sig_mu);
+        uint64_t& cell = sig_value[(size_t)peer * v.signal_cells + d.signal_id];
+        cell += (d.flags & GIN_FLAG_SIGNAL_IS_ADD) ? d.signal_operand : 1ull;
+        val = cell;
+      }
+      write64(si, v.signals[peer] + (uint64_t)v.rank * v.signal_cells + d.signal_id, val);
     }
     if (d.flags & GIN_FLAG_HAS_COUNTER) {
-      if (d.counter_id >= v.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "proxy: counter out of range");
+      // (range-checked before counter_pending was touched)
       ctr_value[d.counter_id] += 1;
-      write64(ctx, v.counters + d.counter_id, ctr_value[d.counter_id]);
+      ctr_touched[d.counter_id] = 1;
       pass.counters.push_back(d.counter_id);
     }
   }
@@ -244,7 +280,10 @@ struct ProxyAgent {
         tail[ctx] = t + 1;
         ginsim_cuda_descriptor d;
         descriptor_decode(raw, &d);  // a malformed descriptor is a protocol bug: fail the run
-        if (d.flags & GIN_FLAG_HAS_COUNTER) counter_pending[d.counter_id].fetch_add(1, std::memory_order_acq_rel);
+        if (d.flags & GIN_FLAG_HAS_COUNTER) {
+          if (d.counter_id >= c->cfg.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "proxy: counter out of range");
+          counter_pending[d.counter_id].fetch_add(1, std::memory_order_acq_rel);
+        }
         post(ctx, d, pass);
         ++work;
         any_dev = true;
@@ -269,18 +308,36 @@ struct ProxyAgent {
       }
     }
     if (work) {
+      // Completion of the pass on the completion stream: it waits for every
+      // copy stream this pass used, then writes the local counters completed
+      // by the pass and the device-visible flush words (every ticket consumed
+      // so far is complete once the copies above are, proxy_backend.cpp:95-128).
+      // One stream writes them all, so they only ever move forward; the copy
+      // streams never wait on each other.
+      const uint32_t S = (uint32_t)streams.size(), comp = completion_index();
+      for (uint32_t si = 0; si < S; ++si) {
+        if (!touched[si] || si == comp) continue;
+        flush_memops(si);
+        cudaEvent_t ev = get_event();
+        GIN_CUDA(cudaEventRecord(ev, streams[si]));
+        GIN_CUDA(cudaStreamWaitEvent(completion_stream(), ev, 0));
+        pass.evs.push_back(ev);
+        touched[si] = 0;
+      }
+      for (uint32_t id : pass.counters) {
+        if (!ctr_touched[id]) continue;
+        ctr_touched[id] = 0;
+        write64(comp, c->host_view.counters + id, ctr_value[id]);
+      }
       for (uint32_t ctx = 0; ctx < n_ctx; ++ctx) {
         if (!pass.host_done[ctx]) pass.host_done[ctx] = host_taken[ctx];
-        // device-visible flush word: every ticket consumed so far is complete
-        // once the copies above have completed (stream order).
-        if (any_dev && consumed[ctx]) write64(ctx, c->host_view.proxy.completed + ctx, consumed[ctx]);
-        if (!touched[ctx]) continue;
-        flush_memops(ctx);
-        cudaEvent_t ev = get_event();
-        GIN_CUDA(cudaEventRecord(ev, stream_of(ctx)));
-        pass.evs.push_back(ev);
-        touched[ctx] = 0;
+        if (any_dev && consumed[ctx]) write64(comp, c->host_view.proxy.completed + ctx, consumed[ctx]);
       }
+      flush_memops(comp);
+      cudaEvent_t ev = get_event();
+      GIN_CUDA(cudaEventRecord(ev, completion_stream()));
+      pass.evs.push_back(ev);
+      touched[comp] = 0;
       pass.stage_end = stage_next;
       inflight.push_back(std::move(pass));
       n_desc.fetch_add(work, std::memory_order_relaxed);
@@ -332,8 +389,10 @@ ProxyPtr proxy_start(Comm* c) {
   DeviceGuard g(c->device);
   p->streams.assign(c->shares_device ? 1u : std::min<uint32_t>(p->n_ctx, 4u), nullptr);
   for (auto& st : p->streams) GIN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  p->memops.assign(p->n_ctx, {});
-  p->touched.assign(p->n_ctx, 0);
+  if (p->streams.size() > 1) GIN_CUDA(cudaStreamCreateWithFlags(&p->comp_stream, cudaStreamNonBlocking));
+  p->memops.assign(p->streams.size() + 1, {});
+  p->touched.assign(p->streams.size() + 1, 0);
+  p->ctr_touched.assign(c->cfg.counter_cells, 0);
   // events are created up front: the agent must never call into the runtime
   // for anything but issuing work once kernels that wait on it are running
   for (int i = 0; i < 256; ++i) {
@@ -387,6 +446,7 @@ void proxy_stop(ProxyPtr& p) {
   if (p->th.joinable()) p->th.join();
   DeviceGuard g(p->c->device);
   for (auto st : p->streams) cudaStreamSynchronize(st);
+  if (p->comp_stream) cudaStreamSynchronize(p->comp_stream);
   for (auto& f : p->inflight)
     for (auto e : f.evs) cudaEventDestroy(e);
   for (auto e : p->free_events) cudaEventDestroy(e);
@@ -394,20 +454,30 @@ void proxy_stop(ProxyPtr& p) {
   if (p->consumed_host) cudaFreeHost(p->consumed_host);
   if (p->stage) cudaFreeHost(p->stage);
   for (auto st : p->streams) cudaStreamDestroy(st);
+  if (p->comp_stream) cudaStreamDestroy(p->comp_stream);
   p.reset();
 }
 
-void proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]) {
+uint64_t proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]) {
   ProxyAgent* p = c->proxy.get();
   if (p->failed.load()) fail(GINSIM_E_GENERIC, "proxy agent failed: " + p->failure);
   std::array<uint8_t, 64> d;
   std::memcpy(d.data(), desc, 64);
   ginsim_cuda_descriptor dd;
   descriptor_decode(desc, &dd);
-  if (dd.flags & GIN_FLAG_HAS_COUNTER) p->counter_pending[dd.counter_id].fetch_add(1, std::memory_order_acq_rel);
+  if (dd.flags & GIN_FLAG_HAS_COUNTER) {
+    if (dd.counter_id >= c->cfg.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "counter out of range");
+    p->counter_pending[dd.counter_id].fetch_add(1, std::memory_order_acq_rel);
+  }
   std::lock_guard<std::mutex> lk(p->hq_mu);
   p->host_queue.emplace_back(ctx, d);
-  p->host_submitted[ctx] += 1;
+  return ++p->host_submitted[ctx];
+}
+
+bool proxy_host_done(Comm* c, uint32_t ctx, uint64_t ticket) {
+  ProxyAgent* p = c->proxy.get();
+  if (p->failed.load()) fail(GINSIM_E_GENERIC, "proxy agent failed: " + p->failure);
+  return p->host_completed[ctx].load(std::memory_order_acquire) >= ticket;
 }
 
 void proxy_host_flush(Comm* c, uint32_t ctx) {
@@ -423,6 +493,34 @@ void proxy_host_flush(Comm* c, uint32_t ctx) {
     if (std::chrono::steady_clock::now() > deadline) fail(GINSIM_E_TIMEOUT, "flush: exceeded timeout");
     std::this_thread::yield();
   }
+}
+
+void proxy_quiesce(Comm* c) {
+  ProxyAgent* p = c->proxy.get();
+  if (!p) return;
+  DeviceGuard g(c->device);
+  std::vector<uint64_t> tickets(p->n_ctx, 0);
+  GIN_CUDA(cudaMemcpy(tickets.data(), c->host_view.proxy.tickets, sizeof(uint64_t) * p->n_ctx, cudaMemcpyDeviceToHost));
+  std::vector<uint64_t> done(p->n_ctx, 0);
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(c->cfg.timeout_ms);
+  for (;;) {
+    GIN_CUDA(cudaMemcpy(done.data(), c->host_view.proxy.completed, sizeof(uint64_t) * p->n_ctx, cudaMemcpyDeviceToHost));
+    bool all = true;
+    for (uint32_t i = 0; i < p->n_ctx; ++i) all &= done[i] >= tickets[i];
+    if (all) break;
+    if (p->failed.load()) fail(GINSIM_E_GENERIC, "proxy agent failed: " + p->failure);
+    if (std::chrono::steady_clock::now() > deadline) fail(GINSIM_E_TIMEOUT, "proxy quiesce: exceeded timeout");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  for (uint32_t i = 0; i < p->n_ctx; ++i) proxy_host_flush(c, i);
+}
+
+void proxy_reset_cells(Comm* c, uint32_t first, uint32_t span) {
+  ProxyAgent* p = c->proxy.get();
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(p->sig_mu);
+  for (uint32_t peer = 0; peer < c->world; ++peer)
+    for (uint32_t i = first; i < first + span; ++i) p->sig_value[(size_t)peer * c->cfg.signal_cells + i] = 0;
 }
 
 bool proxy_counter_pending(Comm* c, uint32_t id) {

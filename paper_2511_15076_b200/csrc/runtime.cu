@@ -213,7 +213,7 @@ static void vmm_free(VmmAlloc& a) {
   a = VmmAlloc{};
 }
 
-char* Comm::map_blob(const ExportBlob& b) {
+char* Comm::map_blob(const ExportBlob& b, std::vector<Mapping>* maps) {
   if (b.bytes == 0 && b.alloc_size == 0) return nullptr;
   if (b.pid == (int32_t)getpid()) {
     if (b.device != device) {
@@ -258,7 +258,7 @@ char* Comm::map_blob(const ExportBlob& b) {
   GIN_CU(cuapi().cuMemSetAccess(m.ptr, m.size, &acc, 1));
   {
     std::lock_guard<std::mutex> lk(mu);
-    imported.push_back(m);
+    (maps ? *maps : imported).push_back(m);
   }
   return reinterpret_cast<char*>(m.ptr + b.offset);
 }
@@ -348,7 +348,7 @@ static void validate_common(Comm* c, uint32_t ctx, uint32_t peer) {
 }
 
 static const Comm::Window& lookup_window(Comm* c, uint32_t w) {
-  if (w >= c->windows.size()) fail(GINSIM_E_UNKNOWN_WINDOW, "window " + std::to_string(w) + " was never registered");
+  if (!c->window_live(w)) fail(GINSIM_E_UNKNOWN_WINDOW, "window " + std::to_string(w) + " is not registered");
   return c->windows[w];
 }
 
@@ -390,6 +390,83 @@ static void encode_host_op(Comm* c, uint8_t opcode, uint32_t peer, uint32_t dst_
   }
   (void)c;
   descriptor_encode(&d, out);
+}
+
+// Direct backend: a host-issued op carrying a local counter is outstanding
+// until the stream has executed it (counter_pending, runtime.cpp:431-438).
+static void note_direct_counter(Comm* c, const ginsim_cuda_action* a, cudaStream_t s) {
+  if (!a || a->counter_id < 0) return;
+  std::lock_guard<std::mutex> lk(c->mu);
+  cudaEvent_t e;
+  if (!c->free_op_events.empty()) {
+    e = c->free_op_events.back();
+    c->free_op_events.pop_back();
+  } else {
+    GIN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  GIN_CUDA(cudaEventRecord(e, s));
+  c->direct_pending.emplace_back(e, (uint32_t)a->counter_id);
+}
+static bool direct_counter_pending(Comm* c, uint32_t id) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  bool pending = false;
+  std::vector<std::pair<cudaEvent_t, uint32_t>> keep;
+  for (auto& pe : c->direct_pending) {
+    const cudaError_t q = cudaEventQuery(pe.first);
+    if (q == cudaSuccess) {
+      c->free_op_events.push_back(pe.first);
+      continue;
+    }
+    if (q != cudaErrorNotReady) GIN_CUDA(q);
+    if (pe.second == id) pending = true;
+    keep.push_back(pe);
+  }
+  c->direct_pending.swap(keep);
+  return pending;
+}
+
+// submit_op (runtime.cpp:474-544) for a host-issued op: validation (ctx, peer,
+// bounds against the peer's capacity and our own, inline width, cell ids),
+// then the direct path (a one-warp device op on `stream`) or the proxy path
+// (a descriptor for the host agent).  Returns the proxy host ticket of the
+// op on its context (0 on the direct backend).
+uint64_t host_op(Comm* c, uint32_t ctx, uint8_t opcode, uint32_t peer, uint32_t dst_win, uint64_t dst_off,
+                 uint32_t src_win, uint64_t src_or_value, uint64_t bytes, const ginsim_cuda_action* action,
+                 cudaStream_t stream) {
+  validate_common(c, ctx, peer);
+  if (opcode == GIN_OP_PUT_INLINE && (bytes == 0 || bytes > 8))
+    fail(GINSIM_E_INVALID_DESCRIPTOR, "put_value width must be 1..8 bytes");
+  if (opcode != GIN_OP_SIGNAL_ONLY) check_range(c, dst_win, peer, dst_off, bytes);
+  if (opcode == GIN_OP_PUT) check_range(c, src_win, c->rank, src_or_value, bytes);
+  validate_action(c, action);
+  if (c->cfg.backend == GIN_BACKEND_PROXY) {
+    uint8_t d[64];
+    encode_host_op(c, opcode, peer, opcode == GIN_OP_SIGNAL_ONLY ? 0 : dst_win, dst_off, src_win, src_or_value, bytes,
+                   action, d);
+    return proxy_host_submit(c, ctx, d);
+  }
+  DeviceGuard g(c->device);
+  if (opcode == GIN_OP_SIGNAL_ONLY) {
+    host_signal_kernel<<<1, 32, 0, stream>>>(c->dev_view, ctx, peer, (uint32_t)action->signal_id,
+                                              action->signal_add ? gin::SignalAdd(action->operand) : gin::SignalInc(),
+                                              action->counter_id);
+  } else {
+    HostOp op{};
+    op.kind = opcode == GIN_OP_PUT ? 0 : 1;
+    op.ctx = ctx;
+    op.peer = peer;
+    op.dst_win = dst_win;
+    op.src_win = src_win;
+    op.dst_off = dst_off;
+    op.src_off_or_value = src_or_value;
+    op.bytes = bytes;
+    op.width = (uint32_t)bytes;
+    op.action = to_action(action);
+    host_op_kernel<<<1, 32, 0, stream>>>(c->dev_view, op);
+  }
+  GIN_CUDA(cudaGetLastError());
+  note_direct_counter(c, action, stream);
+  return 0;
 }
 
 }  // namespace ginsim_b200
@@ -518,6 +595,10 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
   v.proxy.completed = reinterpret_cast<uint64_t*>(lb + off_done);
   v.proxy.mask = cfg.queue_depth - 1;
   v.workspace = reinterpret_cast<unsigned int*>(lb + off_ws);
+  // teams: slot 0 is the world team (id 0, identity; types.cpp:8-14)
+  v.teams[0].id = 0;
+  v.teams[0].n = world;
+  for (uint32_t r = 0; r < GIN_MAX_RANKS; ++r) v.teams[0].members[r] = (uint8_t)r;
   // Exchange and map every rank's signal table.
   ExportBlob mine{};
   mine.pid = (int32_t)getpid();
@@ -580,11 +661,14 @@ int ginsim_cuda_comm_destroy(ginsim_cuda_comm_t comm) {
     cudaDeviceSynchronize();
     if (c->proxy) proxy_stop(c->proxy);
     nvls_teardown(c);
+    for (auto& w : c->windows) c->imported.insert(c->imported.end(), w.maps.begin(), w.maps.end());
     for (auto& m : c->imported) {
       cuapi().cuMemUnmap(m.ptr, m.size);
       cuapi().cuMemAddressFree(m.ptr, m.size);
       cuapi().cuMemRelease(m.handle);
     }
+    for (auto& pe : c->direct_pending) cudaEventDestroy(pe.first);
+    for (auto e : c->free_op_events) cudaEventDestroy(e);
     for (auto& kv : c->allocs) vmm_free(kv.second);
     vmm_free(c->signal_alloc);
     if (c->dev_view) cudaFree(c->dev_view);
@@ -640,13 +724,19 @@ int ginsim_cuda_mem_free(ginsim_cuda_comm_t comm, void* ptr) {
 int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t bytes, uint32_t* window_id) {
   GIN_API_BEGIN
   Comm* c = &comm->impl;
-  if (c->windows.size() >= GIN_MAX_WINDOWS) fail(GINSIM_E_USAGE, "too many windows (max 32)");
+  // Dense ids in call order (runtime.cpp:347-371); an id freed by
+  // window_deregister is reused (lowest first), so every rank that registers
+  // and deregisters in the same order agrees on the ids.
+  uint32_t id = 0;
+  while (id < c->windows.size() && c->windows[id].live) ++id;
+  if (id >= GIN_MAX_WINDOWS)
+    fail(GINSIM_E_USAGE, "too many live windows (max " + std::to_string(GIN_MAX_WINDOWS) + "; deregister unused ones)");
   ExportBlob mine{};
   mine.pid = (int32_t)getpid();
   mine.device = c->device;
   mine.bytes = bytes;
   mine.ptr = (uint64_t)local;
-  mine.window_id = (uint32_t)c->windows.size();
+  mine.window_id = id;
   mine.fd = -1;
   if (bytes > 0) {
     std::lock_guard<std::mutex> lk(c->mu);
@@ -672,22 +762,89 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
     }
   }
   Comm::Window w;
+  w.live = true;
   w.sizes.resize(c->world);
   w.bases.resize(c->world);
   for (uint32_t r = 0; r < c->world; ++r) {
     w.sizes[r] = blobs[r].bytes;
-    w.bases[r] = r == c->rank ? static_cast<char*>(local) : (blobs[r].bytes ? c->map_blob(blobs[r]) : nullptr);
+    w.bases[r] = r == c->rank ? static_cast<char*>(local) : (blobs[r].bytes ? c->map_blob(blobs[r], &w.maps) : nullptr);
   }
-  const uint32_t id = mine.window_id;
   for (uint32_t r = 0; r < c->world; ++r) {
     c->host_view.win[id].base[r] = w.bases[r];
     c->host_view.win[id].size[r] = w.sizes[r];
   }
-  c->host_view.n_windows = id + 1;
-  c->windows.push_back(std::move(w));
+  c->host_view.win_live |= 1ull << id;
+  c->host_view.n_windows = std::max<uint32_t>(c->host_view.n_windows, id + 1);
+  if (id == c->windows.size()) c->windows.push_back(std::move(w));
+  else c->windows[id] = std::move(w);
   c->sync_view();
   c->barrier();  // no rank leaves before every rank has mapped (runtime.cpp:364-367)
   *window_id = id;
+  GIN_API_END
+}
+
+int ginsim_cuda_window_deregister(ginsim_cuda_comm_t comm, uint32_t window_id) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  lookup_window(c, window_id);
+  DeviceGuard g(c->device);
+  GIN_CUDA(cudaDeviceSynchronize());  // no kernel of this rank still uses the window
+  Comm::Window& w = c->windows[window_id];
+  for (auto& m : w.maps) {
+    cuapi().cuMemUnmap(m.ptr, m.size);
+    cuapi().cuMemAddressFree(m.ptr, m.size);
+    cuapi().cuMemRelease(m.handle);
+  }
+  w = Comm::Window{};
+  c->host_view.win[window_id] = GinWindowView{};
+  c->host_view.win_live &= ~(1ull << window_id);
+  c->sync_view();
+  GIN_API_END
+}
+
+int ginsim_cuda_register_team(ginsim_cuda_comm_t comm, uint32_t team_id, const uint32_t* members, uint32_t n) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  // DevComm::register_team (runtime.cpp:329-337): local, members must be in
+  // the world, ids unique (world = id 0 is always present).
+  if (n == 0 || !members) fail(GINSIM_E_USAGE, "team must have members");
+  if (n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "team larger than the world");
+  for (uint32_t i = 0; i < n; ++i)
+    if (members[i] >= c->world) fail(GINSIM_E_INVALID_PEER, "team member " + std::to_string(members[i]) + " out of world");
+  if (team_id > 0xFFFFu) fail(GINSIM_E_USAGE, "team id must fit the descriptor's 16-bit team field");
+  std::lock_guard<std::mutex> lk(c->mu);
+  uint32_t slot = GIN_MAX_TEAMS;
+  for (uint32_t i = 0; i < GIN_MAX_TEAMS; ++i) {
+    if (c->host_view.teams[i].n && c->host_view.teams[i].id == team_id) fail(GINSIM_E_USAGE, "team id already registered");
+    if (!c->host_view.teams[i].n && slot == GIN_MAX_TEAMS) slot = i;
+  }
+  if (slot == GIN_MAX_TEAMS) fail(GINSIM_E_USAGE, "team table full (" + std::to_string(GIN_MAX_TEAMS) + " teams)");
+  GinTeamView t{};
+  t.id = team_id;
+  t.n = n;
+  for (uint32_t i = 0; i < n; ++i) t.members[i] = (uint8_t)members[i];
+  c->host_view.teams[slot] = t;  // the proxy agent reads host_view.teams (written before any op names the team)
+  {
+    DeviceGuard g(c->device);
+    GIN_CUDA(cudaMemcpy(&c->dev_view->teams[slot], &t, sizeof(t), cudaMemcpyHostToDevice));
+  }
+  GIN_API_END
+}
+
+int ginsim_cuda_team(ginsim_cuda_comm_t comm, uint32_t team_id, uint32_t* members, uint32_t* n) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  std::lock_guard<std::mutex> lk(c->mu);
+  for (uint32_t i = 0; i < GIN_MAX_TEAMS; ++i) {
+    const GinTeamView& t = c->host_view.teams[i];
+    if (t.n && t.id == team_id) {
+      if (n) *n = t.n;
+      if (members)
+        for (uint32_t j = 0; j < t.n; ++j) members[j] = t.members[j];
+      return GINSIM_OK;
+    }
+  }
+  fail(GINSIM_E_USAGE, "team " + std::to_string(team_id) + " not registered");
   GIN_API_END
 }
 
@@ -714,59 +871,15 @@ int ginsim_cuda_put(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32
                     uint32_t src_win, uint64_t src_off, uint64_t bytes, const ginsim_cuda_action* action,
                     void* stream) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
-  validate_common(c, ctx, peer);
-  check_range(c, dst_win, peer, dst_off, bytes);
-  check_range(c, src_win, c->rank, src_off, bytes);
-  validate_action(c, action);
-  if (c->cfg.backend == GIN_BACKEND_PROXY) {
-    uint8_t d[64];
-    encode_host_op(c, GIN_OP_PUT, peer, dst_win, dst_off, src_win, src_off, bytes, action, d);
-    proxy_host_submit(c, ctx, d);
-  } else {
-    DeviceGuard g(c->device);
-    HostOp op{};
-    op.kind = 0;
-    op.ctx = ctx;
-    op.peer = peer;
-    op.dst_win = dst_win;
-    op.src_win = src_win;
-    op.dst_off = dst_off;
-    op.src_off_or_value = src_off;
-    op.bytes = bytes;
-    op.action = to_action(action);
-    host_op_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->dev_view, op);
-    GIN_CUDA(cudaGetLastError());
-  }
+  host_op(&comm->impl, ctx, GIN_OP_PUT, peer, dst_win, dst_off, src_win, src_off, bytes, action, (cudaStream_t)stream);
   GIN_API_END
 }
 
 int ginsim_cuda_put_value(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32_t dst_win, uint64_t dst_off,
                           uint64_t le_value, uint32_t width, const ginsim_cuda_action* action, void* stream) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
-  if (width == 0 || width > 8) fail(GINSIM_E_INVALID_DESCRIPTOR, "put_value width must be 1..8 bytes");
-  validate_common(c, ctx, peer);
-  check_range(c, dst_win, peer, dst_off, width);
-  validate_action(c, action);
-  if (c->cfg.backend == GIN_BACKEND_PROXY) {
-    uint8_t d[64];
-    encode_host_op(c, GIN_OP_PUT_INLINE, peer, dst_win, dst_off, GIN_INLINE_WINDOW, le_value, width, action, d);
-    proxy_host_submit(c, ctx, d);
-  } else {
-    DeviceGuard g(c->device);
-    HostOp op{};
-    op.kind = 1;
-    op.ctx = ctx;
-    op.peer = peer;
-    op.dst_win = dst_win;
-    op.dst_off = dst_off;
-    op.src_off_or_value = le_value;
-    op.width = width;
-    op.action = to_action(action);
-    host_op_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->dev_view, op);
-    GIN_CUDA(cudaGetLastError());
-  }
+  host_op(&comm->impl, ctx, GIN_OP_PUT_INLINE, peer, dst_win, dst_off, GIN_INLINE_WINDOW, le_value, width, action,
+          (cudaStream_t)stream);
   GIN_API_END
 }
 
@@ -774,24 +887,13 @@ int ginsim_cuda_signal(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uin
                        uint64_t operand, const ginsim_cuda_action* extra, void* stream) {
   GIN_API_BEGIN
   Comm* c = &comm->impl;
-  validate_common(c, ctx, peer);
   if (signal_id >= c->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal " + std::to_string(signal_id) + " out of range");
-  validate_action(c, extra);
   ginsim_cuda_action a{};
   a.signal_id = (int32_t)signal_id;
   a.signal_add = signal_add;
   a.operand = signal_add ? operand : 1;
   a.counter_id = extra ? extra->counter_id : -1;
-  if (c->cfg.backend == GIN_BACKEND_PROXY) {
-    uint8_t d[64];
-    encode_host_op(c, GIN_OP_SIGNAL_ONLY, peer, 0, 0, GIN_INLINE_WINDOW, 0, 0, &a, d);
-    proxy_host_submit(c, ctx, d);
-  } else {
-    DeviceGuard g(c->device);
-    host_signal_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
-        c->dev_view, ctx, peer, signal_id, signal_add ? gin::SignalAdd(operand) : gin::SignalInc(), a.counter_id);
-    GIN_CUDA(cudaGetLastError());
-  }
+  host_op(c, ctx, GIN_OP_SIGNAL_ONLY, peer, 0, 0, GIN_INLINE_WINDOW, 0, 0, &a, (cudaStream_t)stream);
   GIN_API_END
 }
 
@@ -890,7 +992,7 @@ int ginsim_cuda_reset_counter(ginsim_cuda_comm_t comm, uint32_t id) {
   GIN_API_BEGIN
   Comm* c = &comm->impl;
   if (id >= c->cfg.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "counter " + std::to_string(id) + " out of range");
-  if (proxy_counter_pending(c, id)) {
+  if (proxy_counter_pending(c, id) || direct_counter_pending(c, id)) {
     fail(GINSIM_E_RESET_WHILE_OUTSTANDING, "counter " + std::to_string(id) + " still has operations in flight");
   }
   DeviceGuard g(c->device);

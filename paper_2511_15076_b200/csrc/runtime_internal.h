@@ -127,10 +127,19 @@ struct Comm {
   std::vector<std::pair<uint64_t, uint64_t>> window_sizes_dummy;
 
   struct Window {
+    bool live = false;                       // false after window_deregister (the id is free again)
     std::vector<uint64_t> sizes;
     std::vector<char*> bases;
+    std::vector<Mapping> maps;               // peer regions imported for this window (other processes)
   };
-  std::vector<Window> windows;
+  std::vector<Window> windows;                // indexed by window id
+  bool window_live(uint32_t w) const { return w < windows.size() && windows[w].live; }
+
+  // host-issued direct-backend ops carrying a local counter, not yet known
+  // complete: (event after the op, counter id); reset_counter refuses while
+  // one is outstanding (runtime.cpp:431-438)
+  std::vector<std::pair<cudaEvent_t, uint32_t>> direct_pending;
+  std::vector<cudaEvent_t> free_op_events;
 
   GinDevCommView host_view{};
   GinDevCommView* dev_view = nullptr;         // device copy
@@ -148,14 +157,17 @@ struct Comm {
 
   cudaStream_t op_stream = nullptr;           // host-issued ops / cell reads
   bool shares_device = false;                 // another rank of this comm runs on this device in this process
-  uint32_t moe_cells_next = 0;                // next free signal cell for a MoE handle (ranges are never reused)
+  uint32_t moe_cells_next = 0;                // next never-used signal cell for a MoE handle
+  std::vector<std::pair<uint32_t, uint32_t>> moe_cells_free;  // (first, span) ranges released by moe_destroy
   uint64_t op_counter[8] = {};                // per-workload launch/round counters (host side)
   ProxyPtr proxy;
 
   void allgather(const void* send, void* recv, size_t bytes);
   void barrier();
   void sync_view();                           // push host_view to dev_view
-  char* map_blob(const ExportBlob& b);        // import a peer region into this process
+  // import a peer region into this process; a new mapping is recorded in
+  // *maps (or in `imported` when maps is null)
+  char* map_blob(const ExportBlob& b, std::vector<Mapping>* maps = nullptr);
 };
 
 // Launch helpers shared by the kernel translation units.
@@ -172,9 +184,21 @@ void nvls_teardown(Comm* c);
 // Proxy agent lifecycle (proxy.cu).
 ProxyPtr proxy_start(Comm* c);
 void proxy_stop(ProxyPtr& p);
-void proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]);
+uint64_t proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]);  // returns the op's host ticket on ctx
+bool proxy_host_done(Comm* c, uint32_t ctx, uint64_t ticket);
+// A host-issued op through submit_op's validation (runtime.cu); returns the
+// proxy host ticket (0 on the direct backend, which launches on `stream`).
+uint64_t host_op(Comm* c, uint32_t ctx, uint8_t opcode, uint32_t peer, uint32_t dst_win, uint64_t dst_off,
+                 uint32_t src_win, uint64_t src_or_value, uint64_t bytes, const ginsim_cuda_action* action,
+                 cudaStream_t stream);
 void proxy_host_flush(Comm* c, uint32_t ctx);
 bool proxy_counter_pending(Comm* c, uint32_t id);
+// Waits until the agent has consumed and completed every descriptor the GPU
+// has submitted so far (all contexts) and every host-submitted op.
+void proxy_quiesce(Comm* c);
+// Zeroes the agent's running values of signal cells [first, first+span) toward
+// every peer (the cells' owners zero their sub-cells at the same time).
+void proxy_reset_cells(Comm* c, uint32_t first, uint32_t span);
 void proxy_stats(Comm* c, uint64_t* descs, uint64_t* copies, uint64_t* busy_ns, uint64_t* wall_ns);
 uint32_t proxy_trace(Comm* c, double* out, uint32_t max_records);
 

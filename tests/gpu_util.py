@@ -62,3 +62,15 @@ def malloc(nbytes):
 
 def free(p):
     rt().cudaFree(p)
+
+
+def host_mapped_words(n=16):
+    """Zeroed pinned host words the device can poll: (host address, device pointer)."""
+    L = rt()
+    L.cudaHostAlloc.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t, ctypes.c_uint]
+    L.cudaHostGetDevicePointer.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p, ctypes.c_uint]
+    hp, dp = ctypes.c_void_p(), ctypes.c_void_p()
+    _ck(L.cudaHostAlloc(ctypes.byref(hp), 4 * n, 2), "cudaHostAlloc")  # cudaHostAllocMapped
+    ctypes.memset(hp, 0, 4 * n)
+    _ck(L.cudaHostGetDevicePointer(ctypes.byref(dp), hp, 0), "cudaHostGetDevicePointer")
+    return hp.value, dp.value

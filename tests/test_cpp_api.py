@@ -11,10 +11,10 @@ LIBDIR = os.path.join(ROOT, "paper_2511_15076_b200", "_lib")
 CUDA = "/usr/local/cuda"
 
 
-def _build(tmp_path):
-    exe = str(tmp_path / "ring_ref_api")
+def _build(tmp_path, name="ring_ref_api"):
+    exe = str(tmp_path / name)
     cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I", f"{CUDA}/include",
-           os.path.join(ROOT, "tests", "cpp", "ring_ref_api.cpp"), "-o", exe, "-L", LIBDIR, "-lginsim_b200",
+           os.path.join(ROOT, "tests", "cpp", f"{name}.cpp"), "-o", exe, "-L", LIBDIR, "-lginsim_b200",
            f"-Wl,-rpath,{LIBDIR}", "-L", f"{CUDA}/lib64", "-lcudart", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-3000:]
@@ -34,3 +34,21 @@ def test_cpp_reference_api_ring_on_gpu(tmp_path):
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ring ok" in r.stdout
+
+
+def test_cpp_plugin_boundary_compiles_and_host_checks_pass(tmp_path):
+    exe = _build(tmp_path, "plugin_api")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "host checks ok" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_plugin_boundary_on_gpu(tmp_path):
+    """FabricPlugin through the C ABI on both backends: proxy iput_signal ->
+    test -> retire (action returned once), direct create_context -> post ->
+    poll; sub-team registration and team-relative ops (tests/cpp/plugin_api.cpp)."""
+    exe = _build(tmp_path, "plugin_api")
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "direct plugin ok" in r.stdout and "proxy plugin ok" in r.stdout
