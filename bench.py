@@ -60,6 +60,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip the LL and ping-pong sub-measurements")
+    p.add_argument("--csv", default="", help="prefix: write ping-pong / bw rows in the reference's CSV schema")
     return p.parse_args()
 
 
@@ -322,15 +323,15 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
                                                  rtt.data_ptr(), None))
         dist.barrier()
         if rank == 0:
-            t = np.sort(rtt[:iters].cpu().numpy())
-            p50 = int(t[iters // 2])
-            rows.append({"size_bytes": sz, "iters": iters, "p50_ns": p50, "p99_ns": int(t[min(iters - 1, iters * 99 // 100)]),
-                         "mean_ns": float(t.mean()), "one_way_ns": p50 / 2,
-                         "GBps_per_direction": (2 * sz / (p50 * 1e-9) / 1e9) if sz else None})
+            row = G.summarize(sz, rtt[:iters].cpu().numpy())  # harness_bench.cpp:20-32
+            row["one_way_ns"] = row["p50_ns"] / 2
+            row["GBps_per_direction"] = (2 * sz / (row["p50_ns"] * 1e-9) / 1e9) if sz else None
+            rows.append(row)
     # the raw NVLink round trip with no API: one thread per
     # rank flips a flag word in the peer's signal table (cells 4010/4011)
     floor = {}
-    for mode, name in ((0, "release_acquire"), (1, "relaxed")):
+    for mode, name in ((0, "release_acquire"), (1, "relaxed"), (2, "release_relaxed_poll_fence"),
+                       (3, "release_add_relaxed_poll_fence")):
         if rank in (0, 1):
             G.check(G.lib().ginsim_cuda_rtt_floor(G.comm_handles([comm]), 1, 0, 1, mode, 1000, 100, 4010,
                                                   rtt.data_ptr(), None))
@@ -347,6 +348,32 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
             "PAPER.md:952-958); one-way = RTT/2", "raw_floor": floor,
             "floor_ns": floor.get("release_acquire", {}).get("p50_ns"),
             "csv_schema": "size_bytes,iters,p50_ns,p99_ns,mean_ns,backend=direct,transport=nvlink"}
+
+
+def measure_bw(G, comm, rank, world, dist, torch, dev, window=16):
+    """bw_rank_program (harness_bench.cpp:92-129) on hardware: rank 0 puts
+    `window` messages into rank 1's window, then flushes; per-iteration time
+    (p50/p99/mean, the reference's summarize) and GB/s = window*size/p50."""
+    sizes = [4 << 10, 32 << 10, 256 << 10, 2 << 20, 4 << 20]
+    smax = sizes[-1]
+    sb, rb = comm.mem_alloc(smax), comm.mem_alloc(window * smax)
+    ws = comm.window_register(sb, smax)
+    wr = comm.window_register(rb, window * smax)
+    ns = torch.zeros(200, dtype=torch.int64, device=dev)
+    rows = []
+    for sz in sizes:
+        iters = 200 if sz <= (256 << 10) else 50
+        dist.barrier()
+        if rank == 0:
+            G.check(G.lib().ginsim_cuda_bw(G.comm_handles([comm]), 1, 0, 1, ws, wr, sz, window, iters, 10, 0,
+                                           ns.data_ptr(), None))
+            row = G.summarize(sz, ns[:iters].cpu().numpy())
+            row["GBps"] = window * sz / (row["p50_ns"] * 1e-9) / 1e9
+            row["frac_of_900"] = row["GBps"] / 900.0
+            rows.append(row)
+    dist.barrier()
+    comm.check_device()
+    return {"workload": f"windowed put bandwidth, {window} puts + flush per iteration, rank 0 -> 1", "rows": rows}
 
 
 def measure_a2a(G, comm, rank, world, dist, torch, dev, stream):
@@ -690,6 +717,12 @@ def main():
         comm_x = comms[0]
     ll = None if args.no_extras else measure_ll(G, comm_x, rank, world, dist, torch, dev, stream)
     pp = None if (args.no_extras or world < 2) else measure_pingpong(G, comm_x, rank, world, dist, torch, dev)
+    bw = None if (args.no_extras or world < 2) else measure_bw(G, comm_x, rank, world, dist, torch, dev)
+    if rank == 0 and args.csv and pp:
+        # the reference's CSV schema (harness_bench.cpp:167-178)
+        G.write_csv(args.csv + ".pingpong.csv", pp["rows"])
+        if bw:
+            G.write_csv(args.csv + ".bw.csv", bw["rows"])
     a2a = None if (args.no_extras or world < 2) else measure_a2a(G, comm_x, rank, world, dist, torch, dev, stream)
     barrier = None if (args.no_extras or world < 2) else measure_barrier(G, comm_x, rank, world, dist, torch, dev)
     variants = None
@@ -834,6 +867,7 @@ def main():
         "e2e": e2e,
         "ll": ll,
         "pingpong": pp,
+        "bw": bw,
         "alltoall": a2a,
         "barrier": barrier,
         "variants": variants,

@@ -316,12 +316,22 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
 
 /* Raw NVLink round-trip floor: one thread per rank flips
  * a flag word in the peer's signal table and polls its own -- no put, no API.
- * mode 0 = st.release.sys / ld.acquire.sys, mode 1 = relaxed .sys (no
- * ordering).  rtt_ns_out as for ping-pong (iters u64, written by peer0).
+ * mode 0 = st.release.sys / ld.acquire.sys polls, mode 1 = relaxed .sys (no
+ * ordering), mode 2 = st.release.sys / relaxed polls + one acquire fence,
+ * mode 3 = red.release.sys.add (the signal path) / relaxed polls + one fence.  rtt_ns_out as for ping-pong (iters u64, written by peer0).
  * Cells signal_id (the flag) and signal_id+1 (a launch handshake) must be
  * dedicated to it. */
 int ginsim_cuda_rtt_floor(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1, uint32_t mode,
                           uint32_t iters, uint32_t warmup, uint32_t signal_id, uint64_t* rtt_ns_out, void* stream);
+
+/* Windowed put bandwidth (bw_rank_program, harness_bench.cpp:92-129): rank
+ * peer0 puts `window` messages of `bytes` into peer1's recv_win at w*bytes,
+ * then flushes; ns_out[i] (device, iters u64) = time of timed iteration i
+ * (window puts + flush) after `warmup`.  The puts of an iteration are split
+ * over `ctas` CTAs (0 = auto: 256 KiB per CTA, at most one per SM). */
+int ginsim_cuda_bw(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1, uint32_t send_win,
+                   uint32_t recv_win, uint64_t bytes, uint32_t window, uint32_t iters, uint32_t warmup, uint32_t ctas,
+                   uint64_t* ns_out, void* stream);
 
 /* Roofline probe: copy `bytes` from this rank's src window into `peer`'s dst
  * window (peer == own rank: local HBM copy) `iters` times with the put path's
@@ -402,7 +412,9 @@ int ginsim_cuda_nvls_enabled(ginsim_cuda_comm_t comm, int* enabled);
 /* `iters` back-to-back barriers, one thread per rank, each timed with
  * %globaltimer into ns_out (device, iters u64, rank 0 of the launch):
  * mode 0 = the reference's dissemination BarrierSession on reserved signal
- * cells (runtime.cpp:651-666), mode 1 = NVLS (one multimem.red arrival). */
+ * cells (runtime.cpp:651-666), mode 1 = NVLS (one multimem.red arrival).
+ * The device gin::BarrierSession picks the NVLS form by itself for the world
+ * team whenever the comm bound the multicast object. */
 int ginsim_cuda_barrier_bench(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t mode, uint32_t iters,
                               uint64_t* ns_out, void* stream);
 
@@ -416,6 +428,14 @@ int ginsim_cuda_barrier_bench(const ginsim_cuda_comm_t* comms, uint32_t n, uint3
  * CPU checker computes the digests it expects and compares arrays, so a
  * 3.76 GB window is verified without copying it to the host. */
 int ginsim_cuda_digest(const void* records, uint64_t record_bytes, uint64_t count, uint64_t* out, void* stream);
+
+/* Multicast signal broadcast: adds `amount` to broadcast
+ * cell `id` (0..255, a namespace separate from the signal table) on EVERY
+ * rank of the comm with one multimem.red through the NVLS mapping, issued on
+ * `stream` (device: gin::signal_broadcast).  read_broadcast reads this rank's
+ * copy.  USAGE when the comm has no multicast object. */
+int ginsim_cuda_signal_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t amount, void* stream);
+int ginsim_cuda_read_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* value);
 
 /* ---- DeepEP-style MoE dispatch / combine (harness_moe.cpp:105-250) ---- */
 typedef struct ginsim_cuda_moe_config {

@@ -227,6 +227,10 @@ def _declare(L):
         "ginsim_cuda_plugin_destroy": ([P], c_int),
         "ginsim_cuda_rtt_floor": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, P,
                                    P], c_int),
+        "ginsim_cuda_bw": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32,
+                            c_uint32, c_uint32, P, P], c_int),
+        "ginsim_cuda_signal_broadcast": ([P, c_uint32, c_uint64, P], c_int),
+        "ginsim_cuda_read_broadcast": ([P, c_uint32, POINTER(c_uint64)], c_int),
         "ginsim_cuda_team_ring": ([POINTER(P), c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_uint32, c_uint32, P],
                                   c_int),
         "ginsim_cuda_register_team": ([P, c_uint32, POINTER(c_uint32), c_uint32], c_int),
@@ -430,6 +434,15 @@ class Comm:
         check(lib().ginsim_cuda_nvls_enabled(self.h, byref(v)))
         return bool(v.value)
 
+    def signal_broadcast(self, cell, amount=1, stream=None):
+        """+amount on broadcast cell `cell` of every rank (one NVLS multimem.red)."""
+        check(lib().ginsim_cuda_signal_broadcast(self.h, cell, amount, _stream(stream)))
+
+    def read_broadcast(self, cell):
+        v = c_uint64()
+        check(lib().ginsim_cuda_read_broadcast(self.h, cell, byref(v)))
+        return v.value
+
     def proxy_trace(self, max_records=4096):
         """[(bytes, ctx, host_issue_us, dev_start_us, dev_us)] of the agent's copies
         since the last call (GINSIM_PROXY_TRACE=1 at creation)."""
@@ -497,6 +510,24 @@ def digest(records, record_bytes, count, out, stream=None):
     the device buffer `out` (count u64): the checker compares them with the
     CPU oracle's (ginsim_cuda_digest, include/ginsim_cuda.h)."""
     check(lib().ginsim_cuda_digest(_ptr(records), record_bytes, count, _ptr(out), _stream(stream)))
+
+
+def summarize(size, samples_ns):
+    """BenchRow of harness_bench.cpp:20-32: p50 = s[n/2], p99 = s[min(n-1, 99n/100)], mean."""
+    s = sorted(int(x) for x in samples_ns)
+    n = len(s)
+    row = {"size_bytes": int(size), "iters": n, "p50_ns": 0, "p99_ns": 0, "mean_ns": 0.0}
+    if n:
+        row.update(p50_ns=s[n // 2], p99_ns=s[min(n - 1, (n * 99) // 100)], mean_ns=sum(s) / n)
+    return row
+
+
+def write_csv(path, rows, backend="direct", transport="nvlink", seed=0):
+    """write_csv (harness_bench.cpp:167-178): the reference's benchmark CSV schema."""
+    with open(path, "w") as f:
+        f.write("size_bytes,iters,p50_ns,p99_ns,mean_ns,backend,transport,seed\n")
+        for r in rows:
+            f.write(f"{r['size_bytes']},{r['iters']},{r['p50_ns']},{r['p99_ns']},{r['mean_ns']},{backend},{transport},{seed}\n")
 
 
 def descriptor_encode(d: Descriptor) -> bytes:

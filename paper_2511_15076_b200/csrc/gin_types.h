@@ -18,6 +18,10 @@
 // signal table are reserved for BarrierSession.
 #define GIN_BARRIER_SLOTS 8
 #define GIN_BARRIER_STEPS 8
+// NVLS region (one multicast granule): words [0, 8) = barrier slots,
+// [GIN_BCAST_BASE, GIN_BCAST_BASE + GIN_BCAST_CELLS) = broadcast signal cells.
+#define GIN_BCAST_BASE 64
+#define GIN_BCAST_CELLS 256
 
 // proj/core/include/ginsim/descriptor.hpp:34-45
 #define GIN_OP_PUT 0x01

@@ -105,11 +105,16 @@ __global__ void pingpong_kernel(PingArgs A) {
 // The NVLink round trip with no API in the way: one
 // thread per rank, a flag word in the peer's signal table written with a
 // single store and polled with a single load.  mode 0: st.release.sys /
-// ld.acquire.sys (what a put+signal's signal costs at minimum); mode 1:
-// st.relaxed.sys / ld.relaxed.sys (no ordering at all: the fabric floor).
+// ld.acquire.sys polls; mode 1: st.relaxed.sys / ld.relaxed.sys (no
+// ordering at all: the fabric floor); mode 2: st.release.sys / relaxed polls
+// + one fence.acq_rel.sys once the flag is seen; mode 3: red.release.sys.add
+// (the signal path's release) / relaxed polls + one fence; modes 4 / 5 split
+// the cost: st.release.sys with relaxed polls, st.relaxed with acquire polls
+// (diagnostic only: neither orders anything end to end).
 struct FloorArgs {
   const GinDevCommView* v[GIN_MAX_RANKS];
   uint32_t peer0, peer1, sig, iters, warmup, mode;
+  uint64_t ready[GIN_MAX_RANKS];  // handshake arrivals expected on cell sig+1 (one per call, host-counted)
   uint64_t* rtt;
 };
 
@@ -124,18 +129,21 @@ __global__ void rtt_floor_kernel(FloorArgs A) {
   uint64_t* mine = gin.sub_cell(me, other, A.sig);    // written by the peer
   uint64_t* theirs = gin.sub_cell(other, me, A.sig);  // written by me
   // Launch handshake on cell sig+1: read the flag's current value, then
-  // announce this launch and wait for the peer's announcement -- the peer
-  // writes the flag only after that, so b_mine precedes its first write.
+  // announce this launch and wait for the peer's announcement (the host
+  // counts the calls) -- the peer writes the flag only after that, so
+  // b_mine precedes its first write.
   const uint64_t b_mine = gin::ld_acquire_sys(mine);
   const uint64_t b_theirs = gin::ld_relaxed_sys(theirs);  // my writes continue from earlier calls
-  const uint64_t hs0 = gin::ld_acquire_sys(gin.sub_cell(me, other, A.sig + 1));
   gin::red_release_sys_add(gin.sub_cell(other, me, A.sig + 1), 1);
-  gin.wait_signal_from(other, A.sig + 1, hs0 + 1);
+  gin.wait_signal_from(other, A.sig + 1, A.ready[blockIdx.y]);
   const uint64_t t_start = gin::globaltimer();
   auto wait = [&](uint64_t want) {
     for (uint32_t s = 1;; ++s) {
-      const uint64_t x = A.mode == 0 ? gin::ld_acquire_sys(mine) : gin::ld_relaxed_sys(mine);
-      if (x >= want) return;
+      const uint64_t x = (A.mode == 0 || A.mode == 5) ? gin::ld_acquire_sys(mine) : gin::ld_relaxed_sys(mine);
+      if (x >= want) {
+        if (A.mode == 2 || A.mode == 3) gin::fence_acq_rel_sys();  // one acquire fence after a relaxed poll
+        return;
+      }
       if ((s & 4095) == 0 && gin::globaltimer() - t_start > v->timeout_ns) {
         gin::raise_error(v, GIN_DEVERR_TIMEOUT);
         return;
@@ -143,7 +151,8 @@ __global__ void rtt_floor_kernel(FloorArgs A) {
     }
   };
   auto post = [&](uint64_t x) {
-    if (A.mode == 0) gin::st_release_sys(theirs, x);
+    if (A.mode == 0 || A.mode == 2 || A.mode == 4) gin::st_release_sys(theirs, x);
+    else if (A.mode == 3) gin::red_release_sys_add(theirs, 1);  // the signal path's release-add
     else gin::st_relaxed_sys(theirs, x);
   };
   for (uint32_t i = 1; i <= A.warmup + A.iters; ++i) {
@@ -157,6 +166,48 @@ __global__ void rtt_floor_kernel(FloorArgs A) {
       wait(b_mine + i);
       post(b_theirs + i);
     }
+  }
+}
+
+// ------------------------------------------------------------------ windowed bandwidth
+// bw_rank_program (harness_bench.cpp:92-129): rank peer0 issues `window` puts
+// of `bytes` into peer1's recv window at w*bytes, then flushes, per timed
+// iteration; peer1 is passive (one-sided).  On the GPU the puts of an
+// iteration are spread over the grid's CTAs (CTA b moves its slice of every
+// put), each CTA flushes (fence.acq_rel.sys = local completion) and arrives
+// on a counter; the iteration ends when every CTA has arrived, timed by CTA 0.
+struct BwArgs {
+  LaneViews lv;
+  uint32_t peer0, peer1, send_win, recv_win, window, iters, warmup;
+  uint64_t bytes;
+  uint64_t arrive0[GIN_MAX_RANKS];
+  uint64_t* ns;  // iters entries
+};
+
+__global__ void bw_kernel(BwArgs A) {
+  const GinDevCommView* v = A.lv.v[blockIdx.y];
+  if (v->rank != A.peer0) return;
+  unsigned int* ctr = A.lv.ws[blockIdx.y] + 1024;
+  gin::Gin gin(v, 0);
+  gin::CoopCta cta;
+  const uint32_t G = gridDim.x;
+  const uint64_t per = ((A.bytes + G - 1) / G + 15) & ~15ull;
+  const uint64_t lo = std::min<uint64_t>(A.bytes, per * blockIdx.x), hi = std::min<uint64_t>(A.bytes, lo + per);
+  for (uint32_t i = 0; i < A.warmup + A.iters; ++i) {
+    const uint64_t t0 = gin::globaltimer();
+    if (hi > lo)
+      for (uint32_t w = 0; w < A.window; ++w)
+        gin::coop_copy(cta, gin.window_ptr(A.recv_win, A.peer1, (uint64_t)w * A.bytes + lo),
+                       gin.window_ptr(A.send_win, A.peer0, lo), hi - lo);
+    gin.flush(cta);  // local completion of this CTA's puts (runtime.cpp:460-470)
+    if (threadIdx.x == 0) {
+      atomicAdd(ctr, 1u);
+      const unsigned target = (unsigned)(A.arrive0[blockIdx.y] + (uint64_t)(i + 1) * G);
+      while (*reinterpret_cast<volatile unsigned*>(ctr) - target > 0x7FFFFFFFu) {
+      }
+      if (blockIdx.x == 0 && i >= A.warmup) A.ns[i - A.warmup] = gin::globaltimer() - t0;
+    }
+    cta.sync();
   }
 }
 
@@ -516,7 +567,9 @@ int ginsim_cuda_rtt_floor(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t 
   Comm* c0 = &comms[0]->impl;
   if (peer0 == peer1 || peer0 >= c0->world || peer1 >= c0->world) fail(GINSIM_E_INVALID_PEER, "needs two distinct ranks");
   if (signal_id + 1 >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range (uses signal_id and signal_id+1)");
-  if (mode > 1) fail(GINSIM_E_USAGE, "mode: 0 release/acquire, 1 relaxed");
+  if (mode > 5)
+    fail(GINSIM_E_USAGE, "mode: 0 release/acquire, 1 relaxed, 2 release/relaxed poll+fence, 3 release-add/relaxed "
+                         "poll+fence, 4 release/relaxed poll, 5 relaxed/acquire poll");
   if (iters == 0) fail(GINSIM_E_USAGE, "iterations must be positive");
   DeviceGuard g(c0->device);
   FloorArgs A{};
@@ -527,8 +580,50 @@ int ginsim_cuda_rtt_floor(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t 
   A.warmup = warmup;
   A.mode = mode;
   A.rtt = rtt_ns_out;
-  for (uint32_t i = 0; i < n; ++i) A.v[i] = comms[i]->impl.dev_view;
+  for (uint32_t i = 0; i < n; ++i) {
+    A.v[i] = comms[i]->impl.dev_view;
+    Comm* c = &comms[i]->impl;
+    if (c->rank == peer0 || c->rank == peer1) A.ready[i] = bump_host_counter(c, 9, 1);
+  }
   coop_launch((const void*)rtt_floor_kernel, dim3(1, n), dim3(32), &A, (cudaStream_t)stream);
+  sync_and_check(comms, n, (cudaStream_t)stream);
+  GIN_API_END
+}
+
+int ginsim_cuda_bw(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, uint32_t peer1, uint32_t send_win,
+                   uint32_t recv_win, uint64_t bytes, uint32_t window, uint32_t iters, uint32_t warmup, uint32_t ctas,
+                   uint64_t* ns_out, void* stream) {
+  GIN_API_BEGIN
+  check_same_device(comms, n);
+  Comm* c0 = &comms[0]->impl;
+  if (peer0 == peer1 || peer0 >= c0->world || peer1 >= c0->world) fail(GINSIM_E_INVALID_PEER, "needs two distinct ranks");
+  if (iters == 0 || window == 0 || bytes == 0) fail(GINSIM_E_USAGE, "bw needs iterations, a window and a size");
+  BwArgs A{};
+  A.lv = lanes(comms, n);
+  A.peer0 = peer0;
+  A.peer1 = peer1;
+  A.send_win = send_win;
+  A.recv_win = recv_win;
+  A.window = window;
+  A.iters = iters;
+  A.warmup = warmup;
+  A.bytes = bytes;
+  A.ns = ns_out;
+  int sms = 0;
+  GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device));
+  // 256 KiB of each put per CTA, at most one CTA per SM per emulated rank
+  const uint32_t G = ctas ? ctas : (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms / n, bytes >> 18));
+  for (uint32_t i = 0; i < n; ++i) {
+    Comm* c = &comms[i]->impl;
+    if (c->rank != peer0) continue;
+    if (!c->window_live(send_win) || !c->window_live(recv_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
+    if (c->windows[send_win].sizes[peer0] < bytes || c->windows[recv_win].sizes[peer1] < (uint64_t)window * bytes)
+      fail(GINSIM_E_OUT_OF_BOUNDS, "windows must hold the message (send) and window * message (peer's recv)");
+    const uint64_t adv = (uint64_t)(warmup + iters) * G;
+    A.arrive0[i] = bump_host_counter(c, 8, adv) - adv;
+  }
+  DeviceGuard g(c0->device);
+  coop_launch((const void*)bw_kernel, dim3(G, n), dim3(512), &A, (cudaStream_t)stream);
   sync_and_check(comms, n, (cudaStream_t)stream);
   GIN_API_END
 }
@@ -651,9 +746,15 @@ static void ring_launch(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t te
   A.slot = team_id == 0 ? 0 : 1;
   for (uint32_t i = 0; i < n; ++i) {
     Comm* c = &comms[i]->impl;
-    const uint32_t cell = c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS + A.slot * GIN_BARRIER_STEPS;
     uint64_t done = 0;
-    if (int rc = ginsim_cuda_read_signal(comms[i], cell, &done)) fail(rc, ginsim_cuda_last_error());
+    if (team_id == 0 && c->nvls.on) {  // the world team's BarrierSession runs on the NVLS cells
+      DeviceGuard dg(c->device);
+      GIN_CUDA(cudaMemcpy(&done, reinterpret_cast<uint64_t*>(c->nvls.uc_va) + A.slot, 8, cudaMemcpyDeviceToHost));
+      done /= c->world;
+    } else {
+      const uint32_t cell = c->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS + A.slot * GIN_BARRIER_STEPS;
+      if (int rc = ginsim_cuda_read_signal(comms[i], cell, &done)) fail(rc, ginsim_cuda_last_error());
+    }
     A.lv.base[i] = done;
   }
   coop_launch((const void*)ring_kernel, dim3(1, n), dim3(512), &A, (cudaStream_t)stream);

@@ -14,11 +14,19 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "gin_device.cuh"
 #include "runtime_internal.h"
 
 namespace ginsim_b200 {
+
+// Ranks of one process share rank 0's multicast handle object; the last of
+// them to tear down releases it (a rank released first would leave the
+// others unbinding a dead handle).
+static std::mutex g_mc_mu;
+static std::map<CUmemGenericAllocationHandle, int> g_mc_refs;
 
 struct NvlsBlob {
   int32_t pid, device, supported, fd;
@@ -166,6 +174,10 @@ void nvls_setup(Comm* c) {
   }
   c->nvls.on = true;
   c->nvls.shared = shared_handle;
+  if (mcs[0].pid == me.pid) {  // rank 0's object, held by every rank of this process
+    std::lock_guard<std::mutex> lk(g_mc_mu);
+    g_mc_refs[c->nvls.mc] += 1;
+  }
   c->host_view.nvls_mc = reinterpret_cast<uint64_t*>(c->nvls.mc_va);
   c->host_view.nvls_uc = reinterpret_cast<uint64_t*>(c->nvls.uc_va);
 }
@@ -181,7 +193,16 @@ void nvls_teardown(Comm* c) {
   api.cuMemAddressFree(c->nvls.uc_va, c->nvls.size);
   api.cuMulticastUnbind(c->nvls.mc, (CUdevice)c->device, 0, c->nvls.size);
   api.cuMemRelease(c->nvls.local);
-  if (!c->nvls.shared) api.cuMemRelease(c->nvls.mc);
+  bool release = true;
+  {
+    std::lock_guard<std::mutex> lk(g_mc_mu);
+    auto it = g_mc_refs.find(c->nvls.mc);
+    if (it != g_mc_refs.end()) {  // shared within this process: the last holder releases
+      release = --it->second == 0;
+      if (release) g_mc_refs.erase(it);
+    }
+  }
+  if (release) api.cuMemRelease(c->nvls.mc);
   c->nvls = Comm::Nvls{};
 }
 
@@ -202,7 +223,7 @@ __global__ void barrier_bench_kernel(BarArgs A) {
   const GinDevCommView* v = A.v[blockIdx.y];
   gin::Gin gin(v, 0);
   const gin::Team team = gin::WorldTeam(v->world);
-  gin::BarrierSession bs(gin, team, A.slot, A.round0[blockIdx.y]);
+  gin::BarrierSession bs(gin, team, A.slot, A.round0[blockIdx.y], /*allow_nvls=*/false);  // mode 0 = dissemination
   gin::CoopThread me;
   for (uint32_t i = 1; i <= A.iters; ++i) {
     const uint64_t t0 = gin::globaltimer();
@@ -218,11 +239,36 @@ __global__ void barrier_bench_kernel(BarArgs A) {
   }
 }
 
+__global__ void broadcast_kernel(const GinDevCommView* v, uint32_t id, uint64_t amount) {
+  gin::signal_broadcast(v, gin::CoopThread{}, id, amount);
+}
+
 }  // namespace ginsim_b200
 
 using namespace ginsim_b200;
 
 extern "C" {
+
+int ginsim_cuda_signal_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t amount, void* stream) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  if (!c->nvls.on) fail(GINSIM_E_USAGE, "signal broadcast needs the NVLS multicast object (ginsim_cuda_nvls_enabled)");
+  if (id >= GIN_BCAST_CELLS) fail(GINSIM_E_INVALID_SIGNAL, "broadcast cell " + std::to_string(id) + " out of range");
+  DeviceGuard g(c->device);
+  broadcast_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(c->dev_view, id, amount);
+  GIN_CUDA(cudaGetLastError());
+  GIN_API_END
+}
+
+int ginsim_cuda_read_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* value) {
+  GIN_API_BEGIN
+  Comm* c = &comm->impl;
+  if (!c->nvls.on) fail(GINSIM_E_USAGE, "broadcast cells need the NVLS multicast object");
+  if (id >= GIN_BCAST_CELLS) fail(GINSIM_E_INVALID_SIGNAL, "broadcast cell " + std::to_string(id) + " out of range");
+  DeviceGuard g(c->device);
+  GIN_CUDA(cudaMemcpy(value, reinterpret_cast<uint64_t*>(c->nvls.uc_va) + GIN_BCAST_BASE + id, 8, cudaMemcpyDeviceToHost));
+  GIN_API_END
+}
 
 int ginsim_cuda_nvls_enabled(ginsim_cuda_comm_t comm, int* enabled) {
   *enabled = comm->impl.nvls.on ? 1 : 0;

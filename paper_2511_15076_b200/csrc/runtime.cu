@@ -620,6 +620,16 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
   GIN_CUDA(cudaStreamCreateWithFlags(&c->op_stream, cudaStreamNonBlocking));
   if (cfg.backend == GIN_BACKEND_PROXY) c->proxy = proxy_start(c);
   nvls_setup(c);  // collective; leaves nvls.on = false where multicast is unavailable
+  // Load the host-op kernels now.  Under CUDA's lazy module loading the first
+  // launch of a kernel loads it, and that load waits for the device: a
+  // host-issued put made while a long-running kernel holds the GPU (e.g. a
+  // user kernel spinning on a signal this put delivers) would block until
+  // that kernel ends.
+  {
+    cudaFuncAttributes fa{};
+    GIN_CUDA(cudaFuncGetAttributes(&fa, (const void*)host_op_kernel));
+    GIN_CUDA(cudaFuncGetAttributes(&fa, (const void*)host_signal_kernel));
+  }
   c->sync_view();
   GIN_CUDA(cudaDeviceSynchronize());
   c->barrier();  // nobody signals a peer before every table is mapped

@@ -159,7 +159,7 @@ struct Comm {
   bool shares_device = false;                 // another rank of this comm runs on this device in this process
   uint32_t moe_cells_next = 0;                // next never-used signal cell for a MoE handle
   std::vector<std::pair<uint32_t, uint32_t>> moe_cells_free;  // (first, span) ranges released by moe_destroy
-  uint64_t op_counter[8] = {};                // per-workload launch/round counters (host side)
+  uint64_t op_counter[16] = {};                // per-workload launch/round counters (host side)
   ProxyPtr proxy;
 
   void allgather(const void* send, void* recv, size_t bytes);

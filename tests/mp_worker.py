@@ -98,6 +98,30 @@ def main():
                 torch.cuda.synchronize()
                 comm.check_device()
             res[f"barrier_mode{mode}_p50_ns"] = int(np.sort(ns.cpu().numpy())[250])
+        # the ring (harness_ring.cpp:18-57) across processes: its world-team
+        # BarrierSession runs on the NVLS multicast cells where they exist
+        S = 4096
+        sb, rb = comm.mem_alloc(world * S), comm.mem_alloc(world * S)
+        ws_, wr_ = comm.window_register(sb, world * S), comm.window_register(rb, world * S)
+        dist.barrier()
+        for _ in range(2):
+            # (team 0 = world; signal cell 300: cells from 0 up belong to the MoE handle above)
+            G.check(G.lib().ginsim_cuda_team_ring(G.comm_handles([comm]), 1, 0, ws_, wr_, S, 20, 300, None))
+            comm.check_device()
+            dist.barrier()
+        res["ring_ok"] = True
+        if res["nvls_enabled"]:
+            # multicast signal broadcast: every rank adds rank+1 to cell 7 of
+            # every rank with one multimem.red
+            comm.signal_broadcast(7, rank + 1)
+            torch.cuda.synchronize()
+            want = world * (world + 1) // 2
+            import time
+            t0 = time.time()
+            while comm.read_broadcast(7) < want and time.time() - t0 < 10:
+                time.sleep(0.001)
+            res["broadcast_cell"] = comm.read_broadcast(7)
+            res["broadcast_expected"] = want
     # put+signal ping-pong over NVLink between ranks 0 and 1 (K14)
     if world >= 2 and os.environ.get("MP_PINGPONG", "1") == "1":
         size = 1 << 22

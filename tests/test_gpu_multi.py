@@ -65,7 +65,9 @@ def test_multiprocess_moe_proxy_backend(layout, tokens):
 def test_multiprocess_barriers_dissemination_and_nvls():
     """BarrierSession over real GPUs: the reference's dissemination barrier and
     the NVLS multicast barrier (when the box exposes multicast) both complete
-    1000 rounds on every rank without a device timeout."""
+    1000 rounds on every rank without a device timeout; the ring program's
+    device BarrierSession (NVLS-backed for the world team) runs 40 rounds
+    across processes; a multicast signal broadcast reaches every rank."""
     n = gpu_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -73,8 +75,10 @@ def test_multiprocess_barriers_dissemination_and_nvls():
     res = _torchrun(n, {"MP_TOKENS": 64, "MP_PINGPONG": 0, "MP_BARRIER": 1, "MP_ITERS": 1})
     for r in res:
         assert r["barrier_mode0_p50_ns"] > 0, r
+        assert r["ring_ok"], r
         if r["nvls_enabled"]:
             assert r["barrier_mode1_p50_ns"] > 0, r
+            assert r["broadcast_cell"] == r["broadcast_expected"], r
     print(json.dumps(res))
 
 

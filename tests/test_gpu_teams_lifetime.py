@@ -137,7 +137,8 @@ def test_reset_counter_refused_while_direct_op_in_flight():
         held.record(s)
         G.Gin(cs[0], 0, stream=s.cuda_stream).put(1, w, 0, w, 4096, 4096, counter=2)
         time.sleep(0.05)
-        assert not held.query(), "the occupier must still hold the stream"
+        assert not held.query(), ("the occupier must still hold the stream", ctypes.c_uint32.from_address(rel_host).value,
+                                  hex(rel_host), hex(rel_dev), s.query())
         with pytest.raises(G.ResetWhileOutstanding):
             cs[0].reset_counter(2)
         cs[0].reset_counter(3)  # other counters are free

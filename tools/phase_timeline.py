@@ -4,6 +4,7 @@ for each kernel, per phase, the median and max over CTAs of the phase's
 duration, and the spread of CTA start/end times (tail effects).
 
   python tools/phase_timeline.py                         # N=1
+  TL_RANKS=8 TL_MODE=0 python tools/phase_timeline.py    # the bench's N=1 config: 8 emulated ranks
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/phase_timeline.py
 """
 import json
@@ -48,18 +49,27 @@ def main():
         comm = G.Comm.create(rank, world, local, ag, G.Config(signal_cells=512))
     else:
         rank, world, local = 0, 1, 0
-        comm = G.Comm.create_all([0], G.Config(signal_cells=512))[0]
-    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, int(os.environ.get("TL_MODE", 1)), int(os.environ.get("TL_LAYOUT", 1)), 0, 0))
+    R = int(os.environ.get("TL_RANKS", 1))  # emulated ranks on this GPU (world == 1 only)
+    mode = int(os.environ.get("TL_MODE", 1))
+    cfg = G.MoeConfig(E, K, T, H, mode, int(os.environ.get("TL_LAYOUT", 1)), int(os.environ.get("TL_CTAS", 0)), 0)
+    if world > 1:
+        comms = [comm]
+        moes = [G.Moe(comm, cfg)]
+    else:
+        comms = G.Comm.create_all([0] * R, G.Config(signal_cells=512))
+        moes = G.Moe.create_all(comms, cfg) if R > 1 else [G.Moe(comms[0], cfg)]
     dev = torch.device("cuda", local)
-    x = torch.empty(T * H, dtype=torch.int16, device=dev)
-    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
-    w = torch.empty(T * K, dtype=torch.float32, device=dev)
-    out = torch.empty(T * H, dtype=torch.int16, device=dev)
-    moe.generate(1, (rank + int(os.environ.get("TL_SHIFT", 0))) % world, x, idx, w)
+    xs = [torch.empty(T * H, dtype=torch.int16, device=dev) for _ in moes]
+    idxs = [torch.empty(T * K, dtype=torch.int32, device=dev) for _ in moes]
+    ws = [torch.empty(T * K, dtype=torch.float32 if mode == 1 else torch.int16, device=dev) for _ in moes]
+    outs = [torch.empty(T * H, dtype=torch.int16, device=dev) for _ in moes]
+    for c, m, x, i, w in zip(comms, moes, xs, idxs, ws):
+        m.generate(1, (c.rank + int(os.environ.get("TL_SHIFT", 0))) % max(world, R), x, i, w)
     for _ in range(4):
-        G.Moe.dispatch([moe], [x], [idx])
-        G.Moe.combine([moe], [w], [out])
+        G.Moe.dispatch(moes, xs, idxs)
+        G.Moe.combine(moes, ws, outs)
     torch.cuda.synchronize()
+    moe = moes[0]
     res = {"rank": rank, "world": world, "tokens": T}
     for kern in (0, 1, 2):
         st = moe.phase_times(kern).astype(np.int64)
