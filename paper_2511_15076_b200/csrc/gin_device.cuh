@@ -454,8 +454,19 @@ class Gin {
 
   // Release-add `amount` to cell `id` of world rank `dst` on behalf of this
   // rank; cumulative over everything that happens-before the calling thread.
+  // GPU scope when dst lives on this GPU (emulated ranks), else system scope.
   __device__ void release_signal_raw(uint32_t dst, uint32_t id, uint64_t amount) const {
-    red_release_sys_add(sub_cell(dst, v_->rank, id), amount);
+    if ((v_->same_gpu >> dst) & 1u) {
+      fence_acq_rel_gpu();
+      red_relaxed_sys_add(sub_cell(dst, v_->rank, id), amount);
+    } else {
+      red_release_sys_add(sub_cell(dst, v_->rank, id), amount);
+    }
+  }
+  // The fence a release toward rank `dst` needs: GPU scope on this GPU.
+  __device__ void fence_toward(uint32_t dst) const {
+    if ((v_->same_gpu >> dst) & 1u) fence_acq_rel_gpu();
+    else fence_acq_rel_sys();
   }
 
   // Single-thread wait until cell `id` >= expected (no coop barrier).
@@ -536,9 +547,9 @@ class Gin {
     if (a.signal_id < 0 && a.counter_id < 0) return;
     c.sync();
     if (c.rank() == 0) {
-      if (a.signal_id >= 0) red_release_sys_add(sub_cell(peer, v_->rank, (uint32_t)a.signal_id), a.op.amount());
+      if (a.signal_id >= 0) release_signal_raw(peer, (uint32_t)a.signal_id, a.op.amount());
       if (a.counter_id >= 0) {
-        fence_acq_rel_sys();
+        fence_toward(peer);  // the put is performed where its observers are, then counted
         atomicAdd(reinterpret_cast<unsigned long long*>(v_->counters + a.counter_id), 1ull);
       }
     }

@@ -99,6 +99,9 @@ typedef struct GinDevCommView {
   // this rank's own copy of the same cells.
   uint64_t* nvls_mc;
   uint64_t* nvls_uc;
+  uint32_t same_gpu;              // bit r: rank r's memory is on this rank's GPU (emulated ranks): GPU-scope
+                                  // fences order this rank's writes for its observers, no .sys needed
+  uint32_t pad0;
   uint64_t win_live;              // bit w: window id w is registered (ids are reused after deregister)
   GinWindowView win[GIN_MAX_WINDOWS];
   GinTeamView teams[GIN_MAX_TEAMS];

@@ -329,6 +329,11 @@ static MoeLaunch make_launch(const ginsim_cuda_moe_t* moes, uint32_t n) {
   const char* dy = std::getenv("GINSIM_MOE_SCHED");
   L.dyn = (dy && std::strcmp(dy, "static") == 0) ? 0u : 1u;
   L.coop = moes[0]->coop ? 1u : 0u;
+  // cross-lane work sharing: only when the launch carries every rank of the
+  // comm (emulated ranks, stepped together, so every lane is at the same
+  // iteration); GINSIM_MOE_SHARE=0 turns it off
+  const char* sh = std::getenv("GINSIM_MOE_SHARE");
+  L.share = (n > 1 && n == moes[0]->comm->world && L.coop && L.dyn && !(sh && sh[0] == '0')) ? 1u : 0u;
   const char* sc = std::getenv("GINSIM_PIPE_STAGE_CTAS");
   // own-expert rows are a plain HBM copy; on 48 CTAs it keeps pace with the
   // copy engines without starving them of HBM (tools/proxy_phases.py, N=2:
@@ -430,14 +435,18 @@ static size_t dispatch_smem(const ginsim_cuda_moe_t m, uint32_t G) {
   // control blocks | stages of [destination row (padded to 128 B) | chunk] | own route indices
   const size_t kp = (m->cfg.top_k + 1) & ~1u;
   const size_t dhead = (kp * 8 + 127) & ~(size_t)127;
+  // moe_dispatch_tma_kernel: + per-warp expert counters [kTmaWarps][E] for the
+  // parallel slot assignment (after the own-route table, 16-byte aligned)
+  const size_t whist = m->cfg.layout == 2 ? 0 : (size_t)kTmaWarps * m->cfg.experts * 4 + 16;
   if (m->cfg.mode >= 2) {  // + e4m3 chunk + scales per stage
     const size_t sst = (dhead + m->chunk + m->chunk / 2 + m->chunk / 64 + 15) & ~(size_t)15;
-    return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kDispStages * sst + pairs * 4;
+    return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kDispStages * sst + pairs * 4 +
+           whist;
   }
   const size_t tokens = (size_t)((m->cfg.tokens + G - 1) / G + 1);
   const size_t rowj = m->cfg.layout == 2 ? tokens * m->comm->world * 4 : 0;  // dedup: (t, dst) row indices
   return ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) + (size_t)kTmaWarps * kDispStages * (dhead + m->chunk) +
-         pairs * 4 + rowj;
+         pairs * 4 + rowj + whist;
 }
 static size_t combine_smem(const ginsim_cuda_moe_t m) {
   if (!kernels_of(m).tma_combine) return 0;

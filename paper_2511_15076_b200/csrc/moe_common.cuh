@@ -49,6 +49,8 @@ struct MoeLaunch {
   uint64_t cmsg;                 // combine message bytes (2H; fp8 combine, mode 3: H + H/32)
   uint32_t no_wait;              // profiling only: dispatch returns without acquiring its experts
   uint32_t dyn;                  // TMA kernels: warps grab work in batches from a device counter (1) or static (0)
+  uint32_t share;                // TMA dispatch, every rank of the comm in this launch (emulated): after their
+                                 // static first round, warps take tokens of ANY lane from one launch-wide counter
   uint32_t stage_ctas;           // Proxy pipeline: CTAs that stage (the rest leave the copy engines the HBM)
   uint32_t fanout_ctas;          // layout 2: CTAs that fan received rows out while the others put (0 = all, in turn)
   uint32_t cell0;                // first signal cell of this handle: expert cells, combine flag, rows/chunk cells
@@ -282,7 +284,7 @@ __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDe
     // the counts; for own experts the acquirer is on this GPU (GPU scope)
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::st_relaxed_sys32(cb + (uint64_t)rank * e_local + e_loc, hist[d * e_local + e_loc]);
-    if (d == rank) gin::fence_acq_rel_gpu(); else gin::fence_acq_rel_sys();
+    gin.fence_toward(d);  // (own experts and emulated peers: GPU scope)
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::red_relaxed_sys_add(gin.sub_cell(d, rank, cell0 + e_loc), (1ull << 32) + hist[d * e_local + e_loc]);
   }

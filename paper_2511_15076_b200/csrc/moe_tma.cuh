@@ -124,9 +124,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
 
   __shared__ uint32_t hist_all[kMaxExperts], run[kMaxExperts], prefix_e[kMaxExperts];
   __shared__ char* sbase[GIN_MAX_RANKS];
+  __shared__ uint32_t lane_rank[GIN_MAX_RANKS];
   __shared__ int is_last;
   extern __shared__ __align__(128) char dsm[];
   TmaSmem* ctl = reinterpret_cast<TmaSmem*>(dsm) + warp;
+  // Cross-lane sharing (emulated ranks in one launch, L.share): items carry
+  // their lane in bits 48+; after the static first round warps take tokens of
+  // every lane, round robin, from one launch-wide counter (lane 0's
+  // workspace, one counter per iteration parity), so the lanes' puts end
+  // together.  Each lane's release then waits until every CTA of the launch
+  // has drained its bulk stores (launch-wide arrival counter).
+  const uint32_t nl = gridDim.y, my_lane = blockIdx.y;
+  const bool share = L.share != 0;
+  unsigned long long* sgrab = reinterpret_cast<unsigned long long*>(L.r[0].ws + 40);  // [2] by iteration parity
+  unsigned int* sarrive = L.r[0].ws + 44;
+  if (tid < nl) lane_rank[tid] = L.r[tid].view->rank;
   // per stage: [dst pointers: Kp * 8 bytes, padded to 128][row chunk]
   const uint32_t dhead = (Kp * 8 + 127) & ~127u;
   // fp8: [dst row][bf16 chunk][e4m3 chunk/2][scales chunk/64, padded]
@@ -153,10 +165,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   const uint64_t gw = (uint64_t)b * kTmaWarps + warp, wstride = (uint64_t)G * kTmaWarps;
   const uint64_t lbase = (uint64_t)t0 * parts + warp;  // local mode: warp takes lbase + j*kTmaWarps
   unsigned long long* grab_ctr = reinterpret_cast<unsigned long long*>(R.ws + 10);
+  constexpr uint64_t kLaneShift = 48, kItemMask = (1ull << kLaneShift) - 1;
+  const uint64_t own_lane_bits = (uint64_t)my_lane << kLaneShift;
   auto next_item = [&]() -> uint64_t {  // lane 0 only
     uint64_t it;
     if (!coop) {
       it = lbase + (ctl->cur++) * kTmaWarps;
+    } else if (share && ctl->cur >= kDispStages) {
+      if (ctl->end == 0 || ctl->itc >= ctl->end) {
+        const uint64_t u = atomicAdd(sgrab + (iteration & 1), 1ull);
+        const uint64_t li = (uint64_t)kDispStages * wstride + (u / nl) * parts;
+        if (li >= items) return kNoItem;  // every lane holds as many items: all done
+        ctl->itc = ((u % nl) << kLaneShift) | li;
+        ctl->end = ctl->itc + parts;
+      }
+      return ctl->itc++;
     } else if (L.dyn && ctl->cur >= kDispStages) {
       // after a static, interleaved first round (items gw + s*wstride, so
       // 1000+ warps do not all hit the counter at once and a small launch
@@ -169,20 +192,37 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     } else {
       it = gw + (ctl->cur++) * wstride;
     }
-    return it < items ? it : kNoItem;
+    return it < items ? (it | own_lane_bits) : kNoItem;
   };
   // A stage's mbarrier expects the row chunk AND the token's destination row;
   // the row chunk does not depend on routing, so it can be requested first.
   auto issue_row = [&](int s, uint64_t it) {  // lane 0
-    const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
+    const uint32_t ln = (uint32_t)(it >> kLaneShift);
+    const uint64_t li = it & kItemMask;
+    const uint32_t t = (uint32_t)(li / parts), p = (uint32_t)(li % parts);
     const uint32_t len = tma_chunk_len(payload, chunk, p);
     char* sb = stage + (size_t)s * sstride;
+    const char* xl = ln == my_lane ? x : reinterpret_cast<const char*>(L.r[ln].x);
     gin::tma::mbar_arrive_expect_tx(&ctl->bar[s], len + Kp * 8);
-    gin::tma::load(sb + dhead, x + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
+    gin::tma::load(sb + dhead, xl + (uint64_t)t * payload + (uint64_t)p * chunk, len, &ctl->bar[s]);
   };
+  uint32_t lanes_ready = 1u << my_lane;  // lane 0 of each warp: lanes whose dst_g table is published
   auto issue_dst = [&](int s, uint64_t it) {  // lane 0, once dst_g is published
-    const uint32_t t = (uint32_t)(it / parts);
-    gin::tma::load(stage + (size_t)s * sstride, dst_g + (uint64_t)t * Kp, Kp * 8, &ctl->bar[s]);
+    const uint32_t ln = (uint32_t)(it >> kLaneShift);
+    const uint32_t t = (uint32_t)((it & kItemMask) / parts);
+    if (!((lanes_ready >> ln) & 1u)) {  // another lane's table: wait for its Phase A barrier
+      const unsigned int* b3 = L.r[ln].ws + 5;
+      for (;;) {
+        unsigned cur;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(b3) : "memory");
+        if (cur >= bar_target) break;
+        __nanosleep(64);
+      }
+      gin::tma::fence_proxy_async_global();
+      lanes_ready |= 1u << ln;
+    }
+    char** dg = ln == my_lane ? dst_g : L.r[ln].dst_g;
+    gin::tma::load(stage + (size_t)s * sstride, dg + (uint64_t)t * Kp, Kp * 8, &ctl->bar[s]);
   };
   if (lane == 0) {
     // first round static (warp gw: items [gw*S, gw*S+S)), so 1000+ warps do
@@ -221,21 +261,42 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
       }
     }
   }
+  // Reference slot order (t, k ascending, harness_moe.cpp:143-150), assigned
+  // by all warps at once: warp w owns the w-th contiguous segment of this
+  // CTA's pairs; per-warp expert counts, scanned across warps in segment
+  // order, give each warp its starting slot per expert (whist[w][e]).
+  // Within a segment, 32 pairs at a time: lanes with the same expert rank
+  // themselves by lane (match_any) and the group's lowest lane advances the
+  // warp's running count.
+  uint32_t* whist = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(own) + (((size_t)nq * 4 + 15) & ~(size_t)15));
+  const uint32_t seg = (((nq + kTmaWarps - 1) / kTmaWarps) + 31) & ~31u;
+  const uint32_t q0 = min(nq, warp * seg), q1 = min(nq, q0 + seg);
+  for (uint32_t i = tid; i < (uint32_t)kTmaWarps * E; i += kTmaThreads) whist[i] = 0;
   __syncthreads();
-  if (warp == 0) {
-    // Reference slot order (t, k ascending): 32 pairs at a time; lanes with the
-    // same expert rank themselves by lane (match_any) and the group's lowest
-    // lane advances the expert's running count.
-    for (uint32_t c0 = 0; c0 < nq; c0 += 32) {
+  for (uint32_t q = q0 + lane; q < q1; q += 32) atomicAdd(&whist[warp * E + own[q]], 1u);
+  __syncthreads();
+  for (uint32_t e = tid; e < E; e += kTmaThreads) {
+    uint32_t base = run[e];
+#pragma unroll
+    for (int w = 0; w < kTmaWarps; ++w) {
+      const uint32_t c = whist[w * E + e];
+      whist[w * E + e] = base;
+      base += c;
+    }
+  }
+  __syncthreads();
+  {
+    uint32_t* wrun = whist + warp * E;
+    for (uint32_t c0 = q0; c0 < q1; c0 += 32) {
       const uint32_t q = c0 + lane;
-      const bool valid = q < nq;
+      const bool valid = q < q1;
       const uint32_t e = valid ? own[q] : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, e);
       const uint32_t before = __popc(peers & ((1u << lane) - 1u));
-      const uint32_t base = valid ? run[e] : 0u;
+      const uint32_t base = valid ? wrun[e] : 0u;
       __syncwarp();
       if (valid) {
-        if (before == 0) run[e] = base + __popc(peers);
+        if (before == 0) wrun[e] = base + __popc(peers);
         const uint32_t slot = base + before;
         const uint32_t t = t0 + q / K, k = q % K;
         const uint32_t dst = e / e_local, e_loc = e % e_local;
@@ -263,11 +324,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     const int s = (int)(j % kDispStages);
     const uint64_t it = ctl->itm[s];
     if (it == kNoItem) break;
-    const uint32_t t = (uint32_t)(it / parts), p = (uint32_t)(it % parts);
+    const uint32_t ln = (uint32_t)(it >> kLaneShift);
+    const uint64_t li = it & kItemMask;
+    const uint32_t t = (uint32_t)(li / parts), p = (uint32_t)(li % parts);
     char* sb = stage + (size_t)s * sstride;
     char* const* dp = reinterpret_cast<char* const*>(sb);
     gin::tma::mbar_wait(&ctl->bar[s], (j / kDispStages) & 1);
-    if (p == 0 && lane < K) gin::st_v4(dp[lane] + L.mpay, make_uint4(rank, t, lane, lane + 1));  // meta
+    if (p == 0 && lane < K) gin::st_v4(dp[lane] + L.mpay, make_uint4(lane_rank[ln], t, lane, lane + 1));  // meta
     if (fp8) {  // quantize the chunk in shared memory, 128 elements per warp step
       const uint32_t len = tma_chunk_len(payload, chunk, p);
       for (uint32_t blk = 0; blk < len / 256; ++blk)
@@ -316,10 +379,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     __syncthreads();
     if (tid == 0) R.prof[((uint64_t)0 * 1024 + blockIdx.x) * 8 + 5] = warp_end;
   }
+  if (share) {  // launch-wide: this CTA's stores (of any lane) are drained
+    __syncthreads();
+    if (tid == 0) {
+      gin::fence_acq_rel_gpu();
+      atomicAdd(sarrive, 1u);
+    }
+  }
   arrive_last(R.ws + 0, (unsigned)(iteration * G), &is_last);
   if (is_last) {
     if (tid == 0) *grab_ctr = 0;  // every CTA is past Phase B
     if (tid == 0) *moe_iter_ptr(R, 0) = iteration;  // every CTA has read it (arrival)
+    if (share) {
+      // every lane's items may sit in any CTA: wait for the whole launch
+      if (tid == 0) {
+        const unsigned target = (unsigned)(iteration * (uint64_t)G * nl);
+        for (;;) {
+          unsigned cur;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(sarrive) : "memory");
+          if (cur >= target) break;
+          __nanosleep(32);
+        }
+        if (my_lane == 0) sgrab[(iteration + 1) & 1] = 0;  // the next iteration's counter (untouched now)
+      }
+      __syncthreads();
+    }
     release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0);
   }
   MOE_STAMP(R, 0, 6);

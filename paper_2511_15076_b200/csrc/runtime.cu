@@ -615,6 +615,7 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
     v.signals[r] = r == rank ? reinterpret_cast<uint64_t*>(c->signal_alloc.ptr)
                              : reinterpret_cast<uint64_t*>(c->map_blob(blobs[r]));
     if (r != rank && blobs[r].pid == mine.pid && blobs[r].device == device) c->shares_device = true;
+    if (blobs[r].pid == mine.pid && blobs[r].device == device) v.same_gpu |= 1u << r;
   }
   GIN_CUDA(cudaMalloc(&c->dev_view, sizeof(GinDevCommView)));
   GIN_CUDA(cudaStreamCreateWithFlags(&c->op_stream, cudaStreamNonBlocking));
