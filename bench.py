@@ -834,9 +834,9 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        key = f"R{R}"
-        tr = tr.get(key, tr)
-        traffic = tr.get("dispatch") if dom == "dispatch" else (tr.get("combine", 0) + tr.get("reduce", 0)) or None
+        tr = tr.get(f"R{R}") if world == 1 else None  # captured at N=1 only (profiles/ncu_traffic.json)
+        if tr:
+            traffic = tr.get("dispatch") if dom == "dispatch" else (tr.get("combine", 0) + tr.get("reduce", 0)) or None
     except Exception:  # noqa: BLE001
         pass
     line = {
