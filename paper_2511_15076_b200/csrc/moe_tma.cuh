@@ -268,25 +268,30 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
   // Within a segment, 32 pairs at a time: lanes with the same expert rank
   // themselves by lane (match_any) and the group's lowest lane advances the
   // warp's running count.
+  // (few pairs, e.g. the LL shape's 8 per CTA: warp 0 alone, no scan)
+  const bool one_warp = nq <= 256;
   uint32_t* whist = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(own) + (((size_t)nq * 4 + 15) & ~(size_t)15));
-  const uint32_t seg = (((nq + kTmaWarps - 1) / kTmaWarps) + 31) & ~31u;
-  const uint32_t q0 = min(nq, warp * seg), q1 = min(nq, q0 + seg);
-  for (uint32_t i = tid; i < (uint32_t)kTmaWarps * E; i += kTmaThreads) whist[i] = 0;
-  __syncthreads();
-  for (uint32_t q = q0 + lane; q < q1; q += 32) atomicAdd(&whist[warp * E + own[q]], 1u);
-  __syncthreads();
-  for (uint32_t e = tid; e < E; e += kTmaThreads) {
-    uint32_t base = run[e];
+  const uint32_t seg = one_warp ? nq : (((nq + kTmaWarps - 1) / kTmaWarps) + 31) & ~31u;
+  const uint32_t q0 = one_warp ? (warp == 0 ? 0u : nq) : min(nq, warp * seg);
+  const uint32_t q1 = one_warp ? nq : min(nq, q0 + seg);
+  if (!one_warp) {
+    for (uint32_t i = tid; i < (uint32_t)kTmaWarps * E; i += kTmaThreads) whist[i] = 0;
+    __syncthreads();
+    for (uint32_t q = q0 + lane; q < q1; q += 32) atomicAdd(&whist[warp * E + own[q]], 1u);
+    __syncthreads();
+    for (uint32_t e = tid; e < E; e += kTmaThreads) {
+      uint32_t base = run[e];
 #pragma unroll
-    for (int w = 0; w < kTmaWarps; ++w) {
-      const uint32_t c = whist[w * E + e];
-      whist[w * E + e] = base;
-      base += c;
+      for (int w = 0; w < kTmaWarps; ++w) {
+        const uint32_t c = whist[w * E + e];
+        whist[w * E + e] = base;
+        base += c;
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  {
-    uint32_t* wrun = whist + warp * E;
+  if (q0 < q1) {
+    uint32_t* wrun = one_warp ? run : whist + warp * E;
     for (uint32_t c0 = q0; c0 < q1; c0 += 32) {
       const uint32_t q = c0 + lane;
       const bool valid = q < q1;
