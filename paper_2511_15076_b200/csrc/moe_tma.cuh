@@ -716,11 +716,58 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
   constexpr bool fp8c = FP8C;  // mode 3 (a separate instantiation keeps the bf16 path spill-free)
   const uint32_t payload = 2u * H;
   MOE_STAMP(R, 2, 0);
+  const uint32_t nvec = payload / 16;
+  if (L.share && !MIRROR && !fp8c) {
+    // Emulated ranks: CTAs take chunks of kRedChunk tokens of ANY lane from a
+    // launch-wide counter (lane 0's workspace, one per iteration parity; the
+    // next parity's is zeroed here -- nobody uses it before this kernel ends),
+    // so the lanes finish together.  A CTA acquires a lane's combine flag the
+    // first time it takes a chunk of that lane.
+    constexpr uint32_t kRedChunk = 4;
+    const uint32_t nl = gridDim.y;
+    unsigned int* ctr = L.r[0].ws + 46 + (uint32_t)(iteration & 1);
+    if (b == 0 && blockIdx.y == 0 && tid == 0) L.r[0].ws[46 + (uint32_t)((iteration + 1) & 1)] = 0;
+    const uint32_t chunks_per_lane = (T + kRedChunk - 1) / kRedChunk, total = chunks_per_lane * nl;
+    __shared__ uint32_t s_chunk, s_acquired;
+    if (tid == 0) s_acquired = 0;
+    for (;;) {
+      __syncthreads();
+      if (tid == 0) {
+        s_chunk = atomicAdd(ctr, 1u);
+        const uint32_t ln = s_chunk % nl;
+        if (s_chunk < total && !((s_acquired >> ln) & 1u)) {
+          const MoeRankArgs& Rl = L.r[ln];
+          gin::Gin gl(Rl.view, 0);
+          gl.wait_ge_signal(L.cell0 + e_local, iteration * (uint64_t)T * K);
+          s_acquired |= 1u << ln;
+        }
+      }
+      __syncthreads();
+      const uint32_t c = s_chunk;
+      if (c >= total) break;
+      const uint32_t ln = c % nl, tb = (c / nl) * kRedChunk;
+      const MoeRankArgs& Rl = L.r[ln];
+      const GinDevCommView* vl = Rl.view;
+      const char* crl = vl->win[L.win_combine].base[vl->rank];
+      const uint32_t te = min(T, tb + kRedChunk);
+      for (uint64_t q = (uint64_t)tb * nvec + tid; q < (uint64_t)te * nvec; q += kMoeThreads) {
+        const uint32_t t = (uint32_t)(q / nvec), i = (uint32_t)(q % nvec);
+        uint4 y[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < (int)K) y[k] = gin::ld_na_v4(crl + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+        gin::st_v4(reinterpret_cast<char*>(Rl.out) + (uint64_t)t * payload + 16ull * i,
+                   reduce_vec<KMAX>(y, K, L.mode, Rl.weights, t));
+      }
+    }
+    MOE_STAMP(R, 2, 1);
+    MOE_STAMP(R, 2, 2);
+    return;
+  }
   if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, iteration * (uint64_t)T * K);
   __syncthreads();
   MOE_STAMP(R, 2, 1);
   const char* crecv = v->win[L.win_combine].base[rank];
-  const uint32_t nvec = payload / 16;
   const uint64_t ritems = (uint64_t)T * nvec, rstride = (uint64_t)G * kMoeThreads;
   for (uint64_t q = (uint64_t)b * kMoeThreads + tid; q < ritems; q += rstride) {
     const uint32_t t = (uint32_t)(q / nvec), i = (uint32_t)(q % nvec);
