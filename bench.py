@@ -327,6 +327,19 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
             row["one_way_ns"] = row["p50_ns"] / 2
             row["GBps_per_direction"] = (2 * sz / (row["p50_ns"] * 1e-9) / 1e9) if sz else None
             rows.append(row)
+    # worst-pair scan: 8-byte put+signal RTT between every pair
+    pairs = []
+    if world > 2:
+        for a in range(world):
+            for b in range(a + 1, world):
+                if rank in (a, b):
+                    G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles([comm]), 1, a, b, ws, wr, 8, 500, 50, 4001, 0,
+                                                         rtt.data_ptr(), None))
+                dist.barrier()
+                t = torch.tensor([float(np.sort(rtt[:500].cpu().numpy())[250]) if rank == a else 0.0],
+                                 dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                pairs.append({"pair": [a, b], "p50_ns": int(t.item())})
     # the raw NVLink round trip with no API: one thread per
     # rank flips a flag word in the peer's signal table (cells 4010/4011)
     floor = {}
@@ -347,6 +360,8 @@ def measure_pingpong(G, comm, rank, world, dist, torch, dev):
     return {"rows": rows, "target_us": 5.0, "target_metric": "RTT p50 of an 8-byte put+SignalInc (the paper's metric, "
             "PAPER.md:952-958); one-way = RTT/2", "raw_floor": floor,
             "floor_ns": floor.get("release_acquire", {}).get("p50_ns"),
+            "pair_scan_8B": pairs or None,
+            "worst_pair_8B": max(pairs, key=lambda r: r["p50_ns"]) if pairs else None,
             "csv_schema": "size_bytes,iters,p50_ns,p99_ns,mean_ns,backend=direct,transport=nvlink"}
 
 

@@ -570,6 +570,7 @@ static void check_launch_set(const ginsim_cuda_moe_t* moes, uint32_t n) {
 int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* x,
                              const int32_t* const* idx, void* stream) {
   GIN_API_BEGIN
+  NvtxRange nv("ginsim.moe_dispatch");
   check_launch_set(moes, n);
   MoeLaunch L = make_launch(moes, n);
   DeviceGuard g(moes[0]->comm->device);
@@ -596,6 +597,7 @@ int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const vo
 int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const void* const* weights, void* const* out,
                             void* stream) {
   GIN_API_BEGIN
+  NvtxRange nv("ginsim.moe_combine");
   check_launch_set(moes, n);
   MoeLaunch L = make_launch(moes, n);
   DeviceGuard g(moes[0]->comm->device);

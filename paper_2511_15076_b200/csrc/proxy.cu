@@ -265,6 +265,11 @@ struct ProxyAgent {
 
   size_t progress_once() {
     size_t work = 0;
+    bool ranged = false;  // an NVTX range only around passes that found work: the idle spin stays silent
+    auto range = [&] {
+      if (!ranged) nvtxRangePushA("ginsim.proxy_pass");
+      ranged = true;
+    };
     Pass pass;
     pass.host_done.assign(n_ctx, 0);
     std::vector<uint64_t> consumed(n_ctx, 0);
@@ -284,6 +289,7 @@ struct ProxyAgent {
           if (d.counter_id >= c->cfg.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "proxy: counter out of range");
           counter_pending[d.counter_id].fetch_add(1, std::memory_order_acq_rel);
         }
+        range();
         post(ctx, d, pass);
         ++work;
         any_dev = true;
@@ -300,6 +306,7 @@ struct ProxyAgent {
         lk.unlock();
         ginsim_cuda_descriptor d;
         descriptor_decode(item.second.data(), &d);
+        range();
         post(item.first, d, pass);
         host_taken[item.first] += 1;
         pass.host_done[item.first] = host_taken[item.first];
@@ -345,6 +352,7 @@ struct ProxyAgent {
     // never let the inline staging ring lap an unfinished copy
     while (!inflight.empty() && stage_next - inflight.front().stage_end + 512 > kStage) retire_completed(true);
     retire_completed(false);
+    if (ranged) nvtxRangePop();
     return work;
   }
 

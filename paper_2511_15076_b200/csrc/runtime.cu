@@ -433,6 +433,7 @@ static bool direct_counter_pending(Comm* c, uint32_t id) {
 uint64_t host_op(Comm* c, uint32_t ctx, uint8_t opcode, uint32_t peer, uint32_t dst_win, uint64_t dst_off,
                  uint32_t src_win, uint64_t src_or_value, uint64_t bytes, const ginsim_cuda_action* action,
                  cudaStream_t stream) {
+  NvtxRange nv(opcode == GIN_OP_PUT ? "ginsim.put" : (opcode == GIN_OP_PUT_INLINE ? "ginsim.put_value" : "ginsim.signal"));
   validate_common(c, ctx, peer);
   if (opcode == GIN_OP_PUT_INLINE && (bytes == 0 || bytes > 8))
     fail(GINSIM_E_INVALID_DESCRIPTOR, "put_value width must be 1..8 bytes");
@@ -734,6 +735,7 @@ int ginsim_cuda_mem_free(ginsim_cuda_comm_t comm, void* ptr) {
 
 int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t bytes, uint32_t* window_id) {
   GIN_API_BEGIN
+  NvtxRange nv("ginsim.window_register");
   Comm* c = &comm->impl;
   // Dense ids in call order (runtime.cpp:347-371); an id freed by
   // window_deregister is reused (lowest first), so every rank that registers
@@ -910,6 +912,7 @@ int ginsim_cuda_signal(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uin
 
 int ginsim_cuda_flush(ginsim_cuda_comm_t comm, uint32_t ctx, void* stream) {
   GIN_API_BEGIN
+  NvtxRange nv("ginsim.flush");
   Comm* c = &comm->impl;
   if (ctx >= c->cfg.n_contexts) fail(GINSIM_E_INVALID_CONTEXT, "flush: context out of range");
   if (c->cfg.backend == GIN_BACKEND_PROXY) {

@@ -16,6 +16,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ginsim_cuda.h"
 #include "gin_types.h"
 
@@ -72,6 +74,14 @@ struct CuApi {
   decltype(&::cuDeviceGetAttribute) cuDeviceGetAttribute = nullptr;
 };
 const CuApi& cuapi();
+
+// NVTX range over a host entry point (header-only NVTX v3: a no-op unless a
+// tool such as nsys / ncu --nvtx injects itself), so a profile shows which
+// ginsim call launched what (SURVEY.md §5 tracing).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Scoped current-device switch.
 struct DeviceGuard {
