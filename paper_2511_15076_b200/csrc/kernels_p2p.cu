@@ -203,7 +203,12 @@ __global__ void bw_kernel(BwArgs A) {
     if (threadIdx.x == 0) {
       atomicAdd(ctr, 1u);
       const unsigned target = (unsigned)(A.arrive0[blockIdx.y] + (uint64_t)(i + 1) * G);
+      const uint64_t tw = gin::globaltimer();
       while (*reinterpret_cast<volatile unsigned*>(ctr) - target > 0x7FFFFFFFu) {
+        if (gin::globaltimer() - tw > v->timeout_ns) {
+          gin::raise_error(v, GIN_DEVERR_TIMEOUT);
+          break;
+        }
       }
       if (blockIdx.x == 0 && i >= A.warmup) A.ns[i - A.warmup] = gin::globaltimer() - t0;
     }

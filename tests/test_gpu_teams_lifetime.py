@@ -260,3 +260,34 @@ def test_proxy_contexts_signalling_one_cell_stay_monotone():
             U.set_device(0)
     finally:
         close(cs)
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_timeouts_become_typed_errors_and_the_comm_stays_usable(backend):
+    """Failure detection (runtime.cpp:296-311, Config.timeout_ms): a host wait
+    that is never satisfied raises Timeout after the comm's timeout; a device
+    program waiting for a peer that never launches (ping-pong with only rank
+    0 running) ends its spin at the timeout and raises Timeout through the
+    device error word; afterwards the comm still carries ops."""
+    cs = world(2, backend, timeout_ms=300)
+    try:
+        w, ptrs = register(cs, 4096)
+        t0 = time.time()
+        with pytest.raises(G.Timeout):
+            cs[1].wait_signal(7, 1)
+        assert 0.25 < time.time() - t0 < 5.0
+        rtt = U.malloc(8 * 16)
+        t0 = time.time()
+        with pytest.raises(G.Timeout):
+            G.check(G.lib().ginsim_cuda_pingpong(G.comm_handles(cs[:1]), 1, 0, 1, w, w, 8, 16, 0, 40, 0, rtt, None))
+        assert time.time() - t0 < 10.0
+        U.free(rtt)
+        for c in cs:
+            c.device_error(clear=True)
+        g = G.Gin(cs[0], 0)
+        g.put_value(1, w, 0, 0x5A5A, 2, signal=9)
+        cs[1].wait_signal(9, 1)
+        assert int(U.d2h(ptrs[1], 2, np.uint16)[0]) == 0x5A5A
+        g.flush()
+    finally:
+        close(cs)
