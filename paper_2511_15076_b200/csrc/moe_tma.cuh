@@ -11,10 +11,12 @@ __device__ __forceinline__ void rank_grid_barrier(unsigned int* ctr, unsigned in
   if (threadIdx.x == 0) {
     gin::fence_acq_rel_gpu();
     atomicAdd(ctr, 1u);
+    const uint64_t t0 = gin::globaltimer();
     while (true) {
       unsigned cur;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
       if (cur >= target) break;
+      if (gin::globaltimer() - t0 > 60000000000ull) break;  // 60 s: a broken launch must not hang the GPU
       __nanosleep(20);
     }
   }
@@ -212,10 +214,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
     const uint32_t t = (uint32_t)((it & kItemMask) / parts);
     if (!((lanes_ready >> ln) & 1u)) {  // another lane's table: wait for its Phase A barrier
       const unsigned int* b3 = L.r[ln].ws + 5;
+      const uint64_t tw = gin::globaltimer();
       for (;;) {
         unsigned cur;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(b3) : "memory");
         if (cur >= bar_target) break;
+        if (gin::globaltimer() - tw > v->timeout_ns) {
+          gin::raise_error(v, GIN_DEVERR_TIMEOUT);
+          break;
+        }
         __nanosleep(64);
       }
       gin::tma::fence_proxy_async_global();
@@ -399,10 +406,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
       // every lane's items may sit in any CTA: wait for the whole launch
       if (tid == 0) {
         const unsigned target = (unsigned)(iteration * (uint64_t)G * nl);
+        const uint64_t tw = gin::globaltimer();
         for (;;) {
           unsigned cur;
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(sarrive) : "memory");
           if (cur >= target) break;
+          if (gin::globaltimer() - tw > v->timeout_ns) {
+            gin::raise_error(v, GIN_DEVERR_TIMEOUT);
+            break;
+          }
           __nanosleep(32);
         }
         if (my_lane == 0) sgrab[(iteration + 1) & 1] = 0;  // the next iteration's counter (untouched now)
