@@ -312,6 +312,16 @@ __global__ void host_op_kernel(const GinDevCommView* v, HostOp op) {
   }
 }
 
+// Bulk part of a large host-issued direct put: every SM moves a slice with
+// 128-bit vectors (a one-warp put would crawl); the op's completion action
+// then follows as a zero-byte put in stream order (the kernel boundary orders
+// this kernel's stores before that release).
+__global__ void __launch_bounds__(512) host_copy_kernel(char* dst, const char* src, uint64_t bytes) {
+  const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+  const uint64_t lo = min(bytes, per * blockIdx.x), hi = min(bytes, lo + per);
+  if (hi > lo) gin::coop_copy(gin::CoopCta{}, dst + lo, src + lo, hi - lo);
+}
+
 __global__ void host_signal_kernel(const GinDevCommView* v, uint32_t ctx, uint32_t peer, uint32_t id,
                                    gin::SignalOp op, int32_t counter) {
   gin::Gin gin(v, ctx);
@@ -430,6 +440,8 @@ static bool direct_counter_pending(Comm* c, uint32_t id) {
 // then the direct path (a one-warp device op on `stream`) or the proxy path
 // (a descriptor for the host agent).  Returns the proxy host ticket of the
 // op on its context (0 on the direct backend).
+constexpr uint64_t kHostCopyBulk = 256ull << 10;  // host puts from this size spread over the SMs
+
 uint64_t host_op(Comm* c, uint32_t ctx, uint8_t opcode, uint32_t peer, uint32_t dst_win, uint64_t dst_off,
                  uint32_t src_win, uint64_t src_or_value, uint64_t bytes, const ginsim_cuda_action* action,
                  cudaStream_t stream) {
@@ -461,6 +473,15 @@ uint64_t host_op(Comm* c, uint32_t ctx, uint8_t opcode, uint32_t peer, uint32_t 
     op.dst_off = dst_off;
     op.src_off_or_value = src_or_value;
     op.bytes = bytes;
+    if (opcode == GIN_OP_PUT && bytes >= kHostCopyBulk) {
+      int sms = 0;
+      GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+      const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms, bytes / kHostCopyBulk));
+      host_copy_kernel<<<G, 512, 0, stream>>>(c->windows[dst_win].bases[peer] + dst_off,
+                                              c->windows[src_win].bases[c->rank] + src_or_value, bytes);
+      GIN_CUDA(cudaGetLastError());
+      op.bytes = 0;  // the completion action rides on a zero-byte put after the copy
+    }
     op.width = (uint32_t)bytes;
     op.action = to_action(action);
     host_op_kernel<<<1, 32, 0, stream>>>(c->dev_view, op);
@@ -631,6 +652,7 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
     cudaFuncAttributes fa{};
     GIN_CUDA(cudaFuncGetAttributes(&fa, (const void*)host_op_kernel));
     GIN_CUDA(cudaFuncGetAttributes(&fa, (const void*)host_signal_kernel));
+    GIN_CUDA(cudaFuncGetAttributes(&fa, (const void*)host_copy_kernel));
   }
   c->sync_view();
   GIN_CUDA(cudaDeviceSynchronize());
@@ -929,10 +951,9 @@ static uint64_t read_cells_sum(Comm* c, uint32_t id) {
   DeviceGuard g(c->device);
   std::vector<uint64_t> sub(c->world);
   uint64_t base = 0;
-  for (uint32_t s = 0; s < c->world; ++s) {
-    GIN_CUDA(cudaMemcpy(&sub[s], c->host_view.signals[c->rank] + (uint64_t)s * c->cfg.signal_cells + id, 8,
+  // the world sub-cells of the cell are a strided column: one 2-D copy
+  GIN_CUDA(cudaMemcpy2D(sub.data(), 8, c->host_view.signals[c->rank] + id, (size_t)c->cfg.signal_cells * 8, 8, c->world,
                         cudaMemcpyDeviceToHost));
-  }
   GIN_CUDA(cudaMemcpy(&base, c->host_view.signal_base + id, 8, cudaMemcpyDeviceToHost));
   uint64_t sum = 0;
   for (uint64_t x : sub) sum += x;
