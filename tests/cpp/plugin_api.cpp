@@ -141,6 +141,8 @@ static void run(ginsim::BackendKind backend) {
         EXPECT(retired == 2 && dc.poll() == 0);
         EXPECT(comm->read_counter(2) == 1);
       }
+      std::printf("rank %u: %s ops posted, waiting for the peer's signal\n", r,
+                  backend == ginsim::BackendKind::Proxy ? "proxy" : "direct");
       comm->wait_signal(4, 3);
       barrier.sync();
       cudaDeviceSynchronize();
@@ -152,6 +154,7 @@ static void run(ginsim::BackendKind backend) {
       EXPECT(&comm->team(5) == &t);
       EXPECT(throws<ginsim::UsageError>([&] { comm->register_team(ginsim::Team{5, {0}}); }));
       EXPECT(throws<ginsim::InvalidPeer>([&] { comm->register_team(ginsim::Team{6, {0, 7}}); }));
+      std::printf("rank %u: data checked, team ops\n", r);
       const uint32_t team_peer = r == 1 ? 1u : 0u;  // the other rank, in team-relative numbering
       gin.put_value(t, team_peer, recv, 0, (uint32_t)(0xC0DE0000u + r), ginsim::CompletionAction::signal(6));
       comm->wait_signal(6, 1);
@@ -170,6 +173,7 @@ static void run(ginsim::BackendKind backend) {
 }
 
 int main(int argc, char** argv) {
+  std::setvbuf(stdout, nullptr, _IONBF, 0);  // progress lines survive an abort
   host_checks();
   if (argc > 1 && std::string(argv[1]) == "gpu") {
     run(ginsim::BackendKind::Direct);
