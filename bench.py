@@ -519,6 +519,67 @@ def measure_barrier(G, comm, rank, world, dist, torch, dev, iters=2000):
     return out
 
 
+def measure_overlap(G, comm, rank, world, dist, torch, dev, T, ctas=74, steps=6):
+    """Co-residency: the HT dispatch+combine step on `ctas` CTAs per rank (half
+    the GPU; at N=2 that costs nothing, profiles/r2_ctas_sweep_n2.json) next to
+    a bf16 GEMM stream on a second CUDA stream.  Reports each alone and both
+    together (device time of the joint region, max over ranks)."""
+    H, K, E = HIDDEN, TOPK, EXPERTS
+    moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 0, 1, ctas, 0))
+    x = torch.empty(T * H, dtype=torch.int16, device=dev)
+    idx = torch.empty(T * K, dtype=torch.int32, device=dev)
+    w = torch.empty(T * K, dtype=torch.int16, device=dev)
+    out = torch.empty(T * H, dtype=torch.int16, device=dev)
+    moe.generate(1, rank, x, idx, w)
+    a = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev)
+    bm = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev)
+    cm = torch.empty(8192, 8192, dtype=torch.bfloat16, device=dev)
+    s_moe, s_mm = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+    def moe_steps():
+        for _ in range(steps):
+            G.Moe.dispatch([moe], [x], [idx], stream=s_moe)
+            G.Moe.combine([moe], [w], [out], stream=s_moe)
+
+    def gemms(nm):
+        with torch.cuda.stream(s_mm):
+            for _ in range(nm):
+                torch.matmul(a, bm, out=cm)
+
+    def timed(fn_moe, fn_mm):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s_moe)
+        s_mm.wait_event(e0)
+        if fn_moe:
+            fn_moe()
+        if fn_mm:
+            fn_mm()
+        s_moe.wait_stream(s_mm)
+        e1.record(s_moe)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    moe_steps()
+    gemms(2)
+    torch.cuda.synchronize()
+    t_moe = timed(moe_steps, None)
+    n_mm = max(1, int(round(t_moe / max(1e-3, timed(None, lambda: gemms(1))))))
+    t_mm = timed(None, lambda: gemms(n_mm))
+    t_both = timed(moe_steps, lambda: gemms(n_mm))
+    comm.check_device()
+    moe.destroy()
+    return {"workload": f"{steps} HT dispatch+combine steps on {ctas} CTAs/rank ({T} tokens/rank, u16) next to "
+                        f"{n_mm} bf16 8192^3 GEMMs on a second stream, {world} GPU(s)",
+            "moe_alone_ms": t_moe, "gemm_alone_ms": t_mm, "both_ms": t_both,
+            "overlap_gain": (t_moe + t_mm) / t_both if t_both else None}
+
+
 def measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, layout, mode, label, steps=10):
     """Labelled variants beside the headline (same windows/cells contract,
     tests/test_gpu_moe.py): layout 2 = the compact receive layout with a
@@ -753,6 +814,12 @@ def main():
         if world > 1:
             variants["dedup_ht"] = measure_variant(G, comm_x, rank, world, dist, torch, dev, stream, T, 2, 1,
                                                    "dedup transport (layout 2), bf16")
+    overlap = None
+    if not args.no_extras and world > 1:
+        try:
+            overlap = measure_overlap(G, comm_x, rank, world, dist, torch, dev, T)
+        except Exception as e:  # noqa: BLE001
+            overlap = {"error": str(e)[:200]}
     proxy = None
     if not args.no_extras:
         proxy = {"ll": measure_proxy(G, rank, world, local, dist, torch, dev, stream, allgather, 128, 10),
@@ -887,6 +954,7 @@ def main():
         "barrier": barrier,
         "variants": variants,
         "proxy_vs_direct": proxy,
+        "overlap_with_compute": overlap,
     }
     if world > 1:
         rem_disp = remote_msgs * dmsg
