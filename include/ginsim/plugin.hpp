@@ -10,6 +10,7 @@
 // constructs it, runtime.cpp:197-213).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -43,6 +44,15 @@ struct PutSource {
 };
 
 enum class Opcode : uint8_t { Put = 1, PutInline = 2, SignalOnly = 3 };
+
+// plugin.hpp:48-55 (the posting trace; the issuer is a hash of the thread id)
+struct PluginCall {
+  char op = '?';  // 'p' iput, 's' iput_signal
+  ContextId ctx = 0;
+  RankId peer = 0;
+  uint64_t bytes = 0;
+  uint64_t issuer = 0;
+};
 
 // direct_backend.hpp:17-27
 struct ResolvedOp {
@@ -151,6 +161,18 @@ class FabricPlugin {
     uint64_t n = 0;
     check(ginsim_cuda_plugin_outstanding(h_, &n));
     return static_cast<size_t>(n);
+  }
+
+  void set_call_log_enabled(bool on) { check(ginsim_cuda_plugin_set_call_log(h_, on ? 1 : 0)); }
+  std::vector<PluginCall> call_log() const {
+    uint32_t n = 0;
+    check(ginsim_cuda_plugin_call_log(h_, nullptr, 0, &n));
+    std::vector<ginsim_cuda_plugin_call> raw(n);
+    check(ginsim_cuda_plugin_call_log(h_, raw.data(), n, &n));
+    std::vector<PluginCall> out;
+    for (uint32_t i = 0; i < std::min<uint32_t>(n, (uint32_t)raw.size()); ++i)
+      out.push_back(PluginCall{raw[i].op, (ContextId)raw[i].ctx, raw[i].peer, raw[i].bytes, raw[i].issuer});
+    return out;
   }
 
   DirectContext& create_context(ContextId ctx) {

@@ -262,6 +262,22 @@ int ginsim_cuda_plugin_test(ginsim_cuda_plugin_t plugin, uint64_t request, int* 
  * completion action; UNKNOWN_HANDLE if unknown/retired, GENERIC before completion. */
 int ginsim_cuda_plugin_retire(ginsim_cuda_plugin_t plugin, uint64_t request, ginsim_cuda_action* action);
 int ginsim_cuda_plugin_outstanding(ginsim_cuda_plugin_t plugin, uint64_t* requests);
+/* Posting trace through the boundary, for tests (PluginCall, plugin.hpp:48-55,
+ * plugin.cpp:174-188): op 'p' = put, 's' = put with a remote signal; issuer =
+ * a hash of the posting thread's id.  Enabling clears the log; *n = calls
+ * recorded (the first max_calls are copied). */
+typedef struct ginsim_cuda_plugin_call {
+  char op;
+  uint8_t pad[3];
+  uint32_t ctx;
+  uint32_t peer;
+  uint32_t pad2;
+  uint64_t bytes;
+  uint64_t issuer;
+} ginsim_cuda_plugin_call;
+int ginsim_cuda_plugin_set_call_log(ginsim_cuda_plugin_t plugin, int enabled);
+int ginsim_cuda_plugin_call_log(ginsim_cuda_plugin_t plugin, ginsim_cuda_plugin_call* out, uint32_t max_calls,
+                                uint32_t* n);
 /* create_context (plugin.hpp:105), direct semantics: the posting object of
  * context ctx (one CUDA stream); INVALID_CONTEXT when ctx >= n_contexts. */
 int ginsim_cuda_plugin_create_context(ginsim_cuda_plugin_t plugin, uint32_t ctx, ginsim_cuda_direct_ctx_t* out);

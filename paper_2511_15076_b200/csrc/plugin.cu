@@ -20,9 +20,12 @@
 // The plugin's semantics must match the comm's backend (the reference creates
 // the plugin from the comm's BackendKind, runtime.cpp:197-213); calls of the
 // other semantics raise BackendMismatch as in plugin.cpp:38-43.
+#include <algorithm>
 #include <deque>
+#include <functional>
 #include <map>
 #include <set>
+#include <thread>
 
 #include "runtime_internal.h"
 
@@ -43,6 +46,8 @@ struct ginsim_cuda_plugin_s {
   ginsim_cuda_comm_t comm = nullptr;
   uint32_t semantics = 0;
   std::mutex mu;
+  bool log_calls = false;                          // plugin.cpp:174-188 (posting trace for tests)
+  std::vector<ginsim_cuda_plugin_call> calls;
   std::set<uint32_t> mrs;
   std::map<uint64_t, ginsim_b200::PluginRequest> requests;
   uint64_t next_request = 1;
@@ -61,6 +66,19 @@ struct ginsim_cuda_direct_ctx_s {
 using namespace ginsim_b200;
 
 namespace {
+
+// record_call (plugin.cpp:185-188): 'p' iput, 's' iput_signal / signalling post
+void record_call(ginsim_cuda_plugin_t p, char op, uint32_t ctx, uint32_t peer, uint64_t bytes) {
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (!p->log_calls) return;
+  ginsim_cuda_plugin_call c{};
+  c.op = op;
+  c.ctx = ctx;
+  c.peer = peer;
+  c.bytes = bytes;
+  c.issuer = (uint64_t)std::hash<std::thread::id>{}(std::this_thread::get_id());
+  p->calls.push_back(c);
+}
 
 void require_semantics(ginsim_cuda_plugin_t p, uint32_t k, const char* op) {
   if (p->semantics != k)
@@ -180,6 +198,7 @@ int ginsim_cuda_plugin_iput(ginsim_cuda_plugin_t p, const ginsim_cuda_put_source
   GIN_API_BEGIN
   require_semantics(p, 1, "iput");
   if (action && action->signal_id >= 0) fail(GINSIM_E_GENERIC, "iput does not carry a remote signal; use iput_signal");
+  record_call(p, 'p', ctx, peer, bytes);
   *request = iput_common(p, src, dst_mr, dst_offset, bytes, peer, ctx, nullptr, action);
   GIN_API_END
 }
@@ -190,6 +209,7 @@ int ginsim_cuda_plugin_iput_signal(ginsim_cuda_plugin_t p, const ginsim_cuda_put
                                    const ginsim_cuda_action* action, uint64_t* request) {
   GIN_API_BEGIN
   require_semantics(p, 1, "iput_signal");
+  record_call(p, 's', ctx, peer, bytes);
   ginsim_cuda_action sig{(int32_t)signal_id, signal_add, signal_add ? operand : 1ull, -1, 0};
   *request = iput_common(p, src, dst_mr, dst_offset, bytes, peer, ctx, &sig, action);
   GIN_API_END
@@ -225,6 +245,21 @@ int ginsim_cuda_plugin_outstanding(ginsim_cuda_plugin_t p, uint64_t* n) {
   return GINSIM_OK;
 }
 
+int ginsim_cuda_plugin_set_call_log(ginsim_cuda_plugin_t p, int enabled) {
+  std::lock_guard<std::mutex> lk(p->mu);
+  p->log_calls = enabled != 0;
+  p->calls.clear();
+  return GINSIM_OK;
+}
+
+int ginsim_cuda_plugin_call_log(ginsim_cuda_plugin_t p, ginsim_cuda_plugin_call* out, uint32_t max_calls, uint32_t* n) {
+  std::lock_guard<std::mutex> lk(p->mu);
+  const uint32_t k = (uint32_t)std::min<size_t>(max_calls, p->calls.size());
+  for (uint32_t i = 0; i < k; ++i) out[i] = p->calls[i];
+  if (n) *n = (uint32_t)p->calls.size();
+  return GINSIM_OK;
+}
+
 int ginsim_cuda_plugin_create_context(ginsim_cuda_plugin_t p, uint32_t ctx, ginsim_cuda_direct_ctx_t* out) {
   GIN_API_BEGIN
   require_semantics(p, 0, "create_context");
@@ -247,6 +282,7 @@ int ginsim_cuda_plugin_create_context(ginsim_cuda_plugin_t p, uint32_t ctx, gins
 int ginsim_cuda_direct_post(ginsim_cuda_direct_ctx_t d, const ginsim_cuda_resolved_op* op) {
   GIN_API_BEGIN
   Comm* c = &d->plugin->comm->impl;
+  record_call(d->plugin, op->action.signal_id >= 0 ? 's' : 'p', d->index, op->peer, op->bytes);
   std::lock_guard<std::mutex> lk(d->mu);
   const ginsim_cuda_action* a = &op->action;
   switch (op->opcode) {

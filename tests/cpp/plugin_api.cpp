@@ -78,6 +78,7 @@ static void run(ginsim::BackendKind backend) {
       const uint32_t peer = (r + 1) % kRanks, left = (r + kRanks - 1) % kRanks;
       ginsim::FabricPlugin plugin(*comm, backend);
       if (backend == ginsim::BackendKind::Proxy) {
+        plugin.set_call_log_enabled(true);
         const auto mr_s = plugin.reg_mr(send.id());
         const auto mr_r = plugin.reg_mr(recv.id());
         EXPECT(plugin.reg_mr(send.id()) == mr_s);  // idempotent
@@ -107,6 +108,10 @@ static void run(ginsim::BackendKind backend) {
             plugin.iput(ginsim::PutSource::inline_bytes(0x0102030405060708ull), mr_r, kBytes - 8, 8, peer, 0, {});
         while (!plugin.test(req2)) std::this_thread::yield();
         plugin.retire(req2);
+        // the posting trace: iput_signal, (rejected) iput, inline iput -- in order, from this thread
+        const auto log = plugin.call_log();
+        EXPECT(log.size() == 2 && log[0].op == 's' && log[0].bytes == kBytes && log[0].peer == peer &&
+               log[0].ctx == 1 && log[1].op == 'p' && log[1].bytes == 8 && log[0].issuer == log[1].issuer);
         EXPECT(throws<ginsim::BackendMismatch>([&] { plugin.create_context(0); }));
       } else {
         EXPECT(throws<ginsim::BackendMismatch>([&] {
