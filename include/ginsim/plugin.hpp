@@ -43,8 +43,6 @@ struct PutSource {
   }
 };
 
-enum class Opcode : uint8_t { Put = 1, PutInline = 2, SignalOnly = 3 };
-
 // plugin.hpp:48-55 (the posting trace; the issuer is a hash of the thread id)
 struct PluginCall {
   char op = '?';  // 'p' iput, 's' iput_signal

@@ -10,7 +10,10 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
 #include <cstddef>
+#include <functional>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -150,6 +153,16 @@ class Window {
 // ---------------------------------------------------------------- runtime.hpp:26-58
 enum class BackendKind { Direct, Proxy };
 inline const char* to_string(BackendKind k) { return k == BackendKind::Direct ? "direct" : "proxy"; }
+// runtime.hpp:26-29.  On B200 the "transport" is NVLink peer memory (or one
+// GPU's HBM for emulated ranks) whatever the bootstrap; progress is always
+// asynchronous (the device moves the bytes, the proxy agent is a thread):
+// the fields are kept so reference code compiles, and are informational.
+enum class TransportKind { Inproc, Socket, Nvlink };
+enum class ProgressMode { Threaded, Manual };
+inline const char* to_string(TransportKind k) {
+  return k == TransportKind::Inproc ? "inproc" : (k == TransportKind::Socket ? "socket" : "nvlink");
+}
+enum class Opcode : uint8_t { Put = 1, PutInline = 2, SignalOnly = 3 };
 
 struct Config {
   uint32_t n_contexts = 4;
@@ -158,6 +171,7 @@ struct Config {
   uint32_t counter_cells = 256;
   uint32_t queue_depth = 1024;
   uint64_t timeout_ms = 30'000;
+  ProgressMode progress = ProgressMode::Threaded;  // informational on B200 (always asynchronous)
   int device = -1;  // B200: GPU of this rank (-1 = rank % device count)
   friend bool operator==(const Config&, const Config&) = default;
 
@@ -230,6 +244,8 @@ class DevComm {
   const Config& config() const { return cfg_; }
   BackendKind backend() const { return backend_; }
   const Team& world_team() const { return world_team_; }
+  TransportKind transport_kind() const { return TransportKind::Nvlink; }
+  ProgressMode progress_mode() const { return cfg_.progress; }
   ginsim_cuda_comm_t handle() const { return c_; }
 
   // Collective (runtime.cpp:347-371): `local` are device bytes this rank owns.
@@ -282,6 +298,60 @@ class DevComm {
   void wait_counter(CounterId id, uint64_t expected) { check(ginsim_cuda_wait_counter(c_, id, expected)); }
   void reset_counter(CounterId id) { check(ginsim_cuda_reset_counter(c_, id)); }
   void flush(ContextId ctx) { check(ginsim_cuda_flush(c_, ctx, nullptr)); }
+
+  // runtime.hpp:164-171.  Delivery needs no host pumping on B200 (the device
+  // moves the bytes; the proxy agent runs on its own thread), so a local
+  // progress pass only surfaces device-side failures; it returns 0.
+  size_t pump_local() {
+    check_failed();
+    return 0;
+  }
+  // The simulator's clock; here the host's monotonic clock in ns.
+  uint64_t virtual_now() const {
+    return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  }
+  // runtime.hpp:188-191: poll pred until it holds; Timeout after config().timeout_ms.
+  void wait_until(const std::function<bool()>& pred, const char* what) {
+    const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(cfg_.timeout_ms);
+    uint32_t idle = 0;
+    while (!pred()) {
+      check_failed();
+      if (std::chrono::steady_clock::now() > deadline)
+        throw Timeout(std::string(what) + ": exceeded " + std::to_string(cfg_.timeout_ms) + " ms");
+      if (++idle < 128) std::this_thread::yield();
+      else std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
+
+  // runtime.hpp:180-183 / runtime.cpp:474-544: validate one op and route it to
+  // the backend (team-relative peer; 1-8 byte inline values little-endian).
+  void submit_op(ContextId ctx, const Team& team, uint32_t peer_team_rank, Opcode opcode, WindowId dst_window,
+                 uint64_t dst_offset, WindowId src_window, uint64_t src_offset_or_value, uint64_t bytes,
+                 const CompletionAction& action) {
+    const RankId peer = team_translate(team, peer_team_rank);
+    const ginsim_cuda_action a = action.to_c();
+    switch (opcode) {
+      case Opcode::Put:
+        check(ginsim_cuda_put(c_, ctx, peer, dst_window, dst_offset, src_window, src_offset_or_value, bytes, &a,
+                              nullptr));
+        break;
+      case Opcode::PutInline:
+        check(ginsim_cuda_put_value(c_, ctx, peer, dst_window, dst_offset, src_offset_or_value, (uint32_t)bytes, &a,
+                                    nullptr));
+        break;
+      case Opcode::SignalOnly: {
+        if (!action.remote_signal) throw InvalidDescriptor("SIGNAL_ONLY op without a signal");
+        ginsim_cuda_action extra = a;
+        extra.signal_id = -1;
+        check(ginsim_cuda_signal(c_, ctx, peer, action.remote_signal->id,
+                                 action.remote_signal->op.kind == SignalKind::Add, action.remote_signal->op.operand,
+                                 &extra, nullptr));
+        break;
+      }
+    }
+  }
   void check_failed() const {
     uint32_t code = 0;
     check(ginsim_cuda_device_error(c_, &code, 1));

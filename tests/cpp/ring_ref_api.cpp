@@ -116,6 +116,15 @@ static void ring_gpu() {
       // out-of-bounds puts raise the reference's exception type (types.cpp:52-60)
       EXPECT(throws<ginsim::OutOfBounds>(
           [&] { gin.put(comm->world_team(), (r + 1) % kRanks, recv, kBytes - 7, send, 0, 8); }));
+      // DevComm::submit_op / wait_until / pump_local (runtime.hpp:164-191)
+      comm->submit_op(0, comm->world_team(), (r + 1) % kRanks, ginsim::Opcode::PutInline, recv.id(), 24,
+                      ginsim::kInlineWindow, 0x0A0B, 2, ginsim::CompletionAction::signal(2));
+      comm->wait_until([&] { return comm->read_signal(2) >= 1; }, "submit_op signal");
+      EXPECT(comm->pump_local() == 0);
+      EXPECT(comm->virtual_now() > 0 && comm->transport_kind() == ginsim::TransportKind::Nvlink);
+      EXPECT(throws<ginsim::RankOutOfRange>([&] {
+        comm->submit_op(0, comm->world_team(), 9, ginsim::Opcode::Put, recv.id(), 0, send.id(), 0, 8, {});
+      }));
       barrier.sync();
       comm->check_failed();
       ok[r] = 1;
