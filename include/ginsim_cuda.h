@@ -127,8 +127,11 @@ int ginsim_cuda_mem_free(ginsim_cuda_comm_t comm, void* ptr);
 
 /* DevComm::window_register (runtime.hpp:141, runtime.cpp:347-371).  Collective:
  * every rank contributes `bytes` at `local` (from ginsim_cuda_mem_alloc; or
- * any device pointer when every rank lives in this process); sizes may
- * differ, 0 is allowed.  Dense ids in call order on every rank;
+ * any device pointer when every rank lives in this process; or HOST memory --
+ * e.g. a std::vector, as the reference's host programs register -- which is
+ * pinned and mapped with cudaHostRegister so device ops reach it over PCIe
+ * while the host reads and writes it directly, in-process ranks only); sizes
+ * may differ, 0 is allowed.  Dense ids in call order on every rank;
  * REGISTRATION_MISMATCH when ranks disagree on the id. */
 int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t bytes, uint32_t* window_id);
 /* Collective registration for every rank of an in-process group from one

@@ -360,7 +360,28 @@ struct ProxyAgent {
     DeviceGuard g(c->device);
     t_start = now_ns();
     uint32_t idle = 0;
-    while (!stop.load(std::memory_order_acquire)) {
+    uint64_t stop_seen = 0;
+    for (;;) {
+      // Stop only once drained: descriptors already handed over (host queue,
+      // device rings) are still posted, so a rank that tears down right after
+      // issuing its last signal -- e.g. the closing barrier of a program --
+      // still delivers it (the reference destroys comms only after every
+      // agent joined, harness_launch.cpp:16-63).  Bounded by the comm timeout.
+      if (stop.load(std::memory_order_acquire)) {
+        if (!stop_seen) stop_seen = now_ns();
+        bool queued;
+        {
+          std::lock_guard<std::mutex> lk(hq_mu);
+          queued = !host_queue.empty();
+        }
+        if (!queued) {
+          for (uint32_t ctx = 0; ctx < n_ctx && !queued; ++ctx) {
+            const GinRingSlot* slot = slots[ctx] + (tail[ctx] & (cap - 1));
+            queued = __atomic_load_n(&slot->seq, __ATOMIC_ACQUIRE) == tail[ctx] + 1;
+          }
+        }
+        if ((!queued && inflight.empty()) || now_ns() - stop_seen > c->cfg.timeout_ms * 1000000ull) break;
+      }
       const uint64_t t0 = now_ns();
       size_t w = 0;
       try {
@@ -382,7 +403,7 @@ struct ProxyAgent {
         __builtin_ia32_pause();
       } else if (idle < 40000) {
         sched_yield();
-      } else {
+      } else if (!stop.load(std::memory_order_relaxed)) {
         std::this_thread::sleep_for(std::chrono::microseconds(20));
       }
     }
@@ -480,6 +501,11 @@ uint64_t proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]) {
   std::lock_guard<std::mutex> lk(p->hq_mu);
   p->host_queue.emplace_back(ctx, d);
   return ++p->host_submitted[ctx];
+}
+
+void proxy_check_failed(Comm* c) {
+  ProxyAgent* p = c->proxy.get();
+  if (p && p->failed.load()) fail(GINSIM_E_GENERIC, "proxy agent failed: " + p->failure);
 }
 
 bool proxy_host_done(Comm* c, uint32_t ctx, uint64_t ticket) {

@@ -695,7 +695,10 @@ int ginsim_cuda_comm_destroy(ginsim_cuda_comm_t comm) {
     cudaDeviceSynchronize();
     if (c->proxy) proxy_stop(c->proxy);
     nvls_teardown(c);
-    for (auto& w : c->windows) c->imported.insert(c->imported.end(), w.maps.begin(), w.maps.end());
+    for (auto& w : c->windows) {
+      c->imported.insert(c->imported.end(), w.maps.begin(), w.maps.end());
+      if (w.host_registered) cudaHostUnregister(w.host_registered);
+    }
     for (auto& m : c->imported) {
       cuapi().cuMemUnmap(m.ptr, m.size);
       cuapi().cuMemAddressFree(m.ptr, m.size);
@@ -766,6 +769,32 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
   while (id < c->windows.size() && c->windows[id].live) ++id;
   if (id >= GIN_MAX_WINDOWS)
     fail(GINSIM_E_USAGE, "too many live windows (max " + std::to_string(GIN_MAX_WINDOWS) + "; deregister unused ones)");
+  // Host-memory windows (compatibility with the reference's host programs,
+  // whose windows are std::vector bytes): pageable host memory is pinned and
+  // mapped (cudaHostRegister), so device ops and peers reach it through UVA
+  // while the host keeps reading and writing it directly.  In-process ranks
+  // only: host pages cannot be imported by another process.
+  void* host_registered = nullptr;
+  if (bytes > 0 && local) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, local) != cudaSuccess) {
+      cudaGetLastError();
+      at.type = cudaMemoryTypeUnregistered;
+    }
+    if (at.type == cudaMemoryTypeUnregistered) {
+      DeviceGuard dg(c->device);
+      GIN_CUDA(cudaHostRegister(local, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+      host_registered = local;
+    }
+    if (at.type == cudaMemoryTypeUnregistered || at.type == cudaMemoryTypeHost) {
+      void* dptr = nullptr;
+      GIN_CUDA(cudaHostGetDevicePointer(&dptr, local, 0));
+      if (dptr != local) {
+        if (host_registered) cudaHostUnregister(host_registered);
+        fail(GINSIM_E_USAGE, "host-memory window without a unified address (device pointer differs)");
+      }
+    }
+  }
   ExportBlob mine{};
   mine.pid = (int32_t)getpid();
   mine.device = c->device;
@@ -791,6 +820,7 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
   c->allgather(&mine, blobs.data(), sizeof(ExportBlob));
   for (uint32_t r = 0; r < c->world; ++r) {
     if (blobs[r].window_id != mine.window_id) {
+      if (host_registered) cudaHostUnregister(host_registered);
       fail(GINSIM_E_REGISTRATION_MISMATCH, "window_register call counts differ: rank " + std::to_string(c->rank) +
                                                " at " + std::to_string(mine.window_id) + ", rank " +
                                                std::to_string(r) + " at " + std::to_string(blobs[r].window_id));
@@ -798,6 +828,7 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
   }
   Comm::Window w;
   w.live = true;
+  w.host_registered = host_registered;
   w.sizes.resize(c->world);
   w.bases.resize(c->world);
   for (uint32_t r = 0; r < c->world; ++r) {
@@ -830,6 +861,7 @@ int ginsim_cuda_window_deregister(ginsim_cuda_comm_t comm, uint32_t window_id) {
     cuapi().cuMemAddressFree(m.ptr, m.size);
     cuapi().cuMemRelease(m.handle);
   }
+  if (w.host_registered) cudaHostUnregister(w.host_registered);
   w = Comm::Window{};
   c->host_view.win[window_id] = GinWindowView{};
   c->host_view.win_live &= ~(1ull << window_id);
@@ -964,6 +996,7 @@ static void wait_until(Comm* c, const std::function<bool()>& pred, const char* w
   auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(c->cfg.timeout_ms);
   uint32_t idle = 0;
   while (!pred()) {
+    proxy_check_failed(c);  // a dead agent is a failure now, not a timeout later (runtime.cpp:280-294)
     if (std::chrono::steady_clock::now() > deadline)
       fail(GINSIM_E_TIMEOUT, std::string(what) + ": exceeded " + std::to_string(c->cfg.timeout_ms) + " ms");
     if (++idle < 128) std::this_thread::yield();

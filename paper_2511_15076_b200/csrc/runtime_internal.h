@@ -141,6 +141,7 @@ struct Comm {
     std::vector<uint64_t> sizes;
     std::vector<char*> bases;
     std::vector<Mapping> maps;               // peer regions imported for this window (other processes)
+    void* host_registered = nullptr;         // host-memory window: the pages this rank cudaHostRegister'ed
   };
   std::vector<Window> windows;                // indexed by window id
   bool window_live(uint32_t w) const { return w < windows.size() && windows[w].live; }
@@ -196,6 +197,7 @@ ProxyPtr proxy_start(Comm* c);
 void proxy_stop(ProxyPtr& p);
 uint64_t proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]);  // returns the op's host ticket on ctx
 bool proxy_host_done(Comm* c, uint32_t ctx, uint64_t ticket);
+void proxy_check_failed(Comm* c);  // throws the agent's failure (no-op without an agent)
 // A host-issued op through submit_op's validation (runtime.cu); returns the
 // proxy host ticket (0 on the direct backend, which launches on `stream`).
 uint64_t host_op(Comm* c, uint32_t ctx, uint8_t opcode, uint32_t peer, uint32_t dst_win, uint64_t dst_off,

@@ -162,7 +162,17 @@ static void run(ginsim::BackendKind backend) {
       std::printf("rank %u: data checked, team ops\n", r);
       const uint32_t team_peer = r == 1 ? 1u : 0u;  // the other rank, in team-relative numbering
       gin.put_value(t, team_peer, recv, 0, (uint32_t)(0xC0DE0000u + r), ginsim::CompletionAction::signal(6));
-      comm->wait_signal(6, 1);
+      try {
+        comm->wait_signal(6, 1);
+      } catch (const ginsim::Timeout&) {
+        uint64_t d = 0, cp = 0, busy = 0, wall = 0;
+        if (backend == ginsim::BackendKind::Proxy) ginsim_cuda_proxy_stats(comm->handle(), &d, &cp, &busy, &wall);
+        uint32_t raw = 0;
+        cudaMemcpy(&raw, rbuf.data(), 4, cudaMemcpyDeviceToHost);
+        std::printf("rank %u: TIMEOUT cell6=%llu data=%08x descriptors=%llu copies=%llu\n", r,
+                    (unsigned long long)comm->read_signal(6), raw, (unsigned long long)d, (unsigned long long)cp);
+        throw;
+      }
       uint32_t v = 0;
       cudaMemcpy(&v, rbuf.data(), 4, cudaMemcpyDeviceToHost);
       EXPECT(v == 0xC0DE0000u + left);

@@ -52,3 +52,14 @@ def test_cpp_plugin_boundary_on_gpu(tmp_path):
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "direct plugin ok" in r.stdout and "proxy plugin ok" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_host_memory_windows_on_gpu(tmp_path):
+    """Host-API compatibility: windows backed by std::vector host memory, as the
+    reference's host programs register them, on both backends: a 4-rank ring
+    filled and verified by the host through the windows (tests/cpp/host_windows.cpp)."""
+    exe = _build(tmp_path, "host_windows")
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "direct host-window ring ok" in r.stdout and "proxy host-window ring ok" in r.stdout
