@@ -280,6 +280,30 @@ def test_moe_edge_cases_small_hidden_and_topk_one():
             run.close()
 
 
+@pytest.mark.parametrize("n,engine,layout,mode", [(8, 2, 0, 0), (8, 1, 1, 1), (4, 2, 1, 0), (4, 1, 0, 1)])
+def test_moe_maximum_experts_and_topk(n, engine, layout, mode):
+    """The API's upper limits: 1024 experts and top-32 routing (the KMAX=32
+    kernel instantiations), on both data movers, both layouts and both modes,
+    bit-exact against the oracle's windows and outputs."""
+    E, K, T, H, seed = 1024, 32, 24, 40, 11
+    run = MoeRun(n, E, K, T, H, mode=mode, layout=layout, engine=engine)
+    try:
+        run.generate(seed)
+        run.step()
+        cnt = O.counts(seed, n, E, K, T)
+        for r in range(n):
+            d, comb, _ = O.moe_rank_state(seed, n, E, K, T, H, r, mode=mode, n_cells=512)
+            win = run.dispatch_window(r)
+            if layout == 1:
+                win = O.compact_to_reference(win, cnt, r, n, E // n, T, K, 2 * H + 16)
+            assert (win == d).all(), r
+            assert (run.combine_window(r) == comb).all(), r
+            exp, _ = O.combine(seed, E, K, H, r, T, mode=mode)
+            assert (run.output(r) == exp).all(), r
+    finally:
+        run.close()
+
+
 def test_moe_ht_config_compact_properties():
     """BASELINE HT shape (T=4096, hidden 7168, top-8 of 256) at 8 emulated ranks:
     size-independent properties — per-expert cells equal the oracle's counts,
