@@ -54,7 +54,10 @@ def parse():
     p.add_argument("--mode", type=int, default=0, help="0 = u16 exact (the reference's arithmetic), 1 = bf16")
     p.add_argument("--ranks", type=int, default=0, help="ranks per process (0 = 8 emulated at --gpus 1, else 1)")
     p.add_argument("--no-verify", action="store_true", help="skip the post-run parity check against the oracle")
-    p.add_argument("--layout", type=int, default=1, help="0 = reference layout, 1 = compact, 2 = compact + dedup transport")
+    p.add_argument("--layout", type=int, default=-1,
+                   help="0 = reference layout, 1 = compact, 2 = compact + dedup transport; "
+                        "-1 = auto (1 at --gpus 1, where 8 emulated ranks share HBM; 2 over NVLink). "
+                        "Layouts 1 and 2 end in bit-identical windows and cells.")
     p.add_argument("--ctas", type=int, default=0)
     p.add_argument("--engine", type=int, default=0, help="0 = auto (TMA), 1 = LSU stores, 2 = TMA")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -644,6 +647,7 @@ def verify_step(G, torch, comms, moes, outs, seed, R_total, T, H, K, E, mode, la
     from oracle import oracle as O
     dev = outs[0].device
     dmsg, cmsg = 2 * H + 16, 2 * H
+    layout = 1 if layout == 2 else layout  # the dedup transport ends in layout 1's windows
     slots = (R_total * T * K) if layout == 1 else (E // R_total) * R_total * T
     got = []
     for c, m, o in zip(comms, moes, outs):
@@ -709,6 +713,13 @@ def main():
 
     T, H, K, E = args.tokens, HIDDEN, TOPK, EXPERTS
     seed = 1
+    if args.layout < 0:
+        # Over NVLink the dedup transport (one row per (token, destination
+        # rank), fanned out into the same compact windows by the destination)
+        # moves 0.45x (N=4) .. 0.66x (N=8) of the wire bytes.  With every rank
+        # in one GPU's HBM the fan-out is an extra HBM pass, so N=1 keeps the
+        # direct compact layout.
+        args.layout = 2 if world > 1 else 1
     cfg = G.MoeConfig(E, K, T, H, args.mode, args.layout, args.ctas, args.engine)
     moes = G.Moe.create_all(comms, cfg) if R > 1 else [G.Moe(comms[0], cfg)]
     dev = torch.device("cuda", local)
@@ -727,9 +738,11 @@ def main():
         G.Moe.combine(moes, wb, ob, stream=stream)
 
     e_local = E // R_total
-    remote_msgs = 0
+    remote_msgs = remote_rows = 0
     for c, i in zip(comms, idxs):
-        remote_msgs += int(((i.cpu().numpy().reshape(T, K) // e_local) != c.rank).sum())
+        dst = i.cpu().numpy().reshape(T, K) // e_local
+        remote_msgs += int((dst != c.rank).sum())
+        remote_rows += sum(len(set(int(v) for v in row) - {c.rank}) for row in dst)
     dmsg, cmsg = 2 * H + 16, 2 * H
     bytes_step = step_bytes(R_total, T)
 
@@ -775,7 +788,7 @@ def main():
 
     # --- parity self-check of the measured state (checker, untimed) ------------
     parity = None
-    if not args.no_verify and args.mode in (0, 1) and args.layout in (0, 1):
+    if not args.no_verify and args.mode in (0, 1) and args.layout in (0, 1, 2):
         try:
             parity = verify_step(G, torch, comms, moes, outs, seed, R_total, T, H, K, E, args.mode, args.layout, stream)
         except Exception as e:  # noqa: BLE001
@@ -814,6 +827,12 @@ def main():
         if world > 1:
             variants["dedup_ht"] = measure_variant(G, comm_x, rank, world, dist, torch, dev, stream, T, 2, 1,
                                                    "dedup transport (layout 2), bf16")
+            if args.layout == 2:
+                # the per-message transport the reference's protocol uses, for
+                # the NVLink-fraction figure (every message crosses the link)
+                variants["message_transport_ht"] = measure_variant(
+                    G, comm_x, rank, world, dist, torch, dev, stream, T, 1, args.mode,
+                    "per-message transport (layout 1), headline arithmetic")
     overlap = None
     if not args.no_extras and world > 1:
         try:
@@ -937,7 +956,7 @@ def main():
         "per_gpu_GBps": value / world,
         "parity": parity,
         "roofline": {"bound": "hbm",
-                     "kernel": ({"dispatch": "moe_dispatch_tma_kernel",
+                     "kernel": ({"dispatch": "moe_dispatch_dedup_kernel" if args.layout == 2 else "moe_dispatch_tma_kernel",
                                  "combine": "moe_combine_tma_kernel + moe_combine_reduce_kernel"}[dom]
                                 if args.engine in (0, 2) else f"moe_{dom}_kernel"),
                      "achieved": achieved, "peak": peak,
@@ -957,8 +976,13 @@ def main():
         "overlap_with_compute": overlap,
     }
     if world > 1:
-        rem_disp = remote_msgs * dmsg
-        line["nvlink"] = {"remote_bytes_per_rank_dispatch": rem_disp,
+        rem_msg_bytes = remote_msgs * dmsg
+        rem_disp = remote_rows * (2 * H + 128) if args.layout == 2 else rem_msg_bytes
+        line["nvlink"] = {"transport": "dedup rows (2H + 128 B per remote (token, rank))" if args.layout == 2
+                          else "one message (dmsg) per remote (token, k)",
+                          "remote_bytes_per_rank_dispatch": rem_disp,
+                          "remote_message_bytes_per_rank_dispatch": rem_msg_bytes,
+                          "dispatch_effective_message_GBps_per_gpu": rem_msg_bytes / (d_mean * 1e-3) / 1e9,
                           "dispatch_remote_GBps_per_gpu": rem_disp / (d_mean * 1e-3) / 1e9,
                           "combine_remote_GBps_per_gpu": remote_msgs * cmsg / (c_mean * 1e-3) / 1e9,
                           "frac_of_900": rem_disp / (d_mean * 1e-3) / 1e9 / 900.0,

@@ -73,7 +73,8 @@ struct ginsim_cuda_moe_s {
   uint64_t iteration_dispatch = 0, iteration_combine = 0;
   uint32_t last_ctas = 0;
   uint32_t fanout = 0;  // layout 2: fan-out CTAs (fixed with the grid at the first launch)
-  uint32_t cell0 = 0;   // this handle's signal cells: [cell0, cell0 + e_local + 3 + kDedupChunks)
+  uint32_t cell0 = 0;   // this handle's signal cells: [cell0, cell0 + e_local + 3 + kDedupChunks + kCombineChunks)
+  uint32_t cchunks = 0;  // pipelined combine: source-token chunks (fixed with the grid at the first launch)
   uint32_t cell_span = 0;
   uint64_t* cell_acc = nullptr;  // [e_local] counts consumed so far per local expert cell (wait targets)
 };
@@ -113,7 +114,7 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   // the sub-cells of its own table and its proxy agent's running values,
   // between two barriers, so no stale release of the previous handle can
   // satisfy a wait of the new one.
-  const uint32_t span = e_local + 3 + kDedupChunks;
+  const uint32_t span = e_local + 3 + kDedupChunks + kCombineChunks;
   uint32_t cell0 = UINT32_MAX;
   {
     std::lock_guard<std::mutex> lk(c->mu);
@@ -158,7 +159,8 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
   const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
   // counts [src][e_loc] + row counts [src] + row bounds [src][chunks + 1] (layout 2)
-  const uint64_t nbytes = ((uint64_t)e_local * n + n + n * (kDedupChunks + 1)) * 4;
+  // + pipelined-combine slot bounds [src][kCombineChunks - 1][e_loc]
+  const uint64_t nbytes = ((uint64_t)e_local * n + n + n * (kDedupChunks + 1) + n * (kCombineChunks - 1) * e_local) * 4;
   const uint64_t cbytes = T * K * cmsg;
   if (ginsim_cuda_mem_alloc(comm, dbytes, &m->buf_dispatch)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
   if (ginsim_cuda_mem_alloc(comm, nbytes, &m->buf_counts)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
@@ -205,12 +207,12 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
     if (m->pipe) GIN_CUDA(cudaMalloc(&m->pipe_buf, ((size_t)T * K + kPipeCtrWords) * 4));
   }
   DeviceGuard g(c->device);
-  GIN_CUDA(cudaMalloc(&m->ws, 256));
+  GIN_CUDA(cudaMalloc(&m->ws, kWsBytes));
   GIN_CUDA(cudaMalloc(&m->cell_acc, (size_t)e_local * 8));
   GIN_CUDA(cudaMemset(m->cell_acc, 0, (size_t)e_local * 8));
   GIN_CUDA(cudaMalloc(&m->route, (2 * (size_t)kMaxGrid + 1) * kMaxExperts * 4));
   GIN_CUDA(cudaMalloc(&m->dst_g, (size_t)cfg->tokens * ((cfg->top_k + 1) & ~1u) * sizeof(char*)));
-  GIN_CUDA(cudaMemset(m->ws, 0, 256));
+  GIN_CUDA(cudaMemset(m->ws, 0, kWsBytes));
   // Cooperative route tables from this many (token, k) pairs per rank on
   // (GINSIM_DISPATCH_COOP_MIN_PAIRS; the LL shape, 1024 pairs, stays local).
   const char* cm = std::getenv("GINSIM_DISPATCH_COOP_MIN_PAIRS");
@@ -454,7 +456,9 @@ static size_t combine_smem(const ginsim_cuda_moe_t m) {
   // mode 2 [hdr][scales][bf16 out (codes loaded into its back half)], else [hdr][chunk]
   const size_t c = m->cchunk, scb = (c / 64 + 15) / 16 * 16;
   const size_t sst = m->cfg.mode == 3 ? 128 + c / 2 + 2 * scb : (m->cfg.mode == 2 ? 128 + scb + c : 128 + c);
-  return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * sst;
+  // + pipelined combine: the chunk slot bounds [(C-1)][pairs]
+  const size_t btab = m->cchunks > 1 ? (size_t)(m->cchunks - 1) * m->cfg.experts * 4 : 0;
+  return ((sizeof(TmaSmem) * kCmbWarps + 127) & ~(size_t)127) + (size_t)kCmbWarps * kTmaStages * sst + btab;
 }
 static int combine_threads(const MoeKernels& k) { return k.cthreads; }
 
@@ -494,6 +498,18 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
     m->chunk = chunk;
     m->cchunk = cchunk;
   }
+  // Pipelined combine (moe_common.cuh): one rank per GPU over a real fabric,
+  // cooperative route tables, direct TMA kernels with a separate reduce.
+  // C * E <= kMaxExperts (the send kernel's prefix table).
+  // GINSIM_COMBINE_CHUNKS overrides (0 or 1 = one combine flag at the end).
+  uint32_t cchunks = 0;
+  if (n == 1 && m->comm->world > 1 && m->coop && !m->proxy && !m->pipe && k.tma_dispatch && k.tma_combine && k.reduce) {
+    const char* cc = std::getenv("GINSIM_COMBINE_CHUNKS");
+    cchunks = cc ? (uint32_t)std::strtoul(cc, nullptr, 10) : 4u;
+    cchunks = std::min(cchunks, std::min(kCombineChunks, kMaxExperts / m->cfg.experts));
+    if (cchunks < 2) cchunks = 0;
+  }
+  m->cchunks = cchunks;
   int sms = 0;
   GIN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->comm->device));
   const uint32_t G0 = std::max<uint32_t>(1, (uint32_t)sms / n);
@@ -546,6 +562,7 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   }
   for (uint32_t i = 0; i < n; ++i) {
     moes[i]->fanout = fanout;
+    moes[i]->cchunks = cchunks;
     moes[i]->G = Gd;
     moes[i]->Gc = Gc;
     moes[i]->Gr = Gr;
@@ -578,6 +595,8 @@ int ginsim_cuda_moe_dispatch(const ginsim_cuda_moe_t* moes, uint32_t n, const vo
   const MoeKernels k = kernels_of(moes[0]);
   L.parts = moes[0]->parts;
   L.fanout_ctas = moes[0]->fanout;
+  L.cchunks = moes[0]->cchunks;
+  L.dgrid = moes[0]->G;
   const uint32_t G = moes[0]->G;
   uint32_t chunk = moes[0]->chunk;
   const size_t smem = dispatch_smem(moes[0], G);
@@ -614,10 +633,51 @@ int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const voi
     L.r[i].out = static_cast<uint16_t*>(out[i]);
     L.r[i].iteration = moes[i]->iteration_combine;
   }
+  L.cchunks = moes[0]->cchunks;
+  L.dgrid = moes[0]->G;
   void* args[] = {&L, &chunk};
   const uint32_t Gc = moes[0]->Gc;
-  launch_coop(k.combine, Gc, n, combine_threads(k), combine_smem(moes[0]), args, (cudaStream_t)stream);
+  // Pipelined combine: the send kernel leaves `rs` SMs to the early reducer
+  // (2 full CTAs per SM; nothing fits beside a send CTA -- its registers fill
+  // every SM sub-partition), which is launched as a programmatic dependent of
+  // the send kernel so it runs while that does and reduces chunks 0..C-2 as
+  // they complete; the last chunk at full occupancy once both have finished.
+  // GINSIM_EARLY_RED_SMS overrides the SM split.
+  uint32_t Gs = Gc, rs = 0;
+  if (L.cchunks > 1) {
+    const char* es = std::getenv("GINSIM_EARLY_RED_SMS");
+    rs = es ? (uint32_t)std::strtoul(es, nullptr, 10) : kEarlyRedSms;
+    rs = std::min(rs, Gc / 2);
+    Gs = Gc - rs;
+    // no grid barrier in the send kernel: a plain launch (every CTA resident)
+    GIN_CUDA(cudaLaunchKernel(k.combine, dim3(Gs, n), dim3(combine_threads(k)), args, combine_smem(moes[0]),
+                              (cudaStream_t)stream));
+  } else {
+    launch_coop(k.combine, Gc, n, combine_threads(k), combine_smem(moes[0]), args, (cudaStream_t)stream);
+  }
   if (k.reduce && !L.no_wait && !L.fuse_reduce) {  // profiling harness: the reduce would wait on every source's flag
+    if (L.cchunks > 1 && rs == 0) {  // no SMs for an early reducer: every chunk after the send kernel
+      L.red_first = 0;
+      L.red_last = L.cchunks;
+    } else if (L.cchunks > 1) {
+      MoeLaunch Le = L;
+      Le.red_first = 0;
+      Le.red_last = L.cchunks - 1;
+      void* eargs[] = {&Le, &chunk};
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(2 * rs, n);
+      lc.blockDim = dim3(kMoeThreads);
+      lc.dynamicSmemBytes = 0;
+      lc.stream = (cudaStream_t)stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      GIN_CUDA(cudaLaunchKernelExC(&lc, k.reduce, eargs));
+      L.red_first = L.cchunks - 1;
+      L.red_last = L.cchunks;
+    }
     GIN_CUDA(cudaLaunchKernel(k.reduce, dim3(moes[0]->Gr, n), dim3(kMoeThreads), args, 0, (cudaStream_t)stream));
   }
   moes[0]->last_ctas = Gc * n;

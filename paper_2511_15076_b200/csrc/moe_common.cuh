@@ -9,6 +9,10 @@ constexpr int kMoeThreads = 512;
 constexpr int kMoeWarps = kMoeThreads / 32;
 constexpr uint32_t kMaxExperts = 1024;
 constexpr uint32_t kMaxGrid = 1024;  // CTAs per rank of one launch
+constexpr uint32_t kDedupChunks = 4;      // layout 2: row chunks per source (moe_dedup.cuh)
+constexpr uint32_t kCombineChunks = 8;    // pipelined combine: at most this many source-token chunks
+constexpr uint32_t kEarlyRedSms = 64;     // pipelined combine: SMs the send kernel leaves to the early reducer
+constexpr size_t kWsBytes = 512;          // per-handle workspace words (MoeRankArgs::ws); [64, 64 + kCombineChunks) chunk arrivals
 
 struct MoeRankArgs {
   const GinDevCommView* view;
@@ -54,7 +58,34 @@ struct MoeLaunch {
   uint32_t stage_ctas;           // Proxy pipeline: CTAs that stage (the rest leave the copy engines the HBM)
   uint32_t fanout_ctas;          // layout 2: CTAs that fan received rows out while the others put (0 = all, in turn)
   uint32_t cell0;                // first signal cell of this handle: expert cells, combine flag, rows/chunk cells
+  uint32_t cchunks;              // pipelined combine: source-token chunks C (0 = one combine flag at the end)
+  uint32_t dgrid;                // dispatch grid (CTAs per rank): chunk c = the tokens of CTAs [c*dgrid/C, ...)
+  uint32_t red_first, red_last;  // reduce launch: chunks [red_first, red_last) (pipelined combine)
 };
+
+// Pipelined combine (L.cchunks = C > 1; one rank per GPU, cooperative route
+// tables).  Source tokens are cut into C chunks aligned with the dispatch's
+// CTA token ranges, so chunk c's slot bound for expert e is the prefix row
+// g_pre[c*dgrid/C][e] the route tables already hold.  The dispatch's
+// releasing CTA writes those bounds next to the counts; the combine's send
+// kernel then walks its messages chunk-major, and whoever completes chunk
+// c's sends releases cell e_local + 3 + kDedupChunks + c at each source by
+// the number of messages it sent there.  The source reduces chunk c once
+// the cell holds iteration * tokens(c) * K -- chunks 0..C-2 by a reducer on
+// kEarlyRedSms SMs the send kernel leaves free, started while it runs
+// (programmatic dependent launch), the last chunk by the full-occupancy
+// reducer after it.
+__device__ __forceinline__ uint32_t combine_chunk_t0(uint32_t c, uint32_t C, uint32_t dgrid, uint32_t T) {
+  return c >= C ? T : (uint32_t)((uint64_t)(c * dgrid / C) * T / dgrid);
+}
+// count-window offset (u32 words) of the bounds: [src][c-1][e_loc] for c = 1..C-1
+__device__ __forceinline__ uint64_t combine_bounds_index(uint32_t n, uint32_t e_local, uint32_t src, uint32_t c,
+                                                         uint32_t C) {
+  return (uint64_t)e_local * n + n + (uint64_t)n * (kDedupChunks + 1) + ((uint64_t)src * (C - 1) + (c - 1)) * e_local;
+}
+__device__ __forceinline__ uint32_t combine_chunk_cell(uint32_t cell0, uint32_t e_local, uint32_t c) {
+  return cell0 + e_local + 3 + kDedupChunks + c;
+}
 
 // Per-handle launch counters in device memory (ws words 56..59: [0]
 // dispatch, [1] combine).  A dispatch/combine launch's iteration is the
@@ -275,7 +306,8 @@ __device__ __forceinline__ uint32_t count_index(uint32_t i, uint32_t n, uint32_t
 
 __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDevCommView* v, uint32_t win_counts,
                                                 const uint32_t* hist, uint32_t n, uint32_t rank, uint32_t e_local,
-                                                uint32_t cell0) {
+                                                uint32_t cell0, uint32_t C = 0, const uint32_t* g_pre = nullptr,
+                                                uint32_t pre_stride = 0, uint32_t G = 0) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (uint32_t d = warp; d < n; d += nw) {
     uint32_t* cb = reinterpret_cast<uint32_t*>(v->win[win_counts].base[d]);
@@ -284,6 +316,12 @@ __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDe
     // the counts; for own experts the acquirer is on this GPU (GPU scope)
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::st_relaxed_sys32(cb + (uint64_t)rank * e_local + e_loc, hist[d * e_local + e_loc]);
+    // pipelined combine: the slot bound of every source-token chunk (the
+    // prefix row of the chunk's first CTA), released by the same fence
+    for (uint32_t c = 1; c < C; ++c)
+      for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
+        gin::st_relaxed_sys32(cb + combine_bounds_index(n, e_local, rank, c, C) + e_loc,
+                              __ldcg(g_pre + (size_t)(c * G / C) * pre_stride + d * e_local + e_loc));
     gin.fence_toward(d);  // (own experts and emulated peers: GPU scope)
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::red_relaxed_sys_add(gin.sub_cell(d, rank, cell0 + e_loc), (1ull << 32) + hist[d * e_local + e_loc]);

@@ -37,7 +37,6 @@ namespace ginsim_b200 {
 //      experts' (1<<32)+count on behalf of each source (GPU scope).
 //   D: acquire every local expert as before.
 constexpr uint32_t kRowHdr = 128;
-constexpr uint32_t kDedupChunks = 4;
 
 template <int KMAX>
 __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeLaunch L, uint32_t chunk) {
@@ -320,6 +319,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
         gin::st_relaxed_sys32(cb + (uint64_t)rank * e_local + e_loc, hist_all[d * e_local + e_loc]);
       if (lane == 0) gin::st_relaxed_sys32(cb + (uint64_t)e_local * n + rank, hist_all[E + d]);
+      for (uint32_t c = 1; c < L.cchunks; ++c)  // pipelined combine: chunk slot bounds (moe_common.cuh)
+        for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
+          gin::st_relaxed_sys32(cb + combine_bounds_index(n, e_local, rank, c, L.cchunks) + e_loc,
+                                __ldcg(g_pre + (size_t)(c * G / L.cchunks) * EB + d * e_local + e_loc));
       if (d == rank) {
         gin::fence_acq_rel_gpu();
         for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)

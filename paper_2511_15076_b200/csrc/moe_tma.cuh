@@ -421,7 +421,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_tma_kernel(MoeLau
       }
       __syncthreads();
     }
-    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0);
+    release_experts(gin, v, L.win_counts, hist_all, n, rank, e_local, L.cell0, L.cchunks > 1 ? L.cchunks : 0u,
+                    R.route + (size_t)kMaxGrid * kMaxExperts, E, G);
   }
   MOE_STAMP(R, 0, 6);
   if (tid == 0 && !L.no_wait)
@@ -445,9 +446,17 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   const uint64_t dmsg = L.dmsg, cmsg = L.cmsg;
   const bool fp8 = L.mode >= 2, fp8c = L.mode == 3;
   const uint32_t payload = 2u * H, parts = L.cparts;
+  // pipelined combine (moe_common.cuh): C source-token chunks; the reducer
+  // launched behind this kernel may start as soon as every CTA is resident
+  const uint32_t C = L.cchunks > 1 ? L.cchunks : 1u;
+  const bool chunked = C > 1;
+  if (chunked) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   MOE_STAMP(R, 1, 0);
 
+  // pair_start: exclusive message prefix over pairs (e_loc, src) -- chunked,
+  // over (chunk, pair) in chunk-major order (C * P <= kMaxExperts)
   __shared__ uint32_t cnt[kMaxExperts], pair_start[kMaxExperts + 1], src_prefix[kMaxExperts];
+  __shared__ uint32_t csrc[kCombineChunks * GIN_MAX_RANKS];  // chunked: messages of (chunk, source)
   __shared__ uint32_t warp_tot[kMoeWarps];
   __shared__ uint32_t total_msgs;
   __shared__ int is_last;
@@ -469,10 +478,18 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
 
   const uint32_t P = e_local * n;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(v->win[L.win_counts].base[rank]);
+  // chunked: btab[(c-1)*P + pair] = first slot of chunk c (c = 1..C-1) in the
+  // pair's run, from the dispatch's bounds (after the stage buffers)
+  uint32_t* btab = reinterpret_cast<uint32_t*>(dsm + ((sizeof(TmaSmem) * kTmaWarps + 127) & ~(size_t)127) +
+                                               (size_t)kTmaWarps * kTmaStages * sstride);
   for (uint32_t i = tid; i < P; i += kTmaThreads) {
     const uint32_t c = gin::ld_acquire_sys32(counts + count_index(i, n, e_local));
     cnt[i] = c;
     pair_start[i] = c;
+  }
+  for (uint32_t i = tid; chunked && i < (C - 1) * P; i += kTmaThreads) {
+    const uint32_t c = 1 + i / P, pr = i % P, e_loc = pr / n, src = pr % n;
+    btab[i] = gin::ld_acquire_sys32(counts + combine_bounds_index(n, e_local, src, c, C) + e_loc);
   }
   if (tid < kMoeWarps) warp_tot[tid] = 0;
   if (lane == 0) {
@@ -481,10 +498,28 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   }
   __syncthreads();
   if (L.layout != 0) source_prefix<kTmaWarps>(cnt, src_prefix, n, e_local);
-  // exclusive scan of P <= 1024 entries with 256 threads (4 per thread)
+  const uint32_t NP = chunked ? C * P : P;  // entries of the work prefix
+  if (chunked) {
+    for (uint32_t i = tid; i < NP; i += kTmaThreads) {
+      const uint32_t c = i / P, pr = i % P;
+      const uint32_t lo = c == 0 ? 0u : btab[(c - 1) * P + pr], hi = c + 1 == C ? cnt[pr] : btab[c * P + pr];
+      pair_start[i] = hi - lo;
+    }
+    for (uint32_t i = tid; i < C * n; i += kTmaThreads) {
+      const uint32_t c = i / n, src = i % n;
+      uint32_t m = 0;
+      for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc) {
+        const uint32_t pr = e_loc * n + src;
+        m += (c + 1 == C ? cnt[pr] : btab[c * P + pr]) - (c == 0 ? 0u : btab[(c - 1) * P + pr]);
+      }
+      csrc[i] = m;
+    }
+    __syncthreads();
+  }
+  // exclusive scan of NP <= 1024 entries with 512 threads (2 per thread)
   {
-    const uint32_t per = (P + kTmaThreads - 1) / kTmaThreads;
-    const uint32_t lo = tid * per, hi = min(lo + per, P);
+    const uint32_t per = (NP + kTmaThreads - 1) / kTmaThreads;
+    const uint32_t lo = tid * per, hi = min(lo + per, NP);
     uint32_t local = 0;
     for (uint32_t i = lo; i < hi; ++i) local += pair_start[i];
     uint32_t incl = local;
@@ -512,7 +547,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       r += d;
     }
     __syncthreads();
-    if (tid == 0) pair_start[P] = total_msgs;
+    if (tid == 0) pair_start[NP] = total_msgs;
     __syncthreads();
   }
 
@@ -521,16 +556,19 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   char* const* cbases = v->win[L.win_combine].base;
   const uint64_t items = (uint64_t)total_msgs * parts;
   const uint64_t gw = (uint64_t)b * kTmaWarps + warp, stride = (uint64_t)G * kTmaWarps;
+  // message m of the work order -> its pair (| chunk << 16) and address
   auto locate = [&](uint32_t m, uint32_t& lo_pair) -> const char* {
-    uint32_t lo = 0, hi = P;
+    uint32_t lo = 0, hi = NP;
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
       if (pair_start[mid] <= m) lo = mid; else hi = mid;
     }
-    lo_pair = lo;
-    const uint32_t e_loc = lo / n, src = lo % n, slot = m - pair_start[lo];
+    const uint32_t ch = lo / P, pr = lo % P;
+    lo_pair = pr | (ch << 16);
+    const uint32_t e_loc = pr / n, src = pr % n;
+    const uint32_t slot = (ch == 0 ? 0u : btab[(ch - 1) * P + pr]) + (m - pair_start[lo]);
     const uint64_t moff = L.layout == 0 ? (((uint64_t)e_loc * n + src) * T + slot) * dmsg
-                                        : ((uint64_t)src * T * K + src_prefix[lo] + slot) * dmsg;
+                                        : ((uint64_t)src * T * K + src_prefix[pr] + slot) * dmsg;
     return recv + moff;
   };
   // lane 0: locate the message once, record (expert, source) for the stage and
@@ -572,6 +610,28 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     }
     return it < items ? it : kNoItem;
   };
+  // chunked: a chunk is complete once all its items' stores completed (per
+  // chunk arrival counter in items, ws[64 + c], reset by the completing warp
+  // for the next launch); that warp releases the chunk at every source by the
+  // messages it holds from there (GPU scope toward its own tokens)
+  uint32_t cur_ch = 0xFFFFFFFFu, cur_n = 0;  // lane 0
+  auto chunk_arrive = [&](uint32_t c, uint32_t nitems) {
+    gin::tma::fence_proxy_async_global();
+    gin::fence_acq_rel_gpu();
+    const unsigned total = (pair_start[(c + 1) * P] - pair_start[c * P]) * parts;
+    const unsigned prev = atomicAdd(R.ws + 64 + c, nitems);
+    if (prev + nitems == total) {
+      gin::fence_acq_rel_gpu();
+      R.ws[64 + c] = 0;
+      const uint32_t cell = combine_chunk_cell(L.cell0, e_local, c);
+      for (uint32_t src = 0; src < n; ++src) {
+        const uint32_t m = csrc[c * n + src];
+        if (!m) continue;
+        if (src == rank) gin::red_relaxed_sys_add(gin.sub_cell(src, rank, cell), m);
+        else gin.release_signal_raw(src, cell, m);
+      }
+    }
+  };
   if (lane == 0) {
     ctl->cur = 0;
     ctl->end = 0;
@@ -587,7 +647,8 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
     const uint64_t it = ctl->itm[s];
     if (it == kNoItem) break;
     const uint32_t p = (uint32_t)(it % parts);
-    const uint32_t pr = (uint32_t)reinterpret_cast<uint64_t>(ctl->dptr[s]);
+    const uint32_t packed = (uint32_t)reinterpret_cast<uint64_t>(ctl->dptr[s]);
+    const uint32_t pr = packed & 0xFFFFu, ch = packed >> 16;
     const uint32_t e = rank * e_local + pr / n, src = pr % n;
     const uint32_t len = tma_chunk_len(payload, chunk, p);
     char* sb = stage + (size_t)s * sstride;
@@ -649,6 +710,20 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
         gin::tma::store(cdst + (uint64_t)p * chunk, buf, len);
       }
       gin::tma::commit();
+      if (chunked) {
+        // first item of a later chunk: once every older bulk group completed
+        // (this item's stores stay in flight), count the warp's items of the
+        // previous chunk in (items arrive in increasing order, so chunks too)
+        if (cur_ch != ch) {
+          if (cur_ch != 0xFFFFFFFFu) {
+            gin::tma::wait_done<1>();
+            chunk_arrive(cur_ch, cur_n);
+          }
+          cur_ch = ch;
+          cur_n = 0;
+        }
+        ++cur_n;
+      }
       if (j >= 1) {  // refill the previous item's stage (its store has been reading meanwhile)
         gin::tma::wait_read<1>();
         const int ps = (int)((j - 1) % kTmaStages);
@@ -662,6 +737,7 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
   if (lane == 0) {
     gin::tma::wait_all();
     gin::tma::fence_proxy_async_global();
+    if (chunked && cur_ch != 0xFFFFFFFFu) chunk_arrive(cur_ch, cur_n);
   }
   MOE_STAMP(R, 1, 2);
 
@@ -776,12 +852,60 @@ __global__ void __launch_bounds__(kMoeThreads, 2) moe_combine_reduce_kernel(MoeL
     MOE_STAMP(R, 2, 2);
     return;
   }
+  const char* crecv = v->win[L.win_combine].base[rank];
+  const uint32_t nthr = blockDim.x;
+  const uint64_t rstride = (uint64_t)G * nthr;
+  if (L.cchunks > 1 && !MIRROR) {
+    // pipelined combine: chunks [red_first, red_last) in order, each once its
+    // cell holds every expert rank's messages for the chunk's tokens.  The
+    // iteration is the dispatch's: this grid may start before the send
+    // kernel (whose combine counter it would otherwise read) has finished.
+    const uint32_t C = L.cchunks;
+    const uint64_t it0 = moe_iteration(R, 0, false);
+    // phase stamps of the early reducer: CTA slots 512+ of the reduce table
+    const bool early = L.red_first == 0 && L.red_last < C;
+    auto estamp = [&](int slot) {
+      if (early && R.prof && tid == 0 && b < 512) R.prof[((uint64_t)2 * 1024 + 512 + b) * 8 + slot] = gin::globaltimer();
+    };
+    estamp(0);
+    for (uint32_t c = L.red_first; c < L.red_last; ++c) {
+      const uint32_t ta = combine_chunk_t0(c, C, L.dgrid, T), tb = combine_chunk_t0(c + 1, C, L.dgrid, T);
+      if (tid == 0) gin.wait_ge_signal(combine_chunk_cell(L.cell0, e_local, c), it0 * (uint64_t)(tb - ta) * K);
+      __syncthreads();
+      for (uint64_t q = (uint64_t)ta * nvec + (uint64_t)b * nthr + tid; q < (uint64_t)tb * nvec; q += rstride) {
+        const uint32_t t = (uint32_t)(q / nvec), i = (uint32_t)(q % nvec);
+        if (fp8c) {
+          gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
+                     reduce_fp8_vec<KMAX>(crecv, cmsg, H, t, i, K, R.weights));
+          continue;
+        }
+        uint4 y[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < (int)K) y[k] = gin::ld_na_v4(crecv + ((uint64_t)t * K + k) * cmsg + 16ull * i);
+        gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
+                   reduce_vec<KMAX>(y, K, L.mode, R.weights, t));
+      }
+      estamp(1 + (int)c);
+    }
+    if (early) {
+      estamp(6);
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      estamp(7);
+      return;
+    }
+    MOE_STAMP(R, 2, 1);
+    // the send grid has completed before this one does (stream order for the
+    // next launch; a no-op when launched without the programmatic attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    MOE_STAMP(R, 2, 2);
+    return;
+  }
   if (tid == 0) gin.wait_ge_signal(L.cell0 + e_local, iteration * (uint64_t)T * K);
   __syncthreads();
   MOE_STAMP(R, 2, 1);
-  const char* crecv = v->win[L.win_combine].base[rank];
-  const uint64_t ritems = (uint64_t)T * nvec, rstride = (uint64_t)G * kMoeThreads;
-  for (uint64_t q = (uint64_t)b * kMoeThreads + tid; q < ritems; q += rstride) {
+  const uint64_t ritems = (uint64_t)T * nvec;
+  for (uint64_t q = (uint64_t)b * nthr + tid; q < ritems; q += rstride) {
     const uint32_t t = (uint32_t)(q / nvec), i = (uint32_t)(q % nvec);
     if (fp8c) {
       gin::st_v4(reinterpret_cast<char*>(R.out) + (uint64_t)t * payload + 16ull * i,
