@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
   }
   __syncthreads();
   for (uint32_t e = tid; e < EB; e += kTmaThreads) g_hist[(size_t)b * EB + e] = hist_all[e];
+  MOE_STAMP(R, 0, 1);
   rank_grid_barrier(R.ws + 3, bar_target);
   for (uint32_t e = b + warp * G; e < EB; e += kTmaWarps * G) {
     uint32_t carry = 0;
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     }
     if (lane == 0) g_tot[e] = carry;
   }
+  MOE_STAMP(R, 0, 2);
   rank_grid_barrier(R.ws + 4, bar_target);
   for (uint32_t e = tid; e < EB; e += kTmaThreads) {
     run[e] = __ldcg(g_pre + (size_t)b * EB + e);
@@ -165,7 +167,54 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       gin::red_relaxed_sys_add(gin.sub_cell(tid, rank, L.cell0 + e_local + 2 + C), 1ull);
     }
   }
-  if (warp == 0) {
+  if (nq <= (uint32_t)kTmaWarps * 32) {
+    // Every warp ranks one 32-pair segment (warp w: pairs [32w, 32w+32)).
+    // Cross-warp offsets: an expert's pairs in earlier segments are counted
+    // by scanning own[] (at most 224 broadcast reads); a destination's first
+    // pairs in earlier segments come from per-warp row counts.
+    __shared__ uint32_t rowcnt[kTmaWarps][GIN_MAX_RANKS];
+    if (tid < kTmaWarps * GIN_MAX_RANKS) (&rowcnt[0][0])[tid] = 0;
+    __syncthreads();
+    const uint32_t q = warp * 32 + lane;
+    const bool valid = q < nq;
+    const uint32_t e = valid ? own[q] : 0xFFFFFFFFu;
+    const uint32_t d = valid ? e / e_local : 0xFFFFFFFFu;
+    const uint32_t k = valid ? q % K : 0, qt = q - k;
+    bool first = valid;
+    for (uint32_t k2 = 0; valid && k2 < k; ++k2) first = first && (own[qt + k2] / e_local != d);
+    const uint32_t peers = __match_any_sync(0xffffffffu, e);
+    const uint32_t before = __popc(peers & ((1u << lane) - 1u));
+    const uint32_t fkey = first ? d : 0xFFFFFFFEu;
+    const uint32_t fpeers = __match_any_sync(0xffffffffu, fkey);
+    const uint32_t fbefore = __popc(fpeers & ((1u << lane) - 1u));
+    uint32_t eprior = 0;
+    const uint32_t qlo = min(warp * 32, nq);
+    for (uint32_t q2 = 0; q2 < qlo; ++q2) eprior += own[q2] == e ? 1u : 0u;
+    if (first && fbefore == 0) rowcnt[warp][d] = __popc(fpeers);
+    __syncthreads();
+    uint32_t rprior = 0;
+    for (uint32_t w2 = 0; first && w2 < warp; ++w2) rprior += rowcnt[w2][d];
+    if (valid) {
+      const uint32_t t = t0 + q / K, slot = run[e] + eprior + before, e_loc = e % e_local;
+      const uint64_t pi = (uint64_t)t * Kp + k;
+      ent_g[pi] = (uint64_t)(prefix_e[e] + slot) | ((uint64_t)e_loc << 32);  // position in src's region
+      if (d == rank) {
+        dst_g[pi] = sbase[d] + ((uint64_t)rank * T * K + prefix_e[e] + slot) * dmsg;
+        hdr_g[pi] = 0;
+      } else if (first) {
+        rowj[(t - t0) * n + d] = run[E + d] + rprior + fbefore;  // the j-th row this rank sends to d
+      }
+    }
+    __syncthreads();  // a token's first pair on d may sit in the previous warp's segment
+    if (valid && d != rank) {
+      const uint32_t t = t0 + q / K;
+      const uint64_t pi = (uint64_t)t * Kp + k;
+      const uint32_t j = rowj[(t - t0) * n + d];
+      dst_g[pi] = first ? rbase[d] + ((uint64_t)rank * T + j) * payload : nullptr;
+      hdr_g[pi] = (uint64_t)(rbase[d] + rows_bytes + ((uint64_t)rank * T + j) * kRowHdr);
+    }
+    gin::tma::fence_proxy_async_global();
+  } else if (warp == 0) {  // larger segments: one warp ranks them in order
     for (uint32_t c0 = 0; c0 < nq; c0 += 32) {
       const uint32_t q = c0 + lane;
       const bool valid = q < nq;
@@ -215,6 +264,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
     }
     gin::tma::fence_proxy_async_global();
   }
+  MOE_STAMP(R, 0, 3);
   rank_grid_barrier(R.ws + 5, bar_target);
   MOE_STAMP(R, 0, 4);
 

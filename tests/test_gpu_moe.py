@@ -521,12 +521,15 @@ def test_moe_proxy_pipeline_multi_chunk(n, E, K, T, H, mode, stage_ctas, monkeyp
 
 
 @pytest.mark.parametrize("n,E,K,T,H,mode", [(2, 16, 4, 40, 256, 0), (4, 64, 8, 48, 7168, 1), (8, 64, 8, 32, 7168, 0),
-                                             (8, 256, 8, 64, 7168, 1), (2, 8, 3, 33, 64, 0)])
+                                             (8, 256, 8, 64, 7168, 1), (2, 8, 3, 33, 64, 0),
+                                             (8, 256, 8, 1024, 512, 0), (2, 64, 6, 700, 256, 1)])
 def test_moe_dedup_transport_matches_reference(n, E, K, T, H, mode):
     """Layout 2: one NVLink row per (token, destination rank), fanned out into
     the expert slots by the destination.  Dispatch windows (through the
     compact->reference map), combine windows, expert cells and outputs equal
-    the reference's over repeated steps and a routing change."""
+    the reference's over repeated steps and a routing change.  The larger
+    shapes give CTAs more than 256 pairs (the one-warp slot ranking) and,
+    with K = 6, tokens that straddle two warps' 32-pair segments."""
     run = MoeRun(n, E, K, T, H, mode=mode, layout=2, engine=2)
     try:
         for seed in (1, 6):
