@@ -61,7 +61,22 @@ def main():
     e_local = E // world
     res["cells_exact"] = all(sig[e] == iters * ((world << 32) + int(cnt[rank * e_local + e].sum()))
                              for e in range(e_local)) and sig[e_local] == iters * T * K
-    if layout != 0 and T <= 4096:
+    if mode in (0, 1) and T >= 1024:
+        # every dispatch message and combine record against the oracle's
+        # digests (the bench's own check; the dedup transport ends in layout
+        # 1's windows)
+        dmsg, cmsg = 2 * H + 16, 2 * H
+        lay = 1 if layout == 2 else layout
+        slots = world * T * K if lay == 1 else (E // world) * world * T
+        dd = torch.empty(slots, dtype=torch.int64, device=dev)
+        cd = torch.empty(T * K, dtype=torch.int64, device=dev)
+        G.digest(comm.window_ptr(moe.win_dispatch, rank), dmsg, slots, dd)
+        G.digest(comm.window_ptr(moe.win_combine, rank), cmsg, T * K, cd)
+        torch.cuda.synchronize()
+        d, v, cdig = O.window_digests(seed, world, E, K, T, H, rank, mode=mode, layout=lay)
+        res["dispatch_digests_exact"] = bool((dd.cpu().numpy().view("<u8")[v] == d[v]).all())
+        res["combine_digests_exact"] = bool((cd.cpu().numpy().view("<u8") == cdig).all())
+    if layout != 0 and T <= 4096 and mode in (0, 1):
         # compact window (layouts 1 and 2): every message of a sample carries
         # its source's token row byte for byte and the reference meta
         from tests import gpu_util as U

@@ -30,8 +30,13 @@ def _torchrun(n, env, worker="mp_worker.py"):
     return results
 
 
-@pytest.mark.parametrize("layout,tokens,mode", [(0, 128, 0), (1, 256, 0), (1, 4096, 1), (2, 1024, 0), (2, 4096, 1)])
+@pytest.mark.parametrize("layout,tokens,mode", [(0, 128, 0), (1, 256, 0), (1, 4096, 1), (2, 1024, 0), (2, 4096, 1),
+                                                (0, 1024, 0), (1, 2048, 3)])
 def test_multiprocess_moe_parity(layout, tokens, mode):
+    """Real GPUs, one process each: LL (128/256 tokens, local route tables)
+    and HT shapes (cooperative route tables + the pipelined combine) in all
+    three layouts; the HT cases check every dispatch message and combine
+    record by digest, and the fp8-combine case (mode 3) its outputs."""
     n = gpu_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -43,6 +48,8 @@ def test_multiprocess_moe_parity(layout, tokens, mode):
             assert r["dispatch_window_exact"] and r["combine_window_exact"], r
         if "compact_sample_exact" in r:
             assert r["compact_sample_exact"], r
+        if "dispatch_digests_exact" in r:
+            assert r["dispatch_digests_exact"] and r["combine_digests_exact"], r
 
 
 @pytest.mark.parametrize("layout,tokens", [(0, 128), (1, 1024)])

@@ -73,7 +73,8 @@ def main():
     res = {"rank": rank, "world": world, "tokens": T}
     for kern in (0, 1, 2):
         st = moe.phase_times(kern).astype(np.int64)
-        if not (st[:, 0] > 0).all():  # kernel not launched (LL: reduce fused into the send)
+        st = st[st[:, 0] > 0]  # CTAs that ran (the pipelined combine's send kernel leaves SMs to the reducer)
+        if st.shape[0] == 0:  # kernel not launched (LL: reduce fused into the send)
             continue
         summ, nz = summarize(st)
         phases = {}
