@@ -48,9 +48,28 @@ def main():
     moe.generate(seed, rank, x, idx, w)
     torch.cuda.synchronize()
     res = {"rank": rank, "ok": True}
-    for it in range(iters):  # back to back on one stream: no host sync between steps
+    if os.environ.get("MP_GRAPH") == "1":
+        # one eager step (plans the grids), then the step captured once in a
+        # CUDA graph and replayed: the pipelined combine's programmatic
+        # dependent launch becomes a graph edge; outputs are cleared first so
+        # the replays must rewrite them
         G.Moe.dispatch([moe], [x], [idx])
         G.Moe.combine([moe], [w], [out])
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            G.Moe.dispatch([moe], [x], [idx], stream=s)
+            G.Moe.combine([moe], [w], [out], stream=s)
+        out.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        for it in range(iters - 1):
+            g.replay()
+    else:
+        for it in range(iters):  # back to back on one stream: no host sync between steps
+            G.Moe.dispatch([moe], [x], [idx])
+            G.Moe.combine([moe], [w], [out])
     torch.cuda.synchronize()
     comm.check_device()
     got = out.cpu().numpy().view(np.uint16).reshape(T, H)

@@ -52,6 +52,23 @@ def test_multiprocess_moe_parity(layout, tokens, mode):
             assert r["dispatch_digests_exact"] and r["combine_digests_exact"], r
 
 
+@pytest.mark.parametrize("layout,tokens,mode", [(2, 2048, 0), (1, 1024, 1)])
+def test_multiprocess_moe_step_in_a_cuda_graph(layout, tokens, mode):
+    """The HT step (dedup or per-message transport, pipelined combine with its
+    programmatic dependent launch) captured once in a CUDA graph per process
+    and replayed: every replay is a full step (device iteration counters), and
+    outputs, cells and every window record equal the oracle's."""
+    n = gpu_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = 4 if n >= 4 else 2
+    res = _torchrun(n, {"MP_TOKENS": tokens, "MP_LAYOUT": layout, "MP_MODE": mode, "MP_PINGPONG": 0,
+                        "MP_GRAPH": 1, "MP_ITERS": 4})
+    for r in res:
+        assert r["combine_exact"] and r["cells_exact"], r
+        assert r["dispatch_digests_exact"] and r["combine_digests_exact"], r
+
+
 @pytest.mark.parametrize("layout,tokens", [(0, 128), (1, 1024)])
 def test_multiprocess_moe_proxy_backend(layout, tokens):
     """Proxy backend across real GPUs (each process's host agent copies its
