@@ -70,7 +70,9 @@ typedef struct ginsim_cuda_config {
   uint32_t signal_cells;  /* default 256; top 64 reserved for barriers */
   uint32_t counter_cells; /* default 256 */
   uint32_t queue_depth;   /* proxy ring capacity per context, power of two; default 1024 */
-  uint32_t reserved;
+  uint32_t transport;     /* proxy backend: 0 = the fabric (NVLink peer mappings, copy engines),
+                             1 = socket: GIN1 frames over TCP between the ranks' host agents
+                             (the reference's SocketTransport, socket_transport.cpp:498-590) */
   uint64_t timeout_ms;    /* default 30000 */
 } ginsim_cuda_config;
 
@@ -88,6 +90,18 @@ typedef struct ginsim_cuda_bootstrap {
   void* ctx;
   int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes);
 } ginsim_cuda_bootstrap;
+
+/* comm_init_socket's rendezvous (socket_transport.hpp:117-126,
+ * socket_transport.cpp:178-231): rank 0 listens on host:port (IPv4), every
+ * other rank connects to it; the returned bootstrap's allgather gathers to
+ * rank 0 and broadcasts back.  Keep it alive as long as the comm (window
+ * registration is collective over it); destroy it after the comm. */
+int ginsim_cuda_socket_bootstrap_create(const char* host, uint16_t port, uint32_t world, uint32_t rank,
+                                        uint64_t timeout_ms, ginsim_cuda_bootstrap* out);
+int ginsim_cuda_socket_bootstrap_destroy(ginsim_cuda_bootstrap* boot);
+/* reserve_loopback_port (socket_transport.hpp:128-129): a currently free
+ * loopback TCP port for a launcher. */
+int ginsim_cuda_reserve_loopback_port(uint16_t* port);
 
 typedef struct ginsim_cuda_group_s* ginsim_cuda_group_t;
 typedef struct ginsim_cuda_comm_s* ginsim_cuda_comm_t;
@@ -201,6 +215,11 @@ int ginsim_cuda_snapshot_cells(ginsim_cuda_comm_t comm, uint64_t* signals, uint6
 /* Device error word (device-side Timeout / OutOfBounds ...), 0 if clean;
  * clear != 0 resets it. */
 int ginsim_cuda_device_error(ginsim_cuda_comm_t comm, uint32_t* code, int clear);
+/* Socket transport (Config.transport = 1) statistics of this rank: frames
+ * sent, puts and payload bytes received and performed.  USAGE on a comm that
+ * uses the fabric. */
+int ginsim_cuda_net_stats(ginsim_cuda_comm_t comm, uint64_t* tx_frames, uint64_t* rx_puts, uint64_t* rx_bytes);
+
 /* Proxy agent statistics: descriptors consumed, memcpy calls issued. */
 /* Diagnostics (GINSIM_PROXY_TRACE=1 at comm creation): per agent copy
  * {bytes, ctx, host issue us, device start us, device duration us} since the
@@ -291,6 +310,51 @@ int ginsim_cuda_plugin_create_context(ginsim_cuda_plugin_t plugin, uint32_t ctx,
 int ginsim_cuda_direct_post(ginsim_cuda_direct_ctx_t ctx, const ginsim_cuda_resolved_op* op);
 int ginsim_cuda_direct_poll(ginsim_cuda_direct_ctx_t ctx, uint64_t* retired);
 int ginsim_cuda_direct_outstanding(ginsim_cuda_direct_ctx_t ctx, uint64_t* outstanding);
+
+/* ---------------------------------------------------------------- GIN1 wire codec
+ * The socket transport's framing (proj/core/include/ginsim/wire.hpp:12-67,
+ * proj/core/src/wire.cpp), little-endian, one frame per message:
+ *   header 21 B: magic u32 0x474E4931 "GIN1" | type u8 | src u32 | ctx u16 |
+ *                pad u16 = 0 | seq_or_watermark u64
+ *   PUT     (1): dst_window u32 | dst_offset u64 | len u64 | payload
+ *   SIGNAL  (2): signal_id u32 | op u8 (0 inc, 1 add) | pad 3 | operand u64 (1 for inc)
+ *   ACK     (3): (the seq field suffices)
+ *   CONTROL (4): len u64 | blob
+ * The Proxy backend's socket transport (Config.transport = 1) speaks it; the
+ * codec is exported for tests and for a host that bridges frames itself. */
+#define GINSIM_WIRE_MAGIC 0x474E4931u
+#define GINSIM_WIRE_HEADER_BYTES 21
+enum { GINSIM_WIRE_PUT = 1, GINSIM_WIRE_SIGNAL = 2, GINSIM_WIRE_ACK = 3, GINSIM_WIRE_CONTROL = 4 };
+typedef struct ginsim_cuda_wire_frame {
+  uint32_t type;             /* GINSIM_WIRE_* */
+  uint32_t src_rank;
+  uint16_t ctx;
+  uint16_t pad;
+  uint32_t window_or_signal; /* PUT: dst_window; SIGNAL: signal_id */
+  uint64_t seq_or_watermark;
+  uint64_t dst_offset;       /* PUT */
+  uint32_t signal_add;       /* SIGNAL: 0 inc, 1 add */
+  uint32_t reserved;
+  uint64_t operand;          /* SIGNAL: the amount (encode ignores it for inc and writes 1) */
+  uint64_t body_bytes;       /* PUT payload / CONTROL blob length */
+} ginsim_cuda_wire_frame;
+/* encode_put_frame / encode_signal_frame / encode_ack_frame /
+ * encode_control_frame (wire.hpp:47-53): writes the frame (header + body)
+ * into out; *len = its size.  USAGE when cap < *len (with *len set). */
+int ginsim_cuda_wire_encode(const ginsim_cuda_wire_frame* f, const void* body, void* out, size_t cap, size_t* len);
+/* FrameParser (wire.hpp:57-66): an incremental decoder over a byte stream;
+ * frames may arrive split or coalesced.  next(): *ready = 1 and the frame
+ * (its body copied to `body`) when one is whole; *ready = 0 when more bytes
+ * are needed; MALFORMED_FRAME on a bad magic, type, padding or signal op;
+ * USAGE (nothing consumed, f->body_bytes = the body size) when body_cap is
+ * too small. */
+typedef struct ginsim_cuda_wire_parser_s* ginsim_cuda_wire_parser_t;
+int ginsim_cuda_wire_parser_create(ginsim_cuda_wire_parser_t* out);
+int ginsim_cuda_wire_parser_feed(ginsim_cuda_wire_parser_t p, const void* data, size_t n);
+int ginsim_cuda_wire_parser_next(ginsim_cuda_wire_parser_t p, ginsim_cuda_wire_frame* f, void* body, size_t body_cap,
+                                 int* ready);
+size_t ginsim_cuda_wire_parser_buffered(ginsim_cuda_wire_parser_t p);
+int ginsim_cuda_wire_parser_destroy(ginsim_cuda_wire_parser_t p);
 
 /* ---------------------------------------------------------------- descriptor codec
  * proj/core/src/descriptor.cpp:148-199 (encode_descriptor / decode_descriptor),

@@ -122,10 +122,21 @@ def descriptor_fixture():
         shutil.rmtree(d)
 
 
+def wire_fixture():
+    """GIN1 frames the reference encodes (wire.cpp via ref_driver `wire`):
+    256 seeded frames of every type, with their fields and the exact bytes."""
+    return O.ref_run("wire", "--seed", 0x6171, "--count", 256)
+
+
 def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref missing: run oracle/build_ref.sh first")
     os.makedirs(GOLDEN, exist_ok=True)
+    with open(os.path.join(GOLDEN, "wire.json"), "w") as f:
+        json.dump(wire_fixture(), f)
+    if sys.argv[1:] == ["wire"]:  # only the wire fixture
+        print("wire fixture written to", GOLDEN)
+        return
     with open(os.path.join(GOLDEN, "descriptors.json"), "w") as f:
         json.dump(descriptor_fixture(), f)
     with open(os.path.join(GOLDEN, "ring.json"), "w") as f:

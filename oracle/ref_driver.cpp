@@ -21,6 +21,7 @@
 #include "ginsim/harness.hpp"
 #include "ginsim/proxy_backend.hpp"
 #include "ginsim/runtime.hpp"
+#include "ginsim/wire.hpp"
 
 using namespace ginsim;
 using clk = std::chrono::steady_clock;
@@ -250,9 +251,52 @@ int cmd_ringbench(int argc, char** argv) {
 
 }  // namespace
 
+// GIN1 frames encoded by the reference (wire.cpp) for a seeded set of
+// fields: {"frames": [{"type", "src", "ctx", "seq", "id", "offset", "add",
+// "operand", "body", "hex"}]}.  tests/golden/wire.json pins the B200 codec.
+int cmd_wire(int argc, char** argv) {
+  const uint64_t n = arg_u64(argc, argv, "--count", 64);
+  std::mt19937_64 rng(arg_u64(argc, argv, "--seed", 7));
+  auto hex = [](const std::vector<std::byte>& v) {
+    static const char* d = "0123456789abcdef";
+    std::string s;
+    for (std::byte b : v) {
+      const uint8_t x = std::to_integer<uint8_t>(b);
+      s += d[x >> 4];
+      s += d[x & 15];
+    }
+    return s;
+  };
+  std::printf("{\"frames\":[");
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t type = 1 + (uint32_t)(i % 4);
+    const uint32_t src = (uint32_t)(rng() % 8);
+    const uint16_t ctx = (uint16_t)(rng() % 5);
+    const uint64_t seq = (i % 3 == 0) ? rng() : rng() % 1000;
+    const uint32_t id = (uint32_t)(rng() % 300);
+    const uint64_t off = (i % 5 == 0) ? rng() : rng() % 65536;
+    const bool add = rng() & 1;
+    const uint64_t operand = add ? ((i % 7 == 0) ? rng() : rng() % 100) : 1;
+    const size_t blen = (type == 1 || type == 4) ? (size_t)(i % 9 == 0 ? 0 : rng() % 40) : 0;
+    std::vector<std::byte> body(blen);
+    for (auto& b : body) b = std::byte{(uint8_t)(rng() & 0xFF)};
+    std::vector<std::byte> f;
+    if (type == 1) f = encode_put_frame(src, ctx, seq, id, off, body);
+    else if (type == 2) f = encode_signal_frame(src, ctx, seq, id, add ? SignalOp::add(operand) : SignalOp::inc());
+    else if (type == 3) f = encode_ack_frame(src, ctx, seq);
+    else f = encode_control_frame(src, body);
+    std::printf("%s{\"type\":%u,\"src\":%u,\"ctx\":%u,\"seq\":%llu,\"id\":%u,\"offset\":%llu,\"add\":%d,"
+                "\"operand\":%llu,\"body\":\"%s\",\"hex\":\"%s\"}",
+                i ? "," : "", type, src, (unsigned)ctx, (unsigned long long)seq, id, (unsigned long long)off, add ? 1 : 0,
+                (unsigned long long)operand, hex(body).c_str(), hex(f).c_str());
+  }
+  std::printf("]}\n");
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: ginsim_ref_driver moe-ll|moe-ht|pingpong|bw|ring|descriptors|ringbench ...\n");
+    std::fprintf(stderr, "usage: ginsim_ref_driver moe-ll|moe-ht|pingpong|bw|ring|descriptors|ringbench|wire ...\n");
     return 2;
   }
   const std::string cmd = argv[1];
@@ -264,6 +308,7 @@ int main(int argc, char** argv) {
     if (cmd == "ring") return cmd_ring(argc, argv);
     if (cmd == "descriptors") return cmd_descriptors(argc, argv);
     if (cmd == "ringbench") return cmd_ringbench(argc, argv);
+    if (cmd == "wire") return cmd_wire(argc, argv);
   } catch (const std::exception& e) {
     std::printf("{\"error\":\"%s\"}\n", e.what());
     return 1;

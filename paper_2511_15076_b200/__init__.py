@@ -67,11 +67,13 @@ _BY_CODE = {c.code: c for c in [InvalidDescriptor, MalformedDescriptor, OutOfBou
 class Config(ctypes.Structure):
     """runtime.hpp:29-44 (Config); defaults from ginsim_cuda_config_default."""
     _fields_ = [("n_contexts", c_uint32), ("backend", c_uint32), ("signal_cells", c_uint32),
-                ("counter_cells", c_uint32), ("queue_depth", c_uint32), ("reserved", c_uint32),
+                ("counter_cells", c_uint32), ("queue_depth", c_uint32), ("transport", c_uint32),
                 ("timeout_ms", c_uint64)]
 
     DIRECT = 0
     PROXY = 1
+    FABRIC = 0   # transport: NVLink peer mappings / copy engines
+    SOCKET = 1   # transport: GIN1 frames over TCP between the ranks' agents (Proxy backend)
 
     def __init__(self, **kw):
         super().__init__()
@@ -79,6 +81,8 @@ class Config(ctypes.Structure):
         for k, v in kw.items():
             if k == "backend" and isinstance(v, str):
                 v = {"direct": 0, "proxy": 1}[v]
+            if k == "transport" and isinstance(v, str):
+                v = {"fabric": 0, "nvlink": 0, "socket": 1}[v]
             setattr(self, k, v)
 
     def _py_defaults(self):
@@ -115,6 +119,14 @@ class Descriptor(ctypes.Structure):
 
     def astuple(self):
         return tuple(getattr(self, f[0]) for f in self._fields_)
+
+
+class WireFrame(ctypes.Structure):
+    """One GIN1 frame's fields (wire.hpp:12-45); the body travels separately."""
+    _fields_ = [("type", c_uint32), ("src_rank", c_uint32), ("ctx", c_uint16), ("pad", c_uint16),
+                ("window_or_signal", c_uint32), ("seq_or_watermark", c_uint64), ("dst_offset", c_uint64),
+                ("signal_add", c_uint32), ("reserved", c_uint32), ("operand", c_uint64), ("body_bytes", c_uint64)]
+    PUT, SIGNAL, ACK, CONTROL = 1, 2, 3, 4
 
 
 class MoeConfig(ctypes.Structure):
@@ -235,6 +247,17 @@ def _declare(L):
                                   c_int),
         "ginsim_cuda_register_team": ([P, c_uint32, POINTER(c_uint32), c_uint32], c_int),
         "ginsim_cuda_team": ([P, c_uint32, POINTER(c_uint32), POINTER(c_uint32)], c_int),
+        "ginsim_cuda_wire_encode": ([POINTER(WireFrame), P, P, ctypes.c_size_t, POINTER(ctypes.c_size_t)], c_int),
+        "ginsim_cuda_wire_parser_create": ([POINTER(P)], c_int),
+        "ginsim_cuda_wire_parser_feed": ([P, P, ctypes.c_size_t], c_int),
+        "ginsim_cuda_wire_parser_next": ([P, POINTER(WireFrame), P, ctypes.c_size_t, POINTER(c_int)], c_int),
+        "ginsim_cuda_wire_parser_buffered": ([P], ctypes.c_size_t),
+        "ginsim_cuda_wire_parser_destroy": ([P], c_int),
+        "ginsim_cuda_socket_bootstrap_create": ([c_char_p, ctypes.c_uint16, c_uint32, c_uint32, c_uint64,
+                                                 POINTER(Bootstrap)], c_int),
+        "ginsim_cuda_socket_bootstrap_destroy": ([POINTER(Bootstrap)], c_int),
+        "ginsim_cuda_reserve_loopback_port": ([POINTER(ctypes.c_uint16)], c_int),
+        "ginsim_cuda_net_stats": ([P, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64)], c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name, None)
@@ -456,6 +479,12 @@ class Comm:
         check(lib().ginsim_cuda_proxy_stats(self.h, byref(a), byref(b), byref(c), byref(d)))
         return {"descriptors": a.value, "copies": b.value, "busy_ns": c.value, "wall_ns": d.value}
 
+    def net_stats(self):
+        """Socket transport counters of this rank (Config(transport="socket"))."""
+        a, b, c = c_uint64(), c_uint64(), c_uint64()
+        check(lib().ginsim_cuda_net_stats(self.h, byref(a), byref(b), byref(c)))
+        return {"tx_frames": a.value, "rx_puts": b.value, "rx_bytes": c.value}
+
 
 class Gin:
     """Host-issued per-context handle (runtime.hpp:260-306), executed on the GPU."""
@@ -528,6 +557,55 @@ def write_csv(path, rows, backend="direct", transport="nvlink", seed=0):
         f.write("size_bytes,iters,p50_ns,p99_ns,mean_ns,backend,transport,seed\n")
         for r in rows:
             f.write(f"{r['size_bytes']},{r['iters']},{r['p50_ns']},{r['p99_ns']},{r['mean_ns']},{backend},{transport},{seed}\n")
+
+
+def wire_encode(type, src=0, ctx=0, seq=0, window_or_signal=0, dst_offset=0, signal_add=0, operand=1,
+                body=b"") -> bytes:
+    """encode_{put,signal,ack,control}_frame (wire.hpp:47-53) through the C ABI."""
+    f = WireFrame()
+    f.type, f.src_rank, f.ctx, f.seq_or_watermark = type, src, ctx, seq
+    f.window_or_signal, f.dst_offset, f.signal_add, f.operand = window_or_signal, dst_offset, signal_add, operand
+    f.body_bytes = len(body)
+    n = ctypes.c_size_t()
+    cap = 64 + len(body)
+    out = (c_uint8 * cap)()
+    src_buf = (c_uint8 * max(1, len(body))).from_buffer_copy(body or b"\0")
+    check(lib().ginsim_cuda_wire_encode(byref(f), src_buf, out, cap, byref(n)))
+    return bytes(out[:n.value])
+
+
+class WireParser:
+    """FrameParser (wire.hpp:57-66): feed() bytes as they arrive, next() returns
+    (WireFrame, body bytes) or None; MalformedFrame on garbage."""
+
+    def __init__(self):
+        self.h = c_void_p()
+        check(lib().ginsim_cuda_wire_parser_create(byref(self.h)))
+
+    def feed(self, data: bytes):
+        buf = (c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        check(lib().ginsim_cuda_wire_parser_feed(self.h, buf, len(data)))
+
+    def next(self, body_cap=1 << 20):
+        f = WireFrame()
+        body = (c_uint8 * max(1, body_cap))()
+        ready = c_int()
+        check(lib().ginsim_cuda_wire_parser_next(self.h, byref(f), body, body_cap, byref(ready)))
+        return (f, bytes(body[:f.body_bytes])) if ready.value else None
+
+    def buffered(self):
+        return lib().ginsim_cuda_wire_parser_buffered(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib_loaded():
+            lib().ginsim_cuda_wire_parser_destroy(self.h)
+            self.h = None
+
+
+def reserve_loopback_port() -> int:
+    p = ctypes.c_uint16()
+    check(lib().ginsim_cuda_reserve_loopback_port(byref(p)))
+    return p.value
 
 
 def descriptor_encode(d: Descriptor) -> bytes:
