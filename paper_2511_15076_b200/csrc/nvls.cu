@@ -35,7 +35,8 @@ struct NvlsBlob {
 
 void nvls_setup(Comm* c) {
   const char* env = std::getenv("GINSIM_NVLS");
-  const bool want = !(env && env[0] == '0');
+  // (the socket transport models peers outside the NVLink domain: no multicast)
+  const bool want = !(env && env[0] == '0') && c->cfg.transport == 0;
   const CuApi& api = cuapi();
   NvlsBlob me{};
   me.pid = (int32_t)getpid();

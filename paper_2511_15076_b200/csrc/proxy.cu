@@ -102,6 +102,11 @@ struct ProxyAgent {
   std::string failure;
   std::atomic<bool> failed{false};
 
+  // socket transport (Config.transport = 1): every peer but this rank is
+  // reached through GIN1 frames (net.cu); peers posted to in this pass
+  NetPtr net;
+  std::vector<uint8_t> net_touched;
+
   ProxyAgent(Comm* comm)
       : c(comm),
         host_completed(comm->cfg.n_contexts),
@@ -179,11 +184,53 @@ struct ProxyAgent {
   }
 
   // iput / iput_signal (plugin.hpp:86-90) for one decoded descriptor.
+  // The socket transport's post: the same checks, then the bytes go through
+  // net.cu (staging copy on the peer's stream + a GIN1 frame); the signal is
+  // a frame behind them, applied by the peer's receiver; counters complete
+  // with the peer's acks (the pass's completion stream waits for them).
+  void post_net(uint32_t ctx, const ginsim_cuda_descriptor& d, uint32_t peer, Pass& pass) {
+    const GinDevCommView& v = c->host_view;
+    const uint32_t si = stream_index(peer);
+    if (d.opcode != GIN_OP_SIGNAL_ONLY && d.bytes > 0) {
+      if (d.dst_window >= GIN_MAX_WINDOWS || !((v.win_live >> d.dst_window) & 1ull)) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown destination window");
+      const GinWindowView& dw = v.win[d.dst_window];
+      if (d.dst_offset > dw.size[peer] || d.bytes > dw.size[peer] - d.dst_offset)
+        fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: destination range exceeds capacity");
+      if (d.opcode == GIN_OP_PUT) {
+        if (d.src_window >= GIN_MAX_WINDOWS || !((v.win_live >> d.src_window) & 1ull)) fail(GINSIM_E_UNKNOWN_WINDOW, "proxy: unknown source window");
+        const GinWindowView& sw = v.win[d.src_window];
+        if (d.src_offset_or_value > sw.size[v.rank] || d.bytes > sw.size[v.rank] - d.src_offset_or_value)
+          fail(GINSIM_E_OUT_OF_BOUNDS, "proxy: source range exceeds capacity");
+        flush_memops(si);
+        touched[si] = 1;
+        net_put(net.get(), peer, ctx, d.dst_window, d.dst_offset, sw.base[v.rank] + d.src_offset_or_value, d.bytes,
+                streams[si]);
+      } else {
+        net_put_inline(net.get(), peer, ctx, d.dst_window, d.dst_offset, d.src_offset_or_value, (uint32_t)d.bytes);
+      }
+      net_touched[peer] = 1;
+      n_copies.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (d.flags & GIN_FLAG_HAS_SIGNAL) {
+      if (d.signal_id >= v.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "proxy: signal out of range");
+      net_signal(net.get(), peer, ctx, d.signal_id, (d.flags & GIN_FLAG_SIGNAL_IS_ADD) != 0,
+                 (d.flags & GIN_FLAG_SIGNAL_IS_ADD) ? d.signal_operand : 1ull);
+    }
+    if (d.flags & GIN_FLAG_HAS_COUNTER) {
+      ctr_value[d.counter_id] += 1;
+      ctr_touched[d.counter_id] = 1;
+      pass.counters.push_back(d.counter_id);
+    }
+  }
+
   void post(uint32_t ctx, const ginsim_cuda_descriptor& d, Pass& pass) {
-    (void)ctx;
     const GinDevCommView& v = c->host_view;
     const uint32_t peer = resolve_peer(d.team, d.peer);
     if (peer >= v.world) fail(GINSIM_E_INVALID_PEER, "proxy: descriptor peer out of range");
+    if (net && peer != v.rank) {
+      post_net(ctx, d, peer, pass);
+      return;
+    }
     const uint32_t si = stream_index(peer);
     cudaStream_t stream = streams[si];
     touched[si] = 1;
@@ -331,6 +378,19 @@ struct ProxyAgent {
         pass.evs.push_back(ev);
         touched[si] = 0;
       }
+      if (net) {  // socket peers: local completion = the peer acked every put posted so far
+        for (uint32_t p = 0; p < c->world; ++p) {
+          if (!net_touched[p]) continue;
+          net_touched[p] = 0;
+          CUstreamBatchMemOpParams w{};
+          w.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+          w.waitValue.address = (CUdeviceptr)net_acked_device(net.get(), p);
+          w.waitValue.value64 = net_last_seq(net.get(), p);
+          w.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+          flush_memops(comp);
+          GIN_CU(cuapi().cuStreamBatchMemOp((CUstream)completion_stream(), 1, &w, 0));
+        }
+      }
       for (uint32_t id : pass.counters) {
         if (!ctr_touched[id]) continue;
         ctr_touched[id] = 0;
@@ -380,7 +440,11 @@ struct ProxyAgent {
             queued = __atomic_load_n(&slot->seq, __ATOMIC_ACQUIRE) == tail[ctx] + 1;
           }
         }
-        if ((!queued && inflight.empty()) || now_ns() - stop_seen > c->cfg.timeout_ms * 1000000ull) break;
+        if (!queued && inflight.empty()) break;
+        if (now_ns() - stop_seen > c->cfg.timeout_ms * 1000000ull) {
+          if (net) net_release_waits(net.get());  // a peer that left never acks: let the streams drain
+          break;
+        }
       }
       const uint64_t t0 = now_ns();
       size_t w = 0;
@@ -462,10 +526,16 @@ ProxyPtr proxy_start(Comm* c) {
   const char* tv = std::getenv("GINSIM_PROXY_TRACE");
   p->trace = tv && tv[0] == '1';
   p->ctr_value.assign(c->cfg.counter_cells, 0);
+  if (c->cfg.transport == 1) {  // collective: connects every rank's agent to every other
+    p->net = net_start(c);
+    p->net_touched.assign(c->world, 0);
+  }
   ProxyAgent* raw = p.get();
   p->th = std::thread([raw] { raw->main(); });
   return p;
 }
+
+NetTransport* proxy_net(Comm* c) { return c->proxy ? c->proxy->net.get() : nullptr; }
 
 void ProxyDeleter::operator()(ProxyAgent* p) const { delete p; }
 
@@ -474,6 +544,7 @@ void proxy_stop(ProxyPtr& p) {
   p->stop.store(true, std::memory_order_release);
   if (p->th.joinable()) p->th.join();
   DeviceGuard g(p->c->device);
+  if (p->net) net_release_waits(p->net.get());  // (no-op unless an ack never came)
   for (auto st : p->streams) cudaStreamSynchronize(st);
   if (p->comp_stream) cudaStreamSynchronize(p->comp_stream);
   for (auto& f : p->inflight)
@@ -484,6 +555,7 @@ void proxy_stop(ProxyPtr& p) {
   if (p->stage) cudaFreeHost(p->stage);
   for (auto st : p->streams) cudaStreamDestroy(st);
   if (p->comp_stream) cudaStreamDestroy(p->comp_stream);
+  p->net.reset();  // joins the sender / receiver threads, closes the connections
   p.reset();
 }
 
@@ -506,6 +578,7 @@ uint64_t proxy_host_submit(Comm* c, uint32_t ctx, const uint8_t desc[64]) {
 void proxy_check_failed(Comm* c) {
   ProxyAgent* p = c->proxy.get();
   if (p && p->failed.load()) fail(GINSIM_E_GENERIC, "proxy agent failed: " + p->failure);
+  if (p && p->net) net_check_failed(p->net.get());
 }
 
 bool proxy_host_done(Comm* c, uint32_t ctx, uint64_t ticket) {
@@ -552,9 +625,12 @@ void proxy_quiesce(Comm* c) {
 void proxy_reset_cells(Comm* c, uint32_t first, uint32_t span) {
   ProxyAgent* p = c->proxy.get();
   if (!p) return;
-  std::lock_guard<std::mutex> lk(p->sig_mu);
-  for (uint32_t peer = 0; peer < c->world; ++peer)
-    for (uint32_t i = first; i < first + span; ++i) p->sig_value[(size_t)peer * c->cfg.signal_cells + i] = 0;
+  {
+    std::lock_guard<std::mutex> lk(p->sig_mu);
+    for (uint32_t peer = 0; peer < c->world; ++peer)
+      for (uint32_t i = first; i < first + span; ++i) p->sig_value[(size_t)peer * c->cfg.signal_cells + i] = 0;
+  }
+  if (p->net) net_reset_cells(p->net.get(), first, span);  // socket peers: the receiver keeps the values
 }
 
 bool proxy_counter_pending(Comm* c, uint32_t id) {

@@ -506,7 +506,7 @@ void ginsim_cuda_config_default(ginsim_cuda_config* cfg) {
   cfg->signal_cells = 256;
   cfg->counter_cells = 256;
   cfg->queue_depth = 1024;
-  cfg->reserved = 0;
+  cfg->transport = 0;
   cfg->timeout_ms = 30000;
 }
 
@@ -527,6 +527,12 @@ int ginsim_cuda_config_from_env(ginsim_cuda_config* cfg) {
     if (s == "direct") cfg->backend = GIN_BACKEND_DIRECT;
     else if (s == "proxy") cfg->backend = GIN_BACKEND_PROXY;
     else fail(GINSIM_E_USAGE, "GINSIM_BACKEND must be 'direct' or 'proxy', got '" + s + "'");
+  }
+  if (const char* t = std::getenv("GINSIM_TRANSPORT"); t && *t) {
+    std::string s(t);
+    if (s == "fabric" || s == "nvlink") cfg->transport = 0;
+    else if (s == "socket") cfg->transport = 1;
+    else fail(GINSIM_E_USAGE, "GINSIM_TRANSPORT must be 'fabric' or 'socket', got '" + s + "'");
   }
   uint64_t v;
   if (env_u64("GINSIM_QUEUE_DEPTH", &v)) cfg->queue_depth = (uint32_t)v;
@@ -569,6 +575,9 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
   if (cfg.signal_cells < GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
     fail(GINSIM_E_USAGE, "signal table smaller than the reserved barrier region");
   if (cfg.n_contexts == 0 || cfg.n_contexts > GIN_MAX_CONTEXTS) fail(GINSIM_E_USAGE, "n_contexts must be 1..16");
+  if (cfg.transport > 1) fail(GINSIM_E_USAGE, "transport must be 0 (fabric) or 1 (socket)");
+  if (cfg.transport == 1 && cfg.backend != GIN_BACKEND_PROXY)
+    fail(GINSIM_E_BACKEND_MISMATCH, "the socket transport runs on the Proxy backend (device stores need the fabric)");
   if (cfg.queue_depth == 0 || (cfg.queue_depth & (cfg.queue_depth - 1)))
     fail(GINSIM_E_USAGE, "ring capacity must be a power of two, got " + std::to_string(cfg.queue_depth));
   if (cfg.backend > 1) fail(GINSIM_E_USAGE, "backend must be 0 (direct) or 1 (proxy)");
@@ -634,8 +643,10 @@ int ginsim_cuda_comm_create(uint32_t rank, uint32_t world, int device, const gin
   std::vector<ExportBlob> blobs(world);
   c->allgather(&mine, blobs.data(), sizeof(ExportBlob));
   for (uint32_t r = 0; r < world; ++r) {
+    // (the socket transport reaches peers only through their agents: their
+    // signal tables and windows are not mapped into this process)
     v.signals[r] = r == rank ? reinterpret_cast<uint64_t*>(c->signal_alloc.ptr)
-                             : reinterpret_cast<uint64_t*>(c->map_blob(blobs[r]));
+                             : (cfg.transport == 1 ? nullptr : reinterpret_cast<uint64_t*>(c->map_blob(blobs[r])));
     if (r != rank && blobs[r].pid == mine.pid && blobs[r].device == device) c->shares_device = true;
     if (blobs[r].pid == mine.pid && blobs[r].device == device) v.same_gpu |= 1u << r;
   }
@@ -833,7 +844,8 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
   w.bases.resize(c->world);
   for (uint32_t r = 0; r < c->world; ++r) {
     w.sizes[r] = blobs[r].bytes;
-    w.bases[r] = r == c->rank ? static_cast<char*>(local) : (blobs[r].bytes ? c->map_blob(blobs[r], &w.maps) : nullptr);
+    w.bases[r] = r == c->rank ? static_cast<char*>(local)
+                              : (blobs[r].bytes && c->cfg.transport == 0 ? c->map_blob(blobs[r], &w.maps) : nullptr);
   }
   for (uint32_t r = 0; r < c->world; ++r) {
     c->host_view.win[id].base[r] = w.bases[r];

@@ -124,6 +124,11 @@ struct ProxyDeleter {
   void operator()(ProxyAgent* p) const;
 };
 using ProxyPtr = std::unique_ptr<ProxyAgent, ProxyDeleter>;
+struct NetTransport;  // net.cu: the Proxy backend's socket transport (Config.transport = 1)
+struct NetDeleter {
+  void operator()(NetTransport* t) const;
+};
+using NetPtr = std::unique_ptr<NetTransport, NetDeleter>;
 
 struct Comm {
   uint32_t rank = 0, world = 1;
@@ -213,6 +218,23 @@ void proxy_quiesce(Comm* c);
 void proxy_reset_cells(Comm* c, uint32_t first, uint32_t span);
 void proxy_stats(Comm* c, uint64_t* descs, uint64_t* copies, uint64_t* busy_ns, uint64_t* wall_ns);
 uint32_t proxy_trace(Comm* c, double* out, uint32_t max_records);
+NetTransport* proxy_net(Comm* c);  // the agent's socket transport (null on the fabric)
+
+// Socket transport (net.cu), driven by the proxy agent's thread.  Collective
+// setup over the comm's bootstrap; puts return the peer connection's last
+// sequence number (acked[peer] reaches it once the peer has performed them).
+NetPtr net_start(Comm* c);
+uint64_t net_put(NetTransport* t, uint32_t peer, uint32_t ctx, uint32_t win, uint64_t off, const char* dev_src,
+                 uint64_t bytes, cudaStream_t stream);
+uint64_t net_put_inline(NetTransport* t, uint32_t peer, uint32_t ctx, uint32_t win, uint64_t off, uint64_t value,
+                        uint32_t bytes);
+void net_signal(NetTransport* t, uint32_t peer, uint32_t ctx, uint32_t id, bool add, uint64_t operand);
+uint64_t* net_acked_device(NetTransport* t, uint32_t peer);
+uint64_t net_last_seq(NetTransport* t, uint32_t peer);
+void net_release_waits(NetTransport* t);  // teardown past the timeout: unblock the completion stream
+void net_reset_cells(NetTransport* t, uint32_t first, uint32_t span);
+void net_check_failed(NetTransport* t);
+void net_stats(NetTransport* t, uint64_t* tx_frames, uint64_t* rx_puts, uint64_t* rx_bytes);
 
 // Descriptor codec (descriptor.cpp).
 int descriptor_check(const ginsim_cuda_descriptor* d);

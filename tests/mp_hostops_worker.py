@@ -41,8 +41,13 @@ def main():
         return out
 
     res = {"rank": rank, "device": dev}
-    for backend in ("direct", "proxy"):
-        comm = G.Comm.create(rank, world, dev, allgather, G.Config(backend=backend, timeout_ms=20000))
+    socket = os.environ.get("MP_TRANSPORT") == "socket"
+    # the socket transport (GIN1 frames over TCP between the agents) runs on
+    # the Proxy backend only
+    for backend in (("socket",) if socket else ("direct", "proxy")):
+        cfg = (G.Config(backend="proxy", transport="socket", timeout_ms=20000, signal_cells=512) if backend == "socket"
+               else G.Config(backend=backend, timeout_ms=20000))
+        comm = G.Comm.create(rank, world, dev, allgather, cfg)
         S = 1 << 20
         # separate send and receive windows: a receive slot must never be
         # another put's source (a peer's put could land in it first)
@@ -95,6 +100,45 @@ def main():
         prev = (rank + world - 1) % world
         res[f"{backend}_after_reuse"] = int(U.d2h(buf2, 4, np.uint32)[0]) == 0xABCD0000 + prev
         dist.barrier()
+        if backend == "socket":
+            res["net_stats"] = comm.net_stats()
+            if os.environ.get("MP_SAME_DEVICE") != "1" and world > 1:
+                # device-initiated traffic over the socket transport: the ring
+                # program's Gin puts + signals and its device BarrierSession go
+                # through descriptors -> agent -> GIN1 frames -> the peer's agent
+                S = 4096
+                sb, rb = comm.mem_alloc(world * S), comm.mem_alloc(world * S)
+                ws_, wr_ = comm.window_register(sb, world * S), comm.window_register(rb, world * S)
+                dist.barrier()
+                G.check(G.lib().ginsim_cuda_team_ring(G.comm_handles([comm]), 1, 0, ws_, wr_, S, 6, 300, None))
+                comm.check_device()
+                res["socket_ring_ok"] = True
+                # a small MoE step (Proxy kernels submit every cross-rank byte
+                # as descriptors): outputs equal the oracle's
+                from oracle import oracle as O
+                E, K, T, H = 16 * world, 4, 32, 256
+                moe = G.Moe(comm, G.MoeConfig(E, K, T, H, 0, 0, 0, 0))
+                x = torch.empty(T * H, dtype=torch.int16, device=f"cuda:{dev}")
+                idx = torch.empty(T * K, dtype=torch.int32, device=f"cuda:{dev}")
+                w = torch.empty(T * K, dtype=torch.int16, device=f"cuda:{dev}")
+                out = torch.empty(T * H, dtype=torch.int16, device=f"cuda:{dev}")
+                moe.generate(3, rank, x, idx, w)
+                torch.cuda.synchronize()
+                dist.barrier()
+                for _ in range(2):
+                    G.Moe.dispatch([moe], [x], [idx])
+                    G.Moe.combine([moe], [w], [out])
+                torch.cuda.synchronize()
+                comm.check_device()
+                exp, _ = O.combine(3, E, K, H, rank, T)
+                res["socket_moe_exact"] = bool((out.cpu().numpy().view(np.uint16).reshape(T, H) == exp).all())
+                d, comb, _ = O.moe_rank_state(3, world, E, K, T, H, rank)
+                res["socket_moe_windows_exact"] = bool(
+                    (U.d2h(comm.window_ptr(moe.win_dispatch, rank), len(d)) == d).all() and
+                    (U.d2h(comm.window_ptr(moe.win_combine, rank), len(comb)) == comb).all())
+                dist.barrier()
+                moe.destroy()
+                res["net_stats_after"] = comm.net_stats()
         if os.environ.get("MP_ORDERING") == "1" and backend == "direct":
             channels, nbytes, rounds = 8, 64 << 10, 200
             size = 2 * channels * nbytes

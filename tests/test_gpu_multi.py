@@ -136,6 +136,32 @@ def test_two_processes_on_one_gpu_cross_process_windows():
             assert r[f"{b}_reused_id"] and r[f"{b}_after_reuse"], r
 
 
+def test_socket_transport_between_processes():
+    """the Proxy backend over the socket transport (GIN1 frames
+    over TCP between the ranks' host agents, net.cu) instead of the fabric.
+    Host-issued puts, inline values, signals and counters land byte-exact and
+    window ids are reused; on distinct GPUs the device-initiated ring and a
+    MoE dispatch/combine (Proxy kernels) run over it with exact outputs and
+    windows.  Runs on one GPU (two processes sharing it: host ops only) or
+    across GPUs."""
+    if gpu_count() < 1:
+        pytest.skip("needs a GPU")
+    n = 2 if gpu_count() < 4 else 4
+    env = {"MP_TRANSPORT": "socket"}
+    if gpu_count() < 2:
+        env["MP_SAME_DEVICE"] = 1
+        n = 2
+    res = _torchrun(n, env, worker="mp_hostops_worker.py")
+    for r in res:
+        assert r["socket_payload_exact"] and r["socket_counter"] == n - 1, r
+        assert r["socket_cells"] == [n - 1, n - 1], r
+        assert r["socket_reused_id"] and r["socket_after_reuse"], r
+        assert r["net_stats"]["rx_puts"] >= 2 * (n - 1) and r["net_stats"]["tx_frames"] > 0, r
+        if gpu_count() >= 2:
+            assert r["socket_ring_ok"] and r["socket_moe_exact"] and r["socket_moe_windows_exact"], r
+    print(json.dumps(res))
+
+
 def test_multiprocess_hostops_and_ordering_over_nvlink():
     """Acceptance #1 (acceptance.cpp:63-118) across real GPUs: a signal observed
     by the receiver implies every byte of the put before it on the channel is
