@@ -173,6 +173,9 @@ struct Config {
   uint64_t timeout_ms = 30'000;
   ProgressMode progress = ProgressMode::Threaded;  // informational on B200 (always asynchronous)
   int device = -1;  // B200: GPU of this rank (-1 = rank % device count)
+  // unset = the fabric (NVLink peer mappings); Socket = the Proxy backend's
+  // GIN1-over-TCP transport between the ranks' host agents (comm_init_socket)
+  std::optional<TransportKind> transport;
   friend bool operator==(const Config&, const Config&) = default;
 
   ginsim_cuda_config to_c() const {
@@ -183,6 +186,7 @@ struct Config {
     c.counter_cells = counter_cells;
     c.queue_depth = queue_depth;
     c.timeout_ms = timeout_ms;
+    c.transport = transport == TransportKind::Socket ? 1u : 0u;
     return c;
   }
 };
@@ -194,6 +198,7 @@ inline Config config_from_env(Config base = {}) {
   base.queue_depth = c.queue_depth;
   base.timeout_ms = c.timeout_ms;
   if (!std::getenv("GINSIM_BACKEND")) base.backend.reset();
+  if (std::getenv("GINSIM_TRANSPORT")) base.transport = c.transport ? TransportKind::Socket : TransportKind::Nvlink;
   return base;
 }
 
@@ -228,7 +233,9 @@ class InProcGroup {
 // One rank's communicator (runtime.hpp:123-246).
 class DevComm {
  public:
-  DevComm(ginsim_cuda_comm_t c, std::shared_ptr<InProcGroup> g, Config cfg) : c_(c), group_(std::move(g)), cfg_(cfg) {
+  // `keep` owns the bootstrap the comm registers windows over (an
+  // InProcGroup, or comm_init_socket's rendezvous)
+  DevComm(ginsim_cuda_comm_t c, std::shared_ptr<void> keep, Config cfg) : c_(c), group_(std::move(keep)), cfg_(cfg) {
     uint32_t b = 0;
     check(ginsim_cuda_comm_info(c_, &rank_, &world_, &device_, &b));
     backend_ = b ? BackendKind::Proxy : BackendKind::Direct;
@@ -244,7 +251,7 @@ class DevComm {
   const Config& config() const { return cfg_; }
   BackendKind backend() const { return backend_; }
   const Team& world_team() const { return world_team_; }
-  TransportKind transport_kind() const { return TransportKind::Nvlink; }
+  TransportKind transport_kind() const { return cfg_.transport.value_or(TransportKind::Nvlink); }
   ProgressMode progress_mode() const { return cfg_.progress; }
   ginsim_cuda_comm_t handle() const { return c_; }
 
@@ -373,7 +380,7 @@ class DevComm {
 
  private:
   ginsim_cuda_comm_t c_;
-  std::shared_ptr<InProcGroup> group_;
+  std::shared_ptr<void> group_;
   Config cfg_;
   RankId rank_ = 0;
   uint32_t world_ = 1;
@@ -401,6 +408,36 @@ inline std::unique_ptr<DevComm> comm_init(std::shared_ptr<InProcGroup> group, Ra
   check(ginsim_cuda_comm_create(self, group->world_size(), device, &c, &boot, &h));
   (void)ndev;
   return std::make_unique<DevComm>(h, std::move(group), config);
+}
+
+// comm_init_socket (socket_transport.hpp:117-126): rank 0 hosts the
+// rendezvous at host:port; every rank's Proxy agent then reaches the others
+// with GIN1 frames over TCP (net.cu) -- the path toward peers outside the
+// NVLink domain.  Requires the Proxy backend (unset = Proxy).
+inline std::unique_ptr<DevComm> comm_init_socket(const std::string& host, uint16_t port, uint32_t world_size,
+                                                 RankId self, const Config& config) {
+  if (config.backend && *config.backend != BackendKind::Proxy)
+    throw BackendMismatch("the socket transport runs on the Proxy backend");
+  Config cfg = config;
+  cfg.backend = BackendKind::Proxy;
+  cfg.transport = TransportKind::Socket;
+  std::shared_ptr<ginsim_cuda_bootstrap> boot(new ginsim_cuda_bootstrap{}, [](ginsim_cuda_bootstrap* b) {
+    ginsim_cuda_socket_bootstrap_destroy(b);
+    delete b;
+  });
+  check(ginsim_cuda_socket_bootstrap_create(host.c_str(), port, world_size, self, cfg.timeout_ms, boot.get()));
+  const ginsim_cuda_config c = cfg.to_c();
+  ginsim_cuda_comm_t h = nullptr;
+  check(ginsim_cuda_comm_create(self, world_size, cfg.device >= 0 ? cfg.device : static_cast<int>(self), &c, boot.get(),
+                                &h));
+  return std::make_unique<DevComm>(h, std::move(boot), cfg);
+}
+
+// reserve_loopback_port (socket_transport.hpp:128-129).
+inline uint16_t reserve_loopback_port() {
+  uint16_t p = 0;
+  check(ginsim_cuda_reserve_loopback_port(&p));
+  return p;
 }
 
 // Device memory for windows: cuMemCreate-backed, exportable to peers.

@@ -63,3 +63,21 @@ def test_cpp_host_memory_windows_on_gpu(tmp_path):
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "direct host-window ring ok" in r.stdout and "proxy host-window ring ok" in r.stdout
+
+
+def test_cpp_socket_api_compiles_and_host_checks_pass(tmp_path):
+    exe = _build(tmp_path, "socket_api")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "host checks ok" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_socket_transport_ring_on_gpu(tmp_path):
+    """comm_init_socket (socket_transport.hpp:117-129): three ranks rendezvous on
+    a loopback port and run a put + SignalAdd + counter ring, inline values and
+    barriers over GIN1 frames between their agents (tests/cpp/socket_api.cpp)."""
+    exe = _build(tmp_path, "socket_api")
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "socket ring ok" in r.stdout
