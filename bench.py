@@ -976,6 +976,15 @@ def main():
         "overlap_with_compute": overlap,
     }
     if world > 1:
+        # Over NVLink the dominant kernel's binding resource is the fabric, not
+        # HBM: its remote bytes per launch over its time, against the measured
+        # 705 GB/s ceiling of SM-issued peer writes and 900 nominal
+        dom_remote = remote_msgs * cmsg if dom == "combine" else (
+            remote_rows * (2 * H + 128) if args.layout == 2 else remote_msgs * dmsg)
+        nv = dom_remote / (dom_ms * 1e-3) / 1e9
+        line["roofline"]["binding"] = "nvlink"
+        line["roofline"]["nvlink"] = {"achieved": nv, "peak_sm_write_measured": 705.0, "frac": nv / 705.0,
+                                      "frac_of_900": nv / 900.0, "unit": "GB/s", "remote_bytes_per_launch": dom_remote}
         rem_msg_bytes = remote_msgs * dmsg
         rem_disp = remote_rows * (2 * H + 128) if args.layout == 2 else rem_msg_bytes
         line["nvlink"] = {"transport": "dedup rows (2H + 128 B per remote (token, rank))" if args.layout == 2

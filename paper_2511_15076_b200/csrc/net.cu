@@ -363,7 +363,13 @@ struct NetTransport {
   // ---- receiver thread
   void apply_put(uint32_t src, wire::Frame& f) {
     const GinDevCommView& v = c->host_view;
-    if (f.id >= GIN_MAX_WINDOWS || !((v.win_live >> f.id) & 1ull))
+    // window registration is collective, but a peer may return from it and
+    // put before this rank has recorded the window: give it the comm timeout
+    const uint64_t t0 = mono_ms();
+    while (f.id < GIN_MAX_WINDOWS && !((__atomic_load_n(&v.win_live, __ATOMIC_ACQUIRE) >> f.id) & 1ull) &&
+           mono_ms() - t0 < c->cfg.timeout_ms && !stop.load())
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    if (f.id >= GIN_MAX_WINDOWS || !((__atomic_load_n(&v.win_live, __ATOMIC_ACQUIRE) >> f.id) & 1ull))
       fail(GINSIM_E_UNKNOWN_WINDOW, "socket transport: put into unknown window " + std::to_string(f.id));
     const GinWindowView& w = v.win[f.id];
     if (f.offset > w.size[rank] || f.body.size() > w.size[rank] - f.offset)

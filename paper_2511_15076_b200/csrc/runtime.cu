@@ -851,7 +851,8 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
     c->host_view.win[id].base[r] = w.bases[r];
     c->host_view.win[id].size[r] = w.sizes[r];
   }
-  c->host_view.win_live |= 1ull << id;
+  // (release: the socket transport's receiver thread reads base/size once it sees the bit)
+  __atomic_fetch_or(&c->host_view.win_live, 1ull << id, __ATOMIC_RELEASE);
   c->host_view.n_windows = std::max<uint32_t>(c->host_view.n_windows, id + 1);
   if (id == c->windows.size()) c->windows.push_back(std::move(w));
   else c->windows[id] = std::move(w);
