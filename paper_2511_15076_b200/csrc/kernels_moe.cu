@@ -551,13 +551,14 @@ static void plan(const ginsim_cuda_moe_t* moes, uint32_t n) {
   }
   // layout 2: two thirds of the CTAs fan received rows out while the rest
   // put (48 of 148 CTAs keep NVLink busy; N=4 HT dispatch 318 us vs 373 us
-  // sequential, tools/phase_timeline.py TL_LAYOUT=2; at N=2 the rows are few
-  // and the sequential order is 3% faster).  GINSIM_DEDUP_FANOUT_CTAS
-  // overrides; 0 = every CTA puts, then fans out.
+  // sequential, tools/phase_timeline.py TL_LAYOUT=2); at N=2 half and half
+  // (dispatch 194-197 us vs 213-222 sequential, 220 with 98 fan-out CTAs).
+  // GINSIM_DEDUP_FANOUT_CTAS overrides; 0 = every CTA puts, then fans out.
   uint32_t fanout = 0;
   if (m->cfg.layout == 2) {
     const char* fo = std::getenv("GINSIM_DEDUP_FANOUT_CTAS");
-    fanout = fo ? (uint32_t)std::strtoul(fo, nullptr, 10) : (Gd >= 4 && m->comm->world > 2 ? 2 * Gd / 3 : 0u);
+    fanout = fo ? (uint32_t)std::strtoul(fo, nullptr, 10)
+                : (Gd < 4 || m->comm->world < 2 ? 0u : (m->comm->world == 2 ? Gd / 2 : 2 * Gd / 3));
     if (fanout >= Gd) fanout = Gd - 1;
   }
   for (uint32_t i = 0; i < n; ++i) {

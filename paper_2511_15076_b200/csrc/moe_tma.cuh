@@ -505,14 +505,15 @@ __global__ void __launch_bounds__(kCmbThreads, 1) moe_combine_tma_kernel(MoeLaun
       const uint32_t lo = c == 0 ? 0u : btab[(c - 1) * P + pr], hi = c + 1 == C ? cnt[pr] : btab[c * P + pr];
       pair_start[i] = hi - lo;
     }
-    for (uint32_t i = tid; i < C * n; i += kTmaThreads) {
+    for (uint32_t i = warp; i < C * n; i += kTmaWarps) {  // one warp per (chunk, source)
       const uint32_t c = i / n, src = i % n;
       uint32_t m = 0;
-      for (uint32_t e_loc = 0; e_loc < e_local; ++e_loc) {
+      for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32) {
         const uint32_t pr = e_loc * n + src;
         m += (c + 1 == C ? cnt[pr] : btab[c * P + pr]) - (c == 0 ? 0u : btab[(c - 1) * P + pr]);
       }
-      csrc[i] = m;
+      m = __reduce_add_sync(0xffffffffu, m);
+      if (lane == 0) csrc[i] = m;
     }
     __syncthreads();
   }
