@@ -65,8 +65,8 @@ struct MoeLaunch {
 
 // Pipelined combine (L.cchunks = C > 1; one rank per GPU, cooperative route
 // tables).  Source tokens are cut into C chunks aligned with the dispatch's
-// CTA token ranges, so chunk c's slot bound for expert e is the prefix row
-// g_pre[c*dgrid/C][e] the route tables already hold.  The dispatch's
+// CTA token ranges (combine_chunk_cta), so chunk c's slot bound for expert e
+// is the prefix row g_pre[first CTA of c][e] the route tables already hold.  The dispatch's
 // releasing CTA writes those bounds next to the counts; the combine's send
 // kernel then walks its messages chunk-major, and whoever completes chunk
 // c's sends releases cell e_local + 3 + kDedupChunks + c at each source by
@@ -75,8 +75,15 @@ struct MoeLaunch {
 // kEarlyRedSms SMs the send kernel leaves free, started while it runs
 // (programmatic dependent launch), the last chunk by the full-occupancy
 // reducer after it.
+// First dispatch CTA of chunk c: equal chunks.  (A last chunk half as long,
+// so less is left for after the send kernel, measured worse -- N=2 combine
+// 402 vs 392 us: the early reducer then still holds the larger third chunk
+// when the send ends.)
+__device__ __forceinline__ uint32_t combine_chunk_cta(uint32_t c, uint32_t C, uint32_t G) {
+  return c >= C ? G : c * G / C;
+}
 __device__ __forceinline__ uint32_t combine_chunk_t0(uint32_t c, uint32_t C, uint32_t dgrid, uint32_t T) {
-  return c >= C ? T : (uint32_t)((uint64_t)(c * dgrid / C) * T / dgrid);
+  return c >= C ? T : (uint32_t)((uint64_t)combine_chunk_cta(c, C, dgrid) * T / dgrid);
 }
 // count-window offset (u32 words) of the bounds: [src][c-1][e_loc] for c = 1..C-1
 __device__ __forceinline__ uint64_t combine_bounds_index(uint32_t n, uint32_t e_local, uint32_t src, uint32_t c,
@@ -321,7 +328,7 @@ __device__ __forceinline__ void release_experts(const gin::Gin& gin, const GinDe
     for (uint32_t c = 1; c < C; ++c)
       for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
         gin::st_relaxed_sys32(cb + combine_bounds_index(n, e_local, rank, c, C) + e_loc,
-                              __ldcg(g_pre + (size_t)(c * G / C) * pre_stride + d * e_local + e_loc));
+                              __ldcg(g_pre + (size_t)combine_chunk_cta(c, C, G) * pre_stride + d * e_local + e_loc));
     gin.fence_toward(d);  // (own experts and emulated peers: GPU scope)
     for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
       gin::red_relaxed_sys_add(gin.sub_cell(d, rank, cell0 + e_loc), (1ull << 32) + hist[d * e_local + e_loc]);

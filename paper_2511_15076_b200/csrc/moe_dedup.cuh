@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) moe_dispatch_dedup_kernel(MoeL
       for (uint32_t c = 1; c < L.cchunks; ++c)  // pipelined combine: chunk slot bounds (moe_common.cuh)
         for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
           gin::st_relaxed_sys32(cb + combine_bounds_index(n, e_local, rank, c, L.cchunks) + e_loc,
-                                __ldcg(g_pre + (size_t)(c * G / L.cchunks) * EB + d * e_local + e_loc));
+                                __ldcg(g_pre + (size_t)combine_chunk_cta(c, L.cchunks, G) * EB + d * e_local + e_loc));
       if (d == rank) {
         gin::fence_acq_rel_gpu();
         for (uint32_t e_loc = lane; e_loc < e_local; e_loc += 32)
