@@ -351,10 +351,33 @@ class Comm:
         c._boot_keepalive = (_ag, boot)  # window_register reuses the bootstrap
         return c
 
+    @staticmethod
+    def create_socket(host, port, world, rank, device, config=None):
+        """comm_init_socket (socket_transport.hpp:117-126): rank 0 hosts the
+        rendezvous at host:port (IPv4); the comm runs the Proxy backend with
+        the socket transport (GIN1 frames between the ranks' agents)."""
+        cfg = config or Config()
+        cfg.backend, cfg.transport = Config.PROXY, Config.SOCKET
+        boot = Bootstrap()
+        check(lib().ginsim_cuda_socket_bootstrap_create(host.encode(), port, world, rank, cfg.timeout_ms, byref(boot)))
+        out = c_void_p()
+        try:
+            check(lib().ginsim_cuda_comm_create(rank, world, device, byref(cfg), byref(boot), byref(out)))
+        except Exception:
+            lib().ginsim_cuda_socket_bootstrap_destroy(byref(boot))
+            raise
+        c = Comm(out)
+        c._socket_boot = boot  # window_register reuses the bootstrap; freed after the comm
+        return c
+
     def destroy(self):
         if self.h:
             check(lib().ginsim_cuda_comm_destroy(self.h))
             self.h = None
+        boot = getattr(self, "_socket_boot", None)
+        if boot is not None:
+            lib().ginsim_cuda_socket_bootstrap_destroy(byref(boot))
+            self._socket_boot = None
 
     # -- memory and windows
     def mem_alloc(self, nbytes):

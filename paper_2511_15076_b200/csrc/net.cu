@@ -430,11 +430,15 @@ struct NetTransport {
             }
             if (n == 0) {  // the peer tore down (anything still owed surfaces as a timeout)
               open[i] = 0;
-              pfd[i].events = 0;
+              pfd[i].fd = -1;  // (poll skips it: a hung-up socket would report POLLHUP forever)
               break;
             }
             if (errno == EINTR) continue;
-            break;  // EAGAIN
+            if (errno != EAGAIN && errno != EWOULDBLOCK) {  // reset by a peer that left
+              open[i] = 0;
+              pfd[i].fd = -1;  // (poll skips it: a hung-up socket would report POLLHUP forever)
+            }
+            break;
           }
           wire::Frame f;
           wire::Parser& ps = inbound ? in_parser[peer] : out_parser[peer];

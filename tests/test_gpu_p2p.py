@@ -376,3 +376,4 @@ def test_signal_orders_earlier_puts_under_concurrency(n, channels, rounds, nbyte
             assert c.read_signal(0) == 2 * rounds
     finally:
         close(cs)
+
