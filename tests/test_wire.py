@@ -150,3 +150,55 @@ def test_encode_rejects_a_short_output_buffer_and_bad_ops():
         G.wire_encode(9)
     with pytest.raises(G.UsageError):
         G.wire_encode(W.SIGNAL, signal_add=2)
+
+
+# ---------------------------------------------------------------- socket rendezvous (host only)
+def _rendezvous(world, port, payloads, results, rank):
+    import ctypes
+    boot = G.Bootstrap()
+    try:
+        G.check(G.lib().ginsim_cuda_socket_bootstrap_create(b"127.0.0.1", port, world, rank, 20000, ctypes.byref(boot)))
+        for blob in payloads[rank]:  # successive allgathers reuse the connections
+            n = len(blob)
+            send = (ctypes.c_uint8 * n).from_buffer_copy(blob)
+            recv = (ctypes.c_uint8 * (n * world))()
+            rc = boot.allgather(boot.ctx, ctypes.cast(send, ctypes.c_void_p), ctypes.cast(recv, ctypes.c_void_p), n)
+            results[rank].append((rc, bytes(recv)))
+    except Exception as e:  # noqa: BLE001
+        results[rank].append(("error", repr(e)))
+    finally:
+        G.lib().ginsim_cuda_socket_bootstrap_destroy(ctypes.byref(boot))
+
+
+def test_socket_rendezvous_allgathers_rank_major():
+    """comm_init_socket's rendezvous (socket_transport.cpp:178-231) on its own:
+    rank 0 listens on a port from reserve_loopback_port, the others connect
+    and say hello; every allgather returns the ranks' blobs rank-major, on
+    every rank, call after call (the comm's window registrations reuse it)."""
+    import threading
+    world = 3
+    port = G.reserve_loopback_port()
+    payloads = [[bytes([r] * 8), bytes(range(r, r + 40)), (r * 1000).to_bytes(4, "little")] for r in range(world)]
+    results = [[] for _ in range(world)]
+    ts = [threading.Thread(target=_rendezvous, args=(world, port, payloads, results, r)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(60)
+    for r in range(world):
+        assert len(results[r]) == 3, results[r]
+        for i, (rc, got) in enumerate(results[r]):
+            assert rc == 0 and got == b"".join(payloads[q][i] for q in range(world)), (r, i)
+
+
+def test_socket_rendezvous_rejects_bad_arguments():
+    import ctypes
+    boot = G.Bootstrap()
+    with pytest.raises(G.UsageError):
+        G.check(G.lib().ginsim_cuda_socket_bootstrap_create(b"not-an-ip", 1, 2, 0, 100, ctypes.byref(boot)))
+    with pytest.raises(G.UsageError):
+        G.check(G.lib().ginsim_cuda_socket_bootstrap_create(b"127.0.0.1", 1, 2, 2, 100, ctypes.byref(boot)))
+    # a rank that finds nobody at the rendezvous fails with a bootstrap timeout
+    with pytest.raises(G.BootstrapTimeout):
+        G.check(G.lib().ginsim_cuda_socket_bootstrap_create(b"127.0.0.1", G.reserve_loopback_port(), 2, 1, 300,
+                                                            ctypes.byref(boot)))
