@@ -81,3 +81,22 @@ def test_cpp_socket_transport_ring_on_gpu(tmp_path):
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "socket ring ok" in r.stdout
+
+
+def test_host_codecs_under_address_and_ub_sanitizers(tmp_path):
+    """The host agent's byte codecs -- GIN1 frames (csrc/wire.cpp) and the
+    64-byte descriptors (csrc/descriptor.cpp) -- built from their sources with
+    -fsanitize=address,undefined and driven with random round trips, random
+    piece sizes, random garbage and single-bit corruptions
+    (tests/cpp/sanitize_codecs.cpp): no sanitizer report, every rejection typed."""
+    exe = str(tmp_path / "sanitize_codecs")
+    src = os.path.join(ROOT, "paper_2511_15076_b200", "csrc")
+    cmd = ["g++", "-std=c++17", "-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+           "-I", f"{CUDA}/include", os.path.join(ROOT, "tests", "cpp", "sanitize_codecs.cpp"),
+           os.path.join(src, "wire.cpp"), os.path.join(src, "descriptor.cpp"), "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, ASAN_OPTIONS="detect_leaks=1", UBSAN_OPTIONS="print_stacktrace=1"))
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "frames ok" in r.stdout and "descriptors ok" in r.stdout
