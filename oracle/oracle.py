@@ -17,7 +17,9 @@ from ctypes import POINTER, c_double, c_int, c_uint8, c_uint16, c_uint32, c_uint
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-ORACLE_SO = os.path.join(HERE, "_build", "libginsim_oracle.so")
+# GINSIM_ORACLE_SO: an alternative build of the same C file (the sanitizer
+# test runs the golden checks against an -fsanitize=address,undefined build)
+ORACLE_SO = os.environ.get("GINSIM_ORACLE_SO") or os.path.join(HERE, "_build", "libginsim_oracle.so")
 REF_DRIVER = os.path.join(HERE, "_ref", "ginsim_ref_driver")
 
 _L = None

@@ -3,6 +3,7 @@ with g++ against libginsim_b200.so and runs: host-only checks on CPU, the
 Listing-2 ring (harness_ring.cpp:18-57) on the GPU box."""
 import os
 import subprocess
+import sys
 
 import pytest
 
@@ -100,3 +101,24 @@ def test_host_codecs_under_address_and_ub_sanitizers(tmp_path):
                        env=dict(os.environ, ASAN_OPTIONS="detect_leaks=1", UBSAN_OPTIONS="print_stacktrace=1"))
     assert r.returncode == 0, r.stdout + r.stderr
     assert "frames ok" in r.stdout and "descriptors ok" in r.stdout
+
+
+def test_oracle_golden_checks_under_address_and_ub_sanitizers(tmp_path):
+    """The checker itself: oracle/ginsim_oracle.c rebuilt with
+    -fsanitize=address,undefined and the golden-fixture tests
+    (tests/test_oracle_golden.py: the reference's final states, routing, ring
+    planes, bf16 / fp8 arithmetic) rerun against it -- no sanitizer report."""
+    asan = subprocess.run(["gcc", "-print-file-name=libasan.so"], capture_output=True, text=True).stdout.strip()
+    ubsan = subprocess.run(["gcc", "-print-file-name=libubsan.so"], capture_output=True, text=True).stdout.strip()
+    if not (os.path.isabs(asan) and os.path.isabs(ubsan)):
+        pytest.skip("gcc sanitizer runtimes not found")
+    so = str(tmp_path / "libginsim_oracle.so")
+    r = subprocess.run(["gcc", "-O1", "-g", "-std=c11", "-fPIC", "-ffp-contract=off", "-fsanitize=address,undefined",
+                        "-fno-sanitize-recover=all", "-shared", "-o", so, os.path.join(ROOT, "oracle", "ginsim_oracle.c"),
+                        "-lm"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    env = dict(os.environ, GINSIM_ORACLE_SO=so, LD_PRELOAD=f"{asan} {ubsan}", ASAN_OPTIONS="detect_leaks=0")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_oracle_golden.py"), "-q",
+                        "-p", "no:cacheprovider"], capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " passed" in r.stdout and "ERROR: AddressSanitizer" not in r.stderr and "runtime error" not in r.stderr
