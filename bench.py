@@ -630,6 +630,20 @@ def measure_variant(G, comm, rank, world, dist, torch, dev, stream, T, layout, m
             "remote_wire_bytes_per_rank": wire, "wire_GBps_per_gpu": wire / (disp_us * 1e-6) / 1e9}
 
 
+def launches_per_step(args, world, R, T, K, E):
+    """Kernels one step launches, mirroring the library's choice
+    (csrc/kernels_moe.cu plan(): the pipelined combine runs with one rank per
+    GPU over NVLink, cooperative route tables (T*K >= 8192 pairs) and C =
+    min(GINSIM_COMBINE_CHUNKS or 4, 8, 1024 // E) >= 2 chunks)."""
+    if args.engine not in (0, 2):
+        return 2
+    c = int(os.environ.get("GINSIM_COMBINE_CHUNKS") or 4)
+    c = min(c, 8, 1024 // E)
+    coop = T * K >= int(os.environ.get("GINSIM_DISPATCH_COOP_MIN_PAIRS") or 8192)
+    early = os.environ.get("GINSIM_EARLY_RED_SMS", "64") != "0"
+    return 4 if (world > 1 and R == 1 and coop and c >= 2 and early) else 3
+
+
 def ctypes_stream(stream):
     return None if stream is None else stream.cuda_stream
 
@@ -963,8 +977,9 @@ def main():
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": dom_bytes},
         "clocks": clk,
-        # dispatch + combine-send + reduce kernels per step (one launch covers every emulated rank)
-        "gpu_launches": (3 if args.engine in (0, 2) else 2) * args.steps,
+        # dispatch + combine-send + reduce kernels per step (one launch covers every emulated rank),
+        # + the early reducer of the pipelined combine over NVLink (kernels_moe.cu plan())
+        "gpu_launches": launches_per_step(args, world, R, T, K, E) * args.steps,
         "e2e": e2e,
         "ll": ll,
         "pingpong": pp,

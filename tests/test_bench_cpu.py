@@ -68,3 +68,14 @@ def test_step_bytes_and_workload_strings():
     assert bench.step_bytes(8, 4096) == 8 * 4096 * 8 * ((2 * 7168 + 16) + 2 * 7168)
     assert bench.workload(8, 4096) == ("DeepEP HT dispatch+combine: 8 ranks x 4096 tokens/rank, hidden 7168, "
                                        "top-8 of 256 experts, u16 reference arithmetic")
+
+
+def test_launch_count_claim_follows_the_library_plan(monkeypatch):
+    import types
+    a = types.SimpleNamespace(engine=0)
+    assert bench.launches_per_step(a, 1, 8, 4096, 8, 256) == 3   # N=1: emulated ranks, no early reducer
+    assert bench.launches_per_step(a, 4, 1, 4096, 8, 256) == 4   # NVLink: + the early reducer
+    assert bench.launches_per_step(a, 4, 1, 128, 8, 256) == 3    # LL-sized: local route tables
+    monkeypatch.setenv("GINSIM_COMBINE_CHUNKS", "0")
+    assert bench.launches_per_step(a, 4, 1, 4096, 8, 256) == 3
+    assert bench.launches_per_step(types.SimpleNamespace(engine=1), 4, 1, 4096, 8, 256) == 2
