@@ -161,6 +161,23 @@ def test_config_defaults_and_env(monkeypatch):
         G.check(G.lib().ginsim_cuda_config_from_env(ctypes.byref(c)))
 
 
+def test_config_transport_from_env_and_python(monkeypatch):
+    """Config.transport (the Proxy backend's socket transport):
+    GINSIM_TRANSPORT=socket|fabric; default 0; Python accepts the names."""
+    c = G.Config()
+    assert c.transport == 0
+    monkeypatch.setenv("GINSIM_TRANSPORT", "socket")
+    G.check(G.lib().ginsim_cuda_config_from_env(ctypes.byref(c)))
+    assert c.transport == 1
+    monkeypatch.setenv("GINSIM_TRANSPORT", "fabric")
+    G.check(G.lib().ginsim_cuda_config_from_env(ctypes.byref(c)))
+    assert c.transport == 0
+    monkeypatch.setenv("GINSIM_TRANSPORT", "carrier-pigeon")
+    with pytest.raises(G.UsageError):
+        G.check(G.lib().ginsim_cuda_config_from_env(ctypes.byref(c)))
+    assert G.Config(transport="socket").transport == 1 and G.Config(transport="nvlink").transport == 0
+
+
 def test_inproc_group_validation_without_gpu():
     with pytest.raises(G.UsageError):
         G.check(G.lib().ginsim_cuda_inproc_group_create(0, ctypes.byref(ctypes.c_void_p())))
