@@ -214,3 +214,23 @@ def test_no_contracted_packed_fma_in_the_library():
     sass = subprocess.run([tool, "-sass", G.LIB_PATH], capture_output=True, text=True, check=True).stdout
     assert "FMUL2" in sass  # the packed multiply pipe is in use
     assert "FFMA2" not in sass
+
+
+def test_socket_transport_needs_the_proxy_backend_without_gpu():
+    """comm_create validates the transport before touching the device: the
+    socket transport on the direct backend is a BackendMismatch, an unknown
+    transport a UsageError."""
+    g = ctypes.c_void_p()
+    G.check(G.lib().ginsim_cuda_inproc_group_create(1, ctypes.byref(g)))
+    try:
+        boot = G.Bootstrap()
+        G.check(G.lib().ginsim_cuda_inproc_bootstrap(g, 0, ctypes.byref(boot)))
+        out = ctypes.c_void_p()
+        with pytest.raises(G.BackendMismatch):
+            G.check(G.lib().ginsim_cuda_comm_create(0, 1, 0, ctypes.byref(G.Config(transport="socket")),
+                                                    ctypes.byref(boot), ctypes.byref(out)))
+        with pytest.raises(G.UsageError):
+            G.check(G.lib().ginsim_cuda_comm_create(0, 1, 0, ctypes.byref(G.Config(backend="proxy", transport=2)),
+                                                    ctypes.byref(boot), ctypes.byref(out)))
+    finally:
+        G.lib().ginsim_cuda_inproc_group_destroy(g)
