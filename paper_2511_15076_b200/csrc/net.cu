@@ -286,7 +286,9 @@ struct NetTransport {
   }
 
   // ---- staging ring: FIFO allocation, released in send order
-  char* st_alloc(uint64_t n) {
+  // (agent thread) a contiguous block of n bytes; *release = the bytes the
+  // sender frees after sending it, including the padding skipped to avoid a wrap
+  char* st_alloc(uint64_t n, uint64_t* release) {
     std::unique_lock<std::mutex> lk(st_mu);
     for (;;) {
       const uint64_t used = st_head - st_tail;
@@ -296,15 +298,13 @@ struct NetTransport {
         st_head += pad;
         char* p = staging + st_head % staging_bytes;
         st_head += n;
-        // the release count of this block includes its wrap padding
-        last_alloc = pad + n;
+        *release = pad + n;
         return p;
       }
       if (failed.load()) fail(GINSIM_E_GENERIC, "socket transport failed: " + failure);
       st_cv.wait_for(lk, std::chrono::milliseconds(50));
     }
   }
-  uint64_t last_alloc = 0;
   void st_free(uint64_t n) {
     {
       std::lock_guard<std::mutex> lk(st_mu);
@@ -567,8 +567,8 @@ uint64_t net_put(NetTransport* t, uint32_t peer, uint32_t ctx, uint32_t win, uin
   net_check_failed(t);
   for (uint64_t done = 0; done < bytes;) {
     const uint64_t n = std::min(bytes - done, std::min(NetTransport::kChunk, t->staging_bytes / 4));
-    char* st = t->st_alloc(n);
-    const uint64_t rel = t->last_alloc;
+    uint64_t rel = 0;
+    char* st = t->st_alloc(n, &rel);
     GIN_CUDA(cudaMemcpyAsync(st, dev_src + done, n, cudaMemcpyDeviceToHost, stream));
     cudaEvent_t ev;
     GIN_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
