@@ -301,7 +301,10 @@ struct NetTransport {
         *release = pad + n;
         return p;
       }
-      if (failed.load()) fail(GINSIM_E_GENERIC, "socket transport failed: " + failure);
+      if (failed.load()) {
+        std::lock_guard<std::mutex> fl(fail_mu);  // (never taken before st_mu elsewhere)
+        fail(GINSIM_E_GENERIC, "socket transport failed: " + failure);
+      }
       st_cv.wait_for(lk, std::chrono::milliseconds(50));
     }
   }
