@@ -122,3 +122,12 @@ def test_oracle_golden_checks_under_address_and_ub_sanitizers(tmp_path):
                         "-p", "no:cacheprovider"], capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert " passed" in r.stdout and "ERROR: AddressSanitizer" not in r.stderr and "runtime error" not in r.stderr
+
+
+def test_cpp_launch_harness_compiles_and_host_checks_pass(tmp_path):
+    """ginsim::launch / launch_pool (include/ginsim/harness.hpp, the reference's
+    harness.hpp:13-30): option validation before any device work."""
+    exe = _build(tmp_path, "harness_launch")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "host checks ok" in r.stdout
