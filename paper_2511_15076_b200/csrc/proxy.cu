@@ -74,7 +74,7 @@ struct ProxyAgent {
     std::vector<cudaEvent_t> evs;        // one per context stream with work
     std::vector<uint64_t> host_done;     // per ctx host tickets complete after this pass
     std::vector<uint32_t> counters;      // counter ids completed by this pass
-    uint32_t stage_end;
+    uint32_t stage_begin;                // staging entries [stage_begin, stage_next) of this pass
   };
   std::deque<Pass> inflight;
   std::vector<cudaEvent_t> free_events;
@@ -310,7 +310,15 @@ struct ProxyAgent {
     }
   }
 
+  // Staging entries one pass can take: 64 per device ring + 256 host ops.
+  uint32_t max_stage_per_pass() const { return 64u * n_ctx + 256u; }
+
   size_t progress_once() {
+    // Never let the inline staging ring lap an unfinished copy: the oldest
+    // pass in flight holds the oldest entry whose H2D copy may not have run
+    // yet, and this pass may take up to max_stage_per_pass() more.
+    while (!inflight.empty() && stage_next - inflight.front().stage_begin + max_stage_per_pass() > kStage)
+      retire_completed(true);
     size_t work = 0;
     bool ranged = false;  // an NVTX range only around passes that found work: the idle spin stays silent
     auto range = [&] {
@@ -318,6 +326,7 @@ struct ProxyAgent {
       ranged = true;
     };
     Pass pass;
+    pass.stage_begin = stage_next;
     pass.host_done.assign(n_ctx, 0);
     std::vector<uint64_t> consumed(n_ctx, 0);
     bool any_dev = false;
@@ -405,12 +414,9 @@ struct ProxyAgent {
       GIN_CUDA(cudaEventRecord(ev, completion_stream()));
       pass.evs.push_back(ev);
       touched[comp] = 0;
-      pass.stage_end = stage_next;
       inflight.push_back(std::move(pass));
       n_desc.fetch_add(work, std::memory_order_relaxed);
     }
-    // never let the inline staging ring lap an unfinished copy
-    while (!inflight.empty() && stage_next - inflight.front().stage_end + 512 > kStage) retire_completed(true);
     retire_completed(false);
     if (ranged) nvtxRangePop();
     return work;
