@@ -177,6 +177,7 @@ int ginsim_cuda_plugin_destroy(ginsim_cuda_plugin_t p) {
 
 int ginsim_cuda_plugin_reg_mr(ginsim_cuda_plugin_t p, uint32_t window_id, uint32_t* mr) {
   GIN_API_BEGIN
+  if (!p) fail(GINSIM_E_USAGE, "reg_mr: null plugin");
   Comm* c = &p->comm->impl;
   if (!c->window_live(window_id))
     fail(GINSIM_E_UNKNOWN_WINDOW, "window " + std::to_string(window_id) + " is not registered");
@@ -187,15 +188,18 @@ int ginsim_cuda_plugin_reg_mr(ginsim_cuda_plugin_t p, uint32_t window_id, uint32
 }
 
 int ginsim_cuda_plugin_is_registered(ginsim_cuda_plugin_t p, uint32_t window_id, int* out) {
+  GIN_API_BEGIN
+  if (!p || !out) fail(GINSIM_E_USAGE, "plugin_is_registered: null argument");
   std::lock_guard<std::mutex> lk(p->mu);
   *out = p->mrs.count(window_id) ? 1 : 0;
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 int ginsim_cuda_plugin_iput(ginsim_cuda_plugin_t p, const ginsim_cuda_put_source* src, uint32_t dst_mr,
                             uint64_t dst_offset, uint64_t bytes, uint32_t peer, uint32_t ctx,
                             const ginsim_cuda_action* action, uint64_t* request) {
   GIN_API_BEGIN
+  if (!p || !request) fail(GINSIM_E_USAGE, "iput: null argument");
   require_semantics(p, 1, "iput");
   if (action && action->signal_id >= 0) fail(GINSIM_E_GENERIC, "iput does not carry a remote signal; use iput_signal");
   record_call(p, 'p', ctx, peer, bytes);
@@ -208,6 +212,7 @@ int ginsim_cuda_plugin_iput_signal(ginsim_cuda_plugin_t p, const ginsim_cuda_put
                                    uint32_t signal_id, uint32_t signal_add, uint64_t operand,
                                    const ginsim_cuda_action* action, uint64_t* request) {
   GIN_API_BEGIN
+  if (!p || !request) fail(GINSIM_E_USAGE, "iput_signal: null argument");
   require_semantics(p, 1, "iput_signal");
   record_call(p, 's', ctx, peer, bytes);
   ginsim_cuda_action sig{(int32_t)signal_id, signal_add, signal_add ? operand : 1ull, -1, 0};
@@ -217,6 +222,7 @@ int ginsim_cuda_plugin_iput_signal(ginsim_cuda_plugin_t p, const ginsim_cuda_put
 
 int ginsim_cuda_plugin_test(ginsim_cuda_plugin_t p, uint64_t request, int* done) {
   GIN_API_BEGIN
+  if (!p || !done) fail(GINSIM_E_USAGE, "test: null argument");
   std::lock_guard<std::mutex> lk(p->mu);
   auto it = p->requests.find(request);
   if (it == p->requests.end())
@@ -228,6 +234,7 @@ int ginsim_cuda_plugin_test(ginsim_cuda_plugin_t p, uint64_t request, int* done)
 
 int ginsim_cuda_plugin_retire(ginsim_cuda_plugin_t p, uint64_t request, ginsim_cuda_action* action) {
   GIN_API_BEGIN
+  if (!p) fail(GINSIM_E_USAGE, "retire: null plugin");
   std::lock_guard<std::mutex> lk(p->mu);
   auto it = p->requests.find(request);
   if (it == p->requests.end())
@@ -240,28 +247,35 @@ int ginsim_cuda_plugin_retire(ginsim_cuda_plugin_t p, uint64_t request, ginsim_c
 }
 
 int ginsim_cuda_plugin_outstanding(ginsim_cuda_plugin_t p, uint64_t* n) {
+  GIN_API_BEGIN
+  if (!p || !n) fail(GINSIM_E_USAGE, "plugin_outstanding: null argument");
   std::lock_guard<std::mutex> lk(p->mu);
   *n = p->requests.size();
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 int ginsim_cuda_plugin_set_call_log(ginsim_cuda_plugin_t p, int enabled) {
+  GIN_API_BEGIN
+  if (!p) fail(GINSIM_E_USAGE, "plugin_set_call_log: null plugin");
   std::lock_guard<std::mutex> lk(p->mu);
   p->log_calls = enabled != 0;
   p->calls.clear();
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 int ginsim_cuda_plugin_call_log(ginsim_cuda_plugin_t p, ginsim_cuda_plugin_call* out, uint32_t max_calls, uint32_t* n) {
+  GIN_API_BEGIN
+  if (!p || (max_calls && !out)) fail(GINSIM_E_USAGE, "plugin_call_log: null argument");
   std::lock_guard<std::mutex> lk(p->mu);
   const uint32_t k = (uint32_t)std::min<size_t>(max_calls, p->calls.size());
   for (uint32_t i = 0; i < k; ++i) out[i] = p->calls[i];
   if (n) *n = (uint32_t)p->calls.size();
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 int ginsim_cuda_plugin_create_context(ginsim_cuda_plugin_t p, uint32_t ctx, ginsim_cuda_direct_ctx_t* out) {
   GIN_API_BEGIN
+  if (!p || !out) fail(GINSIM_E_USAGE, "create_context: null argument");
   require_semantics(p, 0, "create_context");
   if (ctx >= p->contexts.size())
     fail(GINSIM_E_INVALID_CONTEXT, "context " + std::to_string(ctx) + " out of range (" +
@@ -281,6 +295,7 @@ int ginsim_cuda_plugin_create_context(ginsim_cuda_plugin_t p, uint32_t ctx, gins
 
 int ginsim_cuda_direct_post(ginsim_cuda_direct_ctx_t d, const ginsim_cuda_resolved_op* op) {
   GIN_API_BEGIN
+  if (!d || !op) fail(GINSIM_E_USAGE, "direct_post: null argument");
   Comm* c = &d->plugin->comm->impl;
   record_call(d->plugin, op->action.signal_id >= 0 ? 's' : 'p', d->index, op->peer, op->bytes);
   std::lock_guard<std::mutex> lk(d->mu);
@@ -317,6 +332,7 @@ int ginsim_cuda_direct_post(ginsim_cuda_direct_ctx_t d, const ginsim_cuda_resolv
 
 int ginsim_cuda_direct_poll(ginsim_cuda_direct_ctx_t d, uint64_t* retired) {
   GIN_API_BEGIN
+  if (!d) fail(GINSIM_E_USAGE, "direct_poll: null context");
   std::lock_guard<std::mutex> lk(d->mu);
   size_t n = 0;
   retire_done(d, &n);
@@ -326,6 +342,7 @@ int ginsim_cuda_direct_poll(ginsim_cuda_direct_ctx_t d, uint64_t* retired) {
 
 int ginsim_cuda_direct_outstanding(ginsim_cuda_direct_ctx_t d, uint64_t* n) {
   GIN_API_BEGIN
+  if (!d || !n) fail(GINSIM_E_USAGE, "direct_outstanding: null argument");
   std::lock_guard<std::mutex> lk(d->mu);
   *n = d->in_flight.size();
   GIN_API_END

@@ -234,3 +234,36 @@ def test_socket_transport_needs_the_proxy_backend_without_gpu():
                                                     ctypes.byref(boot), ctypes.byref(out)))
     finally:
         G.lib().ginsim_cuda_inproc_group_destroy(g)
+
+
+def test_plugin_entry_points_reject_null_handles_without_gpu():
+    """The FabricPlugin C ABI (csrc/plugin.cu; plugin.hpp:64-144) answers a
+    null plugin / context / out-pointer with UsageError instead of
+    dereferencing it; destroying a null plugin is a no-op."""
+    L = G.lib()
+    vp, u32, u64 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64
+    i = ctypes.c_int()
+    n = ctypes.c_uint64()
+    calls = {
+        "ginsim_cuda_plugin_create": lambda: L.ginsim_cuda_plugin_create(vp(), u32(0), ctypes.byref(vp())),
+        "ginsim_cuda_plugin_reg_mr": lambda: L.ginsim_cuda_plugin_reg_mr(vp(), u32(0), None),
+        "ginsim_cuda_plugin_is_registered": lambda: L.ginsim_cuda_plugin_is_registered(vp(), u32(0), ctypes.byref(i)),
+        "ginsim_cuda_plugin_iput": lambda: L.ginsim_cuda_plugin_iput(vp(), None, u32(0), u64(0), u64(0), u32(0),
+                                                                     u32(0), None, ctypes.byref(n)),
+        "ginsim_cuda_plugin_iput_signal": lambda: L.ginsim_cuda_plugin_iput_signal(
+            vp(), None, u32(0), u64(0), u64(0), u32(0), u32(0), u32(0), u32(0), u64(0), None, ctypes.byref(n)),
+        "ginsim_cuda_plugin_test": lambda: L.ginsim_cuda_plugin_test(vp(), u64(1), ctypes.byref(i)),
+        "ginsim_cuda_plugin_retire": lambda: L.ginsim_cuda_plugin_retire(vp(), u64(1), None),
+        "ginsim_cuda_plugin_outstanding": lambda: L.ginsim_cuda_plugin_outstanding(vp(), ctypes.byref(n)),
+        "ginsim_cuda_plugin_set_call_log": lambda: L.ginsim_cuda_plugin_set_call_log(vp(), 1),
+        "ginsim_cuda_plugin_call_log": lambda: L.ginsim_cuda_plugin_call_log(vp(), None, u32(0), None),
+        "ginsim_cuda_plugin_create_context": lambda: L.ginsim_cuda_plugin_create_context(vp(), u32(0),
+                                                                                         ctypes.byref(vp())),
+        "ginsim_cuda_direct_post": lambda: L.ginsim_cuda_direct_post(vp(), None),
+        "ginsim_cuda_direct_poll": lambda: L.ginsim_cuda_direct_poll(vp(), None),
+        "ginsim_cuda_direct_outstanding": lambda: L.ginsim_cuda_direct_outstanding(vp(), ctypes.byref(n)),
+    }
+    for name, call in calls.items():
+        with pytest.raises(G.UsageError):
+            G.check(call())
+    assert L.ginsim_cuda_plugin_destroy(vp()) == 0
