@@ -136,7 +136,7 @@ int ginsim_cuda_copy_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_t d
                            uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t iters, float* ms_out,
                            void* stream) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
   if (peer >= c->world) fail(GINSIM_E_INVALID_PEER, "peer out of range");
   if (c->windows[src_win].sizes[c->rank] < bytes || c->windows[dst_win].sizes[peer] < bytes)
@@ -183,7 +183,7 @@ int ginsim_cuda_copy_bench_ex(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
                               uint64_t bytes, uint32_t engine, uint32_t ctas, uint32_t chunk, uint32_t iters,
                               float* ms_out, void* stream) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
   if (peer >= c->world) fail(GINSIM_E_INVALID_PEER, "peer out of range");
   if (c->windows[src_win].sizes[c->rank] < bytes || c->windows[dst_win].sizes[peer] < bytes)
@@ -308,7 +308,7 @@ int ginsim_cuda_host_op_bench(ginsim_cuda_comm_t comm, uint32_t src_win, uint32_
                               uint32_t kind, uint32_t n_ops, uint32_t batch, uint64_t bytes, float* out,
                               void* stream) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
   if (peer >= c->world || kind > 1 || n_ops == 0 || batch == 0 || batch > 256) fail(GINSIM_E_USAGE, "bad probe arguments");
   const uint64_t span = kind == 0 ? 8ull * n_ops : bytes * n_ops;

@@ -81,9 +81,14 @@ struct ginsim_cuda_moe_s {
 
 extern "C" {
 
+static void check_moe(ginsim_cuda_moe_t moe) {
+  if (!moe) fail(GINSIM_E_USAGE, "null moe handle");
+}
+
 int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config* cfg, ginsim_cuda_moe_t* out) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
+  if (!cfg || !out) fail(GINSIM_E_USAGE, "moe_create: null argument");
   if (cfg->experts == 0 || cfg->experts % c->world) fail(GINSIM_E_USAGE, "experts must be divisible by ranks");
   if (cfg->experts > kMaxExperts) fail(GINSIM_E_USAGE, "at most 1024 experts");
   if (cfg->tokens == 0 || cfg->top_k == 0 || cfg->top_k > cfg->experts || cfg->top_k > 32)
@@ -267,21 +272,26 @@ int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
 }
 
 int ginsim_cuda_moe_cells(ginsim_cuda_moe_t moe, uint32_t* first, uint32_t* span) {
+  GIN_API_BEGIN
+  check_moe(moe);
   if (first) *first = moe->cell0;
   if (span) *span = moe->cell_span;
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 int ginsim_cuda_moe_windows(ginsim_cuda_moe_t moe, uint32_t* d, uint32_t* c, uint32_t* cb) {
+  GIN_API_BEGIN
+  check_moe(moe);
   if (d) *d = moe->win_dispatch;
   if (c) *c = moe->win_counts;
   if (cb) *cb = moe->win_combine;
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 int ginsim_cuda_moe_generate(ginsim_cuda_moe_t moe, uint64_t seed, uint32_t src, void* x, int32_t* idx, void* w,
                              void* stream) {
   GIN_API_BEGIN
+  check_moe(moe);
   const auto& cfg = moe->cfg;
   DeviceGuard g(moe->comm->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -581,6 +591,8 @@ static void launch_coop(const void* kernel, uint32_t G, uint32_t n, int threads,
 
 static void check_launch_set(const ginsim_cuda_moe_t* moes, uint32_t n) {
   if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "launch needs 1..8 ranks");
+  if (!moes) fail(GINSIM_E_USAGE, "null moe handle list");
+  for (uint32_t i = 0; i < n; ++i) check_moe(moes[i]);
   for (uint32_t i = 1; i < n; ++i)
     if (moes[i]->comm->device != moes[0]->comm->device) fail(GINSIM_E_USAGE, "emulated ranks must share a device");
 }
@@ -687,6 +699,7 @@ int ginsim_cuda_moe_combine(const ginsim_cuda_moe_t* moes, uint32_t n, const voi
 
 int ginsim_cuda_moe_phase_times(ginsim_cuda_moe_t moe, uint32_t kernel, uint64_t* out, uint32_t* ctas) {
   GIN_API_BEGIN
+  check_moe(moe);
   if (!moe->prof) fail(GINSIM_E_USAGE, "phase stamps need GINSIM_PROFILE_PHASES=1 at moe_create");
   if (kernel > 2) fail(GINSIM_E_USAGE, "kernel: 0 dispatch, 1 combine send, 2 combine reduce");
   DeviceGuard g(moe->comm->device);
@@ -697,14 +710,18 @@ int ginsim_cuda_moe_phase_times(ginsim_cuda_moe_t moe, uint32_t kernel, uint64_t
 }
 
 int ginsim_cuda_moe_transport(ginsim_cuda_moe_t moe, uint32_t* kind) {
+  GIN_API_BEGIN
+  check_moe(moe);
   if (kind) *kind = moe->pipe ? 2u : (moe->proxy ? 1u : 0u);
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t* threads) {
+  GIN_API_BEGIN
+  check_moe(moe);
   if (ctas) *ctas = moe->last_ctas;
   if (threads) *threads = (uint32_t)kernels_of(moe).threads;
-  return GINSIM_OK;
+  GIN_API_END
 }
 
 }  // extern "C"
@@ -712,6 +729,9 @@ int ginsim_cuda_moe_last_launch(ginsim_cuda_moe_t moe, uint32_t* ctas, uint32_t*
 extern "C" int ginsim_cuda_moe_create_all(const ginsim_cuda_comm_t* comms, uint32_t n,
                                           const ginsim_cuda_moe_config* cfg, ginsim_cuda_moe_t* out) {
   GIN_API_BEGIN
+  if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "need 1..8 comms");
+  if (!comms || !cfg || !out) fail(GINSIM_E_USAGE, "moe_create_all: null argument");
+  for (uint32_t r = 0; r < n; ++r) comm_impl(comms[r]);  // before any rank enters the collective
   std::vector<int> rcs(n, 0);
   std::vector<std::string> msgs(n);
   std::vector<std::thread> ts;

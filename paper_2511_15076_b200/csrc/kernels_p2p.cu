@@ -536,7 +536,7 @@ int ginsim_cuda_pingpong(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t p
   A.rtt = rtt_ns_out;
   A.ctas = bytes >= (1u << 20) ? 16 : (bytes >= (256u << 10) ? 4 : 1);
   for (uint32_t i = 0; i < n; ++i) {
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     if (c->rank != peer0 && c->rank != peer1) continue;
     for (uint32_t w : {send_win, recv_win}) {
       if (!c->window_live(w)) fail(GINSIM_E_UNKNOWN_WINDOW, "ping-pong window not registered");
@@ -587,7 +587,7 @@ int ginsim_cuda_rtt_floor(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t 
   A.rtt = rtt_ns_out;
   for (uint32_t i = 0; i < n; ++i) {
     A.v[i] = comms[i]->impl.dev_view;
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     if (c->rank == peer0 || c->rank == peer1) A.ready[i] = bump_host_counter(c, 9, 1);
   }
   coop_launch((const void*)rtt_floor_kernel, dim3(1, n), dim3(32), &A, (cudaStream_t)stream);
@@ -619,7 +619,7 @@ int ginsim_cuda_bw(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t peer0, 
   // 256 KiB of each put per CTA, at most one CTA per SM per emulated rank
   const uint32_t G = ctas ? ctas : (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms / n, bytes >> 18));
   for (uint32_t i = 0; i < n; ++i) {
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     if (c->rank != peer0) continue;
     if (!c->window_live(send_win) || !c->window_live(recv_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
     if (c->windows[send_win].sizes[peer0] < bytes || c->windows[recv_win].sizes[peer1] < (uint64_t)window * bytes)
@@ -643,7 +643,7 @@ int ginsim_cuda_alltoall(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t s
   if (world < 2) fail(GINSIM_E_USAGE, "all-to-all needs at least 2 ranks");
   if (signal_id >= c0->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal out of range");
   for (uint32_t i = 0; i < n; ++i) {
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     if (!c->window_live(send_win) || !c->window_live(recv_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
     for (uint32_t r = 0; r < world; ++r) {
       if (c->windows[recv_win].sizes[r] < (uint64_t)world * bytes_per_peer ||
@@ -700,7 +700,7 @@ int ginsim_cuda_ordering_stress(const ginsim_cuda_comm_t* comms, uint32_t n, uin
   if (bytes == 0 || bytes % 4 || channels == 0 || 2 * channels > c0->cfg.signal_cells - GIN_BARRIER_SLOTS * GIN_BARRIER_STEPS)
     fail(GINSIM_E_USAGE, "bytes must be a positive multiple of 4; 2*channels signal cells needed");
   for (uint32_t i = 0; i < n; ++i) {
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     if (!c->window_live(src_win) || !c->window_live(dst_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
     for (uint32_t r = 0; r < c->world; ++r)
       if (c->windows[src_win].sizes[r] < 2ull * channels * bytes || c->windows[dst_win].sizes[r] < 2ull * channels * bytes)
@@ -728,7 +728,7 @@ static void ring_launch(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t te
   Comm* c0 = &comms[0]->impl;
   if (c0->world < 2) fail(GINSIM_E_USAGE, "ring exchange needs at least 2 ranks");
   for (uint32_t i = 0; i < n; ++i) {
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     if (!c->window_live(send_win) || !c->window_live(recv_win)) fail(GINSIM_E_UNKNOWN_WINDOW, "window not registered");
     for (uint32_t r = 0; r < c->world; ++r)
       if (c->windows[send_win].sizes[r] < c->world * bytes || c->windows[recv_win].sizes[r] < c->world * bytes)
@@ -750,7 +750,7 @@ static void ring_launch(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t te
   // not desynchronise later ones.
   A.slot = team_id == 0 ? 0 : 1;
   for (uint32_t i = 0; i < n; ++i) {
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     uint64_t done = 0;
     if (team_id == 0 && c->nvls.on) {  // the world team's BarrierSession runs on the NVLS cells
       DeviceGuard dg(c->device);
@@ -785,6 +785,8 @@ int ginsim_cuda_moe_ht_ring(const ginsim_cuda_comm_t* pool, uint32_t n, uint32_t
   GIN_API_BEGIN
   if (n == 0 || n > GIN_MAX_RANKS || n_pool == 0 || n_pool > 8) fail(GINSIM_E_USAGE, "bad pool shape");
   if (slots == 0 || channels == 0 || messages == 0) fail(GINSIM_E_USAGE, "moe-ht needs slots, channels, and messages");
+  if (!pool) fail(GINSIM_E_USAGE, "null communicator pool");
+  for (uint32_t i = 0; i < n * n_pool; ++i) comm_impl(pool[i]);
   Comm* c0 = &pool[0]->impl;
   if (c0->world < 2) fail(GINSIM_E_USAGE, "moe-ht needs at least 2 ranks");
   const uint32_t n_ctx = c0->cfg.n_contexts;

@@ -252,7 +252,7 @@ extern "C" {
 
 int ginsim_cuda_signal_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t amount, void* stream) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (!c->nvls.on) fail(GINSIM_E_USAGE, "signal broadcast needs the NVLS multicast object (ginsim_cuda_nvls_enabled)");
   if (id >= GIN_BCAST_CELLS) fail(GINSIM_E_INVALID_SIGNAL, "broadcast cell " + std::to_string(id) + " out of range");
   DeviceGuard g(c->device);
@@ -263,7 +263,7 @@ int ginsim_cuda_signal_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t 
 
 int ginsim_cuda_read_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* value) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (!c->nvls.on) fail(GINSIM_E_USAGE, "broadcast cells need the NVLS multicast object");
   if (id >= GIN_BCAST_CELLS) fail(GINSIM_E_INVALID_SIGNAL, "broadcast cell " + std::to_string(id) + " out of range");
   DeviceGuard g(c->device);
@@ -272,8 +272,10 @@ int ginsim_cuda_read_broadcast(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* v
 }
 
 int ginsim_cuda_nvls_enabled(ginsim_cuda_comm_t comm, int* enabled) {
-  *enabled = comm->impl.nvls.on ? 1 : 0;
-  return GINSIM_OK;
+  GIN_API_BEGIN
+  if (!enabled) fail(GINSIM_E_USAGE, "nvls_enabled: null argument");
+  *enabled = comm_impl(comm)->nvls.on ? 1 : 0;
+  GIN_API_END
 }
 
 int ginsim_cuda_barrier_bench(const ginsim_cuda_comm_t* comms, uint32_t n, uint32_t mode, uint32_t iters,
@@ -290,7 +292,7 @@ int ginsim_cuda_barrier_bench(const ginsim_cuda_comm_t* comms, uint32_t n, uint3
   A.slot = 2;
   A.ns = ns_out;
   for (uint32_t i = 0; i < n; ++i) {
-    Comm* c = &comms[i]->impl;
+    Comm* c = comm_impl(comms[i]);
     if (mode == 1 && !c->nvls.on) fail(GINSIM_E_USAGE, "NVLS multicast is not enabled on this comm");
     A.v[i] = c->dev_view;
     std::lock_guard<std::mutex> lk(c->mu);

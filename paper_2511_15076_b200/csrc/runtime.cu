@@ -265,6 +265,8 @@ char* Comm::map_blob(const ExportBlob& b, std::vector<Mapping>* maps) {
 
 void check_same_device(const ginsim_cuda_comm_t* comms, uint32_t n) {
   if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "launch needs 1..8 comms");
+  if (!comms) fail(GINSIM_E_USAGE, "null communicator list");
+  for (uint32_t i = 0; i < n; ++i) comm_impl(comms[i]);  // null handles -> UsageError
   for (uint32_t i = 1; i < n; ++i) {
     if (comms[i]->impl.device != comms[0]->impl.device) {
       fail(GINSIM_E_USAGE, "emulated ranks in one launch must share a device; launch per device instead");
@@ -700,7 +702,7 @@ int ginsim_cuda_comm_create_all(uint32_t world, const int* devices, const ginsim
 int ginsim_cuda_comm_destroy(ginsim_cuda_comm_t comm) {
   GIN_API_BEGIN
   if (!comm) return GINSIM_OK;
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   {
     DeviceGuard g(c->device);
     cudaDeviceSynchronize();
@@ -729,26 +731,33 @@ int ginsim_cuda_comm_destroy(ginsim_cuda_comm_t comm) {
 
 int ginsim_cuda_comm_info(ginsim_cuda_comm_t comm, uint32_t* rank, uint32_t* world, int* device, uint32_t* backend) {
   GIN_API_BEGIN
-  if (rank) *rank = comm->impl.rank;
-  if (world) *world = comm->impl.world;
-  if (device) *device = comm->impl.device;
-  if (backend) *backend = comm->impl.cfg.backend;
+  const Comm* c = comm_impl(comm);
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (device) *device = c->device;
+  if (backend) *backend = c->cfg.backend;
   GIN_API_END
 }
 
 int ginsim_cuda_comm_config(ginsim_cuda_comm_t comm, ginsim_cuda_config* out) {
-  *out = comm->impl.cfg;
-  return GINSIM_OK;
+  GIN_API_BEGIN
+  const Comm* c = comm_impl(comm);
+  if (!out) fail(GINSIM_E_USAGE, "comm_config: null argument");
+  *out = c->cfg;
+  GIN_API_END
 }
 
 int ginsim_cuda_devcomm_view(ginsim_cuda_comm_t comm, const void** view) {
-  *view = comm->impl.dev_view;
-  return GINSIM_OK;
+  GIN_API_BEGIN
+  const Comm* c = comm_impl(comm);
+  if (!view) fail(GINSIM_E_USAGE, "devcomm_view: null argument");
+  *view = c->dev_view;
+  GIN_API_END
 }
 
 int ginsim_cuda_mem_alloc(ginsim_cuda_comm_t comm, uint64_t bytes, void** ptr) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   VmmAlloc a = vmm_alloc(c->device, bytes);
   std::lock_guard<std::mutex> lk(c->mu);
   c->allocs[a.ptr] = a;
@@ -758,7 +767,7 @@ int ginsim_cuda_mem_alloc(ginsim_cuda_comm_t comm, uint64_t bytes, void** ptr) {
 
 int ginsim_cuda_mem_free(ginsim_cuda_comm_t comm, void* ptr) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   DeviceGuard g(c->device);
   cudaDeviceSynchronize();
   std::lock_guard<std::mutex> lk(c->mu);
@@ -772,7 +781,8 @@ int ginsim_cuda_mem_free(ginsim_cuda_comm_t comm, void* ptr) {
 int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t bytes, uint32_t* window_id) {
   GIN_API_BEGIN
   NvtxRange nv("ginsim.window_register");
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
+  if (!window_id) fail(GINSIM_E_USAGE, "window_register: null window id pointer");
   // Dense ids in call order (runtime.cpp:347-371); an id freed by
   // window_deregister is reused (lowest first), so every rank that registers
   // and deregisters in the same order agrees on the ids.
@@ -864,7 +874,7 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
 
 int ginsim_cuda_window_deregister(ginsim_cuda_comm_t comm, uint32_t window_id) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   lookup_window(c, window_id);
   DeviceGuard g(c->device);
   GIN_CUDA(cudaDeviceSynchronize());  // no kernel of this rank still uses the window
@@ -884,7 +894,7 @@ int ginsim_cuda_window_deregister(ginsim_cuda_comm_t comm, uint32_t window_id) {
 
 int ginsim_cuda_register_team(ginsim_cuda_comm_t comm, uint32_t team_id, const uint32_t* members, uint32_t n) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   // DevComm::register_team (runtime.cpp:329-337): local, members must be in
   // the world, ids unique (world = id 0 is always present).
   if (n == 0 || !members) fail(GINSIM_E_USAGE, "team must have members");
@@ -913,7 +923,7 @@ int ginsim_cuda_register_team(ginsim_cuda_comm_t comm, uint32_t team_id, const u
 
 int ginsim_cuda_team(ginsim_cuda_comm_t comm, uint32_t team_id, uint32_t* members, uint32_t* n) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   std::lock_guard<std::mutex> lk(c->mu);
   for (uint32_t i = 0; i < GIN_MAX_TEAMS; ++i) {
     const GinTeamView& t = c->host_view.teams[i];
@@ -930,7 +940,7 @@ int ginsim_cuda_team(ginsim_cuda_comm_t comm, uint32_t team_id, uint32_t* member
 
 int ginsim_cuda_window_size(ginsim_cuda_comm_t comm, uint32_t window_id, uint32_t rank, uint64_t* bytes) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   const auto& w = lookup_window(c, window_id);
   if (rank >= c->world) fail(GINSIM_E_RANK_OUT_OF_RANGE, "rank not registered in window");
   *bytes = w.sizes[rank];
@@ -939,7 +949,7 @@ int ginsim_cuda_window_size(ginsim_cuda_comm_t comm, uint32_t window_id, uint32_
 
 int ginsim_cuda_window_ptr(ginsim_cuda_comm_t comm, uint32_t window_id, uint32_t rank, void** ptr) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   const auto& w = lookup_window(c, window_id);
   if (rank >= c->world) fail(GINSIM_E_RANK_OUT_OF_RANGE, "rank not registered in window");
   *ptr = w.bases[rank];
@@ -951,14 +961,14 @@ int ginsim_cuda_put(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32
                     uint32_t src_win, uint64_t src_off, uint64_t bytes, const ginsim_cuda_action* action,
                     void* stream) {
   GIN_API_BEGIN
-  host_op(&comm->impl, ctx, GIN_OP_PUT, peer, dst_win, dst_off, src_win, src_off, bytes, action, (cudaStream_t)stream);
+  host_op(comm_impl(comm), ctx, GIN_OP_PUT, peer, dst_win, dst_off, src_win, src_off, bytes, action, (cudaStream_t)stream);
   GIN_API_END
 }
 
 int ginsim_cuda_put_value(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32_t dst_win, uint64_t dst_off,
                           uint64_t le_value, uint32_t width, const ginsim_cuda_action* action, void* stream) {
   GIN_API_BEGIN
-  host_op(&comm->impl, ctx, GIN_OP_PUT_INLINE, peer, dst_win, dst_off, GIN_INLINE_WINDOW, le_value, width, action,
+  host_op(comm_impl(comm), ctx, GIN_OP_PUT_INLINE, peer, dst_win, dst_off, GIN_INLINE_WINDOW, le_value, width, action,
           (cudaStream_t)stream);
   GIN_API_END
 }
@@ -966,7 +976,7 @@ int ginsim_cuda_put_value(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, 
 int ginsim_cuda_signal(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uint32_t signal_id, uint32_t signal_add,
                        uint64_t operand, const ginsim_cuda_action* extra, void* stream) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (signal_id >= c->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal " + std::to_string(signal_id) + " out of range");
   ginsim_cuda_action a{};
   a.signal_id = (int32_t)signal_id;
@@ -980,7 +990,7 @@ int ginsim_cuda_signal(ginsim_cuda_comm_t comm, uint32_t ctx, uint32_t peer, uin
 int ginsim_cuda_flush(ginsim_cuda_comm_t comm, uint32_t ctx, void* stream) {
   GIN_API_BEGIN
   NvtxRange nv("ginsim.flush");
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (ctx >= c->cfg.n_contexts) fail(GINSIM_E_INVALID_CONTEXT, "flush: context out of range");
   if (c->cfg.backend == GIN_BACKEND_PROXY) {
     proxy_host_flush(c, ctx);
@@ -1019,7 +1029,7 @@ static void wait_until(Comm* c, const std::function<bool()>& pred, const char* w
 
 int ginsim_cuda_read_signal(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* value) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (id >= c->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal " + std::to_string(id) + " out of range");
   *value = read_cells_sum(c, id);
   GIN_API_END
@@ -1027,7 +1037,7 @@ int ginsim_cuda_read_signal(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* valu
 
 int ginsim_cuda_wait_signal(ginsim_cuda_comm_t comm, uint32_t id, uint64_t expected) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (id >= c->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal " + std::to_string(id) + " out of range");
   wait_until(c, [&] { return read_cells_sum(c, id) >= expected; }, "wait_signal");
   GIN_API_END
@@ -1035,7 +1045,7 @@ int ginsim_cuda_wait_signal(ginsim_cuda_comm_t comm, uint32_t id, uint64_t expec
 
 int ginsim_cuda_reset_signal(ginsim_cuda_comm_t comm, uint32_t id) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (id >= c->cfg.signal_cells) fail(GINSIM_E_INVALID_SIGNAL, "signal " + std::to_string(id) + " out of range");
   DeviceGuard g(c->device);
   uint64_t base = 0, sum = 0;
@@ -1055,7 +1065,7 @@ static uint64_t read_counter_raw(Comm* c, uint32_t id) {
 
 int ginsim_cuda_read_counter(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* value) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (id >= c->cfg.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "counter " + std::to_string(id) + " out of range");
   *value = read_counter_raw(c, id);
   GIN_API_END
@@ -1063,7 +1073,7 @@ int ginsim_cuda_read_counter(ginsim_cuda_comm_t comm, uint32_t id, uint64_t* val
 
 int ginsim_cuda_wait_counter(ginsim_cuda_comm_t comm, uint32_t id, uint64_t expected) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (id >= c->cfg.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "counter " + std::to_string(id) + " out of range");
   wait_until(c, [&] { return read_counter_raw(c, id) >= expected; }, "wait_counter");
   GIN_API_END
@@ -1071,7 +1081,7 @@ int ginsim_cuda_wait_counter(ginsim_cuda_comm_t comm, uint32_t id, uint64_t expe
 
 int ginsim_cuda_reset_counter(ginsim_cuda_comm_t comm, uint32_t id) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (id >= c->cfg.counter_cells) fail(GINSIM_E_INVALID_COUNTER, "counter " + std::to_string(id) + " out of range");
   if (proxy_counter_pending(c, id) || direct_counter_pending(c, id)) {
     fail(GINSIM_E_RESET_WHILE_OUTSTANDING, "counter " + std::to_string(id) + " still has operations in flight");
@@ -1085,7 +1095,7 @@ int ginsim_cuda_reset_counter(ginsim_cuda_comm_t comm, uint32_t id) {
 
 int ginsim_cuda_snapshot_cells(ginsim_cuda_comm_t comm, uint64_t* signals, uint64_t* counters) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   DeviceGuard g(c->device);
   GIN_CUDA(cudaDeviceSynchronize());
   const uint32_t cells = c->cfg.signal_cells;
@@ -1108,7 +1118,7 @@ int ginsim_cuda_snapshot_cells(ginsim_cuda_comm_t comm, uint64_t* signals, uint6
 
 int ginsim_cuda_device_error(ginsim_cuda_comm_t comm, uint32_t* code, int clear) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   DeviceGuard g(c->device);
   GIN_CUDA(cudaMemcpy(code, c->host_view.error, 4, cudaMemcpyDeviceToHost));
   if (clear) {
@@ -1120,7 +1130,7 @@ int ginsim_cuda_device_error(ginsim_cuda_comm_t comm, uint32_t* code, int clear)
 
 int ginsim_cuda_proxy_trace(ginsim_cuda_comm_t comm, double* out, uint32_t max_records, uint32_t* n_out) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (!c->proxy) fail(GINSIM_E_BACKEND_MISMATCH, "proxy_trace on a direct-backend comm");
   DeviceGuard g(c->device);
   *n_out = proxy_trace(c, out, max_records);
@@ -1130,7 +1140,7 @@ int ginsim_cuda_proxy_trace(ginsim_cuda_comm_t comm, double* out, uint32_t max_r
 int ginsim_cuda_proxy_stats(ginsim_cuda_comm_t comm, uint64_t* descriptors, uint64_t* copies, uint64_t* busy_ns,
                             uint64_t* wall_ns) {
   GIN_API_BEGIN
-  Comm* c = &comm->impl;
+  Comm* c = comm_impl(comm);
   if (!c->proxy) fail(GINSIM_E_BACKEND_MISMATCH, "proxy_stats on a direct-backend comm");
   proxy_stats(c, descriptors, copies, busy_ns, wall_ns);
   GIN_API_END
@@ -1153,7 +1163,10 @@ int ginsim_cuda_descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* 
 extern "C" int ginsim_cuda_window_register_all(const ginsim_cuda_comm_t* comms, uint32_t n, void* const* ptrs,
                                                const uint64_t* bytes, uint32_t* window_id) {
   GIN_API_BEGIN
-  if (n == 0) fail(GINSIM_E_USAGE, "need at least one comm");
+  if (n == 0 || n > GIN_MAX_RANKS) fail(GINSIM_E_USAGE, "need 1..8 comms");
+  if (!comms || !ptrs || !bytes || !window_id) fail(GINSIM_E_USAGE, "window_register_all: null argument");
+  // every handle checked before any rank enters the collective (a null one would leave the others waiting)
+  for (uint32_t r = 0; r < n; ++r) comm_impl(comms[r]);
   std::vector<int> rcs(n, 0);
   std::vector<std::string> msgs(n);
   std::vector<uint32_t> ids(n, 0);

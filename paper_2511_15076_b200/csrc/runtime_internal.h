@@ -246,3 +246,10 @@ void descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* d);   // th
 struct ginsim_cuda_comm_s {
   ginsim_b200::Comm impl;
 };
+
+// The runtime behind a C-ABI comm handle; a null handle is a UsageError
+// (inside GIN_API_BEGIN / GIN_API_END, so the caller gets GINSIM_E_USAGE).
+inline ginsim_b200::Comm* comm_impl(ginsim_cuda_comm_t comm) {
+  if (!comm) ginsim_b200::fail(GINSIM_E_USAGE, "null communicator handle");
+  return &comm->impl;
+}

@@ -267,3 +267,17 @@ def test_plugin_entry_points_reject_null_handles_without_gpu():
         with pytest.raises(G.UsageError):
             G.check(call())
     assert L.ginsim_cuda_plugin_destroy(vp()) == 0
+
+
+def test_every_handle_entry_point_rejects_null_handles_without_gpu():
+    """Every C-ABI entry point that takes a comm / moe / plugin handle (or a
+    list of them) answers null with UsageError before touching the device --
+    no crash, no rank left waiting in a collective -- and destroy(null) is a
+    no-op (tests/null_handles_worker.py, in a subprocess)."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "null_handles_worker.py")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "all null handles rejected" in r.stdout, r.stdout
+    assert int(r.stdout.split("checked ")[1].split()[0]) >= 50
