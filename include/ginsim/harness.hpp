@@ -1,5 +1,15 @@
-// ginsim/harness.hpp -- the reference's launch helpers over the B200 library:
-// LaunchOptions, launch, launch_pool (proj/core/include/ginsim/harness.hpp:13-30).
+// ginsim/harness.hpp -- the reference's harness over the B200 library
+// (proj/core/include/ginsim/harness.hpp): LaunchOptions, launch, launch_pool
+// (:13-30); RankState (:36-43); the ring exchange (:45-62,
+// harness_ring.cpp:18-57); ping-pong / bandwidth programs, summarize and
+// write_csv (:64-102, harness_bench.cpp:12-178).  The programs run the
+// reference's host protocols unchanged over host windows (std::vector<std::byte>
+// registered as in the reference: the library pins and maps the pages, the
+// device moves the bytes).  They time with the host's monotonic clock (there
+// is no virtual clock on hardware), so a row includes the host-issued op's
+// launch; the device-resident loops are ginsim_cuda_pingpong / ginsim_cuda_bw
+// (include/ginsim_cuda.h).  The MoE demos (run_moe_ll / run_moe_ht) are the
+// device kernels behind ginsim_cuda_moe_* and ginsim_cuda_moe_ht_ring.
 // One host thread per rank; each builds its communicator(s) with comm_init
 // over an InProcGroup (TransportKind::Inproc) or comm_init_socket
 // (TransportKind::Socket, the Proxy backend's GIN1 transport), runs the
@@ -11,8 +21,12 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
 #include <condition_variable>
+#include <cstddef>
 #include <exception>
+#include <fstream>
 #include <functional>
 #include <memory>
 #include <mutex>
@@ -102,6 +116,251 @@ inline void launch_pool(const LaunchOptions& opts, uint32_t n_comms,
 // launch (harness.hpp:22-24): `program` once per rank.
 inline void launch(const LaunchOptions& opts, const std::function<void(DevComm&)>& program) {
   launch_pool(opts, 1, [&](std::vector<DevComm*>& comms) { program(*comms[0]); });
+}
+
+// ------------------------------------------------------------ final state
+// Everything a rank's program observes at the end (harness.hpp:36-43): two
+// backends are equivalent when these match.
+struct RankState {
+  std::vector<std::vector<std::byte>> windows;
+  DevComm::CellSnapshot cells;
+  friend bool operator==(const RankState&, const RankState&) = default;
+};
+using FinalState = std::vector<RankState>;
+
+// ------------------------------------------------------------ ring exchange
+struct RingOptions {
+  uint64_t bytes = 4096;
+  uint32_t rounds = 10;
+};
+
+struct RingReport {
+  uint32_t ranks = 0;
+  uint32_t rounds = 0;
+  FinalState state;
+};
+
+namespace detail {
+// the (sender, round, offset) tag every ring byte carries (harness_ring.cpp:12-14);
+// receivers recompute it, nothing expected travels out of band
+inline std::byte ring_tag(uint32_t sender, uint32_t round, uint64_t i) {
+  return static_cast<std::byte>(sender * 131u + round * 31u + i * 7u + 1u);
+}
+}  // namespace detail
+
+// One rank of the ring (harness_ring.cpp:18-57): per round, put + SignalInc of
+// this rank's slice to the right neighbour, wait for the left neighbour's,
+// verify it, reset the cell, flush (the source is reused next round) and
+// barrier (no rank signals round + 1 before every rank has reset).
+inline void ring_rank_program(DevComm& comm, const RingOptions& ring, RankState* out) {
+  const uint32_t n = comm.world_size(), me = comm.rank();
+  const uint64_t S = ring.bytes;
+  const Team& world = comm.world_team();
+  std::vector<std::byte> send(n * S), recv(n * S);
+  Window& send_w = comm.window_register(send);
+  Window& recv_w = comm.window_register(recv);
+  Gin gin(comm, 0);
+  BarrierSession barrier(gin, world, 0);
+  const uint32_t right = (me + 1) % n, left = (me + n - 1) % n;
+  for (uint32_t round = 0; round < ring.rounds; ++round) {
+    std::byte* slice = send.data() + right * S;
+    for (uint64_t i = 0; i < S; ++i) slice[i] = detail::ring_tag(me, round, i);
+    gin.put(world, right, recv_w, me * S, send_w, right * S, S, CompletionAction::signal(0, SignalOp::inc()));
+    gin.wait_signal(0, 1);
+    const std::byte* got = recv.data() + left * S;
+    for (uint64_t i = 0; i < S; ++i)
+      if (got[i] != detail::ring_tag(left, round, i))
+        throw VerificationFailure("ring: rank " + std::to_string(me) + " round " + std::to_string(round) +
+                                  ": first mismatch at offset " + std::to_string(left * S + i));
+    gin.reset_signal(0);
+    gin.flush();
+    barrier.sync();
+  }
+  if (out) {
+    out->windows = {send, recv};
+    out->cells = comm.snapshot_cells();
+  }
+}
+
+inline RingReport run_ring(const LaunchOptions& opts, const RingOptions& ring) {
+  if (opts.ranks < 2) throw UsageError("ring exchange needs at least 2 ranks");
+  RingReport rep;
+  rep.ranks = opts.ranks;
+  rep.rounds = ring.rounds;
+  rep.state.resize(opts.ranks);
+  launch(opts, [&](DevComm& comm) { ring_rank_program(comm, ring, &rep.state[comm.rank()]); });
+  return rep;
+}
+
+// ------------------------------------------------------------ microbenchmarks
+struct BenchConfig {
+  std::vector<uint64_t> sizes = default_sizes();
+  uint32_t iters = 100;
+  uint32_t warmup = 10;
+  bool wall_clock = true;  // always wall clock on hardware (kept so reference code compiles)
+  std::string csv_path;    // written when non-empty
+
+  // 4 B .. 4 MiB in x2 steps (harness_bench.cpp:12-16)
+  static std::vector<uint64_t> default_sizes() {
+    std::vector<uint64_t> v;
+    for (uint64_t s = 4; s <= (4ull << 20); s <<= 1) v.push_back(s);
+    return v;
+  }
+};
+
+struct BenchRow {
+  uint64_t size_bytes = 0;
+  uint32_t iters = 0;
+  uint64_t p50_ns = 0;
+  uint64_t p99_ns = 0;
+  double mean_ns = 0;
+};
+
+// p50 = s[n/2], p99 = s[min(n-1, 99n/100)] of the sorted samples, and the mean
+// (harness_bench.cpp:20-32; Python summarize).
+inline BenchRow summarize(uint64_t size, std::vector<uint64_t> samples) {
+  BenchRow row;
+  row.size_bytes = size;
+  row.iters = static_cast<uint32_t>(samples.size());
+  if (samples.empty()) return row;
+  std::sort(samples.begin(), samples.end());
+  const size_t n = samples.size();
+  row.p50_ns = samples[n / 2];
+  row.p99_ns = samples[std::min(n - 1, n * 99 / 100)];
+  double total = 0;
+  for (uint64_t s : samples) total += static_cast<double>(s);
+  row.mean_ns = total / static_cast<double>(n);
+  return row;
+}
+
+namespace detail {
+inline uint64_t mono_ns() {
+  return static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                   std::chrono::steady_clock::now().time_since_epoch())
+                                   .count());
+}
+inline uint64_t max_size(const BenchConfig& b) { return *std::max_element(b.sizes.begin(), b.sizes.end()); }
+}  // namespace detail
+
+// Rank 0 times put + SignalInc round trips against rank 1's echo; signal 0
+// counts pings at rank 1 and pongs at rank 0 and is reset between sizes
+// (harness_bench.cpp:46-88).  Rows on rank 0 only.
+inline std::vector<BenchRow> pingpong_rank_program(DevComm& comm, const BenchConfig& bench) {
+  const Team& world = comm.world_team();
+  const uint32_t me = comm.rank();
+  const uint64_t cap = detail::max_size(bench);
+  std::vector<std::byte> send(cap), recv(cap);
+  Window& send_w = comm.window_register(send);
+  Window& recv_w = comm.window_register(recv);
+  Gin gin(comm, 0);
+  BarrierSession barrier(gin, world, 0);
+  std::vector<BenchRow> rows;
+  for (uint64_t size : bench.sizes) {
+    for (uint64_t i = 0; i < size; ++i) send[i] = static_cast<std::byte>(i * 31 + me);
+    barrier.sync();
+    std::vector<uint64_t> samples;
+    samples.reserve(bench.iters);
+    for (uint32_t k = 1; k <= bench.warmup + bench.iters; ++k) {
+      if (me == 0) {
+        const uint64_t t0 = detail::mono_ns();
+        gin.put(world, 1, recv_w, 0, send_w, 0, size, CompletionAction::signal(0, SignalOp::inc()));
+        gin.wait_signal(0, k);
+        const uint64_t dt = detail::mono_ns() - t0;
+        if (k > bench.warmup) samples.push_back(dt);
+      } else {
+        gin.wait_signal(0, k);
+        gin.put(world, 0, recv_w, 0, send_w, 0, size, CompletionAction::signal(0, SignalOp::inc()));
+      }
+    }
+    gin.flush();
+    barrier.sync();  // both ranks idle: the ping counter can be reset
+    gin.reset_signal(0);
+    barrier.sync();
+    if (me == 0) rows.push_back(summarize(size, std::move(samples)));
+  }
+  return rows;
+}
+
+// Rank 0 issues `window` puts then one flush per sample (local completion of
+// the batch); rank 1 is released by a signal per size (harness_bench.cpp:90-128).
+inline std::vector<BenchRow> bw_rank_program(DevComm& comm, const BenchConfig& bench, uint32_t window) {
+  const Team& world = comm.world_team();
+  const uint32_t me = comm.rank();
+  const uint64_t cap = detail::max_size(bench);
+  std::vector<std::byte> send(cap), recv(uint64_t{window} * cap);
+  Window& send_w = comm.window_register(send);
+  Window& recv_w = comm.window_register(recv);
+  Gin gin(comm, 0);
+  BarrierSession barrier(gin, world, 0);
+  std::vector<BenchRow> rows;
+  for (uint64_t size : bench.sizes) {
+    barrier.sync();
+    if (me == 0) {
+      std::vector<uint64_t> samples;
+      for (uint32_t k = 0; k < bench.warmup + bench.iters; ++k) {
+        const uint64_t t0 = detail::mono_ns();
+        for (uint32_t w = 0; w < window; ++w) gin.put(world, 1, recv_w, uint64_t{w} * size, send_w, 0, size);
+        gin.flush();
+        const uint64_t dt = detail::mono_ns() - t0;
+        if (k >= bench.warmup) samples.push_back(dt);
+      }
+      gin.signal(world, 1, 0, SignalOp::inc());
+      rows.push_back(summarize(size, std::move(samples)));
+    } else {
+      gin.wait_signal(0, 1);
+      gin.reset_signal(0);
+    }
+    barrier.sync();
+  }
+  return rows;
+}
+
+// The reference's benchmark CSV (harness_bench.cpp:167-178).  There is no
+// simulated latency model on hardware: the seed column is `seed` (0 unless
+// the caller passes the run's).
+inline void write_csv(const std::string& path, const LaunchOptions& opts, const std::vector<BenchRow>& rows,
+                      uint64_t seed = 0) {
+  std::ofstream f(path);
+  if (!f) throw UsageError("cannot write CSV to " + path);
+  f << "size_bytes,iters,p50_ns,p99_ns,mean_ns,backend,transport,seed\n";
+  const char* backend = to_string(opts.config.backend.value_or(BackendKind::Direct));
+  const char* transport = to_string(opts.transport);
+  for (const BenchRow& r : rows)
+    f << r.size_bytes << ',' << r.iters << ',' << r.p50_ns << ',' << r.p99_ns << ',' << r.mean_ns << ',' << backend
+      << ',' << transport << ',' << seed << '\n';
+}
+
+namespace detail {
+inline void check_bench(const LaunchOptions& opts, const BenchConfig& bench) {
+  if (opts.ranks != 2) throw UsageError("point-to-point benchmarks need exactly 2 ranks");
+  if (bench.sizes.empty() || !std::is_sorted(bench.sizes.begin(), bench.sizes.end()))
+    throw UsageError("bench sizes must be ascending and non-empty");
+  if (bench.iters == 0) throw UsageError("bench iterations must be positive");
+}
+inline std::vector<BenchRow> run_p2p(const LaunchOptions& opts, const BenchConfig& bench,
+                                     const std::function<std::vector<BenchRow>(DevComm&)>& body) {
+  check_bench(opts, bench);
+  std::vector<BenchRow> rows;
+  std::mutex mu;
+  launch(opts, [&](DevComm& comm) {
+    std::vector<BenchRow> mine = body(comm);
+    if (comm.rank() == 0) {
+      std::lock_guard<std::mutex> lk(mu);
+      rows = std::move(mine);
+    }
+  });
+  if (!bench.csv_path.empty()) write_csv(bench.csv_path, opts, rows);
+  return rows;
+}
+}  // namespace detail
+
+// Exactly 2 ranks; rows from rank 0 (harness.hpp:84-89).
+inline std::vector<BenchRow> run_pingpong(const LaunchOptions& opts, const BenchConfig& bench) {
+  return detail::run_p2p(opts, bench, [&](DevComm& c) { return pingpong_rank_program(c, bench); });
+}
+inline std::vector<BenchRow> run_bw(const LaunchOptions& opts, const BenchConfig& bench, uint32_t window = 16) {
+  if (window == 0) throw UsageError("bandwidth window must be positive");
+  return detail::run_p2p(opts, bench, [&](DevComm& c) { return bw_rank_program(c, bench, window); });
 }
 
 }  // namespace ginsim

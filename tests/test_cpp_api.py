@@ -126,8 +126,11 @@ def test_oracle_golden_checks_under_address_and_ub_sanitizers(tmp_path):
 
 def test_cpp_launch_harness_compiles_and_host_checks_pass(tmp_path):
     """ginsim::launch / launch_pool (include/ginsim/harness.hpp, the reference's
-    harness.hpp:13-30): option validation before any device work."""
+    harness.hpp:13-30) and the reference's harness programs (run_ring,
+    run_pingpong, run_bw, summarize, write_csv; harness.hpp:36-102): option
+    validation before any device work, the summary statistics and the CSV
+    schema byte for byte."""
     exe = _build(tmp_path, "harness_launch")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120, cwd=str(tmp_path))
     assert r.returncode == 0, r.stdout + r.stderr
     assert "host checks ok" in r.stdout
