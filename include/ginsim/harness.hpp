@@ -28,6 +28,7 @@
 #include <exception>
 #include <fstream>
 #include <functional>
+#include <initializer_list>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -141,6 +142,13 @@ struct RingReport {
 };
 
 namespace detail {
+// Unpin a program's host windows before its vectors go away (the caller owns
+// window bytes; runtime.cu window_deregister).  Called after the program's
+// closing barrier, when no peer can still write them.
+inline void release(DevComm& comm, std::initializer_list<WindowId> ids) {
+  for (WindowId id : ids) comm.window_deregister(id);
+}
+
 // the (sender, round, offset) tag every ring byte carries (harness_ring.cpp:12-14);
 // receivers recompute it, nothing expected travels out of band
 inline std::byte ring_tag(uint32_t sender, uint32_t round, uint64_t i) {
@@ -180,6 +188,7 @@ inline void ring_rank_program(DevComm& comm, const RingOptions& ring, RankState*
     out->windows = {send, recv};
     out->cells = comm.snapshot_cells();
   }
+  detail::release(comm, {recv_w.id(), send_w.id()});
 }
 
 inline RingReport run_ring(const LaunchOptions& opts, const RingOptions& ring) {
@@ -278,6 +287,7 @@ inline std::vector<BenchRow> pingpong_rank_program(DevComm& comm, const BenchCon
     barrier.sync();
     if (me == 0) rows.push_back(summarize(size, std::move(samples)));
   }
+  detail::release(comm, {recv_w.id(), send_w.id()});
   return rows;
 }
 
@@ -312,6 +322,7 @@ inline std::vector<BenchRow> bw_rank_program(DevComm& comm, const BenchConfig& b
     }
     barrier.sync();
   }
+  detail::release(comm, {recv_w.id(), send_w.id()});
   return rows;
 }
 
