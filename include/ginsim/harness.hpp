@@ -20,11 +20,15 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <spawn.h>
+#include <sys/wait.h>
 
 #include <algorithm>
 #include <chrono>
+#include <cerrno>
 #include <condition_variable>
 #include <cstddef>
+#include <cstring>
 #include <exception>
 #include <fstream>
 #include <functional>
@@ -117,6 +121,50 @@ inline void launch_pool(const LaunchOptions& opts, uint32_t n_comms,
 // launch (harness.hpp:22-24): `program` once per rank.
 inline void launch(const LaunchOptions& opts, const std::function<void(DevComm&)>& program) {
   launch_pool(opts, 1, [&](std::vector<DevComm*>& comms) { program(*comms[0]); });
+}
+
+// launch_processes (harness.hpp:32-34, harness_launch.cpp:77-119): `ranks`
+// copies of `exe` with args + {"--rank", i}, then wait for all of them.
+// ChildFailure names the first rank (in rank order) that exited nonzero or
+// died on a signal, or a spawn that failed.  posix_spawn instead of fork +
+// exec: the caller may already hold a CUDA context, and a forked child of a
+// CUDA process must not touch the runtime before exec.
+inline void launch_processes(const std::string& exe, const std::vector<std::string>& args, uint32_t ranks) {
+  if (ranks == 0) throw UsageError("launch_processes: need at least one rank");
+  std::vector<pid_t> pids(ranks, -1);
+  std::string failure;
+  for (uint32_t r = 0; r < ranks; ++r) {
+    std::vector<std::string> argv_s{exe};
+    argv_s.insert(argv_s.end(), args.begin(), args.end());
+    argv_s.push_back("--rank");
+    argv_s.push_back(std::to_string(r));
+    std::vector<char*> argv;
+    for (auto& a : argv_s) argv.push_back(a.data());
+    argv.push_back(nullptr);
+    const int rc = ::posix_spawn(&pids[r], exe.c_str(), nullptr, nullptr, argv.data(), environ);
+    if (rc != 0) {
+      pids[r] = -1;
+      if (failure.empty()) failure = "rank " + std::to_string(r) + ": spawn of " + exe + " failed: " + std::strerror(rc);
+      break;  // the ranks already running are still reaped below
+    }
+  }
+  for (uint32_t r = 0; r < ranks; ++r) {
+    if (pids[r] < 0) continue;
+    int st = 0;
+    pid_t w;
+    do {
+      w = ::waitpid(pids[r], &st, 0);
+    } while (w < 0 && errno == EINTR);
+    std::string why;
+    if (w < 0)
+      why = "waitpid failed: " + std::string(std::strerror(errno));
+    else if (WIFEXITED(st) && WEXITSTATUS(st) != 0)
+      why = "exited with status " + std::to_string(WEXITSTATUS(st));
+    else if (WIFSIGNALED(st))
+      why = "killed by signal " + std::to_string(WTERMSIG(st));
+    if (!why.empty() && failure.empty()) failure = "rank " + std::to_string(r) + " " + why;
+  }
+  if (!failure.empty()) throw ChildFailure(failure);
 }
 
 // ------------------------------------------------------------ final state

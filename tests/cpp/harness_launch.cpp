@@ -89,6 +89,25 @@ static void host_checks() {
   EXPECT(throws<ginsim::UsageError>([&] { ginsim::run_pingpong(two, b); }));
   b.iters = 4;
   EXPECT(throws<ginsim::UsageError>([&] { ginsim::run_bw(two, b, 0); }));
+
+  // launch_processes (harness_launch.cpp:77-119): argv = exe, args..., --rank, i
+  EXPECT(throws<ginsim::UsageError>([&] { ginsim::launch_processes("/bin/sh", {"-c", "exit 0"}, 0); }));
+  ginsim::launch_processes("/bin/sh", {"-c", "test \"$1\" = --rank && test \"$2\" -lt 4", "sh"}, 4);
+  std::string what;
+  try {
+    ginsim::launch_processes("/bin/sh", {"-c", "exit $(( $2 >= 2 ? 10 + $2 : 0 ))", "sh"}, 4);
+  } catch (const ginsim::ChildFailure& e) {
+    what = e.what();
+  }
+  EXPECT(what.find("rank 2 exited with status 12") != std::string::npos);
+  what.clear();
+  try {
+    ginsim::launch_processes("/bin/sh", {"-c", "test $2 = 1 && kill -9 $$; exit 0", "sh"}, 3);
+  } catch (const ginsim::ChildFailure& e) {
+    what = e.what();
+  }
+  EXPECT(what.find("rank 1 killed by signal 9") != std::string::npos);
+  EXPECT(throws<ginsim::ChildFailure>([&] { ginsim::launch_processes("/nonexistent/exe", {}, 2); }));
   std::printf("host checks ok\n");
 }
 
