@@ -816,6 +816,22 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
       }
     }
   }
+  // a failure below (bootstrap, mismatch, peer mapping) must not leave the
+  // host pages pinned or the peers' regions mapped
+  Comm::Window w;
+  struct Undo {
+    void* host = nullptr;
+    std::vector<Mapping>* maps = nullptr;
+    ~Undo() {
+      if (maps)
+        for (auto& m : *maps) {
+          cuapi().cuMemUnmap(m.ptr, m.size);
+          cuapi().cuMemAddressFree(m.ptr, m.size);
+          cuapi().cuMemRelease(m.handle);
+        }
+      if (host) cudaHostUnregister(host);
+    }
+  } undo{host_registered, &w.maps};
   ExportBlob mine{};
   mine.pid = (int32_t)getpid();
   mine.device = c->device;
@@ -841,13 +857,11 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
   c->allgather(&mine, blobs.data(), sizeof(ExportBlob));
   for (uint32_t r = 0; r < c->world; ++r) {
     if (blobs[r].window_id != mine.window_id) {
-      if (host_registered) cudaHostUnregister(host_registered);
       fail(GINSIM_E_REGISTRATION_MISMATCH, "window_register call counts differ: rank " + std::to_string(c->rank) +
                                                " at " + std::to_string(mine.window_id) + ", rank " +
                                                std::to_string(r) + " at " + std::to_string(blobs[r].window_id));
     }
   }
-  Comm::Window w;
   w.live = true;
   w.host_registered = host_registered;
   w.sizes.resize(c->world);
@@ -857,6 +871,8 @@ int ginsim_cuda_window_register(ginsim_cuda_comm_t comm, void* local, uint64_t b
     w.bases[r] = r == c->rank ? static_cast<char*>(local)
                               : (blobs[r].bytes && c->cfg.transport == 0 ? c->map_blob(blobs[r], &w.maps) : nullptr);
   }
+  undo.host = nullptr;  // the window owns them from here
+  undo.maps = nullptr;
   for (uint32_t r = 0; r < c->world; ++r) {
     c->host_view.win[id].base[r] = w.bases[r];
     c->host_view.win[id].size[r] = w.sizes[r];
