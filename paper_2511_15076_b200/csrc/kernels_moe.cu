@@ -59,6 +59,10 @@ struct ginsim_cuda_moe_s {
   uint32_t* midx = nullptr;
   uint32_t win_rows = 0;
   void* buf_rows = nullptr;
+  // windows this handle registered, bit i = entry i of moe_destroy's owned[]
+  // list (dispatch, counts, combine, rows, stage, cstage, mirror): a create
+  // that failed half way releases exactly what it had
+  uint32_t registered = 0;
   uint64_t* aux_g = nullptr;
   void* buf_stage = nullptr;
   void* buf_cstage = nullptr;
@@ -154,79 +158,90 @@ int ginsim_cuda_moe_create(ginsim_cuda_comm_t comm, const ginsim_cuda_moe_config
   auto m = std::make_unique<ginsim_cuda_moe_s>();
   m->comm = c;
   m->comm_handle = comm;
-  m->cfg = *cfg;
-  m->e_local = e_local;
   m->cell0 = cell0;
   m->cell_span = span;
-  m->parts = cfg->hidden >= 1024 ? 4 : 1;
-  const uint64_t dmsg = (cfg->mode >= 2 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden) + 16;
-  const uint64_t cmsg = cfg->mode == 3 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden;
-  const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
-  const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
-  // counts [src][e_loc] + row counts [src] + row bounds [src][chunks + 1] (layout 2)
-  // + pipelined-combine slot bounds [src][kCombineChunks - 1][e_loc]
-  const uint64_t nbytes = ((uint64_t)e_local * n + n + n * (kDedupChunks + 1) + n * (kCombineChunks - 1) * e_local) * 4;
-  const uint64_t cbytes = T * K * cmsg;
-  if (ginsim_cuda_mem_alloc(comm, dbytes, &m->buf_dispatch)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
-  if (ginsim_cuda_mem_alloc(comm, nbytes, &m->buf_counts)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
-  if (ginsim_cuda_mem_alloc(comm, cbytes, &m->buf_combine)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
-  int rc;
-  if ((rc = ginsim_cuda_window_register(comm, m->buf_dispatch, dbytes, &m->win_dispatch))) fail(rc, ginsim_cuda_last_error());
-  if ((rc = ginsim_cuda_window_register(comm, m->buf_counts, nbytes, &m->win_counts))) fail(rc, ginsim_cuda_last_error());
-  if ((rc = ginsim_cuda_window_register(comm, m->buf_combine, cbytes, &m->win_combine))) fail(rc, ginsim_cuda_last_error());
-  m->proxy = c->cfg.backend == GIN_BACKEND_PROXY;
-  {
-    // Proxy backend, compact layout, 16-byte rows, one put per run: the
-    // pipelined transport (GINSIM_PROXY_PIPE=0 keeps the one-shot LSU staging
-    // kernels; GINSIM_PROXY_COALESCE=0 the reference's one put per message)
-    const char* pv = std::getenv("GINSIM_PROXY_PIPE");
-    const char* cv = std::getenv("GINSIM_PROXY_COALESCE");
-    m->pipe = m->proxy && cfg->layout == 1 && cfg->mode <= 1 && (2u * cfg->hidden) % 16u == 0 &&
-              !(pv && pv[0] == '0') && !(cv && cv[0] == '0');
-  }
-  if (cfg->layout == 2) {
-    // row staging: [src][j] rows of 2H bytes, then [src][j] 128-byte headers
-    const uint64_t rbytes = n * T * (2ull * cfg->hidden + 128);
-    if (ginsim_cuda_mem_alloc(comm, rbytes, &m->buf_rows)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
-    if ((rc = ginsim_cuda_window_register(comm, m->buf_rows, rbytes, &m->win_rows))) fail(rc, ginsim_cuda_last_error());
-    DeviceGuard dgr(c->device);
-    GIN_CUDA(cudaMalloc(&m->aux_g, 2 * (size_t)T * ((K + 1) & ~1ull) * sizeof(uint64_t)));
-  }
-  if (m->proxy) {
-    // Proxy backend: dispatch rows and combine results are staged in local
-    // registered windows the host agent copies from (the reference's staging
-    // windows, harness_moe.cpp:122-130).  Separate windows, so a combine never
-    // overwrites rows the agent may still be copying out for the dispatch.
-    // (pipeline: the counts staged for the count puts follow the rows)
-    const uint64_t sbytes = T * K * dmsg + (m->pipe ? ((uint64_t)cfg->experts * 4 + 15) / 16 * 16 : 0);
-    const uint64_t cbytes2 = n * T * K * cmsg;
-    if (ginsim_cuda_mem_alloc(comm, sbytes, &m->buf_stage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
-    if ((rc = ginsim_cuda_window_register(comm, m->buf_stage, sbytes, &m->win_stage))) fail(rc, ginsim_cuda_last_error());
-    if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_cstage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
-    if ((rc = ginsim_cuda_window_register(comm, m->buf_cstage, cbytes2, &m->win_cstage))) fail(rc, ginsim_cuda_last_error());
-    // combine results in send order ([dst][expert prefix][slot]): one put per run
-    if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_mirror)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
-    if ((rc = ginsim_cuda_window_register(comm, m->buf_mirror, cbytes2, &m->win_mirror))) fail(rc, ginsim_cuda_last_error());
-    DeviceGuard dgm(c->device);
-    GIN_CUDA(cudaMalloc(&m->midx, (size_t)T * K * 4));
-    if (m->pipe) GIN_CUDA(cudaMalloc(&m->pipe_buf, ((size_t)T * K + kPipeCtrWords) * 4));
-  }
-  DeviceGuard g(c->device);
-  GIN_CUDA(cudaMalloc(&m->ws, kWsBytes));
-  GIN_CUDA(cudaMalloc(&m->cell_acc, (size_t)e_local * 8));
-  GIN_CUDA(cudaMemset(m->cell_acc, 0, (size_t)e_local * 8));
-  GIN_CUDA(cudaMalloc(&m->route, (2 * (size_t)kMaxGrid + 1) * kMaxExperts * 4));
-  GIN_CUDA(cudaMalloc(&m->dst_g, (size_t)cfg->tokens * ((cfg->top_k + 1) & ~1u) * sizeof(char*)));
-  GIN_CUDA(cudaMemset(m->ws, 0, kWsBytes));
-  // Cooperative route tables from this many (token, k) pairs per rank on
-  // (GINSIM_DISPATCH_COOP_MIN_PAIRS; the LL shape, 1024 pairs, stays local).
-  const char* cm = std::getenv("GINSIM_DISPATCH_COOP_MIN_PAIRS");
-  const uint64_t coop_min = cm ? std::strtoull(cm, nullptr, 10) : 8192ull;
-  m->coop = (uint64_t)cfg->tokens * cfg->top_k >= coop_min;
-  const char* pp = std::getenv("GINSIM_PROFILE_PHASES");
-  if (pp && pp[0] == '1') {
-    GIN_CUDA(cudaMalloc(&m->prof, 3 * 1024 * 8 * sizeof(uint64_t)));
-    GIN_CUDA(cudaMemset(m->prof, 0, 3 * 1024 * 8 * sizeof(uint64_t)));
+  try {
+    m->cfg = *cfg;
+    m->e_local = e_local;
+    m->parts = cfg->hidden >= 1024 ? 4 : 1;
+    const uint64_t dmsg = (cfg->mode >= 2 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden) + 16;
+    const uint64_t cmsg = cfg->mode == 3 ? (uint64_t)cfg->hidden + cfg->hidden / 32 : 2ull * cfg->hidden;
+    const uint64_t n = c->world, T = cfg->tokens, K = cfg->top_k;
+    const uint64_t dbytes = cfg->layout == 0 ? (uint64_t)e_local * n * T * dmsg : n * T * K * dmsg;
+    // counts [src][e_loc] + row counts [src] + row bounds [src][chunks + 1] (layout 2)
+    // + pipelined-combine slot bounds [src][kCombineChunks - 1][e_loc]
+    const uint64_t nbytes = ((uint64_t)e_local * n + n + n * (kDedupChunks + 1) + n * (kCombineChunks - 1) * e_local) * 4;
+    const uint64_t cbytes = T * K * cmsg;
+    if (ginsim_cuda_mem_alloc(comm, dbytes, &m->buf_dispatch)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+    if (ginsim_cuda_mem_alloc(comm, nbytes, &m->buf_counts)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+    if (ginsim_cuda_mem_alloc(comm, cbytes, &m->buf_combine)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+    auto reg = [&](void* buf, uint64_t bytes, uint32_t* win, uint32_t bit) {
+      const int rc = ginsim_cuda_window_register(comm, buf, bytes, win);
+      if (rc) fail(rc, ginsim_cuda_last_error());
+      m->registered |= 1u << bit;
+    };
+    reg(m->buf_dispatch, dbytes, &m->win_dispatch, 0);
+    reg(m->buf_counts, nbytes, &m->win_counts, 1);
+    reg(m->buf_combine, cbytes, &m->win_combine, 2);
+    m->proxy = c->cfg.backend == GIN_BACKEND_PROXY;
+    {
+      // Proxy backend, compact layout, 16-byte rows, one put per run: the
+      // pipelined transport (GINSIM_PROXY_PIPE=0 keeps the one-shot LSU staging
+      // kernels; GINSIM_PROXY_COALESCE=0 the reference's one put per message)
+      const char* pv = std::getenv("GINSIM_PROXY_PIPE");
+      const char* cv = std::getenv("GINSIM_PROXY_COALESCE");
+      m->pipe = m->proxy && cfg->layout == 1 && cfg->mode <= 1 && (2u * cfg->hidden) % 16u == 0 &&
+                !(pv && pv[0] == '0') && !(cv && cv[0] == '0');
+    }
+    if (cfg->layout == 2) {
+      // row staging: [src][j] rows of 2H bytes, then [src][j] 128-byte headers
+      const uint64_t rbytes = n * T * (2ull * cfg->hidden + 128);
+      if (ginsim_cuda_mem_alloc(comm, rbytes, &m->buf_rows)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+      reg(m->buf_rows, rbytes, &m->win_rows, 3);
+      DeviceGuard dgr(c->device);
+      GIN_CUDA(cudaMalloc(&m->aux_g, 2 * (size_t)T * ((K + 1) & ~1ull) * sizeof(uint64_t)));
+    }
+    if (m->proxy) {
+      // Proxy backend: dispatch rows and combine results are staged in local
+      // registered windows the host agent copies from (the reference's staging
+      // windows, harness_moe.cpp:122-130).  Separate windows, so a combine never
+      // overwrites rows the agent may still be copying out for the dispatch.
+      // (pipeline: the counts staged for the count puts follow the rows)
+      const uint64_t sbytes = T * K * dmsg + (m->pipe ? ((uint64_t)cfg->experts * 4 + 15) / 16 * 16 : 0);
+      const uint64_t cbytes2 = n * T * K * cmsg;
+      if (ginsim_cuda_mem_alloc(comm, sbytes, &m->buf_stage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+      reg(m->buf_stage, sbytes, &m->win_stage, 4);
+      if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_cstage)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+      reg(m->buf_cstage, cbytes2, &m->win_cstage, 5);
+      // combine results in send order ([dst][expert prefix][slot]): one put per run
+      if (ginsim_cuda_mem_alloc(comm, cbytes2, &m->buf_mirror)) fail(GINSIM_E_CUDA, ginsim_cuda_last_error());
+      reg(m->buf_mirror, cbytes2, &m->win_mirror, 6);
+      DeviceGuard dgm(c->device);
+      GIN_CUDA(cudaMalloc(&m->midx, (size_t)T * K * 4));
+      if (m->pipe) GIN_CUDA(cudaMalloc(&m->pipe_buf, ((size_t)T * K + kPipeCtrWords) * 4));
+    }
+    DeviceGuard g(c->device);
+    GIN_CUDA(cudaMalloc(&m->ws, kWsBytes));
+    GIN_CUDA(cudaMalloc(&m->cell_acc, (size_t)e_local * 8));
+    GIN_CUDA(cudaMemset(m->cell_acc, 0, (size_t)e_local * 8));
+    GIN_CUDA(cudaMalloc(&m->route, (2 * (size_t)kMaxGrid + 1) * kMaxExperts * 4));
+    GIN_CUDA(cudaMalloc(&m->dst_g, (size_t)cfg->tokens * ((cfg->top_k + 1) & ~1u) * sizeof(char*)));
+    GIN_CUDA(cudaMemset(m->ws, 0, kWsBytes));
+    // Cooperative route tables from this many (token, k) pairs per rank on
+    // (GINSIM_DISPATCH_COOP_MIN_PAIRS; the LL shape, 1024 pairs, stays local).
+    const char* cm = std::getenv("GINSIM_DISPATCH_COOP_MIN_PAIRS");
+    const uint64_t coop_min = cm ? std::strtoull(cm, nullptr, 10) : 8192ull;
+    m->coop = (uint64_t)cfg->tokens * cfg->top_k >= coop_min;
+    const char* pp = std::getenv("GINSIM_PROFILE_PHASES");
+    if (pp && pp[0] == '1') {
+      GIN_CUDA(cudaMalloc(&m->prof, 3 * 1024 * 8 * sizeof(uint64_t)));
+      GIN_CUDA(cudaMemset(m->prof, 0, 3 * 1024 * 8 * sizeof(uint64_t)));
+    }
+  } catch (...) {
+    // release what this rank allocated and registered, and its cell range
+    // (moe_destroy is local); the rethrown error is the one reported
+    ginsim_cuda_moe_destroy(m.release());
+    throw;
   }
   *out = m.release();
   GIN_API_END
@@ -256,12 +271,16 @@ int ginsim_cuda_moe_destroy(ginsim_cuda_moe_t moe) {
       {moe->win_dispatch, moe->buf_dispatch}, {moe->win_counts, moe->buf_counts}, {moe->win_combine, moe->buf_combine},
       {moe->win_rows, moe->buf_rows},         {moe->win_stage, moe->buf_stage},   {moe->win_cstage, moe->buf_cstage},
       {moe->win_mirror, moe->buf_mirror}};
-  for (const auto& o : owned) {
-    if (!o.second) continue;
-    int rc = ginsim_cuda_window_deregister(ch, o.first);
-    if (rc) fail(rc, ginsim_cuda_last_error());
-    rc = ginsim_cuda_mem_free(ch, o.second);
-    if (rc) fail(rc, ginsim_cuda_last_error());
+  for (uint32_t i = 0; i < sizeof(owned) / sizeof(owned[0]); ++i) {
+    const auto& o = owned[i];
+    if ((moe->registered >> i) & 1u) {
+      const int rc = ginsim_cuda_window_deregister(ch, o.first);
+      if (rc) fail(rc, ginsim_cuda_last_error());
+    }
+    if (o.second) {
+      const int rc = ginsim_cuda_mem_free(ch, o.second);
+      if (rc) fail(rc, ginsim_cuda_last_error());
+    }
   }
   {
     std::lock_guard<std::mutex> lk(c->mu);
