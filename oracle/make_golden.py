@@ -40,6 +40,14 @@ MOE_CONFIGS = [
     (4, 32, 4, 16, 256, 2, "direct"),
     (8, 256, 8, 16, 7168, 1, "direct"),
     (8, 256, 8, 128, 7168, 1, "direct"),  # BASELINE LL config
+    # edge shapes (appended: the GPU golden test covers the first 11)
+    (4, 8, 2, 4, 96, 0, "direct"),        # acceptance.cpp:305-318 (#6 backend equivalence)
+    (4, 8, 2, 4, 96, 13, "proxy"),
+    (2, 4, 4, 3, 32, 9, "direct"),        # top_k == experts: every expert routed
+    (4, 4, 2, 5, 64, 4, "direct"),        # one expert per rank
+    (2, 2, 1, 6, 16, 8, "proxy"),         # the smallest pool
+    (2, 4, 2, 3, 5, 6, "direct"),         # odd hidden (26-byte dispatch messages)
+    (8, 16, 3, 1, 8, 12, "direct"),       # one token per rank on 8 ranks
 ]
 
 
@@ -132,6 +140,11 @@ def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref missing: run oracle/build_ref.sh first")
     os.makedirs(GOLDEN, exist_ok=True)
+    if sys.argv[1:] == ["moe"]:  # only the moe-ll fixture
+        with open(os.path.join(GOLDEN, "moe_ll.json"), "w") as f:
+            json.dump(moe_fixture(), f)
+        print("moe-ll fixture written to", GOLDEN)
+        return
     with open(os.path.join(GOLDEN, "wire.json"), "w") as f:
         json.dump(wire_fixture(), f)
     if sys.argv[1:] == ["wire"]:  # only the wire fixture
