@@ -96,7 +96,12 @@ def moe_fixture():
 
 def ring_fixture():
     out = []
-    for (n, S, rounds, backend) in [(2, 256, 3, "direct"), (4, 512, 25, "proxy"), (8, 4096, 10, "direct")]:
+    # the first three are the GPU test's shapes; then acceptance #5's 100 rounds
+    # (acceptance.cpp:273-300) on 8 ranks over both backends, an odd rank count
+    # with a ragged size, and a one-byte payload
+    for (n, S, rounds, backend) in [(2, 256, 3, "direct"), (4, 512, 25, "proxy"), (8, 4096, 10, "direct"),
+                                    (8, 1024, 100, "proxy"), (8, 1024, 100, "direct"), (3, 333, 7, "direct"),
+                                    (2, 1, 4, "proxy")]:
         d = tempfile.mkdtemp(prefix="gold")
         try:
             O.ref_run("ring", "--ranks", n, "--bytes", S, "--rounds", rounds, "--backend", backend, "--dump", d)
@@ -140,6 +145,11 @@ def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref missing: run oracle/build_ref.sh first")
     os.makedirs(GOLDEN, exist_ok=True)
+    if sys.argv[1:] == ["ring"]:  # only the ring fixture
+        with open(os.path.join(GOLDEN, "ring.json"), "w") as f:
+            json.dump(ring_fixture(), f)
+        print("ring fixture written to", GOLDEN)
+        return
     if sys.argv[1:] == ["moe"]:  # only the moe-ll fixture
         with open(os.path.join(GOLDEN, "moe_ll.json"), "w") as f:
             json.dump(moe_fixture(), f)
