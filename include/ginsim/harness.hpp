@@ -374,11 +374,10 @@ inline std::vector<BenchRow> bw_rank_program(DevComm& comm, const BenchConfig& b
   return rows;
 }
 
-// The reference's benchmark CSV (harness_bench.cpp:167-178).  There is no
-// simulated latency model on hardware: the seed column is `seed` (0 unless
-// the caller passes the run's).
-inline void write_csv(const std::string& path, const LaunchOptions& opts, const std::vector<BenchRow>& rows,
-                      uint64_t seed = 0) {
+// The reference's benchmark CSV (harness_bench.cpp:167-178); the seed column
+// is the config's latency seed, as in the reference.
+inline void write_csv(const std::string& path, const LaunchOptions& opts, const std::vector<BenchRow>& rows) {
+  const uint64_t seed = opts.config.latency.seed;
   std::ofstream f(path);
   if (!f) throw UsageError("cannot write CSV to " + path);
   f << "size_bytes,iters,p50_ns,p99_ns,mean_ns,backend,transport,seed\n";

@@ -164,6 +164,19 @@ inline const char* to_string(TransportKind k) {
 }
 enum class Opcode : uint8_t { Put = 1, PutInline = 2, SignalOnly = 3 };
 
+// fabric.hpp:26-35.  The reference's simulated-fabric latency model.  On B200
+// the fabric is real (NVLink, or one GPU's HBM for emulated ranks): the model
+// is accepted so reference programs compile, and its seed is the CSV's seed
+// column (write_csv); the delays are not applied.
+struct LatencyModel {
+  uint64_t base_delay_ns = 0;
+  uint64_t jitter_ns = 0;
+  uint32_t reorder_window = 0;
+  uint64_t seed = 0;
+  double line_rate_gbps = 0.0;
+  friend bool operator==(const LatencyModel&, const LatencyModel&) = default;
+};
+
 struct Config {
   uint32_t n_contexts = 4;
   std::optional<BackendKind> backend;  // unset = direct
@@ -171,6 +184,9 @@ struct Config {
   uint32_t counter_cells = 256;
   uint32_t queue_depth = 1024;
   uint64_t timeout_ms = 30'000;
+  // runtime.hpp:36-37 defaults; informational on B200 (see LatencyModel)
+  LatencyModel latency{.base_delay_ns = 500, .jitter_ns = 0, .reorder_window = 0, .seed = 0x5EED,
+                       .line_rate_gbps = 16.0};
   ProgressMode progress = ProgressMode::Threaded;  // informational on B200 (always asynchronous)
   int device = -1;  // B200: GPU of this rank (-1 = rank % device count)
   // unset = the fabric (NVLink peer mappings); Socket = the Proxy backend's
@@ -199,6 +215,20 @@ inline Config config_from_env(Config base = {}) {
   base.timeout_ms = c.timeout_ms;
   if (!std::getenv("GINSIM_BACKEND")) base.backend.reset();
   if (std::getenv("GINSIM_TRANSPORT")) base.transport = c.transport ? TransportKind::Socket : TransportKind::Nvlink;
+  // the latency-model variables (runtime.cpp:53-56), parsed as the reference
+  // does (strtoull base 0, the whole string, UsageError otherwise)
+  auto env_u64 = [](const char* name) -> std::optional<uint64_t> {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return std::nullopt;
+    char* end = nullptr;
+    const uint64_t x = std::strtoull(v, &end, 0);
+    if (end == v || *end != '\0') throw UsageError(std::string(name) + ": cannot parse '" + v + "' as an integer");
+    return x;
+  };
+  if (auto v = env_u64("GINSIM_SEED")) base.latency.seed = *v;
+  if (auto v = env_u64("GINSIM_LATENCY_NS")) base.latency.base_delay_ns = *v;
+  if (auto v = env_u64("GINSIM_JITTER_NS")) base.latency.jitter_ns = *v;
+  if (auto v = env_u64("GINSIM_REORDER")) base.latency.reorder_window = static_cast<uint32_t>(*v);
   return base;
 }
 

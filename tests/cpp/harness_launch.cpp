@@ -60,8 +60,20 @@ static void host_checks() {
   // the reference's CSV schema (harness_bench.cpp:167-178)
   ginsim::LaunchOptions co;
   co.config.backend = ginsim::BackendKind::Proxy;
+  EXPECT(co.config.latency.seed == 0x5EED && co.config.latency.base_delay_ns == 500);  // runtime.hpp:36-37
+  co.config.latency.seed = 3;
+  // config_from_env applies the latency variables (runtime.cpp:53-56)
+  setenv("GINSIM_SEED", "0x2A", 1);
+  setenv("GINSIM_REORDER", "8", 1);
+  const ginsim::Config env = ginsim::config_from_env();
+  EXPECT(env.latency.seed == 42 && env.latency.reorder_window == 8 && env.latency.base_delay_ns == 500);
+  setenv("GINSIM_JITTER_NS", "12x", 1);
+  EXPECT(throws<ginsim::UsageError>([] { ginsim::config_from_env(); }));
+  unsetenv("GINSIM_SEED");
+  unsetenv("GINSIM_REORDER");
+  unsetenv("GINSIM_JITTER_NS");
   const char* path = "harness_launch_test.csv";
-  ginsim::write_csv(path, co, {row, ginsim::summarize(128, {5, 6, 7})}, 3);
+  ginsim::write_csv(path, co, {row, ginsim::summarize(128, {5, 6, 7})});
   std::ifstream in(path);
   std::stringstream ss;
   ss << in.rdbuf();
