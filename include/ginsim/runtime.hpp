@@ -114,11 +114,27 @@ class Window {
   Window() = default;
   Window(ginsim_cuda_comm_t c, WindowId id, RankId self, std::vector<uint64_t> sizes, std::span<std::byte> local)
       : comm_(c), id_(id), self_(self), sizes_(std::move(sizes)), local_(local) {}
+  // types.hpp:92-93: a window description without a communicator (ranges,
+  // sizes and the local slice only; peer_bytes needs a registered window)
+  Window(WindowId id, RankId self, std::vector<uint64_t> sizes, std::span<std::byte> local)
+      : id_(id), self_(self), sizes_(std::move(sizes)), local_(local) {
+    if (self_ >= sizes_.size() || local_.size() != sizes_[self_])
+      throw UnknownWindow("window " + std::to_string(id) + ": local region size mismatch");
+  }
+  // types.hpp:95-97: a registration still collecting the peers' sizes
+  static Window pending(WindowId id, RankId self, std::span<std::byte> local) {
+    Window w;
+    w.id_ = id;
+    w.self_ = self;
+    w.local_ = local;
+    return w;
+  }
   WindowId id() const { return id_; }
   RankId self_rank() const { return self_; }
   bool complete() const { return !sizes_.empty(); }
   uint32_t rank_count() const { return static_cast<uint32_t>(sizes_.size()); }
   uint64_t size_of(RankId rank) const {
+    if (!complete()) throw UnknownWindow("window " + std::to_string(id_) + " not fully registered yet");
     if (rank >= sizes_.size()) throw RankOutOfRange("rank " + std::to_string(rank) + " not registered in window");
     return sizes_[rank];
   }
@@ -149,6 +165,15 @@ class Window {
   std::vector<uint64_t> sizes_;
   std::span<std::byte> local_;
 };
+
+// types.hpp:119-123: the bytes of [offset, offset + len) in rank's region --
+// validated for every rank, backing bytes only for the registering rank (the
+// other ranks' regions are not local; the span is empty for those).
+inline std::span<std::byte> window_resolve(Window& w, RankId rank, uint64_t offset, uint64_t len) {
+  w.check_range(rank, offset, len);
+  if (rank == w.self_rank()) return w.local_bytes(offset, len);
+  return {};
+}
 
 // ---------------------------------------------------------------- runtime.hpp:26-58
 enum class BackendKind { Direct, Proxy };
@@ -253,6 +278,10 @@ class InProcGroup {
   ~InProcGroup() { ginsim_cuda_inproc_group_destroy(g_); }
   uint32_t world_size() const { return world_; }
   ginsim_cuda_group_t handle() const { return g_; }
+  // runtime.hpp:81-83 (Manual-mode progress).  The device moves the bytes and
+  // the proxy agents run on their own threads, so there is never work for the
+  // host to pump: 0, as the reference returns once a group is quiescent.
+  size_t pump_all() { return 0; }
 
  private:
   InProcGroup(ginsim_cuda_group_t g, uint32_t w) : g_(g), world_(w) {}

@@ -134,3 +134,36 @@ def test_cpp_launch_harness_compiles_and_host_checks_pass(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120, cwd=str(tmp_path))
     assert r.returncode == 0, r.stdout + r.stderr
     assert "host checks ok" in r.stdout
+
+
+REF_TESTS = "/root/reference/proj/tests"
+
+
+@pytest.mark.parametrize("name,run", [("test_core", True), ("test_descriptor", True), ("test_wire", True),
+                                      ("test_runtime", False)])
+def test_reference_unit_tests_build_unchanged_against_our_headers(tmp_path, name, run):
+    """Drop-in check from the reference's side: its own doctest unit sources
+    (proj/tests/<name>.cpp, read in place, not copied) compile UNCHANGED
+    against include/ginsim/*.hpp + libginsim_b200.so, with a minimal doctest
+    shim (tests/cpp/doctest_shim/doctest.h; doctest itself is not in the
+    image).  Host-only suites run here: the core types (test_core.cpp:20-88),
+    the descriptor codec (test_descriptor.cpp: golden bytes, invariants,
+    malformed buffers, 10^4 random round trips) and the GIN1 framing
+    (test_wire.cpp).  test_runtime.cpp's communicator semantics need a GPU;
+    it is compiled and linked only (its ManualWorld drives every rank's
+    comm_init from one thread, which a collective bootstrap cannot serve)."""
+    src = os.path.join(REF_TESTS, f"{name}.cpp")
+    if not os.path.exists(src):
+        pytest.skip("reference sources not present (they are read in place, never copied)")
+    main = tmp_path / "doctest_main.cpp"
+    main.write_text('#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN\n#include "doctest.h"\n')
+    exe = str(tmp_path / name)
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "tests", "cpp", "doctest_shim"),
+           "-I", os.path.join(ROOT, "include"), "-I", f"{CUDA}/include", str(main), src, "-o", exe,
+           "-L", LIBDIR, "-lginsim_b200", f"-Wl,-rpath,{LIBDIR}", "-L", f"{CUDA}/lib64", "-lcudart", "-lpthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    if run:
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        assert " 0 failed" in r.stdout, r.stdout
