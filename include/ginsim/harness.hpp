@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <spawn.h>
 #include <sys/wait.h>
+#include <unistd.h>  // environ
 
 #include <algorithm>
 #include <chrono>
