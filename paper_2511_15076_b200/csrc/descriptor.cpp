@@ -112,3 +112,25 @@ void descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* d) {
 }
 
 }  // namespace ginsim_b200
+
+// The codec's C ABI (include/ginsim_cuda.h), next to the codec so the host
+// codecs build standalone (the sanitizer tests compile them from source).
+using namespace ginsim_b200;
+
+extern "C" {
+
+int ginsim_cuda_descriptor_encode(const ginsim_cuda_descriptor* d, uint8_t out[64]) {
+  GIN_API_BEGIN
+  if (!d || !out) fail(GINSIM_E_USAGE, "descriptor_encode: null argument");
+  descriptor_encode(d, out);
+  GIN_API_END
+}
+
+int ginsim_cuda_descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* d) {
+  GIN_API_BEGIN
+  if (!in || !d) fail(GINSIM_E_USAGE, "descriptor_decode: null argument");
+  descriptor_decode(in, d);
+  GIN_API_END
+}
+
+}  // extern "C"

@@ -1162,18 +1162,6 @@ int ginsim_cuda_proxy_stats(ginsim_cuda_comm_t comm, uint64_t* descriptors, uint
   GIN_API_END
 }
 
-int ginsim_cuda_descriptor_encode(const ginsim_cuda_descriptor* d, uint8_t out[64]) {
-  GIN_API_BEGIN
-  descriptor_encode(d, out);
-  GIN_API_END
-}
-
-int ginsim_cuda_descriptor_decode(const uint8_t in[64], ginsim_cuda_descriptor* d) {
-  GIN_API_BEGIN
-  descriptor_decode(in, d);
-  GIN_API_END
-}
-
 }  // extern "C"
 
 extern "C" int ginsim_cuda_window_register_all(const ginsim_cuda_comm_t* comms, uint32_t n, void* const* ptrs,

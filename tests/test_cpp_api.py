@@ -167,3 +167,28 @@ def test_reference_unit_tests_build_unchanged_against_our_headers(tmp_path, name
         r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
         assert " 0 failed" in r.stdout, r.stdout
+
+
+def test_reference_codec_unit_tests_under_address_and_ub_sanitizers(tmp_path):
+    """The reference's own codec unit sources (proj/tests/test_descriptor.cpp,
+    test_wire.cpp; read in place) against include/ginsim/{descriptor,wire}.hpp,
+    with the host codecs (csrc/descriptor.cpp, csrc/wire.cpp) built from
+    source under -fsanitize=address,undefined: every case passes, no report."""
+    srcs = [os.path.join(REF_TESTS, f"{n}.cpp") for n in ("test_descriptor", "test_wire")]
+    if not all(os.path.exists(s) for s in srcs):
+        pytest.skip("reference sources not present (they are read in place, never copied)")
+    main = tmp_path / "doctest_main.cpp"
+    main.write_text('#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN\n#include "doctest.h"\n')
+    csrc = os.path.join(ROOT, "paper_2511_15076_b200", "csrc")
+    exe = str(tmp_path / "ref_codecs_asan")
+    cmd = ["g++", "-std=c++20", "-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+           "-I", os.path.join(ROOT, "tests", "cpp", "doctest_shim"), "-I", os.path.join(ROOT, "include"),
+           "-I", f"{CUDA}/include", str(main), *srcs, os.path.join(csrc, "wire.cpp"),
+           os.path.join(csrc, "descriptor.cpp"), os.path.join(ROOT, "tests", "cpp", "codec_runtime_stub.cpp"),
+           "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, ASAN_OPTIONS="detect_leaks=1", UBSAN_OPTIONS="print_stacktrace=1"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "11 test cases, 0 failed" in r.stdout, r.stdout
