@@ -756,12 +756,20 @@ extern "C" int ginsim_cuda_moe_create_all(const ginsim_cuda_comm_t* comms, uint3
   std::vector<std::thread> ts;
   for (uint32_t r = 0; r < n; ++r) {
     ts.emplace_back([&, r] {
+      out[r] = nullptr;
       rcs[r] = ginsim_cuda_moe_create(comms[r], cfg, &out[r]);
       if (rcs[r]) msgs[r] = ginsim_cuda_last_error();
     });
   }
   for (auto& t : ts) t.join();
-  for (uint32_t r = 0; r < n; ++r)
-    if (rcs[r]) fail(rcs[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+  for (uint32_t r = 0; r < n; ++r) {
+    if (!rcs[r]) continue;
+    // one rank failed: the handles the others made are released (no half-built set)
+    for (uint32_t q = 0; q < n; ++q) {
+      if (out[q]) ginsim_cuda_moe_destroy(out[q]);
+      out[q] = nullptr;
+    }
+    fail(rcs[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+  }
   GIN_API_END
 }

@@ -1182,8 +1182,13 @@ extern "C" int ginsim_cuda_window_register_all(const ginsim_cuda_comm_t* comms, 
     });
   }
   for (auto& t : ts) t.join();
-  for (uint32_t r = 0; r < n; ++r)
-    if (rcs[r]) fail(rcs[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+  for (uint32_t r = 0; r < n; ++r) {
+    if (!rcs[r]) continue;
+    // one rank failed: the ranks that registered release the window again
+    for (uint32_t q = 0; q < n; ++q)
+      if (!rcs[q]) ginsim_cuda_window_deregister(comms[q], ids[q]);
+    fail(rcs[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+  }
   *window_id = ids[0];
   GIN_API_END
 }
