@@ -192,3 +192,20 @@ def test_reference_codec_unit_tests_under_address_and_ub_sanitizers(tmp_path):
                        env=dict(os.environ, ASAN_OPTIONS="detect_leaks=1", UBSAN_OPTIONS="print_stacktrace=1"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "11 test cases, 0 failed" in r.stdout, r.stdout
+
+
+def test_cpp_harness_host_paths_under_address_and_ub_sanitizers(tmp_path):
+    """include/ginsim/harness.hpp's host paths (argument checks, summarize,
+    write_csv, launch_processes over posix_spawn, config_from_env) built with
+    -fsanitize=address,undefined and leak detection: no report."""
+    exe = str(tmp_path / "harness_launch_asan")
+    cmd = ["g++", "-std=c++20", "-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+           "-I", os.path.join(ROOT, "include"), "-I", f"{CUDA}/include",
+           os.path.join(ROOT, "tests", "cpp", "harness_launch.cpp"), "-o", exe, "-L", LIBDIR, "-lginsim_b200",
+           f"-Wl,-rpath,{LIBDIR}", "-L", f"{CUDA}/lib64", "-lcudart", "-lpthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120, cwd=str(tmp_path),
+                       env=dict(os.environ, ASAN_OPTIONS="detect_leaks=1", UBSAN_OPTIONS="print_stacktrace=1"))
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "host checks ok" in r.stdout
