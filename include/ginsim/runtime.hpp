@@ -477,6 +477,9 @@ inline std::unique_ptr<DevComm> comm_init_socket(const std::string& host, uint16
                                                  RankId self, const Config& config) {
   if (config.backend && *config.backend != BackendKind::Proxy)
     throw BackendMismatch("the socket transport runs on the Proxy backend");
+  // socket_transport.cpp: the receiver threads are the transport's progress
+  if (config.progress == ProgressMode::Manual)
+    throw UsageError("the socket transport needs threaded progress (ProgressMode::Manual is in-process only)");
   Config cfg = config;
   cfg.backend = BackendKind::Proxy;
   cfg.transport = TransportKind::Socket;

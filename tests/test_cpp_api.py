@@ -140,7 +140,7 @@ REF_TESTS = "/root/reference/proj/tests"
 
 
 @pytest.mark.parametrize("name,run", [("test_core", True), ("test_descriptor", True), ("test_wire", True),
-                                      ("test_runtime", False)])
+                                      ("test_runtime", False), ("test_socket", False)])
 def test_reference_unit_tests_build_unchanged_against_our_headers(tmp_path, name, run):
     """Drop-in check from the reference's side: its own doctest unit sources
     (proj/tests/<name>.cpp, read in place, not copied) compile UNCHANGED
@@ -149,9 +149,10 @@ def test_reference_unit_tests_build_unchanged_against_our_headers(tmp_path, name
     image).  Host-only suites run here: the core types (test_core.cpp:20-88),
     the descriptor codec (test_descriptor.cpp: golden bytes, invariants,
     malformed buffers, 10^4 random round trips) and the GIN1 framing
-    (test_wire.cpp).  test_runtime.cpp's communicator semantics need a GPU;
-    it is compiled and linked only (its ManualWorld drives every rank's
-    comm_init from one thread, which a collective bootstrap cannot serve)."""
+    (test_wire.cpp).  test_runtime.cpp's and test_socket.cpp's communicators
+    need a GPU; they are compiled and linked only (test_runtime's ManualWorld
+    also drives every rank's comm_init from one thread, which a collective
+    bootstrap cannot serve)."""
     src = os.path.join(REF_TESTS, f"{name}.cpp")
     if not os.path.exists(src):
         pytest.skip("reference sources not present (they are read in place, never copied)")
